@@ -1,0 +1,84 @@
+/* oracle/pstokes_oracle.h — TEST INFRASTRUCTURE ONLY (see pstokes_oracle.c).
+ *
+ * Plain-C restatement of the reference solver hot path:
+ * CSR SpMV, ILU(0), GMRES/FGMRES with modified Gram-Schmidt, p-level layouts,
+ * transfers, operator inheritance, the V-cycle, and element condensation.
+ * Reductions follow include/eigen_subset/Eigen/Dense (the arithmetic the
+ * reference is compiled with here), so results are bit-identical to the
+ * reference built in oracle/_ref. Only tests/, __graft_entry__.smoke() and
+ * bench.py's CPU-baseline/reference arm may load this library. */
+#ifndef PSTOKES_ORACLE_H
+#define PSTOKES_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int64_t n;
+  const int64_t* row_ptr;
+  const int32_t* cols;
+  const double* vals;
+} po_csr;
+
+/* DofLayout (dof_layout.hpp:56-85) */
+typedef struct {
+  int scheme;   /* 0 hho-dp, 1 hho-hp, 2 dg */
+  int strategy; /* 0 uncond, 1 v-cond, 2 vp-cond */
+  int k;
+  int n_faces, n_elements;
+  int face_vel, face_press, elem_vel, elem_press;
+} po_layout;
+
+typedef void (*po_apply_fn)(void* ctx, const double* x, double* y);
+
+const char* po_last_error(void);
+
+int po_make_layout(int scheme, int strategy, int k, int n_faces, int n_elements, po_layout* out);
+int64_t po_layout_dim(const po_layout* l);
+int po_coarse_to_fine_map(const po_layout* fine, const po_layout* coarse, int64_t* map);
+
+double po_dot(const double* x, const double* y, int64_t n);
+void po_csr_multiply(const po_csr* a, const double* x, double* y);
+int po_ilu0_factor(const po_csr* a, double* lu, int64_t* diag);
+void po_ilu0_apply(const po_csr* a, const double* lu, const int64_t* diag, const double* x,
+                   double* y);
+/* Returns coarse nnz; with null outputs only counts. */
+int64_t po_inherit(const po_csr* fine, int64_t n_fine, const int64_t* c2f, int64_t n_coarse,
+                   int64_t* row_ptr, int32_t* cols, double* vals);
+
+int po_gmres(po_apply_fn op, void* op_ctx, po_apply_fn pc, void* pc_ctx, int64_t n,
+             const double* rhs, const double* x0, int max_it, double rtol, int left, double* x,
+             int* its, double* rel, int* converged);
+int po_fgmres(po_apply_fn op, void* op_ctx, po_apply_fn pc, void* pc_ctx, int64_t n,
+              const double* rhs, int max_it, double rtol, int restart, double* x, double* hist,
+              int* its, double* rel, int* converged);
+
+typedef struct po_hier po_hier;
+/* Builds levels below `fine` (layout lf): coarse_to_fine maps, inherited
+ * operators, ILU(0) per level; the coarsest level uses ILU-GMRES. */
+po_hier* po_hier_create(const po_csr* fine, const po_layout* lf, const int* degrees, int nlev,
+                        int smoother_iters, double coarse_rtol, int coarse_maxit);
+void po_hier_destroy(po_hier* h);
+int po_hier_nlev(const po_hier* h);
+int64_t po_hier_level_dim(const po_hier* h, int l);
+int64_t po_hier_level_nnz(const po_hier* h, int l);
+void po_hier_level_csr(const po_hier* h, int l, int64_t* row_ptr, int32_t* cols, double* vals);
+void po_hier_level_ilu(const po_hier* h, int l, double* lu);
+int po_vcycle(po_hier* h, int l, const double* d, double* c);
+long long po_hier_coarse_its(const po_hier* h);
+int po_solve(po_hier* h, const double* rhs, double outer_rtol, int outer_maxit, int restart,
+             double* x, double* hist, int* its, long long* coarse_its, int* vcycles, double* rel,
+             int* converged);
+
+/* condense_element (condense.hpp:57-97) on one column-major n x n block. */
+int po_condense(int n, const double* mat, const double* rhs, int n_elim, const int* elim,
+                double* schur, double* reduced_rhs, double* elim_coupling, double* elim_rhs);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif
