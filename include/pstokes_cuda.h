@@ -1,0 +1,160 @@
+/* include/pstokes_cuda.h — C ABI of the B200 solver hot path.
+ *
+ * Drop-in boundary for the solver path of the pstokes reference
+ * (/root/reference/proj/include/pstokes). The reference has no FFI: its hot
+ * path sits behind header-only C++ functions and the ApplyFn callback type
+ * (gmres.hpp:17). Each entry point below names the reference interface it
+ * replaces; include/pstokes_b200/*.hpp wraps them in the reference's C++
+ * signatures and INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - every function returns 0 on success, a PSCU_E* code otherwise; the
+ *    message of the last failure on the calling thread is pscu_last_error();
+ *  - `mem` arguments: PSCU_HOST = host pointers (copied in/out inside the
+ *    call), PSCU_DEVICE = device pointers already on the context's GPU;
+ *  - all work is ordered on the context's stream; calls on one context must
+ *    be serialised by the caller (the reference is single-threaded);
+ *  - there is no CPU fallback: without a usable sm_100 device pscu_create
+ *    fails with PSCU_ENODEV.
+ */
+#ifndef PSTOKES_CUDA_H
+#define PSTOKES_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PSCU_OK = 0,
+  PSCU_EINVAL = 1,     /* std::invalid_argument in the reference */
+  PSCU_ESINGULAR = 2,  /* std::runtime_error: singular block / zero pivot */
+  PSCU_ECUDA = 3,      /* CUDA runtime failure */
+  PSCU_ENODEV = 4,     /* no usable device */
+  PSCU_ENOMEM = 5
+};
+enum { PSCU_HOST = 0, PSCU_DEVICE = 1 };
+enum { PSCU_SMOOTHER_ILU0 = 0, PSCU_SMOOTHER_BJACOBI = 1 };
+enum { PSCU_COARSE_LU = 0, PSCU_COARSE_ILU_GMRES = 1 };
+
+typedef struct pscu_ctx pscu_ctx;
+typedef struct pscu_mat pscu_mat;
+typedef struct pscu_ilu pscu_ilu;
+typedef struct pscu_hier pscu_hier;
+
+/* DofLayout (dof_layout.hpp:56-85). scheme: 0 hho-dp, 1 hho-hp, 2 dg;
+ * strategy: 0 uncond, 1 v-cond, 2 vp-cond. */
+typedef struct {
+  int scheme, strategy, k;
+  int n_faces, n_elements;
+  int face_vel, face_press, elem_vel, elem_press;
+} pscu_layout;
+
+/* LevelConfig (plevels.hpp:23-42) minus the degrees, plus the smoother kind. */
+typedef struct {
+  int smoother;        /* PSCU_SMOOTHER_* (reference: ILU(0)-GMRES) */
+  int smoother_iters;  /* V(s,s) */
+  int coarse;          /* PSCU_COARSE_* */
+  double coarse_rtol;
+  int coarse_maxit;
+} pscu_level_cfg;
+
+/* SolverReport (gmres.hpp:19-27) + device timings. */
+typedef struct {
+  int outer_its;
+  long long coarse_its;
+  int vcycles;
+  double rel_residual;
+  int converged;
+  double t_setup;      /* hierarchy setup, seconds (device events) */
+  double t_solve;      /* setup + FGMRES, seconds: the reference's t_solve */
+} pscu_report;
+
+const char* pscu_last_error(void);
+int pscu_version(void);
+
+/* context ---------------------------------------------------------------- */
+int pscu_create(int device, pscu_ctx** out);
+int pscu_destroy(pscu_ctx* ctx);
+int pscu_synchronize(pscu_ctx* ctx);
+/* Kernel-launch counter (every kernel this library enqueued). */
+long long pscu_launch_count(const pscu_ctx* ctx);
+
+/* CsrMatrix (csr.hpp:19-24) ----------------------------------------------- */
+int pscu_mat_create(pscu_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* cols,
+                    const double* vals, int mem, pscu_mat** out);
+int pscu_mat_destroy(pscu_mat* m);
+int pscu_mat_dims(const pscu_mat* m, int64_t* n, int64_t* nnz);
+int pscu_mat_download(pscu_ctx* ctx, const pscu_mat* m, int64_t* row_ptr, int32_t* cols,
+                      double* vals);
+/* CsrMatrix::multiply (csr.hpp:68-74): y = A x, per-row sequential sums. */
+int pscu_spmv(pscu_ctx* ctx, const pscu_mat* a, const double* x, double* y, int mem);
+
+/* Ilu0 (ilu0.hpp:19-65): factorisation on the device, bit-identical. ------ */
+int pscu_ilu0_create(pscu_ctx* ctx, const pscu_mat* a, pscu_ilu** out);
+int pscu_ilu0_destroy(pscu_ilu* p);
+int pscu_ilu0_factors(pscu_ctx* ctx, const pscu_ilu* p, double* lu_host);
+int pscu_ilu0_apply(pscu_ctx* ctx, const pscu_ilu* p, const double* x, double* y, int mem);
+
+/* layouts and transfers (dof_layout.hpp:87-126, plevels.hpp:47-113) ------- */
+int pscu_layout_make(int scheme, int strategy, int k, int n_faces, int n_elements,
+                     pscu_layout* out);
+int64_t pscu_layout_dim(const pscu_layout* l);
+int pscu_coarse_to_fine(const pscu_layout* fine, const pscu_layout* coarse, int64_t* map);
+/* inherit_matrix (plevels.hpp:93-113) as a device gather. */
+int pscu_inherit(pscu_ctx* ctx, const pscu_mat* fine, const pscu_layout* lf,
+                 const pscu_layout* lc, pscu_mat** out);
+
+/* Krylov (gmres.hpp:103-173) on a device operator ------------------------ */
+/* gmres with ILU(0) preconditioner (pc may be NULL); side 0 right, 1 left. */
+int pscu_gmres(pscu_ctx* ctx, const pscu_mat* a, const pscu_ilu* pc, const double* rhs,
+               const double* x0, int max_it, double rtol, int side, double* x, int* its,
+               double* rel, int* converged, int mem);
+/* fgmres with a fixed ILU(0) preconditioner (pc NULL = identity). */
+int pscu_fgmres(pscu_ctx* ctx, const pscu_mat* a, const pscu_ilu* pc, const double* rhs,
+                int max_it, double rtol, double* x, int* its, double* rel, int* converged,
+                int mem);
+
+/* p-multilevel hierarchy (plevels.hpp:115-239) ---------------------------- */
+int pscu_hier_create(pscu_ctx* ctx, const pscu_mat* fine, const pscu_layout* lf,
+                     const int* degrees, int nlev, const pscu_level_cfg* cfg, pscu_hier** out);
+int pscu_hier_destroy(pscu_hier* h);
+int pscu_hier_nlev(const pscu_hier* h);
+const pscu_mat* pscu_hier_level_mat(const pscu_hier* h, int l);
+const pscu_ilu* pscu_hier_level_ilu(const pscu_hier* h, int l);
+int pscu_vcycle(pscu_ctx* ctx, pscu_hier* h, int level, const double* d, double* c, int mem);
+long long pscu_hier_coarse_its(const pscu_hier* h);
+void pscu_hier_reset(pscu_hier* h);
+/* solve_system (plevels.hpp:217-239) on an assembled system: FGMRES
+ * preconditioned by one V-cycle per iteration. restart = 0 reproduces the
+ * reference (unrestarted); hist (nullable, host) receives |g_{j+1}|/||b||. */
+int pscu_solve(pscu_ctx* ctx, pscu_hier* h, const double* rhs, double rtol, int maxit,
+               int restart, double* x, double* hist, pscu_report* rep, int mem);
+/* One-call drop-in for solve_system: uploads the CSR system, builds the
+ * hierarchy, solves, downloads x (host buffers; copies are timed inside). */
+int pscu_solve_system(pscu_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* cols,
+                      const double* vals, const double* rhs, const pscu_layout* lf,
+                      const int* degrees, int nlev, const pscu_level_cfg* cfg, double rtol,
+                      int maxit, int restart, double* x, double* hist, pscu_report* rep);
+
+/* static condensation (condense.hpp:57-97, assemble.hpp:121-169) --------- */
+/* Batched condense_element over `nelem` elements with identical local size n
+ * and elimination list. mats: nelem column-major n x n blocks; rhs: nelem x n.
+ * Outputs (nullable): schur nelem x nk x nk, reduced_rhs nelem x nk,
+ * elim_coupling nelem x ne x nk, elim_rhs nelem x ne (column-major blocks).
+ * On a near-singular block returns PSCU_ESINGULAR and *bad_element. */
+int pscu_condense_batch(pscu_ctx* ctx, int nelem, int n, const double* mats, const double* rhs,
+                        int n_elim, const int* elim, double* schur, double* reduced_rhs,
+                        double* elim_coupling, double* elim_rhs, int* bad_element, int mem);
+/* ElementCondensation::recover (condense.hpp:28-38) for all elements:
+ * locals[e] (n) from global x through kept_global (nelem x nk). */
+int pscu_recover_batch(pscu_ctx* ctx, int nelem, int n, int n_elim, const int* elim,
+                       const int64_t* kept_global, const double* elim_coupling,
+                       const double* elim_rhs, const double* x, double* locals, int mem);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -461,6 +461,10 @@ int po_fgmres(po_apply_fn op, void* op_ctx, po_apply_fn pc, void* pc_ctx, int64_
           done = 1;
           break;
         }
+        if (j + 1 == mm) { /* cycle exhausted after a failed true-residual check */
+          restart_now = 1;
+          memcpy(x0, xs, sizeof(double) * (size_t)n);
+        }
       } else if (j + 1 == mm) {
         restart_now = 1;
         arnoldi_solution(&ws, x0, m, ws.z, xs);

@@ -454,6 +454,10 @@ static KrylovResult fgmres_hist(const ApplyFn& op, const ApplyFn& pc, const Eige
           return res;
         }
         if (last) return res;
+        if (j + 1 == mm) { // cycle exhausted after a failed true-residual check
+          restart_now = true;
+          x0 = res.x;
+        }
       } else if (j + 1 == mm) {
         restart_now = true;
         x0 = ws.solution(x0, m);

@@ -1,0 +1,113 @@
+"""In-tree build of the sm_100a solver library and (for tests) the oracles.
+
+``build_native()`` compiles paper_2009_13840_b200/csrc/*.cu with nvcc for
+``-gencode arch=compute_100a,code=sm_100a`` into
+paper_2009_13840_b200/libpstokes_b200.so (git-ignored, travels to the GPU
+box with the gpurun snapshot). ``--fmad=false`` and ``-ffp-contract=off``
+keep every floating-point operation individually rounded so the device
+results are bit-identical to the reference's operation order.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OBJ = os.path.join(PKG, "_build")
+LIB = os.path.join(PKG, "libpstokes_b200.so")
+HOST_LIB = os.path.join(PKG, "libpstokes_host.so")
+
+NVCC_FLAGS = [
+    "-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+    "--fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off", "-Wno-deprecated-gpu-targets",
+    "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
+]
+
+
+def _nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found: the CUDA toolkit is required to build the solver")
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build_native(force: bool = False, verbose: bool = False) -> str:
+    nvcc = _nvcc()
+    os.makedirs(OBJ, exist_ok=True)
+    sources = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    headers.append(os.path.join(ROOT, "include", "pstokes_cuda.h"))
+    jobs = []
+    objs = []
+    for src in sources:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJ, src[:-3] + ".o")
+        objs.append(o)
+        if force or _stale(o, [s] + headers):
+            jobs.append([nvcc, *NVCC_FLAGS, "-c", s, "-o", o])
+
+    def run(cmd):
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {cmd[-3]}:\n{r.stderr}")
+
+    with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
+        list(ex.map(run, jobs))
+    if force or jobs or _stale(LIB, objs):
+        run([nvcc, "-shared", "-o", LIB, *objs, "-lcudart"])
+    return LIB
+
+
+def build_host(force: bool = False) -> str:
+    """Host-side input producer (mesh, bases, HHO local blocks, pattern)."""
+    src_dir = os.path.join(PKG, "host")
+    if not os.path.isdir(src_dir):
+        return ""
+    sources = sorted(os.path.join(src_dir, f) for f in os.listdir(src_dir) if f.endswith(".cpp"))
+    headers = [os.path.join(src_dir, f) for f in os.listdir(src_dir) if f.endswith(".hpp")]
+    if not sources:
+        return ""
+    if force or _stale(HOST_LIB, sources + headers):
+        cmd = ["g++", "-std=c++20", "-O3", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off",
+               "-I" + os.path.join(ROOT, "include"), "-I" + src_dir, "-o", HOST_LIB, *sources]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"host build failed:\n{r.stderr}")
+    return HOST_LIB
+
+
+def build_oracle(force: bool = False) -> None:
+    """Builds oracle/_build (C restatement) and, when /root/reference is
+    present, oracle/_ref (the reference compiled in place). Test
+    infrastructure only."""
+    oracle = os.path.join(ROOT, "oracle")
+    targets = ["restatement"]
+    if os.path.isdir("/root/reference/proj/include"):
+        targets.append(os.path.join(oracle, "_ref", "libpstokes_ref.so"))
+    cmd = ["make", "-C", oracle, *targets]
+    if force:
+        cmd.insert(1, "-B")
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"oracle build failed:\n{r.stdout}\n{r.stderr}")
+
+
+if __name__ == "__main__":
+    f = "--force" in sys.argv
+    print(build_native(force=f, verbose=True))
+    print(build_host(force=f))
+    build_oracle(force=f)

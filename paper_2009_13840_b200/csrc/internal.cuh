@@ -1,0 +1,165 @@
+// Internal declarations of the B200 solver library (not installed).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "pstokes_cuda.h"
+
+namespace pscu {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PSCU_CUDA(call)                                                                     \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::pscu::Error(PSCU_ECUDA, std::string(#call ": ") + cudaGetErrorString(e_));    \
+  } while (0)
+
+#define PSCU_LAUNCHED(ctx)                                                                  \
+  do {                                                                                      \
+    (ctx)->launches++;                                                                      \
+    cudaError_t e_ = cudaGetLastError();                                                    \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::pscu::Error(PSCU_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Bit-exact arithmetic helpers: one IEEE-rounded operation each, never fused.
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) {
+      cudaError_t e = cudaMalloc(&p, sizeof(T) * count);
+      if (e != cudaSuccess)
+        throw Error(PSCU_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    if (count > n) alloc(count);
+    if (count) PSCU_CUDA(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& h, cudaStream_t s) { upload(h.data(), h.size(), s); }
+};
+
+/// Fixed-shape reproducible dot product (include/eigen_subset/Eigen/Dense,
+/// internal::repro_lanes / repro_dot_fn): T strided partials, adjacent-pair
+/// binary tree.
+inline int64_t repro_lanes(int64_t n) {
+  int64_t want = (n + 15) / 16, t = 1;
+  while (t < want && t < (int64_t(1) << 18)) t <<= 1;
+  return t;
+}
+
+struct Context;
+
+/// Device CSR (csr.hpp:19-24) plus a host copy of the pattern for schedule
+/// construction.
+struct Csr {
+  int64_t n = 0, nnz = 0;
+  DevBuf<int64_t> row_ptr;
+  DevBuf<int32_t> cols;
+  DevBuf<double> vals;
+  std::vector<int64_t> h_row_ptr;
+  std::vector<int32_t> h_cols;
+};
+
+/// Schedule for one sparse triangular sweep (sync-free, chunked, levelled).
+struct Sweep {
+  int nchunks = 0;
+  int nlevels = 0;
+  int max_chunk_rows = 0;
+  int max_level_rows = 0;
+  DevBuf<int64_t> chunk_begin, chunk_end; // row range of chunk c (processing order)
+  DevBuf<int32_t> chunk_lvl;              // nchunks+1, global level index
+  DevBuf<int32_t> level_ptr;              // nlevels+1 into sched
+  DevBuf<int32_t> sched;                  // row ids, grouped by level
+  DevBuf<int32_t> wait_ptr;               // nlevels+1
+  DevBuf<int32_t> wait_chunk;             // foreign chunk (processing index)
+  DevBuf<int32_t> wait_need;              // required local progress of that chunk
+  DevBuf<uint8_t> exported;               // level publishes progress
+  DevBuf<unsigned long long> progress;    // nchunks, tagged with the launch epoch
+  DevBuf<unsigned long long> ticket;      // 1
+};
+
+struct Ilu {
+  const Csr* a = nullptr;
+  DevBuf<double> lu;
+  DevBuf<int64_t> diag;
+  Sweep fwd, bwd;
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  long long launches = 0;
+  // reduction scratch
+  DevBuf<double> red_partials;     // per-block results
+  DevBuf<unsigned int> red_counter; // last-block counter
+  DevBuf<double> scal;             // device scalars (Hessenberg column etc.)
+  double* h_pinned = nullptr;      // pinned host mirror of scal
+  DevBuf<int> err_flag;
+  size_t scal_cap = 0;
+  ~Context();
+};
+
+// spmv.cu
+void spmv(Context& c, const Csr& a, const double* x, double* y);
+/// r_c[i] = (d - A w)[map[i]] for i < nc (fused residual + restriction).
+void residual_restrict(Context& c, const Csr& a, const double* d, const double* w,
+                       const int64_t* map, int64_t nc, double* rc);
+void upload_csr(Context& c, Csr& m, int64_t n, const int64_t* rp, const int32_t* cols,
+                const double* vals, int mem);
+
+// sptrsv.cu
+void build_sweep(Context& c, const Csr& a, const std::vector<int64_t>& diag, bool forward,
+                 Sweep& s);
+void ilu0_factor(Context& c, Ilu& ilu);
+void ilu0_apply(Context& c, const Ilu& ilu, const double* x, double* y);
+
+// krylov.cu
+double dot(Context& c, const double* x, const double* y, int64_t n);
+void copy(Context& c, double* dst, const double* src, int64_t n);
+void zero(Context& c, double* dst, int64_t n);
+
+} // namespace pscu

@@ -1,0 +1,345 @@
+"""Python mirror of the reference's solver-path API, backed by the sm_100a
+library (include/pstokes_cuda.h). Names and argument meaning follow
+/root/reference/proj/include/pstokes (cited per class); errors map to the
+reference's exception types (ValueError for std::invalid_argument,
+NativeError/RuntimeError for std::runtime_error)."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+SCHEMES = {"hho-dp": 0, "hho-hp": 1, "dg": 2}
+STRATEGIES = {"uncond": 0, "v-cond": 1, "vp-cond": 2, "v&p-cond": 2}
+SMOOTHERS = {"ilu0": 0, "bjacobi": 1}
+COARSE = {"lu": 0, "gmres-ilu": 1}
+
+
+class Context:
+    """One CUDA context/stream (pscu_create)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = N.load()
+        h = C.c_void_p()
+        N.check(self.lib.pscu_create(device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.pscu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def launches(self) -> int:
+        return int(self.lib.pscu_launch_count(self.h))
+
+    def synchronize(self):
+        N.check(self.lib.pscu_synchronize(self.h))
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class CsrMatrix:
+    """Device CsrMatrix (csr.hpp:19-115)."""
+
+    def __init__(self, row_ptr, cols, vals, ctx: Context | None = None, _handle=None, _owner=None):
+        self.ctx = ctx or default_context()
+        self.lib = self.ctx.lib
+        self._owner = _owner
+        if _handle is not None:
+            self.h = C.c_void_p(_handle)
+            self._owned = False
+        else:
+            rp = np.ascontiguousarray(row_ptr, np.int64)
+            cl = np.ascontiguousarray(cols, np.int32)
+            vl = _f64(vals)
+            h = C.c_void_p()
+            N.check(self.lib.pscu_mat_create(self.ctx.h, len(rp) - 1, rp.ctypes.data,
+                                             cl.ctypes.data, vl.ctypes.data, N.PSCU_HOST,
+                                             C.byref(h)))
+            self.h = h
+            self._owned = True
+        n, nnz = C.c_int64(), C.c_int64()
+        self.lib.pscu_mat_dims(self.h, C.byref(n), C.byref(nnz))
+        self.n, self.nnz = n.value, nnz.value
+
+    def __del__(self):
+        if getattr(self, "_owned", False) and getattr(self, "h", None):
+            self.lib.pscu_mat_destroy(self.h)
+            self.h = None
+
+    def download(self):
+        rp = np.zeros(self.n + 1, np.int64)
+        cl = np.zeros(self.nnz, np.int32)
+        vl = np.zeros(self.nnz)
+        N.check(self.lib.pscu_mat_download(self.ctx.h, self.h, rp.ctypes.data, cl.ctypes.data,
+                                           vl.ctypes.data))
+        return rp, cl, vl
+
+    def multiply(self, x) -> np.ndarray:
+        """CsrMatrix::multiply (csr.hpp:68-79)."""
+        x = _f64(x)
+        y = np.zeros(self.n)
+        N.check(self.lib.pscu_spmv(self.ctx.h, self.h, x.ctypes.data, y.ctypes.data, N.PSCU_HOST))
+        return y
+
+
+class Ilu0:
+    """Ilu0 (ilu0.hpp:17-79): factorisation and application on the device."""
+
+    def __init__(self, a: CsrMatrix, _handle=None):
+        self.a = a
+        self.ctx = a.ctx
+        self.lib = a.lib
+        if _handle is not None:
+            self.h = C.c_void_p(_handle)
+            self._owned = False
+        else:
+            h = C.c_void_p()
+            N.check(self.lib.pscu_ilu0_create(self.ctx.h, a.h, C.byref(h)))
+            self.h = h
+            self._owned = True
+
+    def __del__(self):
+        if getattr(self, "_owned", False) and getattr(self, "h", None):
+            self.lib.pscu_ilu0_destroy(self.h)
+            self.h = None
+
+    def factors(self) -> np.ndarray:
+        lu = np.zeros(self.a.nnz)
+        N.check(self.lib.pscu_ilu0_factors(self.ctx.h, self.h, lu.ctypes.data))
+        return lu
+
+    def apply(self, x) -> np.ndarray:
+        x = _f64(x)
+        y = np.zeros(self.a.n)
+        N.check(self.lib.pscu_ilu0_apply(self.ctx.h, self.h, x.ctypes.data, y.ctypes.data,
+                                         N.PSCU_HOST))
+        return y
+
+
+@dataclass
+class KrylovResult:
+    """KrylovResult (gmres.hpp:29-34)."""
+    x: np.ndarray
+    iterations: int
+    rel_residual: float
+    converged: bool
+
+
+def gmres(a: CsrMatrix, precond: Ilu0 | None, rhs, x0, max_it: int, rtol: float,
+          side: str = "right") -> KrylovResult:
+    """gmres (gmres.hpp:103-139) with A and an ILU(0) preconditioner on the
+    device. ``x0=None`` means the zero vector."""
+    rhs = _f64(rhs)
+    x0a = None if x0 is None else _f64(x0)
+    x = np.zeros(a.n)
+    its, rel, conv = C.c_int(), C.c_double(), C.c_int()
+    N.check(a.lib.pscu_gmres(a.ctx.h, a.h, precond.h if precond else None, rhs.ctypes.data,
+                             None if x0a is None else x0a.ctypes.data, max_it, rtol,
+                             1 if side == "left" else 0, x.ctypes.data, C.byref(its),
+                             C.byref(rel), C.byref(conv), N.PSCU_HOST))
+    return KrylovResult(x, its.value, rel.value, bool(conv.value))
+
+
+def fgmres(a: CsrMatrix, precond: Ilu0 | None, rhs, max_it: int, rtol: float) -> KrylovResult:
+    """fgmres (gmres.hpp:145-173) with a fixed ILU(0) (or identity)."""
+    rhs = _f64(rhs)
+    x = np.zeros(a.n)
+    its, rel, conv = C.c_int(), C.c_double(), C.c_int()
+    N.check(a.lib.pscu_fgmres(a.ctx.h, a.h, precond.h if precond else None, rhs.ctypes.data,
+                              max_it, rtol, x.ctypes.data, C.byref(its), C.byref(rel),
+                              C.byref(conv), N.PSCU_HOST))
+    return KrylovResult(x, its.value, rel.value, bool(conv.value))
+
+
+def make_layout(scheme: str | int, strategy: str | int, k: int, n_faces: int,
+                n_elements: int) -> N.Layout:
+    """make_layout (dof_layout.hpp:87-126) from mesh counts."""
+    s = SCHEMES[scheme] if isinstance(scheme, str) else scheme
+    t = STRATEGIES[strategy] if isinstance(strategy, str) else strategy
+    lay = N.Layout()
+    N.check(N.load().pscu_layout_make(s, t, k, n_faces, n_elements, C.byref(lay)))
+    return lay
+
+
+def layout_dim(lay: N.Layout) -> int:
+    return int(N.load().pscu_layout_dim(C.byref(lay)))
+
+
+def coarse_to_fine_map(fine: N.Layout, coarse: N.Layout) -> np.ndarray:
+    """coarse_to_fine_map (plevels.hpp:47-72)."""
+    m = np.zeros(layout_dim(coarse), np.int64)
+    N.check(N.load().pscu_coarse_to_fine(C.byref(fine), C.byref(coarse), m.ctypes.data))
+    return m
+
+
+def inherit_matrix(fine: CsrMatrix, lf: N.Layout, lc: N.Layout) -> CsrMatrix:
+    """inherit_matrix (plevels.hpp:93-113) as a device gather."""
+    h = C.c_void_p()
+    N.check(fine.lib.pscu_inherit(fine.ctx.h, fine.h, C.byref(lf), C.byref(lc), C.byref(h)))
+    m = CsrMatrix(None, None, None, ctx=fine.ctx, _handle=h.value)
+    m._owned = True
+    return m
+
+
+@dataclass
+class LevelConfig:
+    """LevelConfig (plevels.hpp:23-42) + smoother kind and FGMRES restart."""
+    degrees: list
+    smoother_iters: int = 2
+    coarse: str = "lu"
+    coarse_rtol: float = 1e-3
+    coarse_maxit: int = 400
+    outer_rtol: float = 1e-13
+    outer_maxit: int = 1000
+    smoother: str = "ilu0"
+    restart: int = 0
+
+    def native(self) -> N.LevelCfg:
+        return N.LevelCfg(SMOOTHERS[self.smoother], self.smoother_iters, COARSE[self.coarse],
+                          self.coarse_rtol, self.coarse_maxit)
+
+
+@dataclass
+class SolverReport:
+    """SolverReport (gmres.hpp:19-27)."""
+    outer_its: int
+    coarse_its: int
+    vcycles: int
+    rel_residual: float
+    converged: bool
+    t_setup: float
+    t_solve: float
+
+
+class LevelHierarchy:
+    """LevelHierarchy (plevels.hpp:125-212) on the device."""
+
+    def __init__(self, a: CsrMatrix, layout: N.Layout, cfg: LevelConfig):
+        self.a = a
+        self.cfg = cfg
+        self.lib = a.lib
+        self.ctx = a.ctx
+        deg = np.ascontiguousarray(cfg.degrees, np.int32)
+        self._deg = deg
+        h = C.c_void_p()
+        ncfg = cfg.native()
+        N.check(self.lib.pscu_hier_create(self.ctx.h, a.h, C.byref(layout), deg.ctypes.data,
+                                          len(deg), C.byref(ncfg), C.byref(h)))
+        self.h = h
+        self.nlev = len(deg)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.pscu_hier_destroy(self.h)
+            self.h = None
+
+    def level_matrix(self, l: int) -> CsrMatrix:
+        p = self.lib.pscu_hier_level_mat(self.h, l)
+        return CsrMatrix(None, None, None, ctx=self.ctx, _handle=p, _owner=self)
+
+    def level_ilu(self, l: int) -> Ilu0:
+        p = self.lib.pscu_hier_level_ilu(self.h, l)
+        if not p:
+            raise ValueError("level has no ILU(0) factor")
+        return Ilu0(self.level_matrix(l), _handle=p)
+
+    def vcycle(self, l: int, defect) -> np.ndarray:
+        d = _f64(defect)
+        c = np.zeros_like(d)
+        N.check(self.lib.pscu_vcycle(self.ctx.h, self.h, l, d.ctypes.data, c.ctypes.data,
+                                     N.PSCU_HOST))
+        return c
+
+    def coarse_iterations(self) -> int:
+        return int(self.lib.pscu_hier_coarse_its(self.h))
+
+    def reset_counters(self):
+        self.lib.pscu_hier_reset(self.h)
+
+    def solve(self, rhs, rtol: float | None = None, maxit: int | None = None,
+              restart: int | None = None, history: bool = True):
+        """fgmres(A, vcycle) (plevels.hpp:217-239) -> (x, hist, SolverReport)."""
+        rhs = _f64(rhs)
+        rtol = self.cfg.outer_rtol if rtol is None else rtol
+        maxit = self.cfg.outer_maxit if maxit is None else maxit
+        restart = self.cfg.restart if restart is None else restart
+        x = np.zeros(self.a.n)
+        hist = np.zeros(maxit + 1)
+        rep = N.Report()
+        N.check(self.lib.pscu_solve(self.ctx.h, self.h, rhs.ctypes.data, rtol, maxit, restart,
+                                    x.ctypes.data, hist.ctypes.data if history else None,
+                                    C.byref(rep), N.PSCU_HOST))
+        r = SolverReport(rep.outer_its, rep.coarse_its, rep.vcycles, rep.rel_residual,
+                         bool(rep.converged), rep.t_setup, rep.t_solve)
+        return x, hist[: rep.outer_its].copy(), r
+
+
+def solve_system(row_ptr, cols, vals, rhs, layout: N.Layout, cfg: LevelConfig,
+                 ctx: Context | None = None):
+    """solve_system (plevels.hpp:217-239) through the one-call C ABI entry:
+    host CSR + rhs in, x out; upload, setup and solve are all inside the
+    timed t_solve. Returns (x, hist, SolverReport)."""
+    ctx = ctx or default_context()
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cl = np.ascontiguousarray(cols, np.int32)
+    vl = _f64(vals)
+    b = _f64(rhs)
+    deg = np.ascontiguousarray(cfg.degrees, np.int32)
+    n = len(rp) - 1
+    x = np.zeros(n)
+    hist = np.zeros(cfg.outer_maxit + 1)
+    rep = N.Report()
+    ncfg = cfg.native()
+    N.check(ctx.lib.pscu_solve_system(ctx.h, n, rp.ctypes.data, cl.ctypes.data, vl.ctypes.data,
+                                      b.ctypes.data, C.byref(layout), deg.ctypes.data, len(deg),
+                                      C.byref(ncfg), cfg.outer_rtol, cfg.outer_maxit, cfg.restart,
+                                      x.ctypes.data, hist.ctypes.data, C.byref(rep)))
+    r = SolverReport(rep.outer_its, rep.coarse_its, rep.vcycles, rep.rel_residual,
+                     bool(rep.converged), rep.t_setup, rep.t_solve)
+    return x, hist[: rep.outer_its].copy(), r
+
+
+def condense_elements(mats, rhs, elim, ctx: Context | None = None):
+    """Batched condense_element (condense.hpp:57-97) over elements sharing one
+    local size and elimination list. mats: (nelem, n, n), rhs: (nelem, n).
+    Returns dict(schur, reduced_rhs, elim_coupling, elim_rhs) as arrays of
+    per-element matrices (row-major numpy views of column-major blocks)."""
+    ctx = ctx or default_context()
+    mats = np.asarray(mats, np.float64)
+    nelem, n, _ = mats.shape
+    colmajor = np.ascontiguousarray(np.transpose(mats, (0, 2, 1)))
+    b = _f64(rhs).reshape(nelem, n)
+    el = np.ascontiguousarray(elim, np.int32)
+    ne = len(el)
+    nk = n - ne
+    schur = np.zeros((nelem, nk, nk))
+    rr = np.zeros((nelem, nk))
+    coup = np.zeros((nelem, max(ne, 1) * nk))
+    er = np.zeros((nelem, max(ne, 1)))
+    bad = C.c_int(-1)
+    N.check(ctx.lib.pscu_condense_batch(ctx.h, nelem, n, colmajor.ctypes.data, b.ctypes.data, ne,
+                                        el.ctypes.data, schur.ctypes.data, rr.ctypes.data,
+                                        coup.ctypes.data, er.ctypes.data, C.byref(bad),
+                                        N.PSCU_HOST))
+    return dict(schur=np.transpose(schur, (0, 2, 1)), reduced_rhs=rr,
+                elim_coupling=np.transpose(coup[:, : ne * nk].reshape(nelem, nk, ne), (0, 2, 1)),
+                elim_rhs=er[:, :ne])
