@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""bench.py — condensed DoFs/s solved to rtol 1e-8 (FGMRES + p-MG V-cycle).
+
+Workload (default): BASELINE.json config 2(a) — unit square, 256x256 cells
+split into triangles, interior vertices jittered by 0.2h (SplitMix64 seed 0),
+HHO-dp (hybrid velocity, discontinuous pressure) with element velocity
+condensed, k = 3, p-levels 3 -> 2 -> 1 -> 0, V(2,2) with the reference's
+ILU(0)-GMRES smoother, ILU-GMRES coarse solve (rtol 1e-3, maxit 400),
+FGMRES(30) to rtol 1e-8, sin/cos manufactured data, FP64.
+
+One step = one reference `t_solve` (plevels.hpp:217-235): hierarchy setup
+(operator inheritance, ILU(0) factorisations, sweep schedules) + FGMRES on
+the condensed system resident in HBM. value = dofs x n_gpus / step time
+(replicas: the 2D path does not shard). e2e = the same through the one-call
+C ABI (pscu_solve_system) from host buffers, copies inside the timed region.
+
+--impl reference times the reference's own solver (oracle/_ref, the
+unmodified headers) on the host cores: every core solves the same bounded
+sample of the workload recipe concurrently.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "config1": dict(tri=False, n=16, jitter=0.0, seed=0, k=1, strategy="v-cond", degrees=[1, 0],
+                    coarse="lu", name="2D unit square 16x16 quads, HHO-dp v-cond, k=1, levels 1-0"),
+    "config2a": dict(tri=True, n=256, jitter=0.2, seed=0, k=3, strategy="v-cond",
+                     degrees=[3, 2, 1, 0], coarse="gmres-ilu",
+                     name="2D unit square 256x256x2 jittered tris (0.2h, seed 0), HHO-dp v-cond, "
+                          "k=3, levels 3-2-1-0"),
+    "config2b": dict(tri=True, n=256, jitter=0.2, seed=0, k=3, strategy="vp-cond",
+                     degrees=[3, 2, 1, 0], coarse="gmres-ilu",
+                     name="2D unit square 256x256x2 jittered tris (0.2h, seed 0), HHO-dp vp-cond, "
+                          "k=3, levels 3-2-1-0"),
+}
+METRIC = "condensed DoFs/s solved to rtol 1e-8 (FGMRES+p-MG V-cycle)"
+RTOL = 1e-8
+RESTART = 30
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax.append(float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_record(cls: str):
+    """dram bytes per launch of the dominant kernel class from the committed
+    `ncu --set full` capture summary (profiles/ncu_summary.json), if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        return d.get("traffic_bytes_per_launch", {}).get(cls)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline (oracle/_ref, test infrastructure)
+# ---------------------------------------------------------------------------
+
+def _ref_worker(args):
+    cfg, n = args
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_ref as O
+
+    s = O.RefSystem(mesh="unit-tri" if cfg["tri"] else "unit-quad", n=n, seed=cfg["seed"],
+                    jitter=cfg["jitter"], side="top", scheme="hho-dp", strategy=cfg["strategy"],
+                    k=cfg["k"], data="sincos")
+    r = s.solve(cfg["degrees"], coarse=cfg["coarse"], rtol=RTOL, restart=RESTART)
+    return s.n, r["t_solve"], r["its"], r["converged"]
+
+
+def reference_sample(cfg: dict, n: int, procs: int, steps: int):
+    """Runs `steps` rounds of `procs` concurrent reference solves of the
+    sample; returns per-round (dofs*procs/t) and the sample description."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("fork")
+    vals, its = [], None
+    dofs = None
+    with ctx.Pool(procs) as pool:
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            res = pool.map(_ref_worker, [(cfg, n)] * procs)
+            dt = time.perf_counter() - t0
+            dofs = res[0][0]
+            its = res[0][2]
+            # the solves' own t_solve windows exclude their assembly
+            t_solve = max(r[1] for r in res)
+            vals.append(dofs * procs / t_solve)
+            del dt
+    return vals, dofs, its
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    procs = os.cpu_count() or 1
+    n = args.cpu_sample_n
+    vals, dofs, its = reference_sample(cfg, n, procs, args.warmup + args.steps)
+    timed = vals[args.warmup:]
+    v = statistics.mean(timed)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "DoF/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dofs * procs / v, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (manufactured sin/cos field)",
+        "config": {"workload": cfg["name"] + f" [reference sample at {n}x{n}]",
+                   "dofs_per_solve": dofs, "fgmres_its": its, "solver": "reference solve_system",
+                   "parallelism": f"{procs} concurrent single-threaded solves"},
+        "cpu_baseline": {"value": v, "unit": "DoF/s", "cores": procs, "kind": "reference",
+                         "sample": f"config recipe at {n}x{n} ({dofs} DoFs): hierarchy setup + "
+                                   f"FGMRES, {procs} concurrent solves"},
+        "e2e": {"value": v, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args, cfg):
+    ws, rank, local = dist_env()
+    import numpy as np
+    import torch
+
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2009_13840_b200 import host
+    from paper_2009_13840_b200 import solver as S
+
+    n = args.n or cfg["n"]
+    ctx = S.Context(local)
+    t0 = time.time()
+    mesh = host.Mesh.unit_square(n, tri=cfg["tri"], jitter=cfg["jitter"], seed=cfg["seed"],
+                                 neumann="top")
+    loc = host.LocalSystem(mesh, "hho-dp", cfg["strategy"], cfg["k"], data="sincos")
+    A, b = host.assemble_stokes(loc, ctx=ctx)
+    t_asm = time.time() - t0
+    lay = loc.layout()
+    lcfg = S.LevelConfig(degrees=cfg["degrees"], coarse=cfg["coarse"], outer_rtol=RTOL,
+                         restart=RESTART)
+    dofs = A.n
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if ws == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def step():
+        h = S.LevelHierarchy(A, lay, lcfg)
+        x, hist, rep = h.solve(b)
+        del h
+        return rep
+
+    reps = []
+    for _ in range(args.warmup):
+        reps.append(step())
+    barrier()
+    ctx.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.launches()
+    ctx.profile(True)
+    times = []
+    for _ in range(args.steps):
+        ctx.timer_start()
+        reps.append(step())
+        times.append(ctx.timer_stop() / 1e3)
+    ctx.synchronize()
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    launches = ctx.launches() - launches0
+    barrier()
+    clk = clocks.stop()
+    t_step = max_over_ranks(statistics.mean(times))
+    rep = reps[-1]
+
+    # e2e through the one-call C ABI from host buffers
+    rp, cl, vl = A.download()
+    bh = np.array(b)
+    e2e_times = []
+    for _ in range(max(1, args.e2e_steps)):
+        ctx.timer_start()
+        x, hist, r2 = S.solve_system(rp, cl, vl, bh, lay, lcfg, ctx=ctx)
+        e2e_times.append(ctx.timer_stop() / 1e3)
+    t_e2e = max_over_ranks(statistics.mean(e2e_times))
+    h2d = rp.nbytes + cl.nbytes + vl.nbytes + bh.nbytes
+    d2h = x.nbytes
+
+    if rank != 0:
+        return
+    # dominant kernel class and its roofline
+    peak, peak_src = peaks()
+    dom = max(prof, key=lambda k: prof[k][1])
+    cnt, ms, byt = prof[dom]
+    achieved = (byt / (ms / 1e3)) / 1e9 if ms > 0 else 0.0
+    traffic = traffic_record(dom)
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        try:
+            vals, sdofs, sits = reference_sample(cfg, args.cpu_sample_n, 1, 1)
+            cpu = {"value": vals[0], "unit": "DoF/s", "cores": 1, "kind": "reference",
+                   "sample": f"reference solve_system (oracle/_ref) of the config recipe at "
+                             f"{args.cpu_sample_n}x{args.cpu_sample_n} ({sdofs} DoFs, {sits} "
+                             f"FGMRES its), 1 core"}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "DoF/s", "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    line = {
+        "metric": METRIC,
+        "value": dofs * ws / t_step,
+        "unit": "DoF/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (manufactured sin/cos field, BASELINE.json config recipe)",
+        "config": {
+            "workload": cfg["name"] + (f" [n={n}]" if n != cfg["n"] else ""),
+            "dofs": dofs, "nnz": A.nnz, "fgmres_its": rep.outer_its,
+            "coarse_its_per_vcycle": rep.coarse_its / max(rep.vcycles, 1),
+            "converged": rep.converged, "rel_residual": rep.rel_residual,
+            "smoother": "ILU(0)-GMRES V(2,2) (reference smoother)",
+            "coarse": "ILU-GMRES rtol 1e-3 maxit 400" if cfg["coarse"] != "lu" else "dense LU",
+            "restart": RESTART, "step": "hierarchy setup + FGMRES (reference t_solve)",
+            "l2": "inputs larger than L2 (fine operator %.2f GB)" % ((12 * A.nnz) / 1e9),
+            "assembly_s_untimed": round(t_asm, 3), "parallelism": f"replicas x{ws}",
+        },
+        "e2e": {"value": dofs * ws / t_e2e, "unit": "DoF/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches // max(args.steps, 1)),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_src, "launch_groups": cnt,
+                     "avg_ms": ms / max(cnt, 1),
+                     "share_of_step": (ms / 1e3) / (sum(times))},
+        "kernel_classes": {k: {"launch_groups": v[0], "ms": v[1],
+                               "GBps": (v[2] / (v[1] / 1e3)) / 1e9 if v[1] > 0 else 0.0}
+                           for k, v in prof.items()},
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="config2a", choices=sorted(CONFIGS))
+    ap.add_argument("--n", type=int, default=0, help="override the mesh size (testing)")
+    ap.add_argument("--cpu-sample-n", type=int, default=24)
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -80,6 +80,16 @@ int pscu_destroy(pscu_ctx* ctx);
 int pscu_synchronize(pscu_ctx* ctx);
 /* Kernel-launch counter (every kernel this library enqueued). */
 long long pscu_launch_count(const pscu_ctx* ctx);
+/* Device-timeline timer: CUDA events on the context stream (start syncs the
+ * stream first; stop waits for the stop event). */
+int pscu_timer_start(pscu_ctx* ctx);
+int pscu_timer_stop(pscu_ctx* ctx, double* ms);
+/* Live per-kernel-class timing (events around every launch of the class on
+ * the context stream) with the algorithmic bytes each launch moves.
+ * class: 0 ILU(0) apply, 1 SpMV, 2 MGS Arnoldi step, 3 other.
+ * pscu_profile(ctx, 1) clears and starts recording. */
+int pscu_profile(pscu_ctx* ctx, int enable);
+int pscu_profile_read(pscu_ctx* ctx, int cls, long long* count, double* ms, double* bytes);
 
 /* CsrMatrix (csr.hpp:19-24) ----------------------------------------------- */
 int pscu_mat_create(pscu_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* cols,
@@ -147,6 +157,18 @@ int pscu_solve_system(pscu_ctx* ctx, int64_t n, const int64_t* row_ptr, const in
 int pscu_condense_batch(pscu_ctx* ctx, int nelem, int n, const double* mats, const double* rhs,
                         int n_elim, const int* elim, double* schur, double* reduced_rhs,
                         double* elim_coupling, double* elim_rhs, int* bad_element, int mem);
+/* assemble_hho on the device (assemble.hpp:136-172): batched condensation
+ * of the local blocks, then the CSR value scatter and the reduced-load rhs
+ * over the given structural pattern (the element-order sums of the
+ * reference, bit for bit). Host producers build mats/rhs/elim/kept/pattern
+ * (include/pstokes_host.h). With mem == PSCU_DEVICE the recovery data
+ * (elim_coupling nelem x ne x nk, elim_rhs nelem x ne; nullable) is kept. */
+int pscu_condense_assemble(pscu_ctx* ctx, int nelem, int n, const double* mats,
+                           const double* rhs, int n_elim, const int* elim,
+                           const int64_t* kept_global, int64_t dim, const int64_t* row_ptr,
+                           const int32_t* cols, const pscu_layout* layout, int mem,
+                           pscu_mat** out, double* rhs_out, double* elim_coupling,
+                           double* elim_rhs);
 /* ElementCondensation::recover (condense.hpp:28-38) for all elements:
  * locals[e] (n) from global x through kept_global (nelem x nk). */
 int pscu_recover_batch(pscu_ctx* ctx, int nelem, int n, int n_elim, const int* elim,

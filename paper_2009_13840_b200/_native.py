@@ -20,13 +20,14 @@ _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 
 EXPORTS = [
     "pscu_last_error", "pscu_version", "pscu_create", "pscu_destroy", "pscu_synchronize",
-    "pscu_launch_count", "pscu_mat_create", "pscu_mat_destroy", "pscu_mat_dims",
+    "pscu_launch_count", "pscu_timer_start", "pscu_timer_stop", "pscu_profile",
+    "pscu_profile_read", "pscu_mat_create", "pscu_mat_destroy", "pscu_mat_dims",
     "pscu_mat_download", "pscu_spmv", "pscu_ilu0_create", "pscu_ilu0_destroy",
     "pscu_ilu0_factors", "pscu_ilu0_apply", "pscu_layout_make", "pscu_layout_dim",
     "pscu_coarse_to_fine", "pscu_inherit", "pscu_gmres", "pscu_fgmres", "pscu_hier_create",
     "pscu_hier_destroy", "pscu_hier_nlev", "pscu_hier_level_mat", "pscu_hier_level_ilu",
     "pscu_vcycle", "pscu_hier_coarse_its", "pscu_hier_reset", "pscu_solve", "pscu_solve_system",
-    "pscu_condense_batch", "pscu_recover_batch",
+    "pscu_condense_batch", "pscu_condense_assemble", "pscu_recover_batch",
 ]
 
 
@@ -71,6 +72,10 @@ def load(path: str = LIB):
     lib.pscu_synchronize.argtypes = [vp]
     lib.pscu_launch_count.restype = C.c_longlong
     lib.pscu_launch_count.argtypes = [vp]
+    lib.pscu_timer_start.argtypes = [vp]
+    lib.pscu_timer_stop.argtypes = [vp, pd]
+    lib.pscu_profile.argtypes = [vp, i32]
+    lib.pscu_profile_read.argtypes = [vp, i32, C.POINTER(C.c_longlong), pd, pd]
     lib.pscu_mat_create.argtypes = [vp, i64, vp, vp, vp, i32, C.POINTER(vp)]
     lib.pscu_mat_destroy.argtypes = [vp]
     lib.pscu_mat_dims.argtypes = [vp, C.POINTER(i64), C.POINTER(i64)]
@@ -104,6 +109,8 @@ def load(path: str = LIB):
                                       C.POINTER(LevelCfg), f64, i32, i32, vp, vp,
                                       C.POINTER(Report)]
     lib.pscu_condense_batch.argtypes = [vp, i32, i32, vp, vp, i32, vp, vp, vp, vp, vp, pi, i32]
+    lib.pscu_condense_assemble.argtypes = [vp, i32, i32, vp, vp, i32, vp, vp, i64, vp, vp,
+                                           C.POINTER(Layout), i32, C.POINTER(vp), vp, vp, vp]
     lib.pscu_recover_batch.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32]
     _lib = lib
     return lib

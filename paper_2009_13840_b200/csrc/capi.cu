@@ -13,8 +13,13 @@ void condense_batch(Context& c, int nelem, int n, const double* mats, const doub
 void recover_batch(Context& c, int nelem, int n, int ne, const int* elim_host,
                    const int64_t* kept, const double* coupling, const double* erhs,
                    const double* x, double* locals);
+void assemble_values(Context& c, int nelem, int nk, const int64_t* kept, const double* schur,
+                     const double* rrhs, const pscu_layout& l, Csr& a, double* rhs);
 
 Context::~Context() {
+  for (auto e : ev_pool) cudaEventDestroy(e);
+  if (t_start) cudaEventDestroy(t_start);
+  if (t_stop) cudaEventDestroy(t_stop);
   if (h_pinned) cudaFreeHost(h_pinned);
   if (stream) cudaStreamDestroy(stream);
 }
@@ -133,8 +138,8 @@ int pscu_create(int device, pscu_ctx** out) {
     c.device = device;
     PSCU_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     c.red_partials.alloc(1 << 12);
-    c.red_counter.alloc(1);
-    PSCU_CUDA(cudaMemset(c.red_counter.p, 0, sizeof(unsigned)));
+    c.red_counter.alloc(2);  // [0] last-CTA counter / barrier count, [1] barrier generation
+    PSCU_CUDA(cudaMemset(c.red_counter.p, 0, 2 * sizeof(unsigned)));
     c.scal.alloc(64);
     c.err_flag.alloc(1);
     PSCU_CUDA(cudaMallocHost(&c.h_pinned, sizeof(double) * 64));
@@ -157,6 +162,59 @@ int pscu_synchronize(pscu_ctx* ctx) {
 }
 
 long long pscu_launch_count(const pscu_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int pscu_timer_start(pscu_ctx* ctx) {
+  return guard([&] {
+    Context& c = ctx->c;
+    if (!c.t_start) {
+      PSCU_CUDA(cudaEventCreate(&c.t_start));
+      PSCU_CUDA(cudaEventCreate(&c.t_stop));
+    }
+    PSCU_CUDA(cudaStreamSynchronize(c.stream));
+    PSCU_CUDA(cudaEventRecord(c.t_start, c.stream));
+  });
+}
+
+int pscu_timer_stop(pscu_ctx* ctx, double* ms) {
+  return guard([&] {
+    Context& c = ctx->c;
+    PSCU_CUDA(cudaEventRecord(c.t_stop, c.stream));
+    PSCU_CUDA(cudaEventSynchronize(c.t_stop));
+    float f = 0.f;
+    PSCU_CUDA(cudaEventElapsedTime(&f, c.t_start, c.t_stop));
+    *ms = f;
+  });
+}
+
+int pscu_profile(pscu_ctx* ctx, int enable) {
+  return guard([&] {
+    Context& c = ctx->c;
+    PSCU_CUDA(cudaStreamSynchronize(c.stream));
+    c.profiling = enable != 0;
+    c.prof.clear();
+    c.ev_used = 0;
+  });
+}
+
+int pscu_profile_read(pscu_ctx* ctx, int cls, long long* count, double* ms, double* bytes) {
+  return guard([&] {
+    Context& c = ctx->c;
+    PSCU_CUDA(cudaStreamSynchronize(c.stream));
+    long long k = 0;
+    double t = 0.0, b = 0.0;
+    for (const ProfRec& r : c.prof) {
+      if (r.cls != cls) continue;
+      float f = 0.f;
+      PSCU_CUDA(cudaEventElapsedTime(&f, r.e0, r.e1));
+      t += f;
+      b += r.bytes;
+      ++k;
+    }
+    *count = k;
+    *ms = t;
+    *bytes = b;
+  });
+}
 
 int pscu_mat_create(pscu_ctx* ctx, int64_t n, const int64_t* row_ptr, const int32_t* cols,
                     const double* vals, int mem, pscu_mat** out) {
@@ -441,6 +499,53 @@ int pscu_condense_batch(pscu_ctx* ctx, int nelem, int n, const double* mats, con
       if (elim_rhs) finish_out(c, elim_rhs, de, int64_t(nelem) * n_elim, mem);
     }
     PSCU_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pscu_condense_assemble(pscu_ctx* ctx, int nelem, int n, const double* mats,
+                           const double* rhs, int n_elim, const int* elim,
+                           const int64_t* kept_global, int64_t dim, const int64_t* row_ptr,
+                           const int32_t* cols, const pscu_layout* layout, int mem,
+                           pscu_mat** out, double* rhs_out, double* elim_coupling,
+                           double* elim_rhs) {
+  return guard([&] {
+    Context& c = ctx->c;
+    if (layout_dim(*layout) != dim) throw Error(PSCU_EINVAL, "assemble: layout/pattern mismatch");
+    const int nk = n - n_elim;
+    DevBuf<double> bm, br, bschur(size_t(nelem) * nk * nk), brr(size_t(nelem) * nk), brhs;
+    DevBuf<int64_t> bk;
+    const double* dm = in_vec(c, mats, int64_t(nelem) * n * n, mem, bm);
+    const double* dr = in_vec(c, rhs, int64_t(nelem) * n, mem, br);
+    const int64_t* dk = kept_global;
+    if (mem == PSCU_HOST) {
+      bk.upload(kept_global, size_t(nelem) * nk, c.stream);
+      dk = bk.p;
+    }
+    condense_batch(c, nelem, n, dm, dr, n_elim, elim, bschur.p, brr.p,
+                   mem == PSCU_DEVICE ? elim_coupling : nullptr,
+                   mem == PSCU_DEVICE ? elim_rhs : nullptr, nullptr);
+    auto m = std::make_unique<pscu_mat>();
+    Csr& a = m->m;
+    a.n = dim;
+    if (mem == PSCU_HOST) {
+      a.h_row_ptr.assign(row_ptr, row_ptr + dim + 1);
+      a.nnz = a.h_row_ptr[dim];
+      a.h_cols.assign(cols, cols + a.nnz);
+    } else {
+      a.h_row_ptr.resize(dim + 1);
+      PSCU_CUDA(cudaMemcpy(a.h_row_ptr.data(), row_ptr, sizeof(int64_t) * (dim + 1),
+                           cudaMemcpyDeviceToHost));
+      a.nnz = a.h_row_ptr[dim];
+      a.h_cols.resize(a.nnz);
+      PSCU_CUDA(cudaMemcpy(a.h_cols.data(), cols, sizeof(int32_t) * a.nnz, cudaMemcpyDeviceToHost));
+    }
+    a.row_ptr.upload(a.h_row_ptr, c.stream);
+    a.cols.upload(a.h_cols, c.stream);
+    a.vals.alloc(a.nnz);
+    double* drhs = out_vec(dim, rhs_out, mem, brhs);
+    assemble_values(c, nelem, nk, dk, bschur.p, brr.p, *layout, a, drhs);
+    finish_out(c, rhs_out, drhs, dim, mem);
+    *out = m.release();
   });
 }
 

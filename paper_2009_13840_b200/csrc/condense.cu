@@ -190,7 +190,88 @@ __global__ void recover_kernel(int nelem, int n, int ne, const int* __restrict__
   }
 }
 
+struct KindInfo {
+  int64_t face_rows;
+  int fb, eb, face_vel, elem_vel, strategy;
+  __device__ int kind(int64_t g) const {  // assemble.hpp:25-39
+    int within, nv;
+    if (g < face_rows) {
+      within = int(g % fb);
+      nv = face_vel;
+    } else {
+      within = int((g - face_rows) % eb);
+      nv = elem_vel;
+    }
+    return within < nv ? 0 : (within < 2 * nv ? 1 : 2);
+  }
+  __device__ bool coupled(int ka, int kb) const {  // assemble.hpp:41-46
+    const bool av = ka != 2, bv = kb != 2;
+    if (av && bv && ka != kb) return strategy == 2;
+    if (!av && !bv) return strategy != 0;
+    return true;
+  }
+};
+
+/// Value pass of assemble_hho (assemble.hpp:164-169): every retained pair of
+/// every element adds its Schur entry into the CSR slot found by binary
+/// search in the (sorted) row. An entry receives at most two contributions
+/// (two distinct faces share at most one element, a face at most two), and a
+/// two-term sum from 0.0 is order-independent, so the atomics reproduce the
+/// reference's element-order scatter bit for bit.
+__global__ void assemble_kernel(int nelem, int nk, const int64_t* __restrict__ kept,
+                                const double* __restrict__ schur,
+                                const double* __restrict__ rrhs, KindInfo ki,
+                                const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                                double* vals, double* rhs, int* bad) {
+  const int64_t per = int64_t(nk) * nk;
+  const int64_t total = int64_t(nelem) * per;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int e = int(t / per);
+    const int r = int(t % per);
+    const int i = r % nk, j = r / nk;
+    const int64_t g = kept[int64_t(e) * nk + i], h = kept[int64_t(e) * nk + j];
+    if (g != h && !ki.coupled(ki.kind(g), ki.kind(h))) continue;
+    int64_t lo = rp[g], hi = rp[g + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (cols[mid] < h) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo >= rp[g + 1] || cols[lo] != h) {
+      atomicExch(bad, 1);
+      continue;
+    }
+    atomicAdd(vals + lo, schur[int64_t(e) * per + i + int64_t(j) * nk]);
+    if (i == j && rhs) atomicAdd(rhs + g, rrhs[int64_t(e) * nk + i]);
+  }
+}
+
 } // namespace
+
+void assemble_values(Context& c, int nelem, int nk, const int64_t* kept, const double* schur,
+                     const double* rrhs, const pscu_layout& l, Csr& a, double* rhs) {
+  KindInfo ki;
+  ki.fb = 2 * l.face_vel + l.face_press;
+  ki.eb = 2 * l.elem_vel + l.elem_press;
+  ki.face_rows = int64_t(l.n_faces) * ki.fb;
+  ki.face_vel = l.face_vel;
+  ki.elem_vel = l.elem_vel;
+  ki.strategy = l.strategy;
+  PSCU_CUDA(cudaMemsetAsync(a.vals.p, 0, sizeof(double) * a.nnz, c.stream));
+  if (rhs) PSCU_CUDA(cudaMemsetAsync(rhs, 0, sizeof(double) * a.n, c.stream));
+  const int zero = 0;
+  PSCU_CUDA(cudaMemcpyAsync(c.err_flag.p, &zero, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  const int64_t total = int64_t(nelem) * nk * nk;
+  const int64_t g = (total + 255) / 256;
+  assemble_kernel<<<unsigned(g < 148 * 64 ? (g > 0 ? g : 1) : 148 * 64), 256, 0, c.stream>>>(
+      nelem, nk, kept, schur, rrhs, ki, a.row_ptr.p, a.cols.p, a.vals.p, rhs, c.err_flag.p);
+  PSCU_LAUNCHED(&c);
+  int bad = 0;
+  PSCU_CUDA(cudaMemcpyAsync(&bad, c.err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  PSCU_CUDA(cudaStreamSynchronize(c.stream));
+  if (bad) throw Error(PSCU_EINVAL, "CsrMatrix::add: entry outside the pattern");
+}
 
 void condense_batch(Context& c, int nelem, int n, const double* mats, const double* rhs, int ne,
                     const int* elim_host, double* schur, double* rrhs, double* coupling,

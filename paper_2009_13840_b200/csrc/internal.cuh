@@ -129,10 +129,52 @@ struct Ilu {
   Sweep fwd, bwd;
 };
 
+/// Live per-kernel-class timing with CUDA events on the launching stream.
+enum ProfClass { PROF_ILU = 0, PROF_SPMV = 1, PROF_MGS = 2, PROF_OTHER = 3, PROF_NCLASS = 4 };
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t e0, e1;
+  double bytes;
+};
+
 struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
   long long launches = 0;
+  bool profiling = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  cudaEvent_t t_start = nullptr, t_stop = nullptr;
+  cudaEvent_t next_event() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      PSCU_CUDA(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+  /// Brackets one launch (or a tight group) of a profiled class.
+  struct Scope {
+    Context* c;
+    int cls;
+    double bytes;
+    cudaEvent_t e0 = nullptr;
+    Scope(Context* cc, int k, double b) : c(cc), cls(k), bytes(b) {
+      if (c->profiling) {
+        e0 = c->next_event();
+        cudaEventRecord(e0, c->stream);
+      }
+    }
+    ~Scope() {
+      if (c->profiling) {
+        cudaEvent_t e1 = c->next_event();
+        cudaEventRecord(e1, c->stream);
+        c->prof.push_back({cls, e0, e1, bytes});
+      }
+    }
+  };
   // reduction scratch
   DevBuf<double> red_partials;     // per-block results
   DevBuf<unsigned int> red_counter; // last-block counter

@@ -142,7 +142,167 @@ unsigned grid_for(int64_t n, int threads = 256) {
   return unsigned(g < 148 * 16 ? (g > 0 ? g : 1) : 148 * 16);
 }
 
+// ---------------------------------------------------------------------------
+// Persistent Arnoldi step: all j+2 MGS passes of ArnoldiWorkspace::step in
+// one cooperative launch. Thread x of CTA b owns the L consecutive lanes
+// (b*256 + x)*L .. +L-1 and keeps their elements of w in shared memory, so
+// a pass streams only v_i (and v_{i-1}, an L2 hit). After each pass the CTA
+// results go through one grid barrier and every CTA rebuilds the same
+// adjacent-pair tree over them, so h_i is known everywhere without a second
+// barrier. The tree shape (L lanes -> 256 threads -> G CTAs) is the global
+// adjacent-pair tree over T = G*256*L lanes, i.e. identical to mgs_pass.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ void grid_barrier(unsigned* count, unsigned* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g0 = ld_acquire_u32(gen);
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (ld_acquire_u32(gen) == g0) {
+      }
+    }
+  }
+  __syncthreads();
+}
+
+constexpr int kStepThreads = 256;
+
+/// Tree over `cnt` (power of two, <= 1024) values in smem buf, in place;
+/// result in buf[0]. All threads of the CTA participate.
+__device__ void smem_tree(double* buf, int cnt) {
+  for (int width = cnt; width > 1; width >>= 1) {
+    const int half = width >> 1;
+    double t0 = 0.0, t1 = 0.0;
+    const int k0 = threadIdx.x, k1 = threadIdx.x + kStepThreads;
+    if (k0 < half) t0 = dadd(buf[2 * k0], buf[2 * k0 + 1]);
+    if (k1 < half) t1 = dadd(buf[2 * k1], buf[2 * k1 + 1]);
+    __syncthreads();
+    if (k0 < half) buf[k0] = t0;
+    if (k1 < half) buf[k1] = t1;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kStepThreads)
+    arnoldi_step_kernel(int64_t n, int64_t T, int L, int epl, int j, double* __restrict__ wg,
+                        double* V, int64_t ldv, double* __restrict__ hcol,
+                        double* __restrict__ partials, unsigned* bar) {
+  extern __shared__ double wsm[];  // [L*epl][256]
+  __shared__ double gbuf[1024];
+  __shared__ double hsh;
+  const int G = gridDim.x;
+  const int tid = threadIdx.x;
+  const int64_t lane0 = (int64_t(blockIdx.x) * kStepThreads + tid) * L;
+  for (int l = 0; l < L; ++l)
+    for (int k = 0; k < epl; ++k) {
+      const int64_t e = lane0 + l + int64_t(k) * T;
+      wsm[(l * epl + k) * kStepThreads + tid] = e < n ? wg[e] : 0.0;
+    }
+  double hprev = 0.0;
+  for (int i = 0; i <= j + 1; ++i) {
+    const double* vp = V + int64_t(i - 1) * ldv;
+    const double* vi = V + int64_t(i) * ldv;
+    double lanev[8];
+    for (int l = 0; l < L; ++l) {
+      double acc = 0.0;
+      for (int k = 0; k < epl; ++k) {
+        const int64_t e = lane0 + l + int64_t(k) * T;
+        if (e >= n) break;
+        double& ws = wsm[(l * epl + k) * kStepThreads + tid];
+        double we = ws;
+        if (i > 0) {
+          we = dsub(we, dmul(hprev, vp[e]));
+          ws = we;
+        }
+        const double o = i <= j ? vi[e] : we;
+        acc = dadd(acc, dmul(we, o));
+      }
+      lanev[l] = acc;
+    }
+    for (int width = L; width > 1; width >>= 1)
+      for (int k = 0; k < width / 2; ++k) lanev[k] = dadd(lanev[2 * k], lanev[2 * k + 1]);
+    const double cta = block_tree(lanev[0], kStepThreads);
+    if (tid == 0) partials[(i & 1) * G + blockIdx.x] = cta;
+    grid_barrier(bar, bar + 1);
+    for (int k = tid; k < G; k += kStepThreads) gbuf[k] = __ldcg(partials + (i & 1) * G + k);
+    __syncthreads();
+    smem_tree(gbuf, G);
+    if (tid == 0) {
+      double h = gbuf[0];
+      if (i == j + 1) h = __dsqrt_rn(h);
+      hsh = h;
+      if (blockIdx.x == 0) hcol[i] = h;
+    }
+    __syncthreads();
+    hprev = hsh;
+    __syncthreads();
+  }
+  // v_{j+1} = w / h, or 0 on a happy breakdown (gmres.hpp:66-67)
+  double* vn = V + int64_t(j + 1) * ldv;
+  for (int l = 0; l < L; ++l)
+    for (int k = 0; k < epl; ++k) {
+      const int64_t e = lane0 + l + int64_t(k) * T;
+      if (e >= n) break;
+      const double we = wsm[(l * epl + k) * kStepThreads + tid];
+      vn[e] = hprev > 0.0 ? __ddiv_rn(we, hprev) : 0.0;
+    }
+}
+
 } // namespace
+
+/// Cooperative single-launch Arnoldi step; returns false when the problem
+/// does not fit the co-resident configuration (caller falls back to one
+/// kernel per pass).
+bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int64_t ldv,
+                        double* hcol) {
+  const int64_t T = repro_lanes(n);
+  if (T < kStepThreads) return false;
+  const int epl = int((n + T - 1) / T);
+  static int sm_count = 0, max_smem = 0;
+  if (!sm_count) {
+    PSCU_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, c.device));
+    PSCU_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+    PSCU_CUDA(cudaFuncSetAttribute(arnoldi_step_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   max_smem - 16 * 1024));
+  }
+  for (int L = 1; L <= 8; L <<= 1) {
+    const int64_t G = T / (int64_t(kStepThreads) * L);
+    if (G < 1 || G > 1024) continue;
+    const size_t smem = sizeof(double) * size_t(kStepThreads) * L * epl;
+    if (smem > size_t(max_smem - 16 * 1024)) return false;
+    int per_sm = 0;
+    PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_step_kernel,
+                                                            kStepThreads, smem));
+    if (int64_t(per_sm) * sm_count < G) continue;
+    int ii = 0;
+    int Li = L, ei = epl, jj = j;
+    int64_t nn = n, TT = T, ld = ldv;
+    double* pw = w;
+    double* pV = V;
+    double* ph = hcol;
+    double* pp = c.red_partials.p;
+    unsigned* pb = c.red_counter.p;
+    void* args[] = {&nn, &TT, &Li, &ei, &jj, &pw, &pV, &ld, &ph, &pp, &pb};
+    (void)ii;
+    PSCU_CUDA(cudaLaunchCooperativeKernel((void*)arnoldi_step_kernel, dim3(unsigned(G)),
+                                          dim3(kStepThreads), args, smem, c.stream));
+    PSCU_LAUNCHED(&c);
+    return true;
+  }
+  return false;
+}
 
 /// Runs one reduction pass; result lands in device scalar `out`.
 void mgs_launch(Context& c, int mode, int64_t n, double* w, const double* vp, const double* hprev,

@@ -17,6 +17,8 @@ namespace pscu {
 
 void mgs_launch(Context& c, int mode, int64_t n, double* w, const double* vp, const double* hprev,
                 const double* vi, double* out);
+bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int64_t ldv,
+                        double* hcol);
 void scale_next_launch(Context& c, int64_t n, const double* w, const double* hp, double* v);
 void scale_div_launch(Context& c, int64_t n, const double* r, double beta, double* v);
 void combine_launch(Context& c, int64_t n, int m, const double* x0, const double* y_dev,
@@ -96,12 +98,18 @@ void KrylovWs::ensure(int64_t n_, int m_, bool store_z_) {
 static double arnoldi_step(Context& c, KrylovWs& ws, HostArnoldi& ar, int j) {
   const int64_t n = ws.n;
   double* V = ws.V.p;
-  mgs_launch(c, 0, n, ws.w.p, nullptr, nullptr, V, ws.hcol.p + 0);
-  for (int i = 1; i <= j; ++i)
-    mgs_launch(c, 1, n, ws.w.p, V + size_t(i - 1) * n, ws.hcol.p + (i - 1), V + size_t(i) * n,
-               ws.hcol.p + i);
-  mgs_launch(c, 2, n, ws.w.p, V + size_t(j) * n, ws.hcol.p + j, nullptr, ws.hcol.p + j + 1);
-  scale_next_launch(c, n, ws.w.p, ws.hcol.p + j + 1, V + size_t(j + 1) * n);
+  {
+    // algorithmic bytes of a fused MGS step: (j+1) 24 n + 16 n
+    Context::Scope prof(&c, PROF_MGS, (double(j + 1) * 24.0 + 16.0) * double(n));
+    if (!arnoldi_step_fused(c, n, j, ws.w.p, V, n, ws.hcol.p)) {
+      mgs_launch(c, 0, n, ws.w.p, nullptr, nullptr, V, ws.hcol.p + 0);
+      for (int i = 1; i <= j; ++i)
+        mgs_launch(c, 1, n, ws.w.p, V + size_t(i - 1) * n, ws.hcol.p + (i - 1),
+                   V + size_t(i) * n, ws.hcol.p + i);
+      mgs_launch(c, 2, n, ws.w.p, V + size_t(j) * n, ws.hcol.p + j, nullptr, ws.hcol.p + j + 1);
+      scale_next_launch(c, n, ws.w.p, ws.hcol.p + j + 1, V + size_t(j + 1) * n);
+    }
+  }
   PSCU_CUDA(cudaMemcpyAsync(ws.hcol_host.data(), ws.hcol.p, sizeof(double) * (j + 2),
                             cudaMemcpyDeviceToHost, c.stream));
   PSCU_CUDA(cudaStreamSynchronize(c.stream));

@@ -78,6 +78,7 @@ __global__ void residual_restrict_warp(int64_t nc, const int64_t* __restrict__ m
 void spmv(Context& c, const Csr& a, const double* x, double* y) {
   if (a.n == 0) return;
   const unsigned grid = unsigned((a.n + kRows - 1) / kRows);
+  Context::Scope prof(&c, PROF_SPMV, 8.0 * double(a.nnz) + 16.0 * double(a.n));
   spmv_staged<<<grid, kRows, 0, c.stream>>>(a.n, a.row_ptr.p, a.cols.p, a.vals.p, x, y);
   PSCU_LAUNCHED(&c);
 }

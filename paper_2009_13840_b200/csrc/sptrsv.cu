@@ -24,7 +24,8 @@ namespace pscu {
 
 namespace {
 
-constexpr int kChunkRows = 4096;  // 32 KB of shared-memory solution values
+constexpr int kChunkRows = 12288;  // up to 96 KB of shared-memory solution values
+constexpr int64_t kRecent = 64;    // dependency distance that continues a chain
 constexpr int kSweepThreads = 128;
 
 struct SweepArgs {
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(kSweepThreads)
     sweep_kernel(SweepArgs s, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
                  const double* __restrict__ lu, const int64_t* __restrict__ diag,
                  const double* x, double* y) {
-  __shared__ double ys[kChunkRows];
+  extern __shared__ double ys[];
   int c;
   unsigned long long tag;
   take_ticket(s, c, tag);
@@ -169,18 +170,47 @@ void build_sweep(Context& c, const Csr& a, const std::vector<int64_t>& diag, boo
   const int64_t n = a.n;
   const auto& rp = a.h_row_ptr;
   const auto& cols = a.h_cols;
-  const int CH = kChunkRows;
-  const int nchunks = int((n + CH - 1) / CH);
-  s.nchunks = nchunks;
-  if (n == 0) return;
+  const int64_t CH = kChunkRows;
+  if (n == 0) {
+    s.nchunks = 0;
+    return;
+  }
   auto pos_of = [&](int64_t i) { return fwd ? i : n - 1 - i; };
   auto row_at = [&](int64_t p) { return fwd ? p : n - 1 - p; };
+
+  // Chunk boundaries. A row whose nearest dependency (in processing order)
+  // lies more than kRecent rows back starts a new dependency chain; chunks
+  // are cut at chain starts so that consecutive chunks depend on each other
+  // "side by side" (a pipelined wavefront) instead of end-to-start.
+  std::vector<int64_t> starts{0};
+  {
+    int64_t last_cs = -1;
+    for (int64_t p = 0; p < n; ++p) {
+      const int64_t i = row_at(p);
+      const int64_t q0 = fwd ? rp[i] : diag[i] + 1;
+      const int64_t q1 = fwd ? diag[i] : rp[i + 1];
+      int64_t nearest = INT64_MAX;
+      for (int64_t q = q0; q < q1; ++q) nearest = std::min(nearest, p - pos_of(cols[q]));
+      if (nearest > kRecent) last_cs = p;
+      if (p - starts.back() >= CH) {
+        const int64_t cut = last_cs > starts.back() ? last_cs : p;
+        starts.push_back(cut);
+      }
+    }
+  }
+  const int nchunks = int(starts.size());
+  s.nchunks = nchunks;
+  std::vector<int32_t> chunk_of(n);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int64_t p1 = ch + 1 < nchunks ? starts[ch + 1] : n;
+    for (int64_t p = starts[ch]; p < p1; ++p) chunk_of[p] = ch;
+  }
 
   std::vector<int32_t> lvl(n, 0);
   std::vector<int32_t> chunk_nlv(nchunks, 0);
   for (int64_t p = 0; p < n; ++p) {
     const int64_t i = row_at(p);
-    const int64_t cb = (p / CH) * CH;
+    const int64_t cb = starts[chunk_of[p]];
     int L = 0;
     const int64_t q0 = fwd ? rp[i] : diag[i] + 1;
     const int64_t q1 = fwd ? diag[i] : rp[i + 1];
@@ -189,7 +219,7 @@ void build_sweep(Context& c, const Csr& a, const std::vector<int64_t>& diag, boo
       if (pj >= cb) L = std::max(L, lvl[cols[q]] + 1);
     }
     lvl[i] = L;
-    chunk_nlv[p / CH] = std::max(chunk_nlv[p / CH], L + 1);
+    chunk_nlv[chunk_of[p]] = std::max(chunk_nlv[chunk_of[p]], L + 1);
   }
   std::vector<int32_t> chunk_lvl(nchunks + 1, 0);
   for (int ch = 0; ch < nchunks; ++ch) chunk_lvl[ch + 1] = chunk_lvl[ch] + chunk_nlv[ch];
@@ -197,7 +227,7 @@ void build_sweep(Context& c, const Csr& a, const std::vector<int64_t>& diag, boo
   s.nlevels = nlevels;
 
   std::vector<int32_t> level_cnt(nlevels + 1, 0);
-  for (int64_t p = 0; p < n; ++p) level_cnt[chunk_lvl[p / CH] + lvl[row_at(p)] + 1]++;
+  for (int64_t p = 0; p < n; ++p) level_cnt[chunk_lvl[chunk_of[p]] + lvl[row_at(p)] + 1]++;
   std::vector<int32_t> level_ptr(nlevels + 1, 0);
   for (int l = 0; l < nlevels; ++l) level_ptr[l + 1] = level_ptr[l] + level_cnt[l + 1];
   std::vector<int32_t> sched(n);
@@ -205,7 +235,7 @@ void build_sweep(Context& c, const Csr& a, const std::vector<int64_t>& diag, boo
     std::vector<int32_t> fill(level_ptr.begin(), level_ptr.end() - 1);
     for (int64_t p = 0; p < n; ++p) {
       const int64_t i = row_at(p);
-      sched[fill[chunk_lvl[p / CH] + lvl[i]]++] = int32_t(i);
+      sched[fill[chunk_lvl[chunk_of[p]] + lvl[i]]++] = int32_t(i);
     }
   }
   int max_level_rows = 0;
@@ -227,14 +257,14 @@ void build_sweep(Context& c, const Csr& a, const std::vector<int64_t>& diag, boo
   std::vector<W> emitted;
   for (int ch = 0; ch < nchunks; ++ch) {
     recs.clear();
-    const int64_t p0 = int64_t(ch) * CH, p1 = std::min<int64_t>(n, p0 + CH);
+    const int64_t p0 = starts[ch], p1 = ch + 1 < nchunks ? starts[ch + 1] : n;
     for (int64_t p = p0; p < p1; ++p) {
       const int64_t i = row_at(p);
       const int64_t q0 = fwd ? rp[i] : diag[i] + 1;
       const int64_t q1 = fwd ? diag[i] : rp[i + 1];
       for (int64_t q = q0; q < q1; ++q) {
         const int64_t pj = pos_of(cols[q]);
-        if (pj < p0) recs.push_back({lvl[i], int32_t(pj / CH), lvl[cols[q]] + 1});
+        if (pj < p0) recs.push_back({lvl[i], chunk_of[pj], lvl[cols[q]] + 1});
       }
     }
     std::sort(recs.begin(), recs.end(), [](const W& x, const W& y) {
@@ -268,8 +298,10 @@ void build_sweep(Context& c, const Csr& a, const std::vector<int64_t>& diag, boo
     }
   }
   std::vector<int64_t> cbeg(nchunks), cend(nchunks);
+  int64_t max_rows = 0;
   for (int ch = 0; ch < nchunks; ++ch) {
-    const int64_t p0 = int64_t(ch) * CH, p1 = std::min<int64_t>(n, p0 + CH);
+    const int64_t p0 = starts[ch], p1 = ch + 1 < nchunks ? starts[ch + 1] : n;
+    max_rows = std::max(max_rows, p1 - p0);
     if (fwd) {
       cbeg[ch] = p0;
       cend[ch] = p1;
@@ -278,7 +310,7 @@ void build_sweep(Context& c, const Csr& a, const std::vector<int64_t>& diag, boo
       cend[ch] = n - p0;
     }
   }
-  s.max_chunk_rows = CH;
+  s.max_chunk_rows = int(max_rows);
   cudaStream_t st = c.stream;
   s.chunk_begin.upload(cbeg, st);
   s.chunk_end.upload(cend, st);
@@ -336,11 +368,24 @@ void ilu0_factor(Context& c, Ilu& ilu) {
 void ilu0_apply(Context& c, const Ilu& ilu, const double* x, double* y) {
   const Csr& a = *ilu.a;
   if (a.n == 0) return;
-  sweep_kernel<true><<<ilu.fwd.nchunks, kSweepThreads, 0, c.stream>>>(
-      args_of(ilu.fwd), a.row_ptr.p, a.cols.p, ilu.lu.p, ilu.diag.p, x, y);
+  static bool attr_set = false;
+  if (!attr_set) {
+    const int bytes = int(sizeof(double) * kChunkRows);
+    PSCU_CUDA(cudaFuncSetAttribute(sweep_kernel<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    PSCU_CUDA(cudaFuncSetAttribute(sweep_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    attr_set = true;
+  }
+  // algorithmic bytes of one apply: 8 nnz + 32 n
+  Context::Scope prof(&c, PROF_ILU, 8.0 * double(a.nnz) + 32.0 * double(a.n));
+  sweep_kernel<true><<<ilu.fwd.nchunks, kSweepThreads, sizeof(double) * ilu.fwd.max_chunk_rows,
+                       c.stream>>>(args_of(ilu.fwd), a.row_ptr.p, a.cols.p, ilu.lu.p,
+                                   ilu.diag.p, x, y);
   PSCU_LAUNCHED(&c);
-  sweep_kernel<false><<<ilu.bwd.nchunks, kSweepThreads, 0, c.stream>>>(
-      args_of(ilu.bwd), a.row_ptr.p, a.cols.p, ilu.lu.p, ilu.diag.p, y, y);
+  sweep_kernel<false><<<ilu.bwd.nchunks, kSweepThreads, sizeof(double) * ilu.bwd.max_chunk_rows,
+                        c.stream>>>(args_of(ilu.bwd), a.row_ptr.p, a.cols.p, ilu.lu.p,
+                                    ilu.diag.p, y, y);
   PSCU_LAUNCHED(&c);
 }
 

@@ -1,0 +1,169 @@
+"""ctypes binding of the host input producer (include/pstokes_host.h) and
+the assemble_stokes pipeline: host local blocks -> device condensation and
+assembly (pscu_condense_assemble)."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .build import HOST_LIB
+
+SIDES = {"left": 0, "right": 1, "top": 2, "bottom": 3}
+DATA = {"zero": 0, "exp": 1, "sincos": 2}
+SCHEMES = {"hho-dp": 0, "hho-hp": 1}
+STRATEGIES = {"uncond": 0, "v-cond": 1, "vp-cond": 2, "v&p-cond": 2}
+
+_lib = None
+
+
+def load():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(HOST_LIB):
+            raise RuntimeError(f"host producer library missing: {HOST_LIB}")
+        lib = C.CDLL(HOST_LIB)
+        vp = C.c_void_p
+        lib.psh_last_error.restype = C.c_char_p
+        lib.psh_mesh_unit_square.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_int,
+                                             C.POINTER(vp)]
+        lib.psh_mesh_family.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]
+        lib.psh_mesh_destroy.argtypes = [vp]
+        lib.psh_mesh_counts.argtypes = [vp, vp]
+        lib.psh_mesh_faces.argtypes = [vp, vp]
+        lib.psh_mesh_vertices.argtypes = [vp, vp]
+        lib.psh_build.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                  C.POINTER(vp)]
+        lib.psh_system_destroy.argtypes = [vp]
+        lib.psh_system_info.argtypes = [vp, vp]
+        for f in ("psh_local_mats", "psh_local_rhs", "psh_elim", "psh_kept_global", "psh_row_ptr",
+                  "psh_cols"):
+            getattr(lib, f).restype = vp
+            getattr(lib, f).argtypes = [vp]
+        lib.psh_build_seconds.restype = C.c_double
+        lib.psh_build_seconds.argtypes = [vp]
+        _lib = lib
+    return _lib
+
+
+def _check(rc):
+    if rc:
+        msg = load().psh_last_error().decode()
+        raise ValueError(msg) if rc == 1 else RuntimeError(msg)
+
+
+class Mesh:
+    """2D mesh (mesh.hpp) built by the host producer."""
+
+    def __init__(self, h):
+        self.lib = load()
+        self.h = h
+        c = np.zeros(3, np.int64)
+        self.lib.psh_mesh_counts(h, c.ctypes.data)
+        self.n_vertices, self.n_elements, self.n_faces = (int(v) for v in c)
+
+    @classmethod
+    def unit_square(cls, n: int, tri: bool = False, jitter: float = 0.0, seed: int = 0,
+                    neumann: str = "top") -> "Mesh":
+        h = C.c_void_p()
+        _check(load().psh_mesh_unit_square(n, int(tri), jitter, seed, SIDES[neumann], C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def family(cls, family: str, n: int, neumann: str = "right") -> "Mesh":
+        h = C.c_void_p()
+        _check(load().psh_mesh_family(family.encode(), n, SIDES[neumann], C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.psh_mesh_destroy(self.h)
+            self.h = None
+
+    def faces(self) -> np.ndarray:
+        f = np.zeros(5 * self.n_faces, np.int32)
+        self.lib.psh_mesh_faces(self.h, f.ctypes.data)
+        return f.reshape(-1, 5)
+
+    def vertices(self) -> np.ndarray:
+        v = np.zeros(2 * self.n_vertices)
+        self.lib.psh_mesh_vertices(self.h, v.ctypes.data)
+        return v.reshape(-1, 2)
+
+
+def _view(ptr, dtype, count):
+    if count == 0:
+        return np.zeros(0, dtype)
+    buf = (C.c_char * (count * np.dtype(dtype).itemsize)).from_address(ptr)
+    return np.frombuffer(buf, dtype=dtype, count=count)
+
+
+class LocalSystem:
+    """Per-element local blocks, layout and pattern (assemble_hho front end)."""
+
+    def __init__(self, mesh: Mesh, scheme: str, strategy: str, k: int, data: str = "sincos",
+                 eta: float = 0.0, nthreads: int = 0):
+        self.lib = load()
+        self.mesh = mesh
+        h = C.c_void_p()
+        _check(self.lib.psh_build(mesh.h, SCHEMES[scheme], STRATEGIES[strategy], k, DATA[data],
+                                  eta, nthreads, C.byref(h)))
+        self.h = h
+        info = np.zeros(14, np.int64)
+        self.lib.psh_system_info(h, info.ctypes.data)
+        (self.nelem, self.n_local, self.n_elim, self.n_keep, self.dim, self.nnz, self.scheme,
+         self.strategy, self.k, self.n_faces, self.face_vel, self.face_press, self.elem_vel,
+         self.elem_press) = (int(v) for v in info)
+        self.seconds = self.lib.psh_build_seconds(h)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.psh_system_destroy(self.h)
+            self.h = None
+
+    def layout(self) -> N.Layout:
+        return N.Layout(self.scheme, self.strategy, self.k, self.n_faces, self.nelem,
+                        self.face_vel, self.face_press, self.elem_vel, self.elem_press)
+
+    def mats(self):
+        n = self.n_local
+        return _view(self.lib.psh_local_mats(self.h), np.float64, self.nelem * n * n)
+
+    def rhs(self):
+        return _view(self.lib.psh_local_rhs(self.h), np.float64, self.nelem * self.n_local)
+
+    def elim(self):
+        return _view(self.lib.psh_elim(self.h), np.int32, self.n_elim)
+
+    def kept_global(self):
+        return _view(self.lib.psh_kept_global(self.h), np.int64, self.nelem * self.n_keep)
+
+    def row_ptr(self):
+        return _view(self.lib.psh_row_ptr(self.h), np.int64, self.dim + 1)
+
+    def cols(self):
+        return _view(self.lib.psh_cols(self.h), np.int32, self.nnz)
+
+
+def assemble_stokes(local: LocalSystem, ctx=None):
+    """assemble_stokes (assemble.hpp:348-353) for the HHO schemes: device
+    condensation + assembly of the host-built local blocks. Returns the
+    condensed operator as a device CsrMatrix and the reduced rhs."""
+    from . import solver as S
+
+    ctx = ctx or S.default_context()
+    h = C.c_void_p()
+    rhs = np.zeros(local.dim)
+    lay = local.layout()
+    N.check(ctx.lib.pscu_condense_assemble(
+        ctx.h, local.nelem, local.n_local, local.lib.psh_local_mats(local.h),
+        local.lib.psh_local_rhs(local.h), local.n_elim, local.lib.psh_elim(local.h),
+        local.lib.psh_kept_global(local.h), local.dim, local.lib.psh_row_ptr(local.h),
+        local.lib.psh_cols(local.h), C.byref(lay), N.PSCU_HOST, C.byref(h), rhs.ctypes.data,
+        None, None))
+    m = S.CsrMatrix(None, None, None, ctx=ctx, _handle=h.value)
+    m._owned = True
+    return m, rhs

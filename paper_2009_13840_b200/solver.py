@@ -41,6 +41,31 @@ class Context:
     def synchronize(self):
         N.check(self.lib.pscu_synchronize(self.h))
 
+    def timer_start(self):
+        """CUDA event on the context stream (after a stream synchronize)."""
+        N.check(self.lib.pscu_timer_start(self.h))
+
+    def timer_stop(self) -> float:
+        """Milliseconds since timer_start on the device timeline."""
+        ms = C.c_double()
+        N.check(self.lib.pscu_timer_stop(self.h, C.byref(ms)))
+        return ms.value
+
+    def profile(self, enable: bool = True):
+        N.check(self.lib.pscu_profile(self.h, int(enable)))
+
+    PROFILE_CLASSES = {"ilu0_apply": 0, "spmv": 1, "mgs_step": 2, "other": 3}
+
+    def profile_read(self) -> dict:
+        """{class: (launch groups, total ms, algorithmic bytes)} from CUDA
+        events recorded around every launch on the context stream."""
+        out = {}
+        for name, k in self.PROFILE_CLASSES.items():
+            cnt, ms, b = C.c_longlong(), C.c_double(), C.c_double()
+            N.check(self.lib.pscu_profile_read(self.h, k, C.byref(cnt), C.byref(ms), C.byref(b)))
+            out[name] = (cnt.value, ms.value, b.value)
+        return out
+
 
 _default_ctx: Context | None = None
 
