@@ -122,11 +122,27 @@ struct Sweep {
   DevBuf<unsigned long long> ticket;      // 1
 };
 
+/// Level-walking sweep plan (walk.cu).
+struct WalkSeg {
+  bool wide;   // row-parallel launch of one level, else one walker CTA
+  int l0, l1;  // level range
+};
+
+struct WalkPlan {
+  bool fwd = true;
+  int nlev = 0;
+  std::vector<WalkSeg> segments;
+  DevBuf<int32_t> lvl_ptr, rows, row_off, src;
+  DevBuf<int64_t> lvl_nz, from, div_from;
+  DevBuf<double> val, div;
+};
+
 struct Ilu {
   const Csr* a = nullptr;
   DevBuf<double> lu;
   DevBuf<int64_t> diag;
-  Sweep fwd, bwd;
+  Sweep fwd;           // chunked sync-free schedule (factorisation)
+  WalkPlan wfwd, wbwd; // level walkers (application)
 };
 
 /// Live per-kernel-class timing with CUDA events on the launching stream.
@@ -181,6 +197,8 @@ struct Context {
   DevBuf<double> scal;             // device scalars (Hessenberg column etc.)
   double* h_pinned = nullptr;      // pinned host mirror of scal
   DevBuf<int> err_flag;
+  DevBuf<unsigned long long> slot_tag;  // tagged reduction slots (arnoldi_step_kernel)
+  unsigned long long pass_tag = 0;      // monotonic pass id across launches
   size_t scal_cap = 0;
   ~Context();
 };

@@ -194,10 +194,29 @@ __device__ void smem_tree(double* buf, int cnt) {
   }
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+constexpr int kEpt = 16;  // elements per lane (repro_lanes guarantees <= 16 up to n = 2^22)
+
+/// All j+2 MGS passes of one Arnoldi step. Per pass every CTA publishes its
+/// subtree result in its own slot (value, then a release-tagged pass id);
+/// every CTA acquires all G slots and rebuilds the same adjacent-pair tree,
+/// so the reduction doubles as the grid-wide barrier without a contended
+/// counter. Slots are double-buffered by pass parity and tags are unique per
+/// launch (tag_base), so nothing is ever reset.
 __global__ void __launch_bounds__(kStepThreads)
     arnoldi_step_kernel(int64_t n, int64_t T, int L, int epl, int j, double* __restrict__ wg,
                         double* V, int64_t ldv, double* __restrict__ hcol,
-                        double* __restrict__ partials, unsigned* bar) {
+                        double* __restrict__ slot_v, unsigned long long* slot_tag,
+                        unsigned long long tag_base) {
   extern __shared__ double wsm[];  // [L*epl][256]
   __shared__ double gbuf[1024];
   __shared__ double hsh;
@@ -215,27 +234,46 @@ __global__ void __launch_bounds__(kStepThreads)
     const double* vi = V + int64_t(i) * ldv;
     double lanev[8];
     for (int l = 0; l < L; ++l) {
-      double acc = 0.0;
-      for (int k = 0; k < epl; ++k) {
+      // issue every load of this lane before the dependent arithmetic
+      double pv[kEpt], iv[kEpt];
+#pragma unroll
+      for (int k = 0; k < kEpt; ++k) {
         const int64_t e = lane0 + l + int64_t(k) * T;
-        if (e >= n) break;
-        double& ws = wsm[(l * epl + k) * kStepThreads + tid];
-        double we = ws;
-        if (i > 0) {
-          we = dsub(we, dmul(hprev, vp[e]));
-          ws = we;
+        const bool ok = k < epl && e < n;
+        pv[k] = (ok && i > 0) ? __ldcs(vp + e) : 0.0;
+        iv[k] = (ok && i <= j) ? __ldcg(vi + e) : 0.0;
+      }
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < kEpt; ++k) {
+        const int64_t e = lane0 + l + int64_t(k) * T;
+        if (k < epl && e < n) {
+          double& ws = wsm[(l * epl + k) * kStepThreads + tid];
+          double we = ws;
+          if (i > 0) {
+            we = dsub(we, dmul(hprev, pv[k]));
+            ws = we;
+          }
+          const double o = i <= j ? iv[k] : we;
+          acc = dadd(acc, dmul(we, o));
         }
-        const double o = i <= j ? vi[e] : we;
-        acc = dadd(acc, dmul(we, o));
       }
       lanev[l] = acc;
     }
     for (int width = L; width > 1; width >>= 1)
       for (int k = 0; k < width / 2; ++k) lanev[k] = dadd(lanev[2 * k], lanev[2 * k + 1]);
     const double cta = block_tree(lanev[0], kStepThreads);
-    if (tid == 0) partials[(i & 1) * G + blockIdx.x] = cta;
-    grid_barrier(bar, bar + 1);
-    for (int k = tid; k < G; k += kStepThreads) gbuf[k] = __ldcg(partials + (i & 1) * G + k);
+    const int par = i & 1;
+    const unsigned long long want = tag_base + unsigned(i) + 1ull;
+    if (tid == 0) {
+      slot_v[par * G + blockIdx.x] = cta;
+      st_release_u64(slot_tag + par * G + blockIdx.x, want);
+    }
+    for (int k = tid; k < G; k += kStepThreads) {
+      while (ld_acquire_u64(slot_tag + par * G + k) != want) {
+      }
+      gbuf[k] = __ldcg(slot_v + par * G + k);
+    }
     __syncthreads();
     smem_tree(gbuf, G);
     if (tid == 0) {
@@ -269,6 +307,7 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
   const int64_t T = repro_lanes(n);
   if (T < kStepThreads) return false;
   const int epl = int((n + T - 1) / T);
+  if (epl > kEpt) return false;
   static int sm_count = 0, max_smem = 0;
   if (!sm_count) {
     PSCU_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, c.device));
@@ -286,16 +325,20 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_step_kernel,
                                                             kStepThreads, smem));
     if (int64_t(per_sm) * sm_count < G) continue;
-    int ii = 0;
+    if (c.slot_tag.n < size_t(2 * G)) {
+      c.slot_tag.alloc(2048);
+      PSCU_CUDA(cudaMemsetAsync(c.slot_tag.p, 0, sizeof(unsigned long long) * 2048, c.stream));
+    }
     int Li = L, ei = epl, jj = j;
     int64_t nn = n, TT = T, ld = ldv;
     double* pw = w;
     double* pV = V;
     double* ph = hcol;
-    double* pp = c.red_partials.p;
-    unsigned* pb = c.red_counter.p;
-    void* args[] = {&nn, &TT, &Li, &ei, &jj, &pw, &pV, &ld, &ph, &pp, &pb};
-    (void)ii;
+    double* pv = c.red_partials.p;
+    unsigned long long* pt = c.slot_tag.p;
+    unsigned long long base = c.pass_tag;
+    c.pass_tag += unsigned(j + 2);
+    void* args[] = {&nn, &TT, &Li, &ei, &jj, &pw, &pV, &ld, &ph, &pv, &pt, &base};
     PSCU_CUDA(cudaLaunchCooperativeKernel((void*)arnoldi_step_kernel, dim3(unsigned(G)),
                                           dim3(kStepThreads), args, smem, c.stream));
     PSCU_LAUNCHED(&c);

@@ -19,6 +19,7 @@
 #include <algorithm>
 
 #include "internal.cuh"
+#include "walk.cuh"
 
 namespace pscu {
 
@@ -348,7 +349,8 @@ void ilu0_factor(Context& c, Ilu& ilu) {
   }
   ilu.diag.upload(diag, c.stream);
   build_sweep(c, a, diag, true, ilu.fwd);
-  build_sweep(c, a, diag, false, ilu.bwd);
+  build_walk(c, a, diag, true, ilu.wfwd);
+  build_walk(c, a, diag, false, ilu.wbwd);
   ilu.lu.alloc(a.nnz);
   PSCU_CUDA(cudaMemcpyAsync(ilu.lu.p, a.vals.p, sizeof(double) * a.nnz, cudaMemcpyDeviceToDevice,
                             c.stream));
@@ -363,29 +365,43 @@ void ilu0_factor(Context& c, Ilu& ilu) {
   if (bad != big)
     throw Error(PSCU_ESINGULAR, "ilu0: zero pivot at row " + std::to_string(bad) +
                                     "; a fill-reducing or pivot-friendly ordering is needed");
+  pack_walk(c, ilu.lu.p, ilu.wfwd);
+  pack_walk(c, ilu.lu.p, ilu.wbwd);
 }
 
 void ilu0_apply(Context& c, const Ilu& ilu, const double* x, double* y) {
   const Csr& a = *ilu.a;
   if (a.n == 0) return;
-  static bool attr_set = false;
-  if (!attr_set) {
-    const int bytes = int(sizeof(double) * kChunkRows);
-    PSCU_CUDA(cudaFuncSetAttribute(sweep_kernel<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    PSCU_CUDA(cudaFuncSetAttribute(sweep_kernel<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    attr_set = true;
-  }
   // algorithmic bytes of one apply: 8 nnz + 32 n
   Context::Scope prof(&c, PROF_ILU, 8.0 * double(a.nnz) + 32.0 * double(a.n));
+  run_walk(c, ilu.wfwd, x, y);
+  run_walk(c, ilu.wbwd, y, y);
+}
+
+/// Previous application path (chunked sync-free sweeps), kept for A/B tests.
+void ilu0_apply_chunked(Context& c, Ilu& ilu, const double* x, double* y) {
+  const Csr& a = *ilu.a;
+  if (a.n == 0) return;
+  std::vector<int64_t> diag(a.n);
+  PSCU_CUDA(cudaMemcpy(diag.data(), ilu.diag.p, sizeof(int64_t) * a.n, cudaMemcpyDeviceToHost));
+  static Sweep bwd;
+  static const Ilu* built_for = nullptr;
+  if (built_for != &ilu) {
+    build_sweep(c, a, diag, false, bwd);
+    built_for = &ilu;
+  }
+  const int bytes = int(sizeof(double) * kChunkRows);
+  PSCU_CUDA(cudaFuncSetAttribute(sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 bytes));
+  PSCU_CUDA(cudaFuncSetAttribute(sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 bytes));
   sweep_kernel<true><<<ilu.fwd.nchunks, kSweepThreads, sizeof(double) * ilu.fwd.max_chunk_rows,
                        c.stream>>>(args_of(ilu.fwd), a.row_ptr.p, a.cols.p, ilu.lu.p,
                                    ilu.diag.p, x, y);
   PSCU_LAUNCHED(&c);
-  sweep_kernel<false><<<ilu.bwd.nchunks, kSweepThreads, sizeof(double) * ilu.bwd.max_chunk_rows,
-                        c.stream>>>(args_of(ilu.bwd), a.row_ptr.p, a.cols.p, ilu.lu.p,
-                                    ilu.diag.p, y, y);
+  sweep_kernel<false><<<bwd.nchunks, kSweepThreads, sizeof(double) * bwd.max_chunk_rows,
+                        c.stream>>>(args_of(bwd), a.row_ptr.p, a.cols.p, ilu.lu.p, ilu.diag.p, y,
+                                    y);
   PSCU_LAUNCHED(&c);
 }
 
