@@ -217,70 +217,80 @@ __global__ void __launch_bounds__(kStepThreads)
                         double* V, int64_t ldv, double* __restrict__ hcol,
                         double* __restrict__ slot_v, unsigned long long* slot_tag,
                         unsigned long long tag_base) {
-  extern __shared__ double wsm[];  // [L*epl][256]
-  __shared__ double gbuf[1024];
+  // one lane per thread (L == 1): w, v_{i-1} and v_i stay in registers and
+  // v_{i+1} is prefetched while the grid-wide reduction of pass i completes
   __shared__ double hsh;
   const int G = gridDim.x;
   const int tid = threadIdx.x;
-  const int64_t lane0 = (int64_t(blockIdx.x) * kStepThreads + tid) * L;
-  for (int l = 0; l < L; ++l)
-    for (int k = 0; k < epl; ++k) {
-      const int64_t e = lane0 + l + int64_t(k) * T;
-      wsm[(l * epl + k) * kStepThreads + tid] = e < n ? wg[e] : 0.0;
-    }
+  const int64_t lane = int64_t(blockIdx.x) * kStepThreads + tid;
+  double w[kEpt], pv[kEpt], iv[kEpt];
+#pragma unroll
+  for (int k = 0; k < kEpt; ++k) {
+    const int64_t e = lane + int64_t(k) * T;
+    const bool ok = k < epl && e < n;
+    w[k] = ok ? wg[e] : 0.0;
+    iv[k] = ok ? __ldcg(V + e) : 0.0;  // v_0
+    pv[k] = 0.0;
+  }
   double hprev = 0.0;
   for (int i = 0; i <= j + 1; ++i) {
-    const double* vp = V + int64_t(i - 1) * ldv;
-    const double* vi = V + int64_t(i) * ldv;
-    double lanev[8];
-    for (int l = 0; l < L; ++l) {
-      // issue every load of this lane before the dependent arithmetic
-      double pv[kEpt], iv[kEpt];
+    double acc = 0.0;
 #pragma unroll
-      for (int k = 0; k < kEpt; ++k) {
-        const int64_t e = lane0 + l + int64_t(k) * T;
-        const bool ok = k < epl && e < n;
-        pv[k] = (ok && i > 0) ? __ldcs(vp + e) : 0.0;
-        iv[k] = (ok && i <= j) ? __ldcg(vi + e) : 0.0;
+    for (int k = 0; k < kEpt; ++k) {
+      const int64_t e = lane + int64_t(k) * T;
+      if (k < epl && e < n) {
+        if (i > 0) w[k] = dsub(w[k], dmul(hprev, pv[k]));
+        const double o = i <= j ? iv[k] : w[k];
+        acc = dadd(acc, dmul(w[k], o));
       }
-      double acc = 0.0;
-#pragma unroll
-      for (int k = 0; k < kEpt; ++k) {
-        const int64_t e = lane0 + l + int64_t(k) * T;
-        if (k < epl && e < n) {
-          double& ws = wsm[(l * epl + k) * kStepThreads + tid];
-          double we = ws;
-          if (i > 0) {
-            we = dsub(we, dmul(hprev, pv[k]));
-            ws = we;
-          }
-          const double o = i <= j ? iv[k] : we;
-          acc = dadd(acc, dmul(we, o));
-        }
-      }
-      lanev[l] = acc;
     }
-    for (int width = L; width > 1; width >>= 1)
-      for (int k = 0; k < width / 2; ++k) lanev[k] = dadd(lanev[2 * k], lanev[2 * k + 1]);
-    const double cta = block_tree(lanev[0], kStepThreads);
+    const double cta = block_tree(acc, kStepThreads);
     const int par = i & 1;
     const unsigned long long want = tag_base + unsigned(i) + 1ull;
     if (tid == 0) {
       slot_v[par * G + blockIdx.x] = cta;
       st_release_u64(slot_tag + par * G + blockIdx.x, want);
     }
-    for (int k = tid; k < G; k += kStepThreads) {
-      while (ld_acquire_u64(slot_tag + par * G + k) != want) {
+    // prefetch v_{i+1} (independent of h_i) before waiting on the grid
+    if (i + 1 <= j) {
+      const double* vn = V + int64_t(i + 1) * ldv;
+#pragma unroll
+      for (int k = 0; k < kEpt; ++k) {
+        const int64_t e = lane + int64_t(k) * T;
+        pv[k] = iv[k];
+        iv[k] = (k < epl && e < n) ? __ldcg(vn + e) : 0.0;
       }
-      gbuf[k] = __ldcg(slot_v + par * G + k);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kEpt; ++k) pv[k] = iv[k];
     }
-    __syncthreads();
-    smem_tree(gbuf, G);
-    if (tid == 0) {
-      double h = gbuf[0];
-      if (i == j + 1) h = __dsqrt_rn(h);
-      hsh = h;
-      if (blockIdx.x == 0) hcol[i] = h;
+    if (tid < 32) {
+      // warp 0 gathers the G slots (G/32 consecutive per lane when G >= 32)
+      // and rebuilds the adjacent-pair tree with in-lane pairs + shuffles
+      const int per = G >= 32 ? G / 32 : 1;
+      const int nl = G >= 32 ? 32 : G;
+      double v = 0.0;
+      if (tid < nl) {
+        double loc[32];
+        for (int q = 0; q < per; ++q) {
+          const int s = tid * per + q;
+          while (ld_acquire_u64(slot_tag + par * G + s) != want) {
+          }
+          loc[q] = __ldcg(slot_v + par * G + s);
+        }
+        for (int width = per; width > 1; width >>= 1)
+          for (int q = 0; q < width / 2; ++q) loc[q] = dadd(loc[2 * q], loc[2 * q + 1]);
+        v = loc[0];
+      }
+      for (int off = 1; off < nl; off <<= 1) {
+        const double o = __shfl_down_sync(0xffffffffu, v, off);
+        if ((tid & (2 * off - 1)) == 0) v = dadd(v, o);
+      }
+      if (tid == 0) {
+        if (i == j + 1) v = __dsqrt_rn(v);
+        hsh = v;
+        if (blockIdx.x == 0) hcol[i] = v;
+      }
     }
     __syncthreads();
     hprev = hsh;
@@ -288,13 +298,11 @@ __global__ void __launch_bounds__(kStepThreads)
   }
   // v_{j+1} = w / h, or 0 on a happy breakdown (gmres.hpp:66-67)
   double* vn = V + int64_t(j + 1) * ldv;
-  for (int l = 0; l < L; ++l)
-    for (int k = 0; k < epl; ++k) {
-      const int64_t e = lane0 + l + int64_t(k) * T;
-      if (e >= n) break;
-      const double we = wsm[(l * epl + k) * kStepThreads + tid];
-      vn[e] = hprev > 0.0 ? __ddiv_rn(we, hprev) : 0.0;
-    }
+#pragma unroll
+  for (int k = 0; k < kEpt; ++k) {
+    const int64_t e = lane + int64_t(k) * T;
+    if (k < epl && e < n) vn[e] = hprev > 0.0 ? __ddiv_rn(w[k], hprev) : 0.0;
+  }
 }
 
 } // namespace
@@ -308,19 +316,13 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
   if (T < kStepThreads) return false;
   const int epl = int((n + T - 1) / T);
   if (epl > kEpt) return false;
-  static int sm_count = 0, max_smem = 0;
-  if (!sm_count) {
+  static int sm_count = 0;
+  if (!sm_count)
     PSCU_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, c.device));
-    PSCU_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
-    PSCU_CUDA(cudaFuncSetAttribute(arnoldi_step_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   max_smem - 16 * 1024));
-  }
-  for (int L = 1; L <= 8; L <<= 1) {
+  for (int L = 1; L <= 1; L <<= 1) {
     const int64_t G = T / (int64_t(kStepThreads) * L);
     if (G < 1 || G > 1024) continue;
-    const size_t smem = sizeof(double) * size_t(kStepThreads) * L * epl;
-    if (smem > size_t(max_smem - 16 * 1024)) return false;
+    const size_t smem = 0;
     int per_sm = 0;
     PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_step_kernel,
                                                             kStepThreads, smem));

@@ -19,6 +19,8 @@
 // Each row is still computed by one thread with the reference's exact
 // operation sequence, so the result is bit-identical to Ilu0::apply.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.cuh"
 #include "walk.cuh"
@@ -57,35 +59,45 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-struct Stage {
+/// Level data (double-buffered): packed factor entries and per-row inputs.
+struct alignas(16) Stage {
   double val[kMaxNz];
   int32_t src[kMaxNz];
   double xin[kWalkThreads];   // x (forward) or forward result (backward) of each row
   double dv[kWalkThreads];    // backward diagonal
-  int32_t row[kWalkThreads];
-  int32_t off[kWalkThreads + 1];
 };
 
-/// Issues the asynchronous copies of level `lv` into stage `st`.
+/// Level metadata (three-deep): row ids and packed offsets.
+struct alignas(16) Meta {
+  int32_t row[kWalkThreads];
+  int32_t off[kWalkThreads + 4];
+};
+
+/// Copies the row ids / offsets of level lv (two levels ahead of use).
+__device__ void stage_meta(const WalkArgs& a, int lv, Meta& m) {
+  const int k0 = a.lvl_ptr[lv], nr = a.lvl_ptr[lv + 1] - k0;
+  for (int t = threadIdx.x; t < nr; t += blockDim.x) {
+    cp_async4(&m.row[t], a.rows + k0 + t);
+    cp_async4(&m.off[t], a.row_off + k0 + t);
+  }
+  if (threadIdx.x == 0) m.off[nr] = int(a.lvl_nz[lv + 1] - a.lvl_nz[lv]);
+}
+
+/// Copies level lv's packed entries and row inputs (one level ahead); the
+/// row ids come from meta that has already landed.
 template <bool kFwd>
-__device__ void stage_level(const WalkArgs& a, int lv, Stage& st, const double* xin) {
-  const int k0 = a.lvl_ptr[lv], k1 = a.lvl_ptr[lv + 1];
-  const int nr = k1 - k0;
-  const int64_t q0 = a.lvl_nz[lv], q1 = a.lvl_nz[lv + 1];
-  const int nq = int(q1 - q0);
-  // packed values/sources: 16-byte chunks (level starts are 16-byte aligned
-  // and the arrays are padded, so reading past the level end is harmless)
+__device__ void stage_data(const WalkArgs& a, int lv, const Meta& m, Stage& st,
+                           const double* xin) {
+  const int k0 = a.lvl_ptr[lv], nr = a.lvl_ptr[lv + 1] - k0;
+  const int64_t q0 = a.lvl_nz[lv];
+  const int nq = int(a.lvl_nz[lv + 1] - q0);
+  // 16-byte chunks: level starts are 16-byte aligned and the arrays padded
   for (int c = threadIdx.x; c * 2 < nq; c += blockDim.x) cp_async16(&st.val[2 * c], a.val + q0 + 2 * c);
   for (int c = threadIdx.x; c * 4 < nq; c += blockDim.x) cp_async16(&st.src[4 * c], a.src + q0 + 4 * c);
   for (int t = threadIdx.x; t < nr; t += blockDim.x) {
-    const int row = __ldg(a.rows + k0 + t);
-    st.row[t] = row;
-    st.off[t] = __ldg(a.row_off + k0 + t);
-    cp_async8(&st.xin[t], xin + row);
+    cp_async8(&st.xin[t], xin + m.row[t]);
     if (!kFwd) cp_async8(&st.dv[t], a.div + k0 + t);
   }
-  if (threadIdx.x == 0) st.off[nr] = nq;
-  cp_commit();
 }
 
 template <bool kFwd>
@@ -94,16 +106,27 @@ __global__ void __launch_bounds__(kWalkThreads, 1)
   extern __shared__ __align__(16) unsigned char smraw[];
   double* ring = reinterpret_cast<double*>(smraw);
   Stage* stages = reinterpret_cast<Stage*>(smraw + sizeof(double) * kRing);
-  stage_level<kFwd>(a, l0, stages[0], xin);
+  Meta* metas = reinterpret_cast<Meta*>(smraw + sizeof(double) * kRing + 2 * sizeof(Stage));
+  stage_meta(a, l0, metas[0]);
+  if (l0 + 1 < l1) stage_meta(a, l0 + 1, metas[1]);
+  cp_commit();
+  cp_wait_all();
+  __syncthreads();
+  stage_data<kFwd>(a, l0, metas[0], stages[0], xin);
+  cp_commit();
   for (int lv = l0; lv < l1; ++lv) {
-    Stage& st = stages[(lv - l0) & 1];
+    const int r = lv - l0;
+    Stage& st = stages[r & 1];
+    const Meta& mt = metas[r % 3];
     cp_wait_all();
-    __syncthreads();  // stage lv landed; every row of lv-1 is in the ring
-    if (lv + 1 < l1) stage_level<kFwd>(a, lv + 1, stages[(lv + 1 - l0) & 1], xin);
+    __syncthreads();  // data of lv and meta of lv+1 landed; rows of lv-1 are in the ring
+    if (lv + 2 < l1) stage_meta(a, lv + 2, metas[(r + 2) % 3]);
+    if (lv + 1 < l1) stage_data<kFwd>(a, lv + 1, metas[(r + 1) % 3], stages[(r + 1) & 1], xin);
+    cp_commit();
     const int k0 = a.lvl_ptr[lv];
     const int nr = a.lvl_ptr[lv + 1] - k0;
     for (int t = threadIdx.x; t < nr; t += blockDim.x) {
-      const int qa = st.off[t], qb = st.off[t + 1];
+      const int qa = mt.off[t], qb = mt.off[t + 1];
       double acc = st.xin[t];
 #pragma unroll 4
       for (int q = qa; q < qb; ++q) {
@@ -113,7 +136,7 @@ __global__ void __launch_bounds__(kWalkThreads, 1)
       }
       if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
       ring[(k0 + t) & (kRing - 1)] = acc;
-      y[st.row[t]] = acc;
+      y[mt.row[t]] = acc;
     }
   }
 }
@@ -147,7 +170,7 @@ WalkArgs args_of(const WalkPlan& w) {
   return {w.lvl_ptr.p, w.lvl_nz.p, w.rows.p, w.row_off.p, w.val.p, w.src.p, w.div.p};
 }
 
-size_t walk_smem() { return sizeof(double) * kRing + 2 * sizeof(Stage); }
+size_t walk_smem() { return sizeof(double) * kRing + 2 * sizeof(Stage) + 3 * sizeof(Meta); }
 
 } // namespace
 
@@ -230,6 +253,22 @@ void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, bool
         src[q] = in_ring ? (pos[j] & (kRing - 1)) : -(j + 1);
       }
     }
+  }
+  if (getenv("PSCU_DEBUG")) {
+    int64_t ring_hits = 0, far = 0, maxr = 0, maxq = 0;
+    for (int64_t q = 0; q < lvl_nz[nlev]; ++q)
+      if (from[q] >= 0) (src[q] >= 0 ? ring_hits : far)++;
+    for (int l = 0; l < nlev; ++l) {
+      maxr = std::max<int64_t>(maxr, lvl_ptr[l + 1] - lvl_ptr[l]);
+      maxq = std::max<int64_t>(maxq, lvl_nzcnt[l]);
+    }
+    int nwide = 0;
+    for (const auto& s : w.segments) nwide += s.wide;
+    fprintf(stderr,
+            "[walk %s] n=%lld levels=%d segments=%zu (wide %d) max_rows=%lld max_nz=%lld "
+            "ring=%lld far=%lld\n",
+            fwd ? "fwd" : "bwd", (long long)n, nlev, w.segments.size(), nwide, (long long)maxr,
+            (long long)maxq, (long long)ring_hits, (long long)far);
   }
   std::vector<int64_t> dfrom(n);
   for (int k = 0; k < n; ++k) dfrom[k] = diag[rows[k]];
