@@ -135,6 +135,7 @@ struct WalkPlan {
   DevBuf<int32_t> lvl_ptr, rows, row_off, src;
   DevBuf<int64_t> lvl_nz, from, div_from;
   DevBuf<double> val, div;
+  DevBuf<uint8_t> mode;
 };
 
 struct Ilu {

@@ -29,10 +29,12 @@ namespace pscu {
 
 namespace {
 
-constexpr int kWalkThreads = 1024;  // max rows of a narrow level
-constexpr int kMaxNz = 5120;        // max packed entries of a narrow level
+constexpr int kWalkThreads = 1024;  // max rows of a walked level
+constexpr int kStageRows = 512;     // max rows of a staged level
+constexpr int kMaxNz = 2048;        // max packed entries of a staged level
+constexpr int kAhead = 3;           // static data is staged this many levels ahead
+constexpr int kStages = kAhead + 1;
 constexpr int kRing = 4096;         // shared-memory solution ring (positions)
-constexpr int kWideRows = 8192;     // levels with more rows run row-parallel
 
 struct WalkArgs {
   const int32_t* lvl_ptr;   // levels+1 into rows
@@ -42,6 +44,7 @@ struct WalkArgs {
   const double* val;        // packed factor values
   const int32_t* src;       // >= 0 ring slot, < 0: -(row)-1 global source
   const double* div;        // backward: diagonal per schedule position
+  const uint8_t* mode;      // per level: 0 staged, 1 walked from global, 2 wide launch
 };
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -59,35 +62,20 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-/// Level data (double-buffered): packed factor entries and per-row inputs.
+/// Static data of one staged level: packed factor entries, row ids, row
+/// offsets and (backward) diagonals. kStages-deep ring.
 struct alignas(16) Stage {
   double val[kMaxNz];
   int32_t src[kMaxNz];
-  double xin[kWalkThreads];   // x (forward) or forward result (backward) of each row
-  double dv[kWalkThreads];    // backward diagonal
+  double dv[kStageRows];
+  int32_t row[kStageRows];
+  int32_t off[kStageRows + 4];
 };
 
-/// Level metadata (three-deep): row ids and packed offsets.
-struct alignas(16) Meta {
-  int32_t row[kWalkThreads];
-  int32_t off[kWalkThreads + 4];
-};
-
-/// Copies the row ids / offsets of level lv (two levels ahead of use).
-__device__ void stage_meta(const WalkArgs& a, int lv, Meta& m) {
-  const int k0 = a.lvl_ptr[lv], nr = a.lvl_ptr[lv + 1] - k0;
-  for (int t = threadIdx.x; t < nr; t += blockDim.x) {
-    cp_async4(&m.row[t], a.rows + k0 + t);
-    cp_async4(&m.off[t], a.row_off + k0 + t);
-  }
-  if (threadIdx.x == 0) m.off[nr] = int(a.lvl_nz[lv + 1] - a.lvl_nz[lv]);
-}
-
-/// Copies level lv's packed entries and row inputs (one level ahead); the
-/// row ids come from meta that has already landed.
+/// Group B: the static data of level lv (issued kAhead levels ahead).
 template <bool kFwd>
-__device__ void stage_data(const WalkArgs& a, int lv, const Meta& m, Stage& st,
-                           const double* xin) {
+__device__ void stage_static(const WalkArgs& a, int lv, Stage& st) {
+  if (a.mode[lv] != 0) return;
   const int k0 = a.lvl_ptr[lv], nr = a.lvl_ptr[lv + 1] - k0;
   const int64_t q0 = a.lvl_nz[lv];
   const int nq = int(a.lvl_nz[lv + 1] - q0);
@@ -95,9 +83,20 @@ __device__ void stage_data(const WalkArgs& a, int lv, const Meta& m, Stage& st,
   for (int c = threadIdx.x; c * 2 < nq; c += blockDim.x) cp_async16(&st.val[2 * c], a.val + q0 + 2 * c);
   for (int c = threadIdx.x; c * 4 < nq; c += blockDim.x) cp_async16(&st.src[4 * c], a.src + q0 + 4 * c);
   for (int t = threadIdx.x; t < nr; t += blockDim.x) {
-    cp_async8(&st.xin[t], xin + m.row[t]);
+    cp_async4(&st.row[t], a.rows + k0 + t);
+    cp_async4(&st.off[t], a.row_off + k0 + t);
     if (!kFwd) cp_async8(&st.dv[t], a.div + k0 + t);
   }
+  if (threadIdx.x == 0) st.off[nr] = nq;
+}
+
+/// Group A: the right-hand side entries of level lv's rows (row ids from
+/// its already-landed stage).
+__device__ void stage_rhs(const WalkArgs& a, int lv, const Stage& st, double* xb,
+                          const double* xin) {
+  if (a.mode[lv] != 0) return;
+  const int nr = a.lvl_ptr[lv + 1] - a.lvl_ptr[lv];
+  for (int t = threadIdx.x; t < nr; t += blockDim.x) cp_async8(&xb[t], xin + st.row[t]);
 }
 
 template <bool kFwd>
@@ -105,39 +104,67 @@ __global__ void __launch_bounds__(kWalkThreads, 1)
     walk_kernel(WalkArgs a, int l0, int l1, const double* xin, double* y) {
   extern __shared__ __align__(16) unsigned char smraw[];
   double* ring = reinterpret_cast<double*>(smraw);
-  Stage* stages = reinterpret_cast<Stage*>(smraw + sizeof(double) * kRing);
-  Meta* metas = reinterpret_cast<Meta*>(smraw + sizeof(double) * kRing + 2 * sizeof(Stage));
-  stage_meta(a, l0, metas[0]);
-  if (l0 + 1 < l1) stage_meta(a, l0 + 1, metas[1]);
+  double* xbuf = ring + kRing;  // [2][kStageRows]
+  Stage* stages = reinterpret_cast<Stage*>(xbuf + 2 * kStageRows);
+  // prologue: static data of the first kAhead levels, then level l0's rhs
+  for (int d = 0; d < kAhead; ++d) {
+    if (l0 + d < l1) stage_static<kFwd>(a, l0 + d, stages[d]);
+    cp_commit();
+  }
+  cp_wait_all();
+  __syncthreads();
+  stage_rhs(a, l0, stages[0], xbuf, xin);
   cp_commit();
   cp_wait_all();
   __syncthreads();
-  stage_data<kFwd>(a, l0, metas[0], stages[0], xin);
-  cp_commit();
   for (int lv = l0; lv < l1; ++lv) {
     const int r = lv - l0;
-    Stage& st = stages[r & 1];
-    const Meta& mt = metas[r % 3];
-    cp_wait_all();
-    __syncthreads();  // data of lv and meta of lv+1 landed; rows of lv-1 are in the ring
-    if (lv + 2 < l1) stage_meta(a, lv + 2, metas[(r + 2) % 3]);
-    if (lv + 1 < l1) stage_data<kFwd>(a, lv + 1, metas[(r + 1) % 3], stages[(r + 1) & 1], xin);
+    // group A: rhs of lv+1 (its stage landed at the end of the last level);
+    // group B: static data kAhead levels ahead. A is committed first, so
+    // waiting for "all but the newest group" below leaves only B pending.
+    if (lv + 1 < l1) stage_rhs(a, lv + 1, stages[(r + 1) % kStages], xbuf + ((r + 1) & 1) * kStageRows, xin);
+    cp_commit();
+    if (lv + kAhead < l1) stage_static<kFwd>(a, lv + kAhead, stages[(r + kAhead) % kStages]);
     cp_commit();
     const int k0 = a.lvl_ptr[lv];
     const int nr = a.lvl_ptr[lv + 1] - k0;
-    for (int t = threadIdx.x; t < nr; t += blockDim.x) {
-      const int qa = mt.off[t], qb = mt.off[t + 1];
-      double acc = st.xin[t];
+    if (a.mode[lv] == 0) {
+      const Stage& st = stages[r % kStages];
+      const double* xb = xbuf + (r & 1) * kStageRows;
+      for (int t = threadIdx.x; t < nr; t += blockDim.x) {
+        const int qa = st.off[t], qb = st.off[t + 1];
+        double acc = xb[t];
 #pragma unroll 4
-      for (int q = qa; q < qb; ++q) {
-        const int s = st.src[q];
-        const double yv = s >= 0 ? ring[s] : __ldcg(y + (-s - 1));
-        acc = dsub(acc, dmul(st.val[q], yv));
+        for (int q = qa; q < qb; ++q) {
+          const int s = st.src[q];
+          const double yv = s >= 0 ? ring[s] : __ldcg(y + (-s - 1));
+          acc = dsub(acc, dmul(st.val[q], yv));
+        }
+        if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
+        ring[(k0 + t) & (kRing - 1)] = acc;
+        y[st.row[t]] = acc;
       }
-      if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
-      ring[(k0 + t) & (kRing - 1)] = acc;
-      y[mt.row[t]] = acc;
+    } else {
+      // heavy level: operands straight from global memory
+      const int64_t q0 = a.lvl_nz[lv];
+      for (int t = threadIdx.x; t < nr; t += blockDim.x) {
+        const int k = k0 + t;
+        const int row = __ldg(a.rows + k);
+        const int64_t qa = q0 + __ldg(a.row_off + k);
+        const int64_t qb = t + 1 < nr ? q0 + __ldg(a.row_off + k + 1) : a.lvl_nz[lv + 1];
+        double acc = kFwd ? __ldg(xin + row) : __ldcg(xin + row);
+        for (int64_t q = qa; q < qb; ++q) {
+          const int s = __ldg(a.src + q);
+          const double yv = s >= 0 ? ring[s] : __ldcg(y + (-s - 1));
+          acc = dsub(acc, dmul(__ldg(a.val + q), yv));
+        }
+        if (!kFwd) acc = __ddiv_rn(acc, __ldg(a.div + k));
+        ring[k & (kRing - 1)] = acc;
+        y[row] = acc;
+      }
     }
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
   }
 }
 
@@ -167,10 +194,12 @@ __global__ void gather_vals(int64_t m, const int64_t* __restrict__ from,
 }
 
 WalkArgs args_of(const WalkPlan& w) {
-  return {w.lvl_ptr.p, w.lvl_nz.p, w.rows.p, w.row_off.p, w.val.p, w.src.p, w.div.p};
+  return {w.lvl_ptr.p, w.lvl_nz.p, w.rows.p, w.row_off.p, w.val.p, w.src.p, w.div.p, w.mode.p};
 }
 
-size_t walk_smem() { return sizeof(double) * kRing + 2 * sizeof(Stage) + 3 * sizeof(Meta); }
+size_t walk_smem() {
+  return sizeof(double) * (kRing + 2 * kStageRows) + kStages * sizeof(Stage);
+}
 
 } // namespace
 
@@ -207,14 +236,15 @@ void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, bool
     }
   }
   // level kinds: narrow levels (walked) vs wide ones (row-parallel)
-  std::vector<uint8_t> wide(nlev, 0);
+  std::vector<uint8_t> wide(nlev, 0), mode(nlev, 0);
   std::vector<int64_t> lvl_nzcnt(nlev, 0);
   for (int l = 0; l < nlev; ++l) {
     int64_t nz = 0;
     for (int k = lvl_ptr[l]; k < lvl_ptr[l + 1]; ++k) nz += q_end(rows[k]) - q_begin(rows[k]);
     lvl_nzcnt[l] = nz;
-    wide[l] = (lvl_ptr[l + 1] - lvl_ptr[l] > kWalkThreads || nz > kMaxNz - 8) ? 1 : 0;
-    if (lvl_ptr[l + 1] - lvl_ptr[l] > kWideRows) wide[l] = 1;
+    const int rows_l = lvl_ptr[l + 1] - lvl_ptr[l];
+    wide[l] = rows_l > kWalkThreads ? 1 : 0;
+    mode[l] = wide[l] ? 2 : ((rows_l <= kStageRows && nz <= kMaxNz - 8) ? 0 : 1);
   }
   // segments and packed arrays
   std::vector<int64_t> lvl_nz(nlev + 1, 0);
@@ -262,18 +292,20 @@ void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, bool
       maxr = std::max<int64_t>(maxr, lvl_ptr[l + 1] - lvl_ptr[l]);
       maxq = std::max<int64_t>(maxq, lvl_nzcnt[l]);
     }
-    int nwide = 0;
-    for (const auto& s : w.segments) nwide += s.wide;
+    int nwide = 0, nstaged = 0;
+    for (const auto& sg : w.segments) nwide += sg.wide;
+    for (int l = 0; l < nlev; ++l) nstaged += mode[l] == 0;
     fprintf(stderr,
-            "[walk %s] n=%lld levels=%d segments=%zu (wide %d) max_rows=%lld max_nz=%lld "
-            "ring=%lld far=%lld\n",
-            fwd ? "fwd" : "bwd", (long long)n, nlev, w.segments.size(), nwide, (long long)maxr,
+            "[walk %s] n=%lld levels=%d (staged %d) segments=%zu (wide %d) max_rows=%lld "
+            "max_nz=%lld ring=%lld far=%lld\n",
+            fwd ? "fwd" : "bwd", (long long)n, nlev, nstaged, w.segments.size(), nwide, (long long)maxr,
             (long long)maxq, (long long)ring_hits, (long long)far);
   }
   std::vector<int64_t> dfrom(n);
   for (int k = 0; k < n; ++k) dfrom[k] = diag[rows[k]];
   cudaStream_t st = c.stream;
   w.nlev = nlev;
+  w.mode.upload(mode, st);
   w.lvl_ptr.upload(lvl_ptr, st);
   w.lvl_nz.upload(lvl_nz, st);
   w.rows.upload(rows, st);
