@@ -104,46 +104,30 @@ struct Csr {
   std::vector<int32_t> h_cols;
 };
 
-/// Schedule for one sparse triangular sweep (sync-free, chunked, levelled).
-struct Sweep {
-  int nchunks = 0;
-  int nlevels = 0;
-  int max_chunk_rows = 0;
-  int max_level_rows = 0;
-  DevBuf<int64_t> chunk_begin, chunk_end; // row range of chunk c (processing order)
-  DevBuf<int32_t> chunk_lvl;              // nchunks+1, global level index
-  DevBuf<int32_t> level_ptr;              // nlevels+1 into sched
-  DevBuf<int32_t> sched;                  // row ids, grouped by level
-  DevBuf<int32_t> wait_ptr;               // nlevels+1
-  DevBuf<int32_t> wait_chunk;             // foreign chunk (processing index)
-  DevBuf<int32_t> wait_need;              // required local progress of that chunk
-  DevBuf<uint8_t> exported;               // level publishes progress
-  DevBuf<unsigned long long> progress;    // nchunks, tagged with the launch epoch
-  DevBuf<unsigned long long> ticket;      // 1
-};
-
 /// Level-walking sweep plan (walk.cu).
 struct WalkSeg {
-  bool wide;   // row-parallel launch of one level, else one walker CTA
-  int l0, l1;  // level range
+  bool wide;   // row-parallel launch of one sub-level, else one walker CTA
+  int s0, s1;  // sub-level range
 };
 
 struct WalkPlan {
   bool fwd = true;
-  int nlev = 0;
+  int nsub = 0;
+  int64_t npos = 0;
   std::vector<WalkSeg> segments;
-  DevBuf<int32_t> lvl_ptr, rows, row_off, src;
-  DevBuf<int64_t> lvl_nz, from, div_from;
-  DevBuf<double> val, div;
-  DevBuf<uint8_t> mode;
+  DevBuf<int32_t> sl_k, sl_nr, sl_nq, rows, off, opos, src;
+  DevBuf<int64_t> sl_q, from, dfrom;
+  DevBuf<double> val, dv;
+  mutable DevBuf<double> scratch;  // per-apply right-hand sides in position order
 };
 
 struct Ilu {
   const Csr* a = nullptr;
   DevBuf<double> lu;
   DevBuf<int64_t> diag;
-  Sweep fwd;           // chunked sync-free schedule (factorisation)
-  WalkPlan wfwd, wbwd; // level walkers (application)
+  WalkPlan wfwd, wbwd;           // level walkers (application)
+  std::vector<int32_t> flev_ptr; // forward DAG levels (factorisation launches)
+  DevBuf<int32_t> flev_rows;
 };
 
 /// Live per-kernel-class timing with CUDA events on the launching stream.
@@ -213,8 +197,6 @@ void upload_csr(Context& c, Csr& m, int64_t n, const int64_t* rp, const int32_t*
                 const double* vals, int mem);
 
 // sptrsv.cu
-void build_sweep(Context& c, const Csr& a, const std::vector<int64_t>& diag, bool forward,
-                 Sweep& s);
 void ilu0_factor(Context& c, Ilu& ilu);
 void ilu0_apply(Context& c, const Ilu& ilu, const double* x, double* y);
 

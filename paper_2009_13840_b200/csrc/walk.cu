@@ -1,23 +1,28 @@
 // Level-walking sparse triangular sweeps for Ilu0::apply (ilu0.hpp:53-65).
 //
-// The reference applies ILU(0) with two sequential loops. Their dependency
-// DAG under the natural (faces-first) ordering is deep and narrow: thousands
-// of levels of a few hundred rows. Any scheme that pays
-// an inter-SM handshake per level is latency-bound at ~1 us per level, so
-// narrow levels are walked by ONE CTA:
-//   * rows are stored in level order, and for every row the factor entries
-//     it needs are packed contiguously in the reference's summation order
-//     (value + source), so a level's data is one contiguous block;
-//   * while level l is computed, level l+1's block is copied into the other
-//     half of a shared-memory double buffer with cp.async;
-//   * solution values of recently finished rows live in a shared-memory ring
-//     indexed by schedule position (sources farther back than the ring, or
-//     from other segments, are read from global memory);
-//   * one __syncthreads per level, no global-memory handshake at all.
-// Levels too wide for one CTA (e.g. the element-pressure rows, 10^5 per
-// level) run as ordinary row-parallel launches between walker segments.
-// Each row is still computed by one thread with the reference's exact
-// operation sequence, so the result is bit-identical to Ilu0::apply.
+// The reference applies ILU(0) with two sequential loops. Under the natural
+// (faces-first) ordering their dependency DAGs are deep and narrow: hundreds
+// to thousands of levels of a few hundred rows, so any
+// scheme that pays an inter-SM handshake per level is bound by ~1 us per
+// level. Narrow levels are therefore walked by ONE CTA:
+//   * rows are placed in level order ("positions"); each level is cut into
+//     sub-levels of at most kStageRows rows / kMaxNz factor entries (rows of
+//     one level are independent, so any cut is a valid schedule);
+//   * a sub-level's operands are one contiguous, 16-byte-aligned block:
+//     the factor entries it needs in the reference's summation order
+//     (value + source), its row ids, offsets, right-hand sides (gathered into
+//     position order beforehand) and, backward, its diagonals;
+//   * blocks are staged into shared memory kAhead sub-levels ahead with
+//     cp.async (all addresses are static, so the pipeline never waits on a
+//     dependent gather);
+//   * recently computed solution values live in a shared-memory ring indexed
+//     by position; older sources, or sources from other segments, come from
+//     global memory (L2);
+//   * one __syncthreads per sub-level, no global handshake at all.
+// Levels with very many rows (the element-pressure rows) run as ordinary
+// row-parallel launches between walker segments. Every row is computed by
+// one thread with the reference's exact operation sequence, so the result is
+// bit-identical to Ilu0::apply.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -29,28 +34,27 @@ namespace pscu {
 
 namespace {
 
-constexpr int kWalkThreads = 1024;  // max rows of a walked level
-constexpr int kStageRows = 512;     // max rows of a staged level
-constexpr int kMaxNz = 2048;        // max packed entries of a staged level
-constexpr int kAhead = 3;           // static data is staged this many levels ahead
+constexpr int kWalkThreads = 512;
+constexpr int kStageRows = 512;   // rows of a sub-level
+constexpr int kMaxNz = 2560;      // factor entries of a sub-level (multiple of 4)
+constexpr int kAhead = 3;         // sub-levels staged ahead
 constexpr int kStages = kAhead + 1;
-constexpr int kRing = 4096;         // shared-memory solution ring (positions)
+constexpr int kRing = 4096;       // shared-memory solution ring (positions, power of 2)
+constexpr int kWideRows = 4096;   // levels with more rows run row-parallel
 
 struct WalkArgs {
-  const int32_t* lvl_ptr;   // levels+1 into rows
-  const int64_t* lvl_nz;    // levels+1 into packed entries (16-byte aligned starts)
-  const int32_t* rows;      // row id per schedule position
-  const int32_t* row_off;   // packed offset of a row relative to its level start
-  const double* val;        // packed factor values
-  const int32_t* src;       // >= 0 ring slot, < 0: -(row)-1 global source
-  const double* div;        // backward: diagonal per schedule position
-  const uint8_t* mode;      // per level: 0 staged, 1 walked from global, 2 wide launch
+  const int32_t* sl_k;    // sub-level start position (multiple of 4)
+  const int32_t* sl_nr;   // rows of the sub-level
+  const int64_t* sl_q;    // packed entry start (multiple of 4), nsub + 1
+  const int32_t* sl_nq;   // real packed entries of the sub-level
+  const int32_t* rows;    // row id per position (-1 padding)
+  const int32_t* off;     // packed offset of a row within its sub-level
+  const int32_t* opos;    // forward: backward position of the row
+  const double* val;      // packed factor values
+  const int32_t* src;     // >= 0 ring slot, < 0: -(row)-1 global source
+  const double* dv;       // backward: diagonal per position
 };
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = unsigned(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned s = unsigned(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
@@ -60,127 +64,101 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-/// Static data of one staged level: packed factor entries, row ids, row
-/// offsets and (backward) diagonals. kStages-deep ring.
 struct alignas(16) Stage {
   double val[kMaxNz];
   int32_t src[kMaxNz];
+  double rhs[kStageRows];
   double dv[kStageRows];
   int32_t row[kStageRows];
+  int32_t opos[kStageRows];
   int32_t off[kStageRows + 4];
 };
 
-/// Group B: the static data of level lv (issued kAhead levels ahead).
+/// Issues the asynchronous copies of sub-level s into `st` (static addresses).
 template <bool kFwd>
-__device__ void stage_static(const WalkArgs& a, int lv, Stage& st) {
-  if (a.mode[lv] != 0) return;
-  const int k0 = a.lvl_ptr[lv], nr = a.lvl_ptr[lv + 1] - k0;
-  const int64_t q0 = a.lvl_nz[lv];
-  const int nq = int(a.lvl_nz[lv + 1] - q0);
-  // 16-byte chunks: level starts are 16-byte aligned and the arrays padded
-  for (int c = threadIdx.x; c * 2 < nq; c += blockDim.x) cp_async16(&st.val[2 * c], a.val + q0 + 2 * c);
-  for (int c = threadIdx.x; c * 4 < nq; c += blockDim.x) cp_async16(&st.src[4 * c], a.src + q0 + 4 * c);
-  for (int t = threadIdx.x; t < nr; t += blockDim.x) {
-    cp_async4(&st.row[t], a.rows + k0 + t);
-    cp_async4(&st.off[t], a.row_off + k0 + t);
-    if (!kFwd) cp_async8(&st.dv[t], a.div + k0 + t);
+__device__ void stage(const WalkArgs& a, int s, Stage& st, const double* rhs) {
+  const int k0 = a.sl_k[s], nr = a.sl_nr[s];
+  const int nr4 = (nr + 3) & ~3;
+  const int64_t q0 = a.sl_q[s];
+  const int nq = int(a.sl_q[s + 1] - q0);
+  const int t = threadIdx.x, T = blockDim.x;
+  for (int c = t; c * 2 < nq; c += T) cp_async16(&st.val[2 * c], a.val + q0 + 2 * c);
+  for (int c = t; c * 4 < nq; c += T) cp_async16(&st.src[4 * c], a.src + q0 + 4 * c);
+  for (int c = t; c * 2 < nr4; c += T) cp_async16(&st.rhs[2 * c], rhs + k0 + 2 * c);
+  for (int c = t; c * 4 < nr4; c += T) {
+    cp_async16(&st.row[4 * c], a.rows + k0 + 4 * c);
+    cp_async16(&st.off[4 * c], a.off + k0 + 4 * c);
+    if (kFwd) cp_async16(&st.opos[4 * c], a.opos + k0 + 4 * c);
   }
-  if (threadIdx.x == 0) st.off[nr] = nq;
-}
-
-/// Group A: the right-hand side entries of level lv's rows (row ids from
-/// its already-landed stage).
-__device__ void stage_rhs(const WalkArgs& a, int lv, const Stage& st, double* xb,
-                          const double* xin) {
-  if (a.mode[lv] != 0) return;
-  const int nr = a.lvl_ptr[lv + 1] - a.lvl_ptr[lv];
-  for (int t = threadIdx.x; t < nr; t += blockDim.x) cp_async8(&xb[t], xin + st.row[t]);
+  if (!kFwd)
+    for (int c = t; c * 2 < nr4; c += T) cp_async16(&st.dv[2 * c], a.dv + k0 + 2 * c);
+  if (t == 0) cp_async4(&st.off[nr], a.sl_nq + s);
 }
 
 template <bool kFwd>
 __global__ void __launch_bounds__(kWalkThreads, 1)
-    walk_kernel(WalkArgs a, int l0, int l1, const double* xin, double* y) {
+    walk_kernel(WalkArgs a, int s0, int s1, const double* rhs, double* y, double* yb) {
   extern __shared__ __align__(16) unsigned char smraw[];
   double* ring = reinterpret_cast<double*>(smraw);
-  double* xbuf = ring + kRing;  // [2][kStageRows]
-  Stage* stages = reinterpret_cast<Stage*>(xbuf + 2 * kStageRows);
-  // prologue: static data of the first kAhead levels, then level l0's rhs
+  Stage* stages = reinterpret_cast<Stage*>(smraw + sizeof(double) * kRing);
   for (int d = 0; d < kAhead; ++d) {
-    if (l0 + d < l1) stage_static<kFwd>(a, l0 + d, stages[d]);
+    if (s0 + d < s1) stage<kFwd>(a, s0 + d, stages[d], rhs);
     cp_commit();
   }
-  cp_wait_all();
+  asm volatile("cp.async.wait_group %0;" ::"n"(kAhead - 1) : "memory");
   __syncthreads();
-  stage_rhs(a, l0, stages[0], xbuf, xin);
-  cp_commit();
-  cp_wait_all();
-  __syncthreads();
-  for (int lv = l0; lv < l1; ++lv) {
-    const int r = lv - l0;
-    // group A: rhs of lv+1 (its stage landed at the end of the last level);
-    // group B: static data kAhead levels ahead. A is committed first, so
-    // waiting for "all but the newest group" below leaves only B pending.
-    if (lv + 1 < l1) stage_rhs(a, lv + 1, stages[(r + 1) % kStages], xbuf + ((r + 1) & 1) * kStageRows, xin);
+  for (int s = s0; s < s1; ++s) {
+    const int r = s - s0;
+    if (s + kAhead < s1) stage<kFwd>(a, s + kAhead, stages[(r + kAhead) % kStages], rhs);
     cp_commit();
-    if (lv + kAhead < l1) stage_static<kFwd>(a, lv + kAhead, stages[(r + kAhead) % kStages]);
-    cp_commit();
-    const int k0 = a.lvl_ptr[lv];
-    const int nr = a.lvl_ptr[lv + 1] - k0;
-    if (a.mode[lv] == 0) {
-      const Stage& st = stages[r % kStages];
-      const double* xb = xbuf + (r & 1) * kStageRows;
-      for (int t = threadIdx.x; t < nr; t += blockDim.x) {
-        const int qa = st.off[t], qb = st.off[t + 1];
-        double acc = xb[t];
+    const Stage& st = stages[r % kStages];
+    const int k0 = a.sl_k[s], nr = a.sl_nr[s];
+    for (int t = threadIdx.x; t < nr; t += blockDim.x) {
+      const int qa = st.off[t], qb = st.off[t + 1];
+      double acc = st.rhs[t];
 #pragma unroll 4
-        for (int q = qa; q < qb; ++q) {
-          const int s = st.src[q];
-          const double yv = s >= 0 ? ring[s] : __ldcg(y + (-s - 1));
-          acc = dsub(acc, dmul(st.val[q], yv));
-        }
-        if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
-        ring[(k0 + t) & (kRing - 1)] = acc;
-        y[st.row[t]] = acc;
+      for (int q = qa; q < qb; ++q) {
+        const int sv = st.src[q];
+        const double yv = sv >= 0 ? ring[sv] : __ldcg(y + (-sv - 1));
+        acc = dsub(acc, dmul(st.val[q], yv));
       }
-    } else {
-      // heavy level: operands straight from global memory
-      const int64_t q0 = a.lvl_nz[lv];
-      for (int t = threadIdx.x; t < nr; t += blockDim.x) {
-        const int k = k0 + t;
-        const int row = __ldg(a.rows + k);
-        const int64_t qa = q0 + __ldg(a.row_off + k);
-        const int64_t qb = t + 1 < nr ? q0 + __ldg(a.row_off + k + 1) : a.lvl_nz[lv + 1];
-        double acc = kFwd ? __ldg(xin + row) : __ldcg(xin + row);
-        for (int64_t q = qa; q < qb; ++q) {
-          const int s = __ldg(a.src + q);
-          const double yv = s >= 0 ? ring[s] : __ldcg(y + (-s - 1));
-          acc = dsub(acc, dmul(__ldg(a.val + q), yv));
-        }
-        if (!kFwd) acc = __ddiv_rn(acc, __ldg(a.div + k));
-        ring[k & (kRing - 1)] = acc;
-        y[row] = acc;
-      }
+      if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
+      ring[(k0 + t) & (kRing - 1)] = acc;
+      y[st.row[t]] = acc;
+      if (kFwd) yb[st.opos[t]] = acc;
     }
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    // everything but the newest kAhead-1 groups landed: sub-level s+1 is in
+    asm volatile("cp.async.wait_group %0;" ::"n"(kAhead - 1) : "memory");
     __syncthreads();
   }
 }
 
-/// Row-parallel level (too wide for one CTA): every source is global.
+/// Row-parallel sub-level (a level too wide for one CTA): global sources.
 template <bool kFwd>
-__global__ void wide_kernel(WalkArgs a, int lv, const double* xin, double* y) {
-  const int k0 = a.lvl_ptr[lv], k1 = a.lvl_ptr[lv + 1];
-  const int64_t q0 = a.lvl_nz[lv];
-  for (int k = k0 + int(blockIdx.x * blockDim.x + threadIdx.x); k < k1; k += gridDim.x * blockDim.x) {
-    const int row = a.rows[k];
-    const int64_t qa = q0 + a.row_off[k];
-    const int64_t qb = (k + 1 < k1) ? q0 + a.row_off[k + 1] : a.lvl_nz[lv + 1];
-    double acc = xin[row];
+__global__ void wide_kernel(WalkArgs a, int s, const double* rhs, double* y, double* yb) {
+  const int k0 = a.sl_k[s], nr = a.sl_nr[s];
+  const int64_t q0 = a.sl_q[s];
+  const int nq = a.sl_nq[s];
+  for (int t = int(blockIdx.x * blockDim.x + threadIdx.x); t < nr; t += gridDim.x * blockDim.x) {
+    const int k = k0 + t;
+    const int64_t qa = q0 + a.off[k];
+    const int64_t qb = q0 + (t + 1 < nr ? a.off[k + 1] : nq);
+    double acc = rhs[k];
     for (int64_t q = qa; q < qb; ++q) acc = dsub(acc, dmul(a.val[q], __ldcg(y + (-a.src[q] - 1))));
-    if (!kFwd) acc = __ddiv_rn(acc, a.div[k]);
-    y[row] = acc;
+    if (!kFwd) acc = __ddiv_rn(acc, a.dv[k]);
+    y[a.rows[k]] = acc;
+    if (kFwd) yb[a.opos[k]] = acc;
+  }
+}
+
+/// Right-hand side in position order: xs[k] = x[rows[k]].
+__global__ void gather_rhs(int64_t npos, const int32_t* __restrict__ rows,
+                           const double* __restrict__ x, double* __restrict__ xs) {
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < npos;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    const int r = rows[k];
+    xs[k] = r >= 0 ? x[r] : 0.0;
   }
 }
 
@@ -194,148 +172,204 @@ __global__ void gather_vals(int64_t m, const int64_t* __restrict__ from,
 }
 
 WalkArgs args_of(const WalkPlan& w) {
-  return {w.lvl_ptr.p, w.lvl_nz.p, w.rows.p, w.row_off.p, w.val.p, w.src.p, w.div.p, w.mode.p};
+  return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_nq.p, w.rows.p, w.off.p,
+          w.opos.p, w.val.p,  w.src.p,  w.dv.p};
 }
 
-size_t walk_smem() {
-  return sizeof(double) * (kRing + 2 * kStageRows) + kStages * sizeof(Stage);
+size_t walk_smem() { return sizeof(double) * kRing + kStages * sizeof(Stage); }
+
+unsigned grid1(int64_t n) {
+  const int64_t g = (n + 255) / 256;
+  return unsigned(g < 148 * 8 ? (g > 0 ? g : 1) : 148 * 8);
 }
 
-} // namespace
-
-void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, bool fwd, WalkPlan& w) {
+/// DAG levels of one sweep in processing order.
+std::vector<int32_t> dag_levels(const Csr& a, const std::vector<int64_t>& diag, bool fwd,
+                                int& nlev) {
   const int64_t n = a.n;
   const auto& rp = a.h_row_ptr;
   const auto& cols = a.h_cols;
-  w.fwd = fwd;
-  w.segments.clear();
-  if (n == 0) return;
-  auto q_begin = [&](int64_t i) { return fwd ? rp[i] : diag[i] + 1; };
-  auto q_end = [&](int64_t i) { return fwd ? diag[i] : rp[i + 1]; };
-  // DAG levels in processing order
   std::vector<int32_t> lvl(n, 0);
-  int nlev = 0;
+  nlev = 0;
   for (int64_t p = 0; p < n; ++p) {
     const int64_t i = fwd ? p : n - 1 - p;
+    const int64_t q0 = fwd ? rp[i] : diag[i] + 1, q1 = fwd ? diag[i] : rp[i + 1];
     int L = 0;
-    for (int64_t q = q_begin(i); q < q_end(i); ++q) L = std::max(L, lvl[cols[q]] + 1);
+    for (int64_t q = q0; q < q1; ++q) L = std::max(L, lvl[cols[q]] + 1);
     lvl[i] = L;
     nlev = std::max(nlev, L + 1);
   }
-  std::vector<int32_t> lvl_ptr(nlev + 1, 0);
+  return lvl;
+}
+
+struct HostPlan {
+  std::vector<int32_t> sl_k, sl_nr, sl_nq, rows, off, src, pos;
+  std::vector<int64_t> sl_q, from, dfrom;
+  std::vector<uint8_t> sl_wide;
+  int64_t npos = 0;
+};
+
+/// Positions, sub-levels and packed operands of one sweep.
+HostPlan plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
+  const int64_t n = a.n;
+  const auto& rp = a.h_row_ptr;
+  const auto& cols = a.h_cols;
+  auto q_begin = [&](int64_t i) { return fwd ? rp[i] : diag[i] + 1; };
+  auto q_end = [&](int64_t i) { return fwd ? diag[i] : rp[i + 1]; };
+  int nlev = 0;
+  const std::vector<int32_t> lvl = dag_levels(a, diag, fwd, nlev);
+  std::vector<int32_t> lvl_ptr(nlev + 1, 0), order(n);
   for (int64_t i = 0; i < n; ++i) lvl_ptr[lvl[i] + 1]++;
   for (int l = 0; l < nlev; ++l) lvl_ptr[l + 1] += lvl_ptr[l];
-  std::vector<int32_t> rows(n), pos(n);
   {
     std::vector<int32_t> fill(lvl_ptr.begin(), lvl_ptr.end() - 1);
     for (int64_t p = 0; p < n; ++p) {
       const int64_t i = fwd ? p : n - 1 - p;
-      const int32_t k = fill[lvl[i]]++;
-      rows[k] = int32_t(i);
-      pos[i] = k;
+      order[fill[lvl[i]]++] = int32_t(i);
     }
   }
-  // level kinds: narrow levels (walked) vs wide ones (row-parallel)
-  std::vector<uint8_t> wide(nlev, 0), mode(nlev, 0);
-  std::vector<int64_t> lvl_nzcnt(nlev, 0);
+  HostPlan h;
+  h.pos.assign(n, -1);
+  int64_t k = 0, q = 0;
+  auto open_sub = [&](bool wide) {
+    k = (k + 3) & ~int64_t(3);
+    q = (q + 3) & ~int64_t(3);
+    h.sl_k.push_back(int32_t(k));
+    h.sl_nr.push_back(0);
+    h.sl_q.push_back(q);
+    h.sl_nq.push_back(0);
+    h.sl_wide.push_back(wide ? 1 : 0);
+  };
   for (int l = 0; l < nlev; ++l) {
-    int64_t nz = 0;
-    for (int k = lvl_ptr[l]; k < lvl_ptr[l + 1]; ++k) nz += q_end(rows[k]) - q_begin(rows[k]);
-    lvl_nzcnt[l] = nz;
-    const int rows_l = lvl_ptr[l + 1] - lvl_ptr[l];
-    wide[l] = rows_l > kWalkThreads ? 1 : 0;
-    mode[l] = wide[l] ? 2 : ((rows_l <= kStageRows && nz <= kMaxNz - 8) ? 0 : 1);
+    const int nrl = lvl_ptr[l + 1] - lvl_ptr[l];
+    const bool wide = nrl > kWideRows;
+    open_sub(wide);
+    for (int j = lvl_ptr[l]; j < lvl_ptr[l + 1]; ++j) {
+      const int32_t i = order[j];
+      const int64_t nz = q_end(i) - q_begin(i);
+      if (!wide && (h.sl_nr.back() == kStageRows || h.sl_nq.back() + nz > kMaxNz - 4)) open_sub(false);
+      h.pos[i] = int32_t(k++);
+      h.sl_nr.back()++;
+      h.sl_nq.back() += int32_t(nz);
+      q += nz;
+    }
   }
-  // segments and packed arrays
-  std::vector<int64_t> lvl_nz(nlev + 1, 0);
-  for (int l = 0; l < nlev; ++l) lvl_nz[l + 1] = lvl_nz[l] + ((lvl_nzcnt[l] + 3) / 4) * 4;
-  const int64_t total = lvl_nz[nlev] + 8;
-  std::vector<int64_t> from(total, -1);
-  std::vector<int32_t> src(total, 0), row_off(n, 0);
-  std::vector<int32_t> seg_of_level(nlev, -1);
+  h.sl_q.push_back((q + 3) & ~int64_t(3));
+  h.npos = (k + 3) & ~int64_t(3);
+  const int nsub = int(h.sl_k.size());
+  // walker segments (for the ring-source rule)
+  std::vector<int32_t> seg_of(nsub);
   int seg = -1;
-  for (int l = 0; l < nlev; ++l) {
-    if (wide[l]) {
-      w.segments.push_back({true, l, l + 1});
-      ++seg;
-    } else if (l == 0 || wide[l - 1]) {
-      w.segments.push_back({false, l, l + 1});
-      ++seg;
-    } else {
-      w.segments.back().l1 = l + 1;
-    }
-    seg_of_level[l] = seg;
+  for (int s = 0; s < nsub; ++s) {
+    if (h.sl_wide[s] || s == 0 || h.sl_wide[s - 1]) ++seg;
+    seg_of[s] = seg;
   }
-  for (int l = 0; l < nlev; ++l) {
-    int64_t q = lvl_nz[l];
-    const int kend = lvl_ptr[l + 1];
-    for (int k = lvl_ptr[l]; k < kend; ++k) {
-      const int64_t i = rows[k];
-      row_off[k] = int32_t(q - lvl_nz[l]);
-      for (int64_t p = q_begin(i); p < q_end(i); ++p, ++q) {
+  std::vector<int32_t> sub_of_pos(h.npos + 4, -1);
+  for (int s = 0; s < nsub; ++s)
+    for (int t = 0; t < h.sl_nr[s]; ++t) sub_of_pos[h.sl_k[s] + t] = s;
+  h.rows.assign(h.npos + 4, -1);
+  h.off.assign(h.npos + 4, 0);
+  h.dfrom.assign(h.npos + 4, -1);
+  const int64_t total = h.sl_q.back() + 8;
+  h.from.assign(total, -1);
+  h.src.assign(total, 0);
+  // rows by position, then the packed operands of each sub-level in row order
+  for (int64_t i = 0; i < n; ++i) h.rows[h.pos[i]] = int32_t(i);
+  for (int s = 0; s < nsub; ++s) {
+    int64_t qq = h.sl_q[s];
+    const int64_t kend = h.sl_k[s] + h.sl_nr[s];
+    for (int t = 0; t < h.sl_nr[s]; ++t) {
+      const int64_t kp = h.sl_k[s] + t;
+      const int32_t i = h.rows[kp];
+      h.off[kp] = int32_t(qq - h.sl_q[s]);
+      h.dfrom[kp] = diag[i];
+      for (int64_t p = q_begin(i); p < q_end(i); ++p, ++qq) {
         const int32_t j = cols[p];
-        from[q] = p;
-        const int lj = lvl[j];
-        // ring slot only inside the same walked segment and close enough
-        // that no row of this level can overwrite it (kRing positions)
-        const bool in_ring = !wide[l] && seg_of_level[lj] == seg_of_level[l] &&
-                             int64_t(kend) - int64_t(pos[j]) <= kRing;
-        src[q] = in_ring ? (pos[j] & (kRing - 1)) : -(j + 1);
+        h.from[qq] = p;
+        const int sj = sub_of_pos[h.pos[j]];
+        const bool in_ring = !h.sl_wide[s] && seg_of[sj] == seg_of[s] &&
+                             kend - int64_t(h.pos[j]) <= kRing;
+        h.src[qq] = in_ring ? (h.pos[j] & (kRing - 1)) : -(j + 1);
       }
     }
   }
-  if (getenv("PSCU_DEBUG")) {
-    int64_t ring_hits = 0, far = 0, maxr = 0, maxq = 0;
-    for (int64_t q = 0; q < lvl_nz[nlev]; ++q)
-      if (from[q] >= 0) (src[q] >= 0 ? ring_hits : far)++;
-    for (int l = 0; l < nlev; ++l) {
-      maxr = std::max<int64_t>(maxr, lvl_ptr[l + 1] - lvl_ptr[l]);
-      maxq = std::max<int64_t>(maxq, lvl_nzcnt[l]);
-    }
-    int nwide = 0, nstaged = 0;
-    for (const auto& sg : w.segments) nwide += sg.wide;
-    for (int l = 0; l < nlev; ++l) nstaged += mode[l] == 0;
-    fprintf(stderr,
-            "[walk %s] n=%lld levels=%d (staged %d) segments=%zu (wide %d) max_rows=%lld "
-            "max_nz=%lld ring=%lld far=%lld\n",
-            fwd ? "fwd" : "bwd", (long long)n, nlev, nstaged, w.segments.size(), nwide, (long long)maxr,
-            (long long)maxq, (long long)ring_hits, (long long)far);
-  }
-  std::vector<int64_t> dfrom(n);
-  for (int k = 0; k < n; ++k) dfrom[k] = diag[rows[k]];
+  return h;
+}
+
+void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   cudaStream_t st = c.stream;
-  w.nlev = nlev;
-  w.mode.upload(mode, st);
-  w.lvl_ptr.upload(lvl_ptr, st);
-  w.lvl_nz.upload(lvl_nz, st);
-  w.rows.upload(rows, st);
-  w.row_off.upload(row_off, st);
-  w.src.upload(src, st);
-  w.from.upload(from, st);
-  w.val.alloc(total);
+  w.fwd = fwd;
+  w.nsub = int(h.sl_k.size());
+  w.npos = h.npos;
+  w.segments.clear();
+  for (int s = 0; s < w.nsub; ++s) {
+    if (h.sl_wide[s]) w.segments.push_back({true, s, s + 1});
+    else if (s == 0 || h.sl_wide[s - 1]) w.segments.push_back({false, s, s + 1});
+    else w.segments.back().s1 = s + 1;
+  }
+  w.sl_k.upload(h.sl_k, st);
+  w.sl_nr.upload(h.sl_nr, st);
+  w.sl_q.upload(h.sl_q, st);
+  w.sl_nq.upload(h.sl_nq, st);
+  w.rows.upload(h.rows, st);
+  w.off.upload(h.off, st);
+  w.src.upload(h.src, st);
+  w.from.upload(h.from, st);
+  w.val.alloc(h.from.size());
   if (!fwd) {
-    w.div_from.upload(dfrom, st);
-    w.div.alloc(n);
+    w.dfrom.upload(h.dfrom, st);
+    w.dv.alloc(h.dfrom.size());
   } else {
-    w.div.alloc(1);
+    w.dv.alloc(4);
+  }
+}
+
+} // namespace
+
+void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, WalkPlan& wf,
+                WalkPlan& wb) {
+  if (a.n == 0) return;
+  const HostPlan hf = plan_sweep(a, diag, true);
+  const HostPlan hb = plan_sweep(a, diag, false);
+  upload_plan(c, hf, true, wf);
+  upload_plan(c, hb, false, wb);
+  // forward results are written straight into backward position order
+  std::vector<int32_t> opos(hf.rows.size(), 0);
+  for (size_t k = 0; k < hf.rows.size(); ++k)
+    if (hf.rows[k] >= 0) opos[k] = hb.pos[hf.rows[k]];
+  wf.opos.upload(opos, c.stream);
+  wb.opos.alloc(4);
+  wf.scratch.alloc(size_t(hf.npos) + 8);  // rhs in forward position order
+  wb.scratch.alloc(size_t(hb.npos) + 8);  // forward result in backward position order
+  PSCU_CUDA(cudaMemsetAsync(wb.scratch.p, 0, sizeof(double) * (hb.npos + 8), c.stream));
+  if (getenv("PSCU_DEBUG")) {
+    for (const HostPlan* h : {&hf, &hb}) {
+      int64_t ring = 0, far = 0;
+      for (size_t q = 0; q < h->from.size(); ++q)
+        if (h->from[q] >= 0) (h->src[q] >= 0 ? ring : far)++;
+      int nw = 0;
+      for (auto x : h->sl_wide) nw += x;
+      fprintf(stderr, "[walk %s] n=%lld sublevels=%zu (wide %d) positions=%lld ring=%lld far=%lld\n",
+              h == &hf ? "fwd" : "bwd", (long long)a.n, h->sl_k.size(), nw, (long long)h->npos,
+              (long long)ring, (long long)far);
+    }
   }
 }
 
 void pack_walk(Context& c, const double* lu, WalkPlan& w) {
-  if (w.val.n == 0) return;
   const int64_t m = int64_t(w.val.n);
-  gather_vals<<<unsigned(std::min<int64_t>((m + 255) / 256, 148 * 32)), 256, 0, c.stream>>>(
-      m, w.from.p, lu, w.val.p);
-  PSCU_LAUNCHED(&c);
+  if (m) {
+    gather_vals<<<grid1(m), 256, 0, c.stream>>>(m, w.from.p, lu, w.val.p);
+    PSCU_LAUNCHED(&c);
+  }
   if (!w.fwd) {
-    const int64_t nd = int64_t(w.div.n);
-    gather_vals<<<unsigned(std::min<int64_t>((nd + 255) / 256, 148 * 32)), 256, 0, c.stream>>>(
-        nd, w.div_from.p, lu, w.div.p);
+    const int64_t nd = int64_t(w.dv.n);
+    gather_vals<<<grid1(nd), 256, 0, c.stream>>>(nd, w.dfrom.p, lu, w.dv.p);
     PSCU_LAUNCHED(&c);
   }
 }
 
-void run_walk(Context& c, const WalkPlan& w, const double* xin, double* y) {
+static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y, double* yb) {
   static bool attr = false;
   if (!attr) {
     PSCU_CUDA(cudaFuncSetAttribute(walk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -347,14 +381,25 @@ void run_walk(Context& c, const WalkPlan& w, const double* xin, double* y) {
   const WalkArgs a = args_of(w);
   for (const WalkSeg& s : w.segments) {
     if (s.wide) {
-      if (w.fwd) wide_kernel<true><<<148 * 8, 256, 0, c.stream>>>(a, s.l0, xin, y);
-      else wide_kernel<false><<<148 * 8, 256, 0, c.stream>>>(a, s.l0, xin, y);
+      if (w.fwd) wide_kernel<true><<<148 * 4, 256, 0, c.stream>>>(a, s.s0, rhs, y, yb);
+      else wide_kernel<false><<<148 * 4, 256, 0, c.stream>>>(a, s.s0, rhs, y, yb);
     } else {
-      if (w.fwd) walk_kernel<true><<<1, kWalkThreads, walk_smem(), c.stream>>>(a, s.l0, s.l1, xin, y);
-      else walk_kernel<false><<<1, kWalkThreads, walk_smem(), c.stream>>>(a, s.l0, s.l1, xin, y);
+      if (w.fwd)
+        walk_kernel<true><<<1, kWalkThreads, walk_smem(), c.stream>>>(a, s.s0, s.s1, rhs, y, yb);
+      else
+        walk_kernel<false><<<1, kWalkThreads, walk_smem(), c.stream>>>(a, s.s0, s.s1, rhs, y, yb);
     }
     PSCU_LAUNCHED(&c);
   }
+}
+
+void run_walk(Context& c, const WalkPlan& wf, const WalkPlan& wb, const double* x, double* y) {
+  // rhs into forward position order, forward sweep (also scattering its
+  // result into backward position order), backward sweep in place on y
+  gather_rhs<<<grid1(wf.npos), 256, 0, c.stream>>>(wf.npos, wf.rows.p, x, wf.scratch.p);
+  PSCU_LAUNCHED(&c);
+  run_one(c, wf, wf.scratch.p, y, wb.scratch.p);
+  run_one(c, wb, wb.scratch.p, y, nullptr);
 }
 
 } // namespace pscu

@@ -7,10 +7,12 @@
 
 namespace pscu {
 
-void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, bool fwd, WalkPlan& w);
+/// Builds the forward and backward plans of an ILU(0) factor's pattern.
+void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, WalkPlan& wf,
+                WalkPlan& wb);
 /// Gathers the factor values into the packed order (after every refactor).
 void pack_walk(Context& c, const double* lu, WalkPlan& w);
-/// Forward: y = L^-1 x (unit L). Backward: y = U^-1 xin (in place allowed).
-void run_walk(Context& c, const WalkPlan& w, const double* xin, double* y);
+/// y = (LU)^-1 x; x may alias y.
+void run_walk(Context& c, const WalkPlan& wf, const WalkPlan& wb, const double* x, double* y);
 
 } // namespace pscu
