@@ -55,16 +55,6 @@ struct WalkArgs {
   const double* dv;       // backward: diagonal per position
 };
 
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  const unsigned s = unsigned(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = unsigned(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-
 struct alignas(16) Stage {
   double val[kMaxNz];
   int32_t src[kMaxNz];
@@ -73,49 +63,80 @@ struct alignas(16) Stage {
   int32_t row[kStageRows];
   int32_t opos[kStageRows];
   int32_t off[kStageRows + 4];
+  int32_t nq[4];  // real entry count of the sub-level (end of its last row)
 };
 
-/// Issues the asynchronous copies of sub-level s into `st` (static addresses).
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return unsigned(__cvta_generic_to_shared(p));
+}
+
+/// One TMA bulk copy global -> shared completing on mbarrier `bar`.
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  if (bytes == 0) return;
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+/// Thread 0: stages sub-level s into `st` with one bulk copy per operand
+/// array (all addresses static and 16-byte aligned).
 template <bool kFwd>
-__device__ void stage(const WalkArgs& a, int s, Stage& st, const double* rhs) {
+__device__ void issue(const WalkArgs& a, int s, Stage& st, uint64_t* bar, const double* rhs) {
   const int k0 = a.sl_k[s], nr = a.sl_nr[s];
-  const int nr4 = (nr + 3) & ~3;
+  const unsigned nr4 = unsigned((nr + 3) & ~3);
   const int64_t q0 = a.sl_q[s];
-  const int nq = int(a.sl_q[s + 1] - q0);
-  const int t = threadIdx.x, T = blockDim.x;
-  for (int c = t; c * 2 < nq; c += T) cp_async16(&st.val[2 * c], a.val + q0 + 2 * c);
-  for (int c = t; c * 4 < nq; c += T) cp_async16(&st.src[4 * c], a.src + q0 + 4 * c);
-  for (int c = t; c * 2 < nr4; c += T) cp_async16(&st.rhs[2 * c], rhs + k0 + 2 * c);
-  for (int c = t; c * 4 < nr4; c += T) {
-    cp_async16(&st.row[4 * c], a.rows + k0 + 4 * c);
-    cp_async16(&st.off[4 * c], a.off + k0 + 4 * c);
-    if (kFwd) cp_async16(&st.opos[4 * c], a.opos + k0 + 4 * c);
-  }
-  if (!kFwd)
-    for (int c = t; c * 2 < nr4; c += T) cp_async16(&st.dv[2 * c], a.dv + k0 + 2 * c);
-  if (t == 0) cp_async4(&st.off[nr], a.sl_nq + s);
+  const unsigned nq = unsigned(a.sl_q[s + 1] - q0);
+  const unsigned bytes = nq * 12u + nr4 * (8u + 4u + 4u) + (kFwd ? nr4 * 4u : nr4 * 8u) + 16u;
+  // order this thread's view of the slot (read by the CTA through the
+  // generic proxy before the last barrier) before the async-proxy writes
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+  bulk_copy(st.val, a.val + q0, nq * 8u, bar);
+  bulk_copy(st.src, a.src + q0, nq * 4u, bar);
+  bulk_copy(st.rhs, rhs + k0, nr4 * 8u, bar);
+  bulk_copy(st.row, a.rows + k0, nr4 * 4u, bar);
+  bulk_copy(st.off, a.off + k0, nr4 * 4u, bar);
+  if (kFwd) bulk_copy(st.opos, a.opos + k0, nr4 * 4u, bar);
+  else bulk_copy(st.dv, a.dv + k0, nr4 * 8u, bar);
+  bulk_copy(st.nq, a.sl_nq + 4 * s, 16u, bar);
 }
 
 template <bool kFwd>
 __global__ void __launch_bounds__(kWalkThreads, 1)
     walk_kernel(WalkArgs a, int s0, int s1, const double* rhs, double* y, double* yb) {
   extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t bars[kStages];
   double* ring = reinterpret_cast<double*>(smraw);
   Stage* stages = reinterpret_cast<Stage*>(smraw + sizeof(double) * kRing);
-  for (int d = 0; d < kAhead; ++d) {
-    if (s0 + d < s1) stage<kFwd>(a, s0 + d, stages[d], rhs);
-    cp_commit();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[i])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int d = 0; d < kStages && s0 + d < s1; ++d) issue<kFwd>(a, s0 + d, stages[d], &bars[d], rhs);
   }
-  asm volatile("cp.async.wait_group %0;" ::"n"(kAhead - 1) : "memory");
   __syncthreads();
   for (int s = s0; s < s1; ++s) {
     const int r = s - s0;
-    if (s + kAhead < s1) stage<kFwd>(a, s + kAhead, stages[(r + kAhead) % kStages], rhs);
-    cp_commit();
-    const Stage& st = stages[r % kStages];
+    const int slot = r % kStages;
+    const Stage& st = stages[slot];
+    mbar_wait(&bars[slot], unsigned((r / kStages) & 1));
     const int k0 = a.sl_k[s], nr = a.sl_nr[s];
     for (int t = threadIdx.x; t < nr; t += blockDim.x) {
-      const int qa = st.off[t], qb = st.off[t + 1];
+      const int qa = st.off[t], qb = t + 1 < nr ? st.off[t + 1] : st.nq[0];
       double acc = st.rhs[t];
 #pragma unroll 4
       for (int q = qa; q < qb; ++q) {
@@ -128,9 +149,9 @@ __global__ void __launch_bounds__(kWalkThreads, 1)
       y[st.row[t]] = acc;
       if (kFwd) yb[st.opos[t]] = acc;
     }
-    // everything but the newest kAhead-1 groups landed: sub-level s+1 is in
-    asm volatile("cp.async.wait_group %0;" ::"n"(kAhead - 1) : "memory");
-    __syncthreads();
+    __syncthreads();  // slot consumed, ring entries of s visible
+    if (threadIdx.x == 0 && s + kStages < s1)
+      issue<kFwd>(a, s + kStages, stages[slot], &bars[slot], rhs);
   }
 }
 
@@ -139,7 +160,7 @@ template <bool kFwd>
 __global__ void wide_kernel(WalkArgs a, int s, const double* rhs, double* y, double* yb) {
   const int k0 = a.sl_k[s], nr = a.sl_nr[s];
   const int64_t q0 = a.sl_q[s];
-  const int nq = a.sl_nq[s];
+  const int nq = a.sl_nq[4 * s];
   for (int t = int(blockIdx.x * blockDim.x + threadIdx.x); t < nr; t += gridDim.x * blockDim.x) {
     const int k = k0 + t;
     const int64_t qa = q0 + a.off[k];
@@ -310,7 +331,11 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   w.sl_k.upload(h.sl_k, st);
   w.sl_nr.upload(h.sl_nr, st);
   w.sl_q.upload(h.sl_q, st);
-  w.sl_nq.upload(h.sl_nq, st);
+  {
+    std::vector<int32_t> nq4(size_t(w.nsub) * 4, 0);  // stride 4: one 16-byte bulk copy each
+    for (int s = 0; s < w.nsub; ++s) nq4[size_t(s) * 4] = h.sl_nq[s];
+    w.sl_nq.upload(nq4, st);
+  }
   w.rows.upload(h.rows, st);
   w.off.upload(h.off, st);
   w.src.upload(h.src, st);

@@ -16,7 +16,8 @@ t = time.perf_counter()
 h = S.LevelHierarchy(A, loc.layout(), S.LevelConfig(degrees=[3, 2, 1, 0], coarse="gmres-ilu"))
 print(f"hierarchy setup {time.perf_counter()-t:.3f} s", flush=True)
 lib = ctx.lib
-for l in range(4):
+levels = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else range(4)
+for l in levels:
     ilu = h.level_ilu(l)
     m = h.level_matrix(l)
     x = torch.randn(m.n, dtype=torch.float64, device="cuda")
