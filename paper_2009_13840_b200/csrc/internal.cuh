@@ -115,8 +115,8 @@ struct WalkPlan {
   int nsub = 0;
   int64_t npos = 0;
   std::vector<WalkSeg> segments;
-  DevBuf<int32_t> sl_k, sl_nr, sl_nq, rows, off, opos, src;
-  DevBuf<int64_t> sl_q, from, dfrom;
+  DevBuf<int32_t> sl_k, sl_nr, sl_hdr, rows, off, opos, src, far;
+  DevBuf<int64_t> sl_q, sl_f, from, dfrom;
   DevBuf<double> val, dv;
   mutable DevBuf<double> scratch;  // per-apply right-hand sides in position order
 };

@@ -35,24 +35,28 @@ namespace pscu {
 namespace {
 
 constexpr int kWalkThreads = 512;
+constexpr int kProducers = 256;    // two producer warps per stage slot (TMA issue + far gathers)
 constexpr int kStageRows = 512;   // rows of a sub-level
 constexpr int kMaxNz = 2560;      // factor entries of a sub-level (multiple of 4)
 constexpr int kAhead = 3;         // sub-levels staged ahead
 constexpr int kStages = kAhead + 1;
 constexpr int kRing = 4096;       // shared-memory solution ring (positions, power of 2)
+constexpr int kMaxFar = 512;      // sources outside the ring, per sub-level
 constexpr int kWideRows = 4096;   // levels with more rows run row-parallel
 
 struct WalkArgs {
   const int32_t* sl_k;    // sub-level start position (multiple of 4)
   const int32_t* sl_nr;   // rows of the sub-level
   const int64_t* sl_q;    // packed entry start (multiple of 4), nsub + 1
-  const int32_t* sl_nq;   // real packed entries of the sub-level
+  const int32_t* sl_hdr;  // per sub-level {k0, rows, real entries, any global source}
   const int32_t* rows;    // row id per position (-1 padding)
   const int32_t* off;     // packed offset of a row within its sub-level
   const int32_t* opos;    // forward: backward position of the row
   const double* val;      // packed factor values
   const int32_t* src;     // >= 0 ring slot, < 0: -(row)-1 global source
   const double* dv;       // backward: diagonal per position
+  const int64_t* sl_f;    // far-source list start per sub-level (nsub + 1)
+  const int32_t* far;     // far source rows, per sub-level
 };
 
 struct alignas(16) Stage {
@@ -63,7 +67,8 @@ struct alignas(16) Stage {
   int32_t row[kStageRows];
   int32_t opos[kStageRows];
   int32_t off[kStageRows + 4];
-  int32_t nq[4];  // real entry count of the sub-level (end of its last row)
+  int32_t hdr[4];  // k0, rows, real entries (end of the last row), far sources
+  double farv[kMaxFar];  // values of the sources outside the ring (gathered)
 };
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
@@ -90,8 +95,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
-/// Thread 0: stages sub-level s into `st` with one bulk copy per operand
-/// array (all addresses static and 16-byte aligned).
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+/// Producer lane: stages sub-level s into `st` with one bulk copy per
+/// operand array (all addresses static and 16-byte aligned).
 template <bool kFwd>
 __device__ void issue(const WalkArgs& a, int s, Stage& st, uint64_t* bar, const double* rhs) {
   const int k0 = a.sl_k[s], nr = a.sl_nr[s];
@@ -99,12 +108,11 @@ __device__ void issue(const WalkArgs& a, int s, Stage& st, uint64_t* bar, const 
   const int64_t q0 = a.sl_q[s];
   const unsigned nq = unsigned(a.sl_q[s + 1] - q0);
   const unsigned bytes = nq * 12u + nr4 * (8u + 4u + 4u) + (kFwd ? nr4 * 4u : nr4 * 8u) + 16u;
-  // order this thread's view of the slot (read by the CTA through the
-  // generic proxy before the last barrier) before the async-proxy writes
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
                "r"(bytes)
                : "memory");
+  bulk_copy(st.hdr, a.sl_hdr + 4 * s, 16u, bar);
   bulk_copy(st.val, a.val + q0, nq * 8u, bar);
   bulk_copy(st.src, a.src + q0, nq * 4u, bar);
   bulk_copy(st.rhs, rhs + k0, nr4 * 8u, bar);
@@ -112,46 +120,96 @@ __device__ void issue(const WalkArgs& a, int s, Stage& st, uint64_t* bar, const 
   bulk_copy(st.off, a.off + k0, nr4 * 4u, bar);
   if (kFwd) bulk_copy(st.opos, a.opos + k0, nr4 * 4u, bar);
   else bulk_copy(st.dv, a.dv + k0, nr4 * 8u, bar);
-  bulk_copy(st.nq, a.sl_nq + 4 * s, 16u, bar);
 }
 
+template <bool kFwd, bool kAnyFar>
+__device__ __forceinline__ void walk_rows(const Stage& st, double* ring, double* y, double* yb) {
+  const int k0 = st.hdr[0], nr = st.hdr[1];
+  for (int t = threadIdx.x; t < nr; t += kWalkThreads) {
+    const int qa = st.off[t], qb = t + 1 < nr ? st.off[t + 1] : st.hdr[2];
+    double acc = st.rhs[t];
+#pragma unroll 4
+    for (int q = qa; q < qb; ++q) {
+      const int sv = st.src[q];
+      double yv;
+      if (kAnyFar) yv = sv >= 0 ? ring[sv] : st.farv[-sv - 1];
+      else yv = ring[sv];
+      acc = dsub(acc, dmul(st.val[q], yv));
+    }
+    if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
+    ring[(k0 + t) & (kRing - 1)] = acc;
+    y[st.row[t]] = acc;
+    if (kFwd) yb[st.opos[t]] = acc;
+  }
+}
+
+/// Warp-specialised walker: kWalkThreads consumer threads compute one
+/// sub-level after another (one named barrier per sub-level); one extra
+/// producer warp keeps kStages sub-levels in flight with TMA bulk copies,
+/// reusing a slot once the consumers have released it.
 template <bool kFwd>
-__global__ void __launch_bounds__(kWalkThreads, 1)
-    walk_kernel(WalkArgs a, int s0, int s1, const double* rhs, double* y, double* yb) {
+__global__ void __launch_bounds__(kWalkThreads + kProducers, 1)
+    walk_kernel(WalkArgs a, int s0, int s1, const double* rhs, double* y, double* yb,
+                int experiment) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ __align__(8) uint64_t bars[kStages];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   double* ring = reinterpret_cast<double*>(smraw);
   Stage* stages = reinterpret_cast<Stage*>(smraw + sizeof(double) * kRing);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bars[i])) : "memory");
+    for (int i = 0; i < kStages; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_addr(&full[i])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&empty[i])) : "memory");
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int d = 0; d < kStages && s0 + d < s1; ++d) issue<kFwd>(a, s0 + d, stages[d], &bars[d], rhs);
   }
   __syncthreads();
-  for (int s = s0; s < s1; ++s) {
-    const int r = s - s0;
-    const int slot = r % kStages;
-    const Stage& st = stages[slot];
-    mbar_wait(&bars[slot], unsigned((r / kStages) & 1));
-    const int k0 = a.sl_k[s], nr = a.sl_nr[s];
-    for (int t = threadIdx.x; t < nr; t += blockDim.x) {
-      const int qa = st.off[t], qb = t + 1 < nr ? st.off[t + 1] : st.nq[0];
-      double acc = st.rhs[t];
-#pragma unroll 4
-      for (int q = qa; q < qb; ++q) {
-        const int sv = st.src[q];
-        const double yv = sv >= 0 ? ring[sv] : __ldcg(y + (-sv - 1));
-        acc = dsub(acc, dmul(st.val[q], yv));
+  if (threadIdx.x >= kWalkThreads) {
+    // producer warps: thread 0 of them issues the bulk copies; all of them
+    // gather the sources outside the ring (final: they lie >= kRing
+    // positions, hence >= kStages sub-levels, back, or in an earlier launch)
+    // with several independent loads in flight per lane, then one of them
+    // makes the second arrival on the slot's full barrier
+    // producer warp pair w owns slot w: sub-levels s0 + w, s0 + w + kStages, ...
+    const int pw = (threadIdx.x - kWalkThreads) >> 6, lane = (threadIdx.x - kWalkThreads) & 63;
+    const int slot = pw;
+    for (int s = s0 + pw; s < s1; s += kStages) {
+      const int r = s - s0;
+      if (r >= kStages) mbar_wait(&empty[slot], unsigned((r / kStages - 1) & 1));
+      if (lane == 0) issue<kFwd>(a, s, stages[slot], &full[slot], rhs);
+      const int64_t f0 = a.sl_f[s], nf = a.sl_f[s + 1] - f0;
+      double* fv = stages[slot].farv;
+      for (int64_t base = 0; base < nf; base += 8 * 64) {
+        int32_t idx[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t f = base + u * 64 + lane;
+          idx[u] = f < nf ? __ldg(a.far + f0 + f) : -1;
+        }
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = idx[u] >= 0 ? __ldcg(y + idx[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t f = base + u * 64 + lane;
+          if (f < nf) fv[f] = v[u];
+        }
       }
-      if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
-      ring[(k0 + t) & (kRing - 1)] = acc;
-      y[st.row[t]] = acc;
-      if (kFwd) yb[st.opos[t]] = acc;
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + pw) : "memory");
+      if (lane == 0) mbar_arrive(&full[slot]);
     }
-    __syncthreads();  // slot consumed, ring entries of s visible
-    if (threadIdx.x == 0 && s + kStages < s1)
-      issue<kFwd>(a, s + kStages, stages[slot], &bars[slot], rhs);
+    return;
+  }
+  for (int s = s0; s < s1; ++s) {
+    const int r = s - s0, slot = r % kStages;
+    const Stage& st = stages[slot];
+    mbar_wait(&full[slot], unsigned((r / kStages) & 1));
+    if (experiment != 1) {
+      if (st.hdr[3]) walk_rows<kFwd, true>(st, ring, y, yb);
+      else walk_rows<kFwd, false>(st, ring, y, yb);
+    }
+    // consumers only: the slot is free and the ring entries of s visible
+    asm volatile("bar.sync 1, %0;" ::"n"(kWalkThreads) : "memory");
+    if (threadIdx.x == 0) mbar_arrive(&empty[slot]);
   }
 }
 
@@ -160,7 +218,7 @@ template <bool kFwd>
 __global__ void wide_kernel(WalkArgs a, int s, const double* rhs, double* y, double* yb) {
   const int k0 = a.sl_k[s], nr = a.sl_nr[s];
   const int64_t q0 = a.sl_q[s];
-  const int nq = a.sl_nq[4 * s];
+  const int nq = a.sl_hdr[4 * s + 2];
   for (int t = int(blockIdx.x * blockDim.x + threadIdx.x); t < nr; t += gridDim.x * blockDim.x) {
     const int k = k0 + t;
     const int64_t qa = q0 + a.off[k];
@@ -193,8 +251,8 @@ __global__ void gather_vals(int64_t m, const int64_t* __restrict__ from,
 }
 
 WalkArgs args_of(const WalkPlan& w) {
-  return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_nq.p, w.rows.p, w.off.p,
-          w.opos.p, w.val.p,  w.src.p,  w.dv.p};
+  return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_hdr.p, w.rows.p, w.off.p,
+          w.opos.p, w.val.p,  w.src.p,  w.dv.p,  w.sl_f.p, w.far.p};
 }
 
 size_t walk_smem() { return sizeof(double) * kRing + kStages * sizeof(Stage); }
@@ -224,7 +282,8 @@ std::vector<int32_t> dag_levels(const Csr& a, const std::vector<int64_t>& diag, 
 }
 
 struct HostPlan {
-  std::vector<int32_t> sl_k, sl_nr, sl_nq, rows, off, src, pos;
+  std::vector<int32_t> sl_k, sl_nr, sl_nq, sl_nfar, rows, off, src, pos, far;
+  std::vector<int64_t> sl_f;
   std::vector<int64_t> sl_q, from, dfrom;
   std::vector<uint8_t> sl_wide;
   int64_t npos = 0;
@@ -252,6 +311,9 @@ HostPlan plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
   HostPlan h;
   h.pos.assign(n, -1);
   int64_t k = 0, q = 0;
+  int64_t seg_start = 0;      // first position of the current walker segment
+  std::vector<int32_t> far_mark(n, -1);
+  int cur_far = 0;
   auto open_sub = [&](bool wide) {
     k = (k + 3) & ~int64_t(3);
     q = (q + 3) & ~int64_t(3);
@@ -260,15 +322,41 @@ HostPlan plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
     h.sl_q.push_back(q);
     h.sl_nq.push_back(0);
     h.sl_wide.push_back(wide ? 1 : 0);
+    cur_far = 0;
   };
+  // a source is served by the ring when it lies in the same walker segment
+  // within kRing positions of the sub-level's largest possible end
+  auto ring_ok = [&](int64_t k0, int32_t j) {
+    return h.pos[j] >= seg_start && k0 + kStageRows + 3 - int64_t(h.pos[j]) <= kRing;
+  };
+  bool prev_wide = true;
   for (int l = 0; l < nlev; ++l) {
     const int nrl = lvl_ptr[l + 1] - lvl_ptr[l];
     const bool wide = nrl > kWideRows;
     open_sub(wide);
+    if (!wide && prev_wide) seg_start = h.sl_k.back();
+    prev_wide = wide;
     for (int j = lvl_ptr[l]; j < lvl_ptr[l + 1]; ++j) {
       const int32_t i = order[j];
       const int64_t nz = q_end(i) - q_begin(i);
-      if (!wide && (h.sl_nr.back() == kStageRows || h.sl_nq.back() + nz > kMaxNz - 4)) open_sub(false);
+      int nfar = 0;
+      if (!wide) {
+        const int sid = int(h.sl_k.size()) - 1;
+        for (int64_t p = q_begin(i); p < q_end(i); ++p)
+          if (!ring_ok(h.sl_k.back(), cols[p]) && far_mark[cols[p]] != sid) ++nfar;
+        if (h.sl_nr.back() == kStageRows || h.sl_nq.back() + nz > kMaxNz - 4 ||
+            cur_far + nfar > kMaxFar) {
+          open_sub(false);
+          const int sid2 = int(h.sl_k.size()) - 1;
+          nfar = 0;
+          for (int64_t p = q_begin(i); p < q_end(i); ++p)
+            if (!ring_ok(h.sl_k.back(), cols[p]) && far_mark[cols[p]] != sid2) ++nfar;
+        }
+        const int sid3 = int(h.sl_k.size()) - 1;
+        for (int64_t p = q_begin(i); p < q_end(i); ++p)
+          if (!ring_ok(h.sl_k.back(), cols[p])) far_mark[cols[p]] = sid3;
+        cur_far += nfar;
+      }
       h.pos[i] = int32_t(k++);
       h.sl_nr.back()++;
       h.sl_nq.back() += int32_t(nz);
@@ -296,9 +384,12 @@ HostPlan plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
   h.src.assign(total, 0);
   // rows by position, then the packed operands of each sub-level in row order
   for (int64_t i = 0; i < n; ++i) h.rows[h.pos[i]] = int32_t(i);
+  std::vector<int32_t> far_idx(n, -1), far_sub(n, -1);
+  h.sl_f.assign(nsub + 1, 0);
   for (int s = 0; s < nsub; ++s) {
     int64_t qq = h.sl_q[s];
-    const int64_t kend = h.sl_k[s] + h.sl_nr[s];
+    const int64_t kcons = h.sl_k[s] + kStageRows + 3;
+    int nf = 0;
     for (int t = 0; t < h.sl_nr[s]; ++t) {
       const int64_t kp = h.sl_k[s] + t;
       const int32_t i = h.rows[kp];
@@ -307,12 +398,26 @@ HostPlan plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
       for (int64_t p = q_begin(i); p < q_end(i); ++p, ++qq) {
         const int32_t j = cols[p];
         h.from[qq] = p;
+        if (h.sl_wide[s]) {
+          h.src[qq] = -(j + 1);  // wide launches read global memory directly
+          continue;
+        }
         const int sj = sub_of_pos[h.pos[j]];
-        const bool in_ring = !h.sl_wide[s] && seg_of[sj] == seg_of[s] &&
-                             kend - int64_t(h.pos[j]) <= kRing;
-        h.src[qq] = in_ring ? (h.pos[j] & (kRing - 1)) : -(j + 1);
+        const bool in_ring = seg_of[sj] == seg_of[s] && kcons - int64_t(h.pos[j]) <= kRing;
+        if (in_ring) {
+          h.src[qq] = h.pos[j] & (kRing - 1);
+        } else {
+          if (far_sub[j] != s) {
+            far_sub[j] = s;
+            far_idx[j] = nf++;
+            h.far.push_back(j);
+          }
+          h.src[qq] = -(far_idx[j] + 1);
+        }
       }
     }
+    h.sl_f[s + 1] = h.sl_f[s] + nf;
+    h.sl_nfar.push_back(nf);
   }
   return h;
 }
@@ -330,11 +435,20 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   }
   w.sl_k.upload(h.sl_k, st);
   w.sl_nr.upload(h.sl_nr, st);
+  w.sl_f.upload(h.sl_f, st);
+  if (h.far.empty()) w.far.alloc(4);
+  else w.far.upload(h.far, st);
   w.sl_q.upload(h.sl_q, st);
   {
-    std::vector<int32_t> nq4(size_t(w.nsub) * 4, 0);  // stride 4: one 16-byte bulk copy each
-    for (int s = 0; s < w.nsub; ++s) nq4[size_t(s) * 4] = h.sl_nq[s];
-    w.sl_nq.upload(nq4, st);
+    // {k0, rows, real entries, any global source}: one 16-byte bulk copy each
+    std::vector<int32_t> hdr(size_t(w.nsub) * 4, 0);
+    for (int s = 0; s < w.nsub; ++s) {
+      hdr[size_t(s) * 4] = h.sl_k[s];
+      hdr[size_t(s) * 4 + 1] = h.sl_nr[s];
+      hdr[size_t(s) * 4 + 2] = h.sl_nq[s];
+      hdr[size_t(s) * 4 + 3] = h.sl_wide[s] ? 0 : h.sl_nfar[s];
+    }
+    w.sl_hdr.upload(hdr, st);
   }
   w.rows.upload(h.rows, st);
   w.off.upload(h.off, st);
@@ -404,15 +518,16 @@ static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y,
     attr = true;
   }
   const WalkArgs a = args_of(w);
+  static const int experiment = getenv("PSCU_WALK_EXPERIMENT") ? atoi(getenv("PSCU_WALK_EXPERIMENT")) : 0;
   for (const WalkSeg& s : w.segments) {
     if (s.wide) {
       if (w.fwd) wide_kernel<true><<<148 * 4, 256, 0, c.stream>>>(a, s.s0, rhs, y, yb);
       else wide_kernel<false><<<148 * 4, 256, 0, c.stream>>>(a, s.s0, rhs, y, yb);
     } else {
       if (w.fwd)
-        walk_kernel<true><<<1, kWalkThreads, walk_smem(), c.stream>>>(a, s.s0, s.s1, rhs, y, yb);
+        walk_kernel<true><<<1, kWalkThreads + kProducers, walk_smem(), c.stream>>>(a, s.s0, s.s1, rhs, y, yb, experiment);
       else
-        walk_kernel<false><<<1, kWalkThreads, walk_smem(), c.stream>>>(a, s.s0, s.s1, rhs, y, yb);
+        walk_kernel<false><<<1, kWalkThreads + kProducers, walk_smem(), c.stream>>>(a, s.s0, s.s1, rhs, y, yb, experiment);
     }
     PSCU_LAUNCHED(&c);
   }
