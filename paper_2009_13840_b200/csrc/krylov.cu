@@ -264,28 +264,17 @@ __global__ void __launch_bounds__(kStepThreads)
 #pragma unroll
       for (int k = 0; k < kEpt; ++k) pv[k] = iv[k];
     }
-    if (tid < 32) {
-      // warp 0 gathers the G slots (G/32 consecutive per lane when G >= 32)
-      // and rebuilds the adjacent-pair tree with in-lane pairs + shuffles
-      const int per = G >= 32 ? G / 32 : 1;
-      const int nl = G >= 32 ? 32 : G;
+    {
+      // thread k < G acquires slot k (one round trip for all of them) and
+      // the CTA rebuilds the adjacent-pair tree over the G values
       double v = 0.0;
-      if (tid < nl) {
-        double loc[32];
-        for (int q = 0; q < per; ++q) {
-          const int s = tid * per + q;
-          while (ld_acquire_u64(slot_tag + par * G + s) != want) {
-          }
-          loc[q] = __ldcg(slot_v + par * G + s);
+      if (tid < G) {
+        while (ld_acquire_u64(slot_tag + par * G + tid) != want) {
         }
-        for (int width = per; width > 1; width >>= 1)
-          for (int q = 0; q < width / 2; ++q) loc[q] = dadd(loc[2 * q], loc[2 * q + 1]);
-        v = loc[0];
+        v = __ldcg(slot_v + par * G + tid);
       }
-      for (int off = 1; off < nl; off <<= 1) {
-        const double o = __shfl_down_sync(0xffffffffu, v, off);
-        if ((tid & (2 * off - 1)) == 0) v = dadd(v, o);
-      }
+      __syncthreads();  // warp 0 finished reading block_tree's scratch of this pass
+      v = block_tree(v, G);
       if (tid == 0) {
         if (i == j + 1) v = __dsqrt_rn(v);
         hsh = v;
