@@ -212,7 +212,9 @@ constexpr int kEpt = 16;  // elements per lane (repro_lanes guarantees <= 16 up 
 /// so the reduction doubles as the grid-wide barrier without a contended
 /// counter. Slots are double-buffered by pass parity and tags are unique per
 /// launch (tag_base), so nothing is ever reset.
-__global__ void __launch_bounds__(kStepThreads)
+// two CTAs per SM (<= 128 registers) so up to 296 CTAs are co-resident:
+// n = 525k (the 256^2 coarse level) needs T = 65536 lanes = 256 CTAs
+__global__ void __launch_bounds__(kStepThreads, 2)
     arnoldi_step_kernel(int64_t n, int64_t T, int L, int epl, int j, double* __restrict__ wg,
                         double* V, int64_t ldv, double* __restrict__ hcol,
                         double* __restrict__ slot_v, unsigned long long* slot_tag,
@@ -264,9 +266,9 @@ __global__ void __launch_bounds__(kStepThreads)
 #pragma unroll
       for (int k = 0; k < kEpt; ++k) pv[k] = iv[k];
     }
-    {
-      // thread k < G acquires slot k (one round trip for all of them) and
-      // the CTA rebuilds the adjacent-pair tree over the G values
+    if (blockIdx.x == 0) {
+      // root CTA: thread k < G acquires slot k (one round trip), rebuilds
+      // the adjacent-pair tree and publishes the result under one tag
       double v = 0.0;
       if (tid < G) {
         while (ld_acquire_u64(slot_tag + par * G + tid) != want) {
@@ -278,8 +280,14 @@ __global__ void __launch_bounds__(kStepThreads)
       if (tid == 0) {
         if (i == j + 1) v = __dsqrt_rn(v);
         hsh = v;
-        if (blockIdx.x == 0) hcol[i] = v;
+        hcol[i] = v;
+        slot_v[2 * G + par] = v;
+        st_release_u64(slot_tag + 2 * G + par, want);
       }
+    } else if (tid == 0) {
+      // every other CTA polls the single published result
+      while (ld_acquire_u64(slot_tag + 2 * G + par) != want) __nanosleep(20);
+      hsh = __ldcg(slot_v + 2 * G + par);
     }
     __syncthreads();
     hprev = hsh;
