@@ -49,11 +49,7 @@ RTOL = 1e-8
 RESTART = 30
 
 
-def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+from paper_2009_13840_b200.replicas import Replicas, dist_env  # noqa: E402
 
 
 class ClockSampler:
@@ -201,13 +197,9 @@ def run_reference(args, cfg):
 def run_ours(args, cfg):
     ws, rank, local = dist_env()
     import numpy as np
-    import torch
 
-    if ws > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rep_group = Replicas("nccl")
+    barrier, max_over_ranks = rep_group.barrier, rep_group.max_over_ranks
     from paper_2009_13840_b200 import host
     from paper_2009_13840_b200 import solver as S
 
@@ -223,19 +215,6 @@ def run_ours(args, cfg):
     lcfg = S.LevelConfig(degrees=cfg["degrees"], coarse=cfg["coarse"], outer_rtol=RTOL,
                          restart=RESTART)
     dofs = A.n
-
-    def barrier():
-        if ws > 1:
-            import torch.distributed as dist
-            dist.barrier()
-
-    def max_over_ranks(x: float) -> float:
-        if ws == 1:
-            return x
-        import torch.distributed as dist
-        t = torch.tensor([x], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
 
     def step():
         h = S.LevelHierarchy(A, lay, lcfg)
