@@ -15,8 +15,10 @@ the condensed system resident in HBM. value = dofs x n_gpus / step time
 C ABI (pscu_solve_system) from host buffers, copies inside the timed region.
 
 --impl reference times the reference's own solver (oracle/_ref, the
-unmodified headers) on the host cores: every core solves the same bounded
-sample of the workload recipe concurrently.
+unmodified headers) on the host cores: every core (bounded by memory) runs
+the same bounded sample of the workload concurrently — for config 2 the
+recipe at 128x128, one FGMRES iteration per step, extrapolated to the full
+solve as t_setup + its x t_iteration (see reference_timed).
 """
 from __future__ import annotations
 
@@ -34,15 +36,18 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     "config1": dict(tri=False, n=16, jitter=0.0, seed=0, k=1, strategy="v-cond", degrees=[1, 0],
-                    coarse="lu", name="2D unit square 16x16 quads, HHO-dp v-cond, k=1, levels 1-0"),
+                    coarse="lu", name="2D unit square 16x16 quads, HHO-dp v-cond, k=1, levels 1-0",
+                    ref_sample_n=16, outer_its=None),
     "config2a": dict(tri=True, n=256, jitter=0.2, seed=0, k=3, strategy="v-cond",
                      degrees=[3, 2, 1, 0], coarse="gmres-ilu",
                      name="2D unit square 256x256x2 jittered tris (0.2h, seed 0), HHO-dp v-cond, "
-                          "k=3, levels 3-2-1-0"),
+                          "k=3, levels 3-2-1-0",
+                     ref_sample_n=128, outer_its=45),
     "config2b": dict(tri=True, n=256, jitter=0.2, seed=0, k=3, strategy="vp-cond",
                      degrees=[3, 2, 1, 0], coarse="gmres-ilu",
                      name="2D unit square 256x256x2 jittered tris (0.2h, seed 0), HHO-dp vp-cond, "
-                          "k=3, levels 3-2-1-0"),
+                          "k=3, levels 3-2-1-0",
+                     ref_sample_n=128, outer_its=None),
 }
 METRIC = "condensed DoFs/s solved to rtol 1e-8 (FGMRES+p-MG V-cycle)"
 RTOL = 1e-8
@@ -132,59 +137,97 @@ def traffic_record(cls: str):
 # ---------------------------------------------------------------------------
 
 def _ref_worker(args):
-    cfg, n = args
+    """One reference process: assemble the sample (untimed, like the
+    reference's own t_solve), then time hierarchy setup + FGMRES."""
+    cfg, n, mode, rounds, maxit = args
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_ref as O
 
     s = O.RefSystem(mesh="unit-tri" if cfg["tri"] else "unit-quad", n=n, seed=cfg["seed"],
                     jitter=cfg["jitter"], side="top", scheme="hho-dp", strategy=cfg["strategy"],
                     k=cfg["k"], data="sincos")
-    r = s.solve(cfg["degrees"], coarse=cfg["coarse"], rtol=RTOL, restart=RESTART)
-    return s.n, r["t_solve"], r["its"], r["converged"]
+    out = []
+    for _ in range(rounds):
+        t_setup, stamps = s.solve_timed(cfg["degrees"], maxit, coarse=cfg["coarse"], rtol=RTOL,
+                                        restart=RESTART)
+        out.append((t_setup, stamps.tolist()))
+    return s.n, out
 
 
-def reference_sample(cfg: dict, n: int, procs: int, steps: int):
-    """Runs `steps` rounds of `procs` concurrent reference solves of the
-    sample; returns per-round (dofs*procs/t) and the sample description."""
+def _ref_procs(n_cells: int) -> int:
+    """All host cores, bounded by memory (~2 GB per 128^2 k=3 sample)."""
+    procs = os.cpu_count() or 1
+    try:
+        import psutil
+
+        per = max(0.25e9, 2.5e9 * (n_cells / 128.0) ** 2)
+        procs = max(1, min(procs, int(psutil.virtual_memory().available * 0.8 // per)))
+    except Exception:
+        pass
+    return procs
+
+
+def reference_timed(cfg: dict, n: int, procs: int, warmup: int, steps: int):
+    """Reference solver timing on the host cores (oracle/_ref: the unmodified
+    reference headers). `procs` processes each run the same sample.
+
+    full mode (sample == workload size): every step is one complete solve,
+    t_solve = setup + all FGMRES iterations (the reference's own t_solve).
+    sampled mode (sample smaller than the workload): every step is one FGMRES
+    iteration (one V-cycle + Arnoldi step) of the sample; the solve time is
+    t_setup + its * t_iteration with `its` the workload's FGMRES iteration
+    count, i.e. the sample's per-DoF cost of a setup and an iteration applied
+    to the full solve (both scale linearly with the DoFs at fixed levels).
+    Returns (per-step DoF/s values, sample DoFs, description)."""
     import multiprocessing as mp
 
-    ctx = mp.get_context("fork")
-    vals, its = [], None
-    dofs = None
-    with ctx.Pool(procs) as pool:
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            res = pool.map(_ref_worker, [(cfg, n)] * procs)
-            dt = time.perf_counter() - t0
-            dofs = res[0][0]
-            its = res[0][2]
-            # the solves' own t_solve windows exclude their assembly
-            t_solve = max(r[1] for r in res)
-            vals.append(dofs * procs / t_solve)
-            del dt
-    return vals, dofs, its
+    full = n == cfg["n"]
+    if full:
+        job = (cfg, n, "full", warmup + steps, 1000)
+    else:
+        job = (cfg, n, "sampled", 1, warmup + steps)
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_ref_worker, [job] * procs)
+    dofs = res[0][0]
+    vals = []
+    if full:
+        for r in range(warmup + steps):
+            t = max(w[1][r][0] + w[1][r][1][-1] for w in res)  # slowest process
+            vals.append(dofs * procs / t)
+        its = len(res[0][1][0][1])
+        desc = (f"reference solve_system recipe at {n}x{n} ({dofs} DoFs, {its} FGMRES its), "
+                f"{procs} concurrent single-threaded processes, one solve per step")
+        return vals[warmup:], dofs, desc, None
+    its_full = cfg["outer_its"]
+    t_setup = max(w[1][0][0] for w in res)
+    for k in range(warmup, warmup + steps):
+        t_it = max((w[1][0][1][k] - (w[1][0][1][k - 1] if k else 0.0)) for w in res)
+        vals.append(dofs * procs / (t_setup + its_full * t_it))
+    desc = (f"reference hierarchy setup + FGMRES iterations of the recipe at {n}x{n} "
+            f"({dofs} DoFs), {procs} concurrent single-threaded processes; one step = one "
+            f"FGMRES iteration, solve time = t_setup + {its_full} x t_iteration "
+            f"({its_full} = the workload's FGMRES iteration count)")
+    return vals, dofs, desc, t_setup
 
 
 def run_reference(args, cfg):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    procs = os.cpu_count() or 1
-    n = args.cpu_sample_n
-    vals, dofs, its = reference_sample(cfg, n, procs, args.warmup + args.steps)
-    timed = vals[args.warmup:]
-    v = statistics.mean(timed)
+    n = args.ref_sample_n or cfg["ref_sample_n"]
+    procs = _ref_procs(n)
+    vals, dofs, desc, _ = reference_timed(cfg, n, procs, args.warmup, args.steps)
+    v = statistics.mean(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "DoF/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dofs * procs / v, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (manufactured sin/cos field)",
-        "config": {"workload": cfg["name"] + f" [reference sample at {n}x{n}]",
-                   "dofs_per_solve": dofs, "fgmres_its": its, "solver": "reference solve_system",
-                   "parallelism": f"{procs} concurrent single-threaded solves"},
+        "config": {"workload": cfg["name"], "sample": f"{n}x{n}", "sample_dofs": dofs,
+                   "solver": "reference LevelHierarchy + FGMRES(30)",
+                   "parallelism": f"{procs} concurrent single-threaded processes"},
         "cpu_baseline": {"value": v, "unit": "DoF/s", "cores": procs, "kind": "reference",
-                         "sample": f"config recipe at {n}x{n} ({dofs} DoFs): hierarchy setup + "
-                                   f"FGMRES, {procs} concurrent solves"},
+                         "sample": desc},
         "e2e": {"value": v, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -268,11 +311,10 @@ def run_ours(args, cfg):
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
         try:
-            vals, sdofs, sits = reference_sample(cfg, args.cpu_sample_n, 1, 1)
+            sn = args.ref_sample_n or cfg["ref_sample_n"]
+            vals, sdofs, desc, _ = reference_timed(cfg, sn, 1, 0, 1)
             cpu = {"value": vals[0], "unit": "DoF/s", "cores": 1, "kind": "reference",
-                   "sample": f"reference solve_system (oracle/_ref) of the config recipe at "
-                             f"{args.cpu_sample_n}x{args.cpu_sample_n} ({sdofs} DoFs, {sits} "
-                             f"FGMRES its), 1 core"}
+                   "sample": desc}
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "DoF/s", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -325,7 +367,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="config2a", choices=sorted(CONFIGS))
     ap.add_argument("--n", type=int, default=0, help="override the mesh size (testing)")
-    ap.add_argument("--cpu-sample-n", type=int, default=24)
+    ap.add_argument("--ref-sample-n", type=int, default=0,
+                    help="mesh size of the reference / cpu_baseline sample (default per config)")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

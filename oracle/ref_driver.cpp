@@ -420,7 +420,9 @@ void ref_hier_reset(void* h) { static_cast<Hier*>(h)->h->reset_counters(); }
 /// Restart: after `restart` iterations without triggering the convergence
 /// check, x0 <- x_m and the Arnoldi process restarts from b - A x0.
 static KrylovResult fgmres_hist(const ApplyFn& op, const ApplyFn& pc, const Eigen::VectorXd& rhs,
-                                int max_it, double rtol, int restart, std::vector<double>& hist) {
+                                int max_it, double rtol, int restart, std::vector<double>& hist,
+                                std::vector<double>* stamps = nullptr) {
+  const auto t_begin = std::chrono::steady_clock::now();
   KrylovResult res;
   const double bnorm = rhs.norm();
   if (bnorm == 0.0) {
@@ -443,6 +445,9 @@ static KrylovResult fgmres_hist(const ApplyFn& op, const ApplyFn& pc, const Eige
       const double est = ws.step(j, op(ws.z[j]));
       ++total;
       hist.push_back(est / bnorm);
+      if (stamps)
+        stamps->push_back(
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t_begin).count());
       const int m = j + 1;
       const bool last = total == max_it;
       if (est <= rtol * bnorm || ws.last_subdiag == 0.0 || last) {
@@ -508,6 +513,40 @@ int ref_solve(void* sysh, const int* degrees, int nlev, int smoother_iters, int 
     *vcycles = vc;
     *rel = r.rel_residual;
     *converged = r.converged;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+/// Timing sample for bench.py's reference arm: the reference LevelHierarchy
+/// setup (t_setup) and the end time of every FGMRES iteration after it
+/// (stamps[i], seconds from the start of the iteration loop), restart as
+/// given, stopping after `outer_maxit` iterations or on convergence.
+int ref_solve_timed(void* sysh, const int* degrees, int nlev, int smoother_iters, int coarse_kind,
+                    double coarse_rtol, int coarse_maxit, double outer_rtol, int outer_maxit,
+                    int restart, double* t_setup, double* stamps, int* its) {
+  try {
+    const System* s = static_cast<System*>(sysh);
+    LevelConfig cfg;
+    cfg.degrees.assign(degrees, degrees + nlev);
+    cfg.smoother_iters = smoother_iters;
+    cfg.coarse = coarse_kind ? CoarseSolver::IluGmres : CoarseSolver::Lu;
+    cfg.coarse_rtol = coarse_rtol;
+    cfg.coarse_maxit = coarse_maxit;
+    cfg.outer_rtol = outer_rtol;
+    cfg.outer_maxit = outer_maxit;
+    const auto t0 = std::chrono::steady_clock::now();
+    LevelHierarchy hier(s->mesh, s->sys, cfg);
+    *t_setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    ApplyFn op = [s](const Eigen::VectorXd& v) { return s->sys.a.multiply(v); };
+    ApplyFn pc = [&hier](const Eigen::VectorXd& d) { return hier.vcycle(0, d); };
+    std::vector<double> hv, st;
+    const KrylovResult r =
+        fgmres_hist(op, pc, s->sys.rhs, outer_maxit, outer_rtol, restart, hv, &st);
+    for (std::size_t i = 0; i < st.size(); ++i) stamps[i] = st[i];
+    *its = static_cast<int>(st.size());
+    (void)r;
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

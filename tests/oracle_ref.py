@@ -100,6 +100,10 @@ def ref_lib():
                                   C.POINTER(C.c_int), C.POINTER(C.c_longlong), C.POINTER(C.c_int),
                                   C.POINTER(C.c_double), C.POINTER(C.c_int),
                                   C.POINTER(C.c_double)]
+        lib.ref_solve_timed.argtypes = [vp, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_double,
+                                        C.c_int, C.c_double, C.c_int, C.c_int,
+                                        C.POINTER(C.c_double), C.c_void_p, C.POINTER(C.c_int)]
+        lib.ref_solve_timed.restype = C.c_int
         lib.ref_solve_system.argtypes = [vp, _i32p, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
                                          _f64p, C.POINTER(C.c_int), C.POINTER(C.c_longlong),
                                          C.POINTER(C.c_int), C.POINTER(C.c_double),
@@ -266,6 +270,21 @@ class RefSystem:
             raise RuntimeError(_err(self.lib))
         return dict(x=x, hist=hist[: its.value].copy(), its=its.value, coarse_its=cits.value,
                     vcycles=vcs.value, rel=rel.value, converged=bool(conv.value), t_solve=ts.value)
+
+    def solve_timed(self, degrees, maxit, smoother_iters=2, coarse="gmres-ilu", coarse_rtol=1e-3,
+                    coarse_maxit=400, rtol=1e-8, restart=0):
+        """Reference hierarchy setup time and per-iteration end times of the
+        first `maxit` FGMRES iterations (bench.py's reference arm)."""
+        deg = np.asarray(degrees, np.int32)
+        stamps = np.zeros(maxit + 1)
+        t_setup, its = C.c_double(), C.c_int()
+        rc = self.lib.ref_solve_timed(self.h, deg.ctypes.data, len(deg), smoother_iters,
+                                      int(coarse != "lu"), C.c_double(coarse_rtol), coarse_maxit,
+                                      C.c_double(rtol), maxit, restart, C.byref(t_setup),
+                                      stamps.ctypes.data, C.byref(its))
+        if rc:
+            raise RuntimeError(_err(self.lib))
+        return t_setup.value, stamps[: its.value].copy()
 
     def solve_system(self, degrees, smoother_iters=2, coarse="lu", rtol=1e-13, maxit=1000):
         deg = np.asarray(degrees, np.int32)

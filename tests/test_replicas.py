@@ -54,7 +54,7 @@ def test_reference_arm_rank0_only():
     """bench.py --impl reference under torchrun N=2: one JSON line (rank 0),
     the other rank exits 0 without work."""
     r = _torchrun(2, ["bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1",
-                      "--warmup", "0", "--cpu-sample-n", "4", "--config", "config1"], 29633)
+                      "--warmup", "0", "--config", "config1"], 29633)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1
