@@ -57,10 +57,12 @@ _lib = None
 
 
 def load(path: str = LIB):
-    """Loads the native library (raises if it is missing)."""
+    """Loads the native library (raises if it is missing). PSCU_LIB overrides
+    the path (experimental builds in tools/)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("PSCU_LIB", path)
     if not os.path.exists(path):
         raise RuntimeError(f"native solver library missing: {path} (run __graft_entry__.build())")
     lib = C.CDLL(path)

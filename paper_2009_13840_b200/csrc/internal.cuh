@@ -106,18 +106,23 @@ struct Csr {
 
 /// Level-walking sweep plan (walk.cu).
 struct WalkSeg {
-  bool wide;   // row-parallel launch of one sub-level, else one walker CTA
-  int s0, s1;  // sub-level range
+  bool wide;   // row-parallel launch of one chunk, else one walker cluster
+  int s0, s1;  // chunk range
 };
 
 struct WalkPlan {
   bool fwd = true;
-  int nsub = 0;
+  int C = 1;     // CTAs of the walker cluster (one chunk each per sub-level)
+  bool flow = false;  // single-CTA dataflow walker
+  int nsub = 0;  // chunks
   int64_t npos = 0;
   std::vector<WalkSeg> segments;
-  DevBuf<int32_t> sl_k, sl_nr, sl_hdr, rows, off, opos, src, far;
-  DevBuf<int64_t> sl_q, sl_f, from, dfrom;
+  DevBuf<int32_t> sl_k, sl_nr, sl_hdr, rows, off, dp, opos, src, far, sfar;
+  DevBuf<int64_t> sl_q, sl_f, sl_s, from, dfrom;
   DevBuf<double> val, dv;
+  DevBuf<int4> meta;               // per position {length / offset, row, backward position, 0}
+  mutable DevBuf<double> sfv;      // per-apply values of the static out-of-ring sources
+  std::vector<int64_t> h_sl_s;     // static list start per chunk (host copy)
   mutable DevBuf<double> scratch;  // per-apply right-hand sides in position order
 };
 

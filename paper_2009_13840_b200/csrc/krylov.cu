@@ -9,6 +9,8 @@
 // subtree with warp shuffles (offsets 1,2,4,8,16 = adjacent pairs) and
 // shared memory, and the last CTA to finish reduces the per-CTA results,
 // so each MGS pass is one kernel with no host round trip.
+#include <cstdlib>
+
 #include "internal.cuh"
 
 namespace pscu {
@@ -206,14 +208,27 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
 
 constexpr int kEpt = 16;  // elements per lane (repro_lanes guarantees <= 16 up to n = 2^22)
 
+__device__ __forceinline__ void st_pair(ulonglong2* p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+__device__ __forceinline__ ulonglong2 ld_pair(const ulonglong2* p) {
+  ulonglong2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p)
+               : "memory");
+  return v;
+}
+
 /// All j+2 MGS passes of one Arnoldi step. Per pass every CTA publishes its
-/// subtree result in its own slot (value, then a release-tagged pass id);
-/// every CTA acquires all G slots and rebuilds the same adjacent-pair tree,
-/// so the reduction doubles as the grid-wide barrier without a contended
-/// counter. Slots are double-buffered by pass parity and tags are unique per
-/// launch (tag_base), so nothing is ever reset.
+/// subtree result in its own slot; the root CTA gathers all G slots,
+/// rebuilds the adjacent-pair tree and publishes the result. Slots are
+/// double-buffered by pass parity and tags are unique per launch (tag_base),
+/// so nothing is ever reset.
+///   kPairs false: value + release-tagged pass id (release/acquire).
+///   kPairs true: {value bits, value bits ^ tag} in one relaxed 16-byte store.
 // two CTAs per SM (<= 128 registers) so up to 296 CTAs are co-resident:
 // n = 525k (the 256^2 coarse level) needs T = 65536 lanes = 256 CTAs
+template <bool kPairs>
 __global__ void __launch_bounds__(kStepThreads, 2)
     arnoldi_step_kernel(int64_t n, int64_t T, int L, int epl, int j, double* __restrict__ wg,
                         double* V, int64_t ldv, double* __restrict__ hcol,
@@ -250,8 +265,13 @@ __global__ void __launch_bounds__(kStepThreads, 2)
     const int par = i & 1;
     const unsigned long long want = tag_base + unsigned(i) + 1ull;
     if (tid == 0) {
-      slot_v[par * G + blockIdx.x] = cta;
-      st_release_u64(slot_tag + par * G + blockIdx.x, want);
+      if (kPairs) {
+        const unsigned long long bits = __double_as_longlong(cta);
+        st_pair(reinterpret_cast<ulonglong2*>(slot_tag) + par * G + blockIdx.x, bits, bits ^ want);
+      } else {
+        slot_v[par * G + blockIdx.x] = cta;
+        st_release_u64(slot_tag + par * G + blockIdx.x, want);
+      }
     }
     // prefetch v_{i+1} (independent of h_i) before waiting on the grid
     if (i + 1 <= j) {
@@ -266,7 +286,37 @@ __global__ void __launch_bounds__(kStepThreads, 2)
 #pragma unroll
       for (int k = 0; k < kEpt; ++k) pv[k] = iv[k];
     }
-    if (blockIdx.x == 0) {
+    if (kPairs) {
+      // relaxed 16-byte {value, value ^ tag} pairs: a pair is accepted only
+      // when its two words agree on this pass's tag (a torn read never
+      // passes), so neither side needs a fence: the value is the only datum
+      ulonglong2* pairs = reinterpret_cast<ulonglong2*>(slot_tag);
+      if (blockIdx.x == 0) {
+        double v = 0.0;
+        if (tid < G) {
+          ulonglong2 p;
+          do {
+            p = ld_pair(pairs + par * G + tid);
+          } while ((p.x ^ p.y) != want);
+          v = __longlong_as_double(p.x);
+        }
+        __syncthreads();  // warp 0 finished reading block_tree's scratch of this pass
+        v = block_tree(v, G);
+        if (tid == 0) {
+          if (i == j + 1) v = __dsqrt_rn(v);
+          hsh = v;
+          hcol[i] = v;
+          const unsigned long long rb = __double_as_longlong(v);
+          st_pair(pairs + 2 * G + par, rb, rb ^ want);
+        }
+      } else if (tid == 0) {
+        ulonglong2 p;
+        do {
+          p = ld_pair(pairs + 2 * G + par);
+        } while ((p.x ^ p.y) != want);
+        hsh = __longlong_as_double(p.x);
+      }
+    } else if (blockIdx.x == 0) {
       // root CTA: thread k < G acquires slot k (one round trip), rebuilds
       // the adjacent-pair tree and publishes the result under one tag
       double v = 0.0;
@@ -321,8 +371,12 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     if (G < 1 || G > 1024) continue;
     const size_t smem = 0;
     int per_sm = 0;
-    PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_step_kernel,
-                                                            kStepThreads, smem));
+    static const bool pairs = [] {
+      const char* e = getenv("PSCU_MGS_PAIRS");
+      return e ? atoi(e) != 0 : true;
+    }();
+    void* fn = pairs ? (void*)arnoldi_step_kernel<true> : (void*)arnoldi_step_kernel<false>;
+    PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kStepThreads, smem));
     if (int64_t(per_sm) * sm_count < G) continue;
     if (c.slot_tag.n < size_t(2 * G)) {
       c.slot_tag.alloc(2048);
@@ -338,7 +392,7 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     unsigned long long base = c.pass_tag;
     c.pass_tag += unsigned(j + 2);
     void* args[] = {&nn, &TT, &Li, &ei, &jj, &pw, &pV, &ld, &ph, &pv, &pt, &base};
-    PSCU_CUDA(cudaLaunchCooperativeKernel((void*)arnoldi_step_kernel, dim3(unsigned(G)),
+    PSCU_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(G)),
                                           dim3(kStepThreads), args, smem, c.stream));
     PSCU_LAUNCHED(&c);
     return true;

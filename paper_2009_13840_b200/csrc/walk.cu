@@ -3,29 +3,33 @@
 // The reference applies ILU(0) with two sequential loops. Under the natural
 // (faces-first) ordering their dependency DAGs are deep and narrow: hundreds
 // to thousands of levels of a few hundred rows, so any
-// scheme that pays an inter-SM handshake per level is bound by ~1 us per
-// level. Narrow levels are therefore walked by ONE CTA:
-//   * rows are placed in level order ("positions"); each level is cut into
-//     sub-levels of at most kStageRows rows / kMaxNz factor entries (rows of
-//     one level are independent, so any cut is a valid schedule);
-//   * a sub-level's operands are one contiguous, 16-byte-aligned block:
-//     the factor entries it needs in the reference's summation order
-//     (value + source), its row ids, offsets, right-hand sides (gathered into
-//     position order beforehand) and, backward, its diagonals;
-//   * blocks are staged into shared memory kAhead sub-levels ahead with
-//     cp.async (all addresses are static, so the pipeline never waits on a
-//     dependent gather);
-//   * recently computed solution values live in a shared-memory ring indexed
-//     by position; older sources, or sources from other segments, come from
-//     global memory (L2);
-//   * one __syncthreads per sub-level, no global handshake at all.
-// Levels with very many rows (the element-pressure rows) run as ordinary
-// row-parallel launches between walker segments. Every row is computed by
-// one thread with the reference's exact operation sequence, so the result is
-// bit-identical to Ilu0::apply.
+// scheme that pays an inter-SM handshake through global memory per level is
+// bound by ~1 us per level. Narrow levels are therefore walked by ONE thread
+// block cluster of C CTAs (C = 1..8, chosen per sweep from the level width):
+//   * rows are placed in level order; every level is cut into "sub-levels"
+//     (at most C chunks of <= kStageRows rows / kMaxNz factor entries, one
+//     chunk per CTA; rows of a level are independent, so any cut is valid);
+//   * a chunk's operands are one contiguous, 16-byte-aligned block: the
+//     factor entries it needs in the reference's summation order (value +
+//     source), row ids, offsets, right-hand sides (gathered into position
+//     order beforehand), diagonals (backward), out-of-ring source list;
+//   * per CTA, warp-specialised producers stage chunks kStages ahead with TMA
+//     bulk copies and gather the out-of-ring sources; consumers compute;
+//   * solution values of recent rows live in per-CTA shared-memory rings;
+//     a row reads sources computed by another CTA of the cluster through
+//     DSMEM (ld.shared::cluster); sources older than the ring window come
+//     from the producers' gather (they are >= 8 sub-levels old, i.e. final);
+//   * one named barrier per sub-level inside a CTA, plus (C > 1) one
+//     all-to-all mbarrier handshake over the cluster.
+// Levels with very many rows (element-pressure rows) run as row-parallel
+// launches between walker segments. Every row is computed by one thread with
+// the reference's exact operation sequence, so the result is bit-identical
+// to Ilu0::apply.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "internal.cuh"
 #include "walk.cuh"
@@ -34,48 +38,59 @@ namespace pscu {
 
 namespace {
 
-constexpr int kWalkThreads = 512;
-constexpr int kProducers = 256;    // two producer warps per stage slot (TMA issue + far gathers)
-constexpr int kStageRows = 512;   // rows of a sub-level
-constexpr int kMaxNz = 2560;      // factor entries of a sub-level (multiple of 4)
-constexpr int kAhead = 3;         // sub-levels staged ahead
-constexpr int kStages = kAhead + 1;
-constexpr int kRing = 4096;       // shared-memory solution ring (positions, power of 2)
-constexpr int kMaxFar = 512;      // sources outside the ring, per sub-level
-constexpr int kWideRows = 4096;   // levels with more rows run row-parallel
+constexpr int kWalkThreads = 512;  // consumer threads per CTA (one row each)
+constexpr int kProdWarps = 4;      // producer warps per stage slot
+constexpr int kProducers = 32 * kProdWarps * 4;
+constexpr int kStageRows = kWalkThreads;  // rows of a chunk
+constexpr int kMaxNz = 2560;       // factor entries of a chunk (multiple of 4)
+constexpr int kStages = 4;         // chunks in flight per CTA
+constexpr int kRing = 4096;        // per-CTA solution ring (local positions, power of 2)
+constexpr int kWideRows = 4096;    // levels with more rows run row-parallel
+constexpr int kMaxCluster = 8;
+constexpr int kMaxDiag = 128;      // longest row (factor entries) of a walker chunk
 
 struct WalkArgs {
-  const int32_t* sl_k;    // sub-level start position (multiple of 4)
-  const int32_t* sl_nr;   // rows of the sub-level
-  const int64_t* sl_q;    // packed entry start (multiple of 4), nsub + 1
-  const int32_t* sl_hdr;  // per sub-level {k0, rows, real entries, any global source}
+  const int32_t* sl_k;    // chunk start position (multiple of 4)
+  const int32_t* sl_nr;   // rows of the chunk
+  const int64_t* sl_q;    // packed entry start (multiple of 4), nchunks + 1
+  const int32_t* sl_hdr;  // per chunk {k0, rows, entries, far, ring start, diagonals, dp start, 0}
   const int32_t* rows;    // row id per position (-1 padding)
-  const int32_t* off;     // packed offset of a row within its sub-level
+  const int32_t* off;     // walker chunks: row length; wide chunks: row offset in the chunk
+  const int32_t* dp;      // walker chunks: start of diagonal u within the chunk
+  const int4* meta;       // walker chunks, per position: {row length, row, backward position, 0}
   const int32_t* opos;    // forward: backward position of the row
   const double* val;      // packed factor values
-  const int32_t* src;     // >= 0 ring slot, < 0: -(row)-1 global source
+  const int32_t* src;     // >= 0: (rank << 12) | ring slot, -1: out-of-ring source
   const double* dv;       // backward: diagonal per position
-  const int64_t* sl_f;    // far-source list start per sub-level (nsub + 1)
-  const int32_t* far;     // far source rows, per sub-level
+  const int64_t* sl_f;    // in-segment out-of-ring entries: list start per chunk (nchunks + 1)
+  const int2* far;        // ... {entry offset in chunk, source row}
+  const int64_t* sl_s;    // static out-of-ring entries (sources final before the launch)
+  const int2* sfar;       // ... {entry offset in chunk, source row}
+  const double* sfv;      // ... their source values, gathered before the launch
+  long long* trace;       // PSCU_WALK_TRACE: per-sub-level clock64 stamps of CTA 0
 };
+
+constexpr int kTraceSub = 4096;
+#define WALK_TRACE(cond, r, k)                                       \
+  do {                                                               \
+    if (a.trace && (cond) && (r) < kTraceSub)                        \
+      a.trace[((rank) * kTraceSub + (r)) * 16 + (k)] = clock64();    \
+  } while (0)
 
 struct alignas(16) Stage {
   double val[kMaxNz];
   int32_t src[kMaxNz];
   double rhs[kStageRows];
   double dv[kStageRows];
-  int32_t row[kStageRows];
-  int32_t opos[kStageRows];
-  int32_t off[kStageRows + 4];
-  int32_t hdr[4];  // k0, rows, real entries (end of the last row), far sources
-  double farv[kMaxFar];  // values of the sources outside the ring (gathered)
+  int4 meta[kStageRows];
+  int32_t dptr[kMaxDiag];
+  int32_t hdr[8];
 };
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return unsigned(__cvta_generic_to_shared(p));
 }
 
-/// One TMA bulk copy global -> shared completing on mbarrier `bar`.
 __device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   if (bytes == 0) return;
   asm volatile(
@@ -89,7 +104,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
@@ -99,126 +124,391 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
-/// Producer lane: stages sub-level s into `st` with one bulk copy per
-/// operand array (all addresses static and 16-byte aligned).
+__device__ __forceinline__ unsigned map_rank(const void* p, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+/// Stages chunk `ch` into `st` (one bulk copy per operand array).
 template <bool kFwd>
-__device__ void issue(const WalkArgs& a, int s, Stage& st, uint64_t* bar, const double* rhs) {
-  const int k0 = a.sl_k[s], nr = a.sl_nr[s];
+__device__ void issue(const WalkArgs& a, int ch, Stage& st, uint64_t* bar, const double* rhs) {
+  const int k0 = a.sl_k[ch], nr = a.sl_nr[ch];
   const unsigned nr4 = unsigned((nr + 3) & ~3);
-  const int64_t q0 = a.sl_q[s];
-  const unsigned nq = unsigned(a.sl_q[s + 1] - q0);
-  const unsigned bytes = nq * 12u + nr4 * (8u + 4u + 4u) + (kFwd ? nr4 * 4u : nr4 * 8u) + 16u;
+  const int64_t q0 = a.sl_q[ch];
+  const unsigned nq = unsigned(a.sl_q[ch + 1] - q0);
+  const int* hd = a.sl_hdr + 8 * ch;
+  const unsigned nd4 = unsigned((hd[5] + 3) & ~3);
+  const unsigned bytes = nq * 12u + nr4 * (8u + 16u) + (kFwd ? 0u : nr4 * 8u) + nd4 * 4u + 32u;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
                "r"(bytes)
                : "memory");
-  bulk_copy(st.hdr, a.sl_hdr + 4 * s, 16u, bar);
+  bulk_copy(st.hdr, a.sl_hdr + 8 * ch, 32u, bar);
   bulk_copy(st.val, a.val + q0, nq * 8u, bar);
   bulk_copy(st.src, a.src + q0, nq * 4u, bar);
   bulk_copy(st.rhs, rhs + k0, nr4 * 8u, bar);
-  bulk_copy(st.row, a.rows + k0, nr4 * 4u, bar);
-  bulk_copy(st.off, a.off + k0, nr4 * 4u, bar);
-  if (kFwd) bulk_copy(st.opos, a.opos + k0, nr4 * 4u, bar);
-  else bulk_copy(st.dv, a.dv + k0, nr4 * 8u, bar);
+  bulk_copy(st.meta, a.meta + k0, nr4 * 16u, bar);
+  bulk_copy(st.dptr, a.dp + hd[6], nd4 * 4u, bar);
+  if (!kFwd) bulk_copy(st.dv, a.dv + k0, nr4 * 8u, bar);
 }
 
-template <bool kFwd, bool kAnyFar>
-__device__ __forceinline__ void walk_rows(const Stage& st, double* ring, double* y, double* yb) {
-  const int k0 = st.hdr[0], nr = st.hdr[1];
-  for (int t = threadIdx.x; t < nr; t += kWalkThreads) {
-    const int qa = st.off[t], qb = t + 1 < nr ? st.off[t + 1] : st.hdr[2];
-    double acc = st.rhs[t];
-#pragma unroll 4
-    for (int q = qa; q < qb; ++q) {
-      const int sv = st.src[q];
-      double yv;
-      if (kAnyFar) yv = sv >= 0 ? ring[sv] : st.farv[-sv - 1];
-      else yv = ring[sv];
-      acc = dsub(acc, dmul(st.val[q], yv));
-    }
-    if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
-    ring[(k0 + t) & (kRing - 1)] = acc;
-    y[st.row[t]] = acc;
-    if (kFwd) yb[st.opos[t]] = acc;
+/// Products first (entry-parallel: every rounded product val * y is
+/// independent; loads batched per thread, ring values of other CTAs through
+/// DSMEM), then one thread per row folds its products in the reference's
+/// order: the same rounded operations as the sequential loop. Out-of-ring
+/// entries (src -1) already hold their product (producers).
+template <bool kCluster>
+__device__ __forceinline__ void walk_products(Stage& st, double* ring, int rank) {
+  constexpr int kPer = (kMaxNz + kWalkThreads - 1) / kWalkThreads;
+  const int nq = st.hdr[2];
+  int sv[kPer];
+  double pv[kPer], yv[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int q = threadIdx.x + u * kWalkThreads;
+    sv[u] = q < nq ? st.src[q] : -1;
+    pv[u] = q < nq ? st.val[q] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const double* p = ring + (sv[u] & (kRing - 1));
+    if (kCluster && sv[u] >= 0 && (sv[u] >> 12) != rank)
+      p = cooperative_groups::this_cluster().map_shared_rank(p, unsigned(sv[u] >> 12));
+    yv[u] = *p;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int q = threadIdx.x + u * kWalkThreads;
+    if (sv[u] >= 0) st.val[q] = dmul(pv[u], yv[u]);
   }
 }
 
-/// Warp-specialised walker: kWalkThreads consumer threads compute one
-/// sub-level after another (one named barrier per sub-level); one extra
-/// producer warp keeps kStages sub-levels in flight with TMA bulk copies,
-/// reusing a slot once the consumers have released it.
+/// Entries sit diagonal-major (entry u of row t at dptr[u] + t): a warp's
+/// fold loads are unit-stride, conflict-free.
+/// Returns false for threads without a row; the caller stores acc to y (and
+/// yb) after the sub-level's cluster handshake, whose release fence then
+/// never waits on these global stores.
+template <bool kFwd>
+__device__ __forceinline__ bool walk_rows(const Stage& st, double* ring, double& acc, int4& m) {
+  const int nr = st.hdr[1], r0 = st.hdr[4];
+  const int t = threadIdx.x;  // kStageRows == kWalkThreads: one row per thread
+  if (t >= nr) return false;
+  m = st.meta[t];
+  const int len = m.x;
+  acc = st.rhs[t];
+  for (int u0 = 0; u0 < len; u0 += 8) {
+    const int4 d0 = *reinterpret_cast<const int4*>(st.dptr + u0);
+    const int4 d1 = *reinterpret_cast<const int4*>(st.dptr + u0 + 4);
+    const int d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = u0 + u < len ? st.val[d[u] + t] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u0 + u < len) acc = dsub(acc, v[u]);
+  }
+  if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
+  ring[(r0 + t) & (kRing - 1)] = acc;
+  return true;
+}
+
+/// CTA `rank` of a C-CTA cluster walks chunks c0 + rank, c0 + rank + C, ...
+/// (one chunk per sub-level). Consumers: kWalkThreads threads; producers:
+/// kProdWarps warps per stage slot, which stage the chunk (TMA) and then
+/// turn its out-of-ring entries into products from global memory.
 template <bool kFwd>
 __global__ void __launch_bounds__(kWalkThreads + kProducers, 1)
-    walk_kernel(WalkArgs a, int s0, int s1, const double* rhs, double* y, double* yb,
-                int experiment) {
+    walk_kernel(WalkArgs a, int c0, int nsl, int C, const double* rhs, double* y, double* yb) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+  __shared__ __align__(8) uint64_t landed[kStages], full[kStages], empty[kStages], level[2];
   double* ring = reinterpret_cast<double*>(smraw);
   Stage* stages = reinterpret_cast<Stage*>(smraw + sizeof(double) * kRing);
+  const unsigned rank = C > 1 ? cluster_rank() : 0u;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_addr(&full[i])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&landed[i])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])) : "memory");
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&empty[i])) : "memory");
+    }
+    for (int i = 0; i < 2; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&level[i])), "r"(C)
+                   : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (C > 1) cluster_sync_all();
+  else __syncthreads();
+  if (threadIdx.x >= kWalkThreads) {
+    // producer group g (kProdWarps warps) owns slot g: sub-levels g, g + kStages, ...
+    constexpr int kGroup = 32 * kProdWarps;
+    const int pg = (threadIdx.x - kWalkThreads) / kGroup;
+    const int lane = (threadIdx.x - kWalkThreads) % kGroup;
+    const int slot = pg;
+    for (int r = pg; r < nsl; r += kStages) {
+      const int ch = c0 + r * C + int(rank);
+      const unsigned ph = unsigned((r / kStages) & 1);
+      WALK_TRACE(lane == 0, r, 8);
+      if (r >= kStages) mbar_wait(&empty[slot], ph ^ 1u);
+      WALK_TRACE(lane == 0, r, 9);
+      if (lane == 0) issue<kFwd>(a, ch, stages[slot], &landed[slot], rhs);
+      // out-of-ring sources: static ones (earlier launches) were gathered
+      // into sfv before this launch; in-segment ones are >= 8 sub-levels old,
+      // final since every CTA finished sub-level r - kStages
+      const int64_t s0 = a.sl_s[ch], ns = a.sl_s[ch + 1] - s0;
+      const int64_t f0 = a.sl_f[ch], nf = a.sl_f[ch + 1] - f0;
+      double* val = stages[slot].val;
+      mbar_wait(&landed[slot], ph);
+      WALK_TRACE(lane == 0, r, 10);
+      for (int64_t base = 0; base < ns; base += 8 * kGroup) {
+        int off[8];
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t f = base + u * kGroup + lane;
+          off[u] = f < ns ? __ldg(&a.sfar[s0 + f].x) : -1;
+          v[u] = f < ns ? __ldg(a.sfv + s0 + f) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (off[u] >= 0) val[off[u]] = dmul(val[off[u]], v[u]);
+      }
+      for (int64_t base = 0; base < nf; base += 4 * kGroup) {
+        int2 e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t f = base + u * kGroup + lane;
+          e[u] = f < nf ? __ldg(a.far + f0 + f) : make_int2(-1, 0);
+        }
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = e[u].x >= 0 ? __ldcg(y + e[u].y) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e[u].x >= 0) val[e[u].x] = dmul(val[e[u].x], v[u]);
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(2 + pg), "n"(kGroup) : "memory");
+      WALK_TRACE(lane == 0, r, 11);
+      if (lane == 0) mbar_arrive(&full[slot]);
+    }
+  } else {
+    for (int r = 0; r < nsl; ++r) {
+      const int slot = r % kStages;
+      Stage& st = stages[slot];
+      WALK_TRACE(threadIdx.x == 0, r, 0);
+      mbar_wait(&full[slot], unsigned((r / kStages) & 1));
+      WALK_TRACE(threadIdx.x == 0, r, 1);
+      if (C > 1) walk_products<true>(st, ring, int(rank));
+      else walk_products<false>(st, ring, 0);
+      asm volatile("bar.sync 1, %0;" ::"n"(kWalkThreads) : "memory");
+      WALK_TRACE(threadIdx.x == 0, r, 2);
+      double acc;
+      int4 m;
+      const bool mine = walk_rows<kFwd>(st, ring, acc, m);
+      asm volatile("bar.sync 1, %0;" ::"n"(kWalkThreads) : "memory");
+      WALK_TRACE(threadIdx.x == 0, r, 3);
+      if (C > 1) {
+        // all-to-all: this CTA's ring entries of sub-level r are published
+        // (release) to every CTA; wait until every CTA has published (acquire)
+        if (threadIdx.x < unsigned(C)) {
+          const unsigned remote = map_rank(&level[r & 1], threadIdx.x);
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+                       : "memory");
+        }
+        mbar_wait_cluster(&level[r & 1], unsigned((r >> 1) & 1));
+      }
+      WALK_TRACE(threadIdx.x == 0, r, 4);
+      if (mine) {
+        y[m.y] = acc;
+        if (kFwd) yb[m.z] = acc;
+      }
+      if (threadIdx.x == 0) mbar_arrive(&empty[slot]);
+    }
+  }
+  // no CTA may leave while its ring can still be read remotely
+  if (C > 1) cluster_sync_all();
+}
+
+// ---------------------------------------------------------------------------
+// Dataflow walker (one CTA): no per-level barrier. Chunks are consecutive
+// rows in level order (spanning levels); every row waits only for its own
+// sources, published in a shared-memory ring as self-validating 16-byte pairs
+// {value bits, value bits ^ tag(position)} -- a reader accepts a slot when
+// the pair carries its source's tag, so neither side needs a fence and a
+// stale or torn slot is never used. Consumer threads run at most two chunks
+// apart (each waits for chunk i - 2 to complete before starting chunk i), so
+// a slot is rewritten (position + kRing) only after all of its readers ran.
+// ---------------------------------------------------------------------------
+
+constexpr int kFlowStages = 3;
+#ifndef PSCU_FLOW_BACKOFF
+#define PSCU_FLOW_BACKOFF 64
+#endif
+constexpr unsigned kFlowBackoff = PSCU_FLOW_BACKOFF;
+
+__device__ __forceinline__ unsigned long long flow_tag(int pos) {
+  return (unsigned long long)(unsigned(pos) + 1ull) * 0x9E3779B97F4A7C15ull;
+}
+
+__device__ __forceinline__ void ring_put(ulonglong2* slot, double v, int pos) {
+  const unsigned long long b = __double_as_longlong(v);
+  asm volatile("st.volatile.shared.v2.u64 [%0], {%1, %2};" ::"r"(smem_addr(slot)), "l"(b),
+               "l"(b ^ flow_tag(pos))
+               : "memory");
+}
+
+__device__ __forceinline__ double ring_get(const ulonglong2* slot, int pos) {
+  const unsigned long long want = flow_tag(pos);
+  unsigned long long x, y;
+  for (;;) {
+    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y)
+                 : "r"(smem_addr(slot))
+                 : "memory");
+    if ((x ^ y) == want) break;
+    __nanosleep(kFlowBackoff);  // leave the shared-memory pipe to the rows being computed
+  }
+  return __longlong_as_double(x);
+}
+
+template <bool kFwd>
+__global__ void __launch_bounds__(kWalkThreads + 64 * kFlowStages, 1)
+    flow_kernel(WalkArgs a, int c0, int nch, const double* rhs, double* y, double* yb) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t landed[kFlowStages], full[kFlowStages], empty[kFlowStages];
+  ulonglong2* ring = reinterpret_cast<ulonglong2*>(smraw);
+  Stage* stages = reinterpret_cast<Stage*>(smraw + sizeof(ulonglong2) * kRing);
+  const unsigned rank = 0;  // WALK_TRACE
+  for (int i = threadIdx.x; i < kRing; i += blockDim.x) ring[i] = make_ulonglong2(0ull, 0ull);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kFlowStages; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&landed[i])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&empty[i])),
+                   "r"(kWalkThreads)
+                   : "memory");
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (threadIdx.x >= kWalkThreads) {
-    // producer warps: thread 0 of them issues the bulk copies; all of them
-    // gather the sources outside the ring (final: they lie >= kRing
-    // positions, hence >= kStages sub-levels, back, or in an earlier launch)
-    // with several independent loads in flight per lane, then one of them
-    // makes the second arrival on the slot's full barrier
-    // producer warp pair w owns slot w: sub-levels s0 + w, s0 + w + kStages, ...
-    const int pw = (threadIdx.x - kWalkThreads) >> 6, lane = (threadIdx.x - kWalkThreads) & 63;
-    const int slot = pw;
-    for (int s = s0 + pw; s < s1; s += kStages) {
-      const int r = s - s0;
-      if (r >= kStages) mbar_wait(&empty[slot], unsigned((r / kStages - 1) & 1));
-      if (lane == 0) issue<kFwd>(a, s, stages[slot], &full[slot], rhs);
-      const int64_t f0 = a.sl_f[s], nf = a.sl_f[s + 1] - f0;
-      double* fv = stages[slot].farv;
-      for (int64_t base = 0; base < nf; base += 8 * 64) {
-        int32_t idx[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int64_t f = base + u * 64 + lane;
-          idx[u] = f < nf ? __ldg(a.far + f0 + f) : -1;
-        }
+    // producer pair of warps g owns slot g: chunks g, g + kFlowStages, ...
+    constexpr int kGroup = 64;
+    const int pg = (threadIdx.x - kWalkThreads) / kGroup;
+    const int lane = (threadIdx.x - kWalkThreads) % kGroup;
+    const int slot = pg;
+    for (int r = pg; r < nch; r += kFlowStages) {
+      const int ch = c0 + r;
+      const unsigned ph = unsigned((r / kFlowStages) & 1);
+      WALK_TRACE(lane == 0, r, 8);
+      if (r >= kFlowStages) mbar_wait(&empty[slot], ph ^ 1u);
+      WALK_TRACE(lane == 0, r, 9);
+      if (lane == 0) issue<kFwd>(a, ch, stages[slot], &landed[slot], rhs);
+      // out-of-ring sources: static ones were gathered before this launch;
+      // in-segment ones lie >= 5 chunks back, complete since every consumer
+      // finished chunk r - kFlowStages
+      const int64_t s0 = a.sl_s[ch], ns = a.sl_s[ch + 1] - s0;
+      const int64_t f0 = a.sl_f[ch], nf = a.sl_f[ch + 1] - f0;
+      double* val = stages[slot].val;
+      mbar_wait(&landed[slot], ph);
+      WALK_TRACE(lane == 0, r, 10);
+      for (int64_t base = 0; base < ns; base += 8 * kGroup) {
+        int off[8];
         double v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = idx[u] >= 0 ? __ldcg(y + idx[u]) : 0.0;
-#pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const int64_t f = base + u * 64 + lane;
-          if (f < nf) fv[f] = v[u];
+          const int64_t f = base + u * kGroup + lane;
+          off[u] = f < ns ? __ldg(&a.sfar[s0 + f].x) : -1;
+          v[u] = f < ns ? __ldg(a.sfv + s0 + f) : 0.0;
         }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (off[u] >= 0) val[off[u]] = dmul(val[off[u]], v[u]);
       }
-      asm volatile("bar.sync %0, 64;" ::"r"(2 + pw) : "memory");
+      for (int64_t base = 0; base < nf; base += 4 * kGroup) {
+        int2 e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t f = base + u * kGroup + lane;
+          e[u] = f < nf ? __ldg(a.far + f0 + f) : make_int2(-1, 0);
+        }
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = e[u].x >= 0 ? __ldcg(y + e[u].y) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e[u].x >= 0) val[e[u].x] = dmul(val[e[u].x], v[u]);
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(2 + pg), "n"(kGroup) : "memory");
+      WALK_TRACE(lane == 0, r, 11);
       if (lane == 0) mbar_arrive(&full[slot]);
     }
-    return;
-  }
-  for (int s = s0; s < s1; ++s) {
-    const int r = s - s0, slot = r % kStages;
-    const Stage& st = stages[slot];
-    mbar_wait(&full[slot], unsigned((r / kStages) & 1));
-    if (experiment != 1) {
-      if (st.hdr[3]) walk_rows<kFwd, true>(st, ring, y, yb);
-      else walk_rows<kFwd, false>(st, ring, y, yb);
+  } else {
+    const int t = threadIdx.x;
+    for (int r = 0; r < nch; ++r) {
+      const int slot = r % kFlowStages;
+      WALK_TRACE(t == 0, r, 0);
+      if (r >= 2) {
+        // bounded skew: chunk r - 2 complete (its ring slots may be reused)
+        const int r2 = r - 2;
+        mbar_wait(&empty[r2 % kFlowStages], unsigned((r2 / kFlowStages) & 1));
+      }
+      mbar_wait(&full[slot], unsigned((r / kFlowStages) & 1));
+      WALK_TRACE(t == 0, r, 1);
+      WALK_TRACE(t == 0, r, 2);
+      const Stage& st = stages[slot];
+      const int nr = st.hdr[1];
+      if (t < nr) {
+        const int4 m = st.meta[t];
+        const int len = m.x;
+        double acc = st.rhs[t];
+        for (int u0 = 0; u0 < len; u0 += 8) {
+          int sv[8];
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const bool ok = u0 + u < len;
+            const int e = ok ? st.dptr[u0 + u] + t : 0;
+            sv[u] = ok ? st.src[e] : -1;
+            v[u] = ok ? st.val[e] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (u0 + u < len) {
+              const double p = sv[u] >= 0 ? dmul(v[u], ring_get(ring + (sv[u] & (kRing - 1)), sv[u]))
+                                          : v[u];
+              acc = dsub(acc, p);
+            }
+          }
+        }
+        if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
+        const int pos = st.hdr[4] + t;
+        ring_put(ring + (pos & (kRing - 1)), acc, pos);
+        y[m.y] = acc;
+        if (kFwd) yb[m.z] = acc;
+      }
+      WALK_TRACE(t == 0, r, 3);
+      WALK_TRACE(t == 0, r, 4);
+      mbar_arrive(&empty[slot]);
     }
-    // consumers only: the slot is free and the ring entries of s visible
-    asm volatile("bar.sync 1, %0;" ::"n"(kWalkThreads) : "memory");
-    if (threadIdx.x == 0) mbar_arrive(&empty[slot]);
   }
 }
 
-/// Row-parallel sub-level (a level too wide for one CTA): global sources.
+/// Row-parallel chunk (a level too wide for one CTA): global sources.
 template <bool kFwd>
-__global__ void wide_kernel(WalkArgs a, int s, const double* rhs, double* y, double* yb) {
-  const int k0 = a.sl_k[s], nr = a.sl_nr[s];
-  const int64_t q0 = a.sl_q[s];
-  const int nq = a.sl_hdr[4 * s + 2];
+__global__ void wide_kernel(WalkArgs a, int ch, const double* rhs, double* y, double* yb) {
+  const int k0 = a.sl_k[ch], nr = a.sl_nr[ch];
+  const int64_t q0 = a.sl_q[ch];
+  const int nq = a.sl_hdr[8 * ch + 2];
   for (int t = int(blockIdx.x * blockDim.x + threadIdx.x); t < nr; t += gridDim.x * blockDim.x) {
     const int k = k0 + t;
     const int64_t qa = q0 + a.off[k];
@@ -229,6 +519,14 @@ __global__ void wide_kernel(WalkArgs a, int s, const double* rhs, double* y, dou
     y[a.rows[k]] = acc;
     if (kFwd) yb[a.opos[k]] = acc;
   }
+}
+
+/// Values of the static out-of-ring sources of one walker launch.
+__global__ void gather_static(int64_t m, const int2* __restrict__ sfar, const double* __restrict__ y,
+                              double* __restrict__ sfv) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < m;
+       e += int64_t(gridDim.x) * blockDim.x)
+    sfv[e] = y[sfar[e].y];
 }
 
 /// Right-hand side in position order: xs[k] = x[rows[k]].
@@ -251,8 +549,10 @@ __global__ void gather_vals(int64_t m, const int64_t* __restrict__ from,
 }
 
 WalkArgs args_of(const WalkPlan& w) {
-  return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_hdr.p, w.rows.p, w.off.p,
-          w.opos.p, w.val.p,  w.src.p,  w.dv.p,  w.sl_f.p, w.far.p};
+  return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_hdr.p, w.rows.p, w.off.p, w.dp.p, w.meta.p,
+          w.opos.p, w.val.p,  w.src.p,  w.dv.p,     w.sl_f.p,
+          reinterpret_cast<const int2*>(w.far.p), w.sl_s.p,
+          reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr};
 }
 
 size_t walk_smem() { return sizeof(double) * kRing + kStages * sizeof(Stage); }
@@ -282,15 +582,19 @@ std::vector<int32_t> dag_levels(const Csr& a, const std::vector<int64_t>& diag, 
 }
 
 struct HostPlan {
-  std::vector<int32_t> sl_k, sl_nr, sl_nq, sl_nfar, rows, off, src, pos, far;
-  std::vector<int64_t> sl_f;
-  std::vector<int64_t> sl_q, from, dfrom;
+  int C = 1;
+  bool flow = false;  // single-CTA dataflow walker (flow_kernel), chunks span levels
+  std::vector<int32_t> sl_k, sl_nr, sl_nq, sl_nfar, sl_r0, rows, off, src, pos;
+  std::vector<int32_t> far, sfar;  // pairs {entry offset in chunk, source row}
+  std::vector<int64_t> sl_f, sl_s, sl_q, from, dfrom;
+  std::vector<int32_t> dp, sl_d, sl_nd;  // walker chunks: diagonal starts (padded to 4)
   std::vector<uint8_t> sl_wide;
   int64_t npos = 0;
 };
 
-/// Positions, sub-levels and packed operands of one sweep.
-HostPlan plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
+/// Positions, chunks and packed operands of one sweep for a C-CTA walker.
+void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C, bool flow,
+                HostPlan& h) {
   const int64_t n = a.n;
   const auto& rp = a.h_row_ptr;
   const auto& cols = a.h_cols;
@@ -308,13 +612,14 @@ HostPlan plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
       order[fill[lvl[i]]++] = int32_t(i);
     }
   }
-  HostPlan h;
+  h = HostPlan{};
+  h.C = C;
+  h.flow = flow;
   h.pos.assign(n, -1);
+  std::vector<int32_t> lpos(n, -1), chunk_of_row(n, -1);
+  std::vector<int64_t> lcount(C, 0);  // per-CTA local positions (ring index)
   int64_t k = 0, q = 0;
-  int64_t seg_start = 0;      // first position of the current walker segment
-  std::vector<int32_t> far_mark(n, -1);
-  int cur_far = 0;
-  auto open_sub = [&](bool wide) {
+  auto open_chunk = [&](bool wide, int rank) {
     k = (k + 3) & ~int64_t(3);
     q = (q + 3) & ~int64_t(3);
     h.sl_k.push_back(int32_t(k));
@@ -322,109 +627,260 @@ HostPlan plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
     h.sl_q.push_back(q);
     h.sl_nq.push_back(0);
     h.sl_wide.push_back(wide ? 1 : 0);
-    cur_far = 0;
+    if (!wide) lcount[rank] = (lcount[rank] + 3) & ~int64_t(3);
+    h.sl_r0.push_back(wide ? 0 : int32_t(lcount[rank] & 0x7fffffff));
   };
-  // a source is served by the ring when it lies in the same walker segment
-  // within kRing positions of the sub-level's largest possible end
-  auto ring_ok = [&](int64_t k0, int32_t j) {
-    return h.pos[j] >= seg_start && k0 + kStageRows + 3 - int64_t(h.pos[j]) <= kRing;
-  };
-  bool prev_wide = true;
-  for (int l = 0; l < nlev; ++l) {
-    const int nrl = lvl_ptr[l + 1] - lvl_ptr[l];
-    const bool wide = nrl > kWideRows;
-    open_sub(wide);
-    if (!wide && prev_wide) seg_start = h.sl_k.back();
-    prev_wide = wide;
-    for (int j = lvl_ptr[l]; j < lvl_ptr[l + 1]; ++j) {
-      const int32_t i = order[j];
+  // places the collected rows of the open chunk, longest first: diagonal u
+  // of a chunk is then a prefix of its rows, stored contiguously
+  std::vector<int32_t> members;
+  auto commit = [&](int rank) {
+    std::stable_sort(members.begin(), members.end(), [&](int32_t x, int32_t y2) {
+      return q_end(x) - q_begin(x) > q_end(y2) - q_begin(y2);
+    });
+    for (const int32_t i : members) {
       const int64_t nz = q_end(i) - q_begin(i);
-      int nfar = 0;
-      if (!wide) {
-        const int sid = int(h.sl_k.size()) - 1;
-        for (int64_t p = q_begin(i); p < q_end(i); ++p)
-          if (!ring_ok(h.sl_k.back(), cols[p]) && far_mark[cols[p]] != sid) ++nfar;
-        if (h.sl_nr.back() == kStageRows || h.sl_nq.back() + nz > kMaxNz - 4 ||
-            cur_far + nfar > kMaxFar) {
-          open_sub(false);
-          const int sid2 = int(h.sl_k.size()) - 1;
-          nfar = 0;
-          for (int64_t p = q_begin(i); p < q_end(i); ++p)
-            if (!ring_ok(h.sl_k.back(), cols[p]) && far_mark[cols[p]] != sid2) ++nfar;
-        }
-        const int sid3 = int(h.sl_k.size()) - 1;
-        for (int64_t p = q_begin(i); p < q_end(i); ++p)
-          if (!ring_ok(h.sl_k.back(), cols[p])) far_mark[cols[p]] = sid3;
-        cur_far += nfar;
-      }
+      if (nz > kMaxDiag) throw Error(PSCU_ECUDA, "walk plan: row exceeds the diagonal capacity");
       h.pos[i] = int32_t(k++);
+      lpos[i] = int32_t(lcount[rank]++);
+      chunk_of_row[i] = int(h.sl_k.size()) - 1;
       h.sl_nr.back()++;
       h.sl_nq.back() += int32_t(nz);
       q += nz;
     }
+    members.clear();
+  };
+  auto wide_level = [&](int l) {
+    open_chunk(true, 0);
+    for (int j = lvl_ptr[l]; j < lvl_ptr[l + 1]; ++j) {
+      const int32_t i = order[j];
+      const int64_t nz = q_end(i) - q_begin(i);
+      h.pos[i] = int32_t(k++);
+      chunk_of_row[i] = int(h.sl_k.size()) - 1;
+      h.sl_nr.back()++;
+      h.sl_nq.back() += int32_t(nz);
+      q += nz;
+    }
+  };
+  if (flow) {
+    // dataflow chunks: consecutive rows in level order, across level
+    // boundaries (rows wait on their own sources, not on levels)
+    int64_t cnz = 0;
+    bool open = false;
+    for (int l = 0; l < nlev; ++l) {
+      if (lvl_ptr[l + 1] - lvl_ptr[l] > kWideRows) {
+        if (open) commit(0);
+        open = false;
+        wide_level(l);
+        continue;
+      }
+      for (int j = lvl_ptr[l]; j < lvl_ptr[l + 1]; ++j) {
+        const int32_t i = order[j];
+        const int64_t nz = q_end(i) - q_begin(i);
+        if (open && (int(members.size()) == kStageRows || cnz + nz > kMaxNz - 8)) {
+          commit(0);
+          open = false;
+        }
+        if (!open) {
+          open_chunk(false, 0);
+          open = true;
+          cnz = 0;
+        }
+        members.push_back(i);
+        cnz += nz;
+      }
+    }
+    if (open) commit(0);
+  }
+  for (int l = 0; l < nlev && !flow; ++l) {
+    const int nrl = lvl_ptr[l + 1] - lvl_ptr[l];
+    if (nrl > kWideRows) {
+      wide_level(l);
+      continue;
+    }
+    // sub-levels of C chunks: row and entry budgets per chunk
+    const int row_cap = kStageRows;
+    const int64_t nz_cap = kMaxNz - 8;
+    int j = lvl_ptr[l];
+    while (j < lvl_ptr[l + 1]) {
+      // rows of this sub-level: up to C chunks; balance the entries
+      int64_t rem_nz = 0;
+      int jend = j, rows_left = 0;
+      for (int jj = j; jj < lvl_ptr[l + 1]; ++jj) {
+        const int64_t nz = q_end(order[jj]) - q_begin(order[jj]);
+        if (rows_left + 1 > C * row_cap || rem_nz + nz > C * nz_cap) break;
+        rem_nz += nz;
+        ++rows_left;
+        jend = jj + 1;
+      }
+      if (jend == j) jend = j + 1;  // a single huge row still gets a chunk
+      const int64_t target = (rem_nz + C - 1) / C;
+      int jj = j;
+      for (int rank = 0; rank < C; ++rank) {
+        open_chunk(false, rank);
+        int64_t cnz = 0;
+        members.clear();
+        while (jj < jend) {
+          const int32_t i = order[jj];
+          const int64_t nz = q_end(i) - q_begin(i);
+          const int cnt = int(members.size());
+          if (cnt > 0 && rank + 1 < C && (cnz + nz > target || cnt == row_cap)) break;
+          if (cnt > 0 && (cnt == row_cap || cnz + nz > nz_cap)) break;
+          members.push_back(i);
+          cnz += nz;
+          ++jj;
+        }
+        commit(rank);
+      }
+      // rows the balancing left over start the next sub-level
+      j = jj;
+    }
   }
   h.sl_q.push_back((q + 3) & ~int64_t(3));
   h.npos = (k + 3) & ~int64_t(3);
-  const int nsub = int(h.sl_k.size());
-  // walker segments (for the ring-source rule)
-  std::vector<int32_t> seg_of(nsub);
+  const int nch = int(h.sl_k.size());
+  // walker segments: maximal runs of non-wide chunks (C chunks per sub-level)
+  std::vector<int32_t> seg_of(nch);
   int seg = -1;
-  for (int s = 0; s < nsub; ++s) {
-    if (h.sl_wide[s] || s == 0 || h.sl_wide[s - 1]) ++seg;
-    seg_of[s] = seg;
+  for (int c = 0; c < nch; ++c) {
+    if (h.sl_wide[c] || c == 0 || h.sl_wide[c - 1]) ++seg;
+    seg_of[c] = seg;
   }
-  std::vector<int32_t> sub_of_pos(h.npos + 4, -1);
-  for (int s = 0; s < nsub; ++s)
-    for (int t = 0; t < h.sl_nr[s]; ++t) sub_of_pos[h.sl_k[s] + t] = s;
+  // local ring end of every rank at every sub-level (for the validity rule)
   h.rows.assign(h.npos + 4, -1);
   h.off.assign(h.npos + 4, 0);
   h.dfrom.assign(h.npos + 4, -1);
   const int64_t total = h.sl_q.back() + 8;
   h.from.assign(total, -1);
   h.src.assign(total, 0);
-  // rows by position, then the packed operands of each sub-level in row order
   for (int64_t i = 0; i < n; ++i) h.rows[h.pos[i]] = int32_t(i);
-  std::vector<int32_t> far_idx(n, -1), far_sub(n, -1);
-  h.sl_f.assign(nsub + 1, 0);
-  for (int s = 0; s < nsub; ++s) {
-    int64_t qq = h.sl_q[s];
-    const int64_t kcons = h.sl_k[s] + kStageRows + 3;
-    int nf = 0;
-    for (int t = 0; t < h.sl_nr[s]; ++t) {
-      const int64_t kp = h.sl_k[s] + t;
+  h.sl_f.assign(nch + 1, 0);
+  h.sl_s.assign(nch + 1, 0);
+  // chunk index -> (segment start chunk, sub-level index within segment)
+  std::vector<int32_t> seg_first(nch, 0);
+  for (int c = 0; c < nch; ++c) seg_first[c] = (c > 0 && seg_of[c] == seg_of[c - 1]) ? seg_first[c - 1] : c;
+  // per chunk: the ring end (exclusive local position) of every rank at the
+  // end of this chunk's sub-level
+  h.sl_d.assign(nch, 0);
+  h.sl_nd.assign(nch, 0);
+  for (int c = 0; c < nch; ++c) {
+    int nf = 0, ns = 0;
+    const int sub = (c - seg_first[c]) / C;
+    const int sub_first = seg_first[c] + sub * C;
+    const int nr = h.sl_nr[c];
+    auto len_of = [&](int t) { return int(q_end(h.rows[h.sl_k[c] + t]) - q_begin(h.rows[h.sl_k[c] + t])); };
+    // entry index of (row t, entry u): row-contiguous for wide chunks, else
+    // diagonal-major (rows sorted by length, descending)
+    std::vector<int32_t> dstart;
+    if (!h.sl_wide[c]) {
+      const int nd = nr ? len_of(0) : 0;
+      dstart.assign(nd + 1, 0);
+      for (int u = 0, t = nr; u < nd; ++u) {
+        while (t > 0 && len_of(t - 1) <= u) --t;
+        dstart[u + 1] = dstart[u] + t;
+      }
+      h.sl_d[c] = int32_t(h.dp.size());
+      h.sl_nd[c] = nd;
+      for (int u = 0; u < nd; ++u) h.dp.push_back(dstart[u]);
+      while (h.dp.size() & 3) h.dp.push_back(0);
+    }
+    int64_t roff = 0;
+    for (int t = 0; t < nr; ++t) {
+      const int64_t kp = h.sl_k[c] + t;
       const int32_t i = h.rows[kp];
-      h.off[kp] = int32_t(qq - h.sl_q[s]);
+      const int len = len_of(t);
+      h.off[kp] = h.sl_wide[c] ? int32_t(roff) : len;
       h.dfrom[kp] = diag[i];
-      for (int64_t p = q_begin(i); p < q_end(i); ++p, ++qq) {
-        const int32_t j = cols[p];
+      for (int u = 0; u < len; ++u) {
+        const int64_t p = q_begin(i) + u;
+        const int64_t e = h.sl_wide[c] ? roff + u : int64_t(dstart[u]) + t;  // offset in chunk
+        const int64_t qq = h.sl_q[c] + e;
+        const int32_t jr = cols[p];
         h.from[qq] = p;
-        if (h.sl_wide[s]) {
-          h.src[qq] = -(j + 1);  // wide launches read global memory directly
+        if (h.sl_wide[c]) {
+          h.src[qq] = -(jr + 1);  // wide launches read global memory directly
           continue;
         }
-        const int sj = sub_of_pos[h.pos[j]];
-        const bool in_ring = seg_of[sj] == seg_of[s] && kcons - int64_t(h.pos[j]) <= kRing;
+        const int cj = chunk_of_row[jr];
+        bool in_ring = false;
+        int owner = 0;
+        if (flow && !h.sl_wide[cj] && seg_of[cj] == seg_of[c]) {
+          // dataflow: position s is overwritten by s + kRing, written no
+          // earlier than chunk c + 2 (consumers run at most two chunks apart)
+          const int cn = (c + 1 < nch && seg_of[c + 1] == seg_of[c]) ? c + 1 : c;
+          in_ring = int64_t(h.sl_r0[cn]) + h.sl_nr[cn] - int64_t(lpos[jr]) <= kRing;
+        } else if (!h.sl_wide[cj] && seg_of[cj] == seg_of[c]) {
+          owner = (cj - seg_first[cj]) % C;
+          // the owner's ring end at this sub-level: its chunk in this sub-level
+          const int oc = sub_first + owner;
+          const int64_t oend = (oc < nch && seg_of[oc] == seg_of[c])
+                                   ? int64_t(h.sl_r0[oc]) + h.sl_nr[oc]
+                                   : int64_t(lpos[jr]) + 1;
+          in_ring = oend - int64_t(lpos[jr]) <= kRing;
+        }
         if (in_ring) {
-          h.src[qq] = h.pos[j] & (kRing - 1);
+          // dataflow walker: the source's position (slot and readiness tag)
+          h.src[qq] = flow ? lpos[jr] : (owner << 12) | (lpos[jr] & (kRing - 1));
+        } else if (h.sl_wide[cj] || seg_of[cj] != seg_of[c]) {
+          // final before this launch: gathered into sfv, product by a producer
+          h.src[qq] = -1;
+          h.sfar.push_back(int32_t(e));
+          h.sfar.push_back(jr);
+          ++ns;
         } else {
-          if (far_sub[j] != s) {
-            far_sub[j] = s;
-            far_idx[j] = nf++;
-            h.far.push_back(j);
-          }
-          h.src[qq] = -(far_idx[j] + 1);
+          // out of the ring window: a producer forms this product from y
+          h.src[qq] = -1;
+          h.far.push_back(int32_t(e));
+          h.far.push_back(jr);
+          ++nf;
         }
       }
+      roff += len;
     }
-    h.sl_f[s + 1] = h.sl_f[s] + nf;
-    h.sl_nfar.push_back(nf);
+    h.sl_f[c + 1] = h.sl_f[c] + nf;
+    h.sl_s[c + 1] = h.sl_s[c] + ns;
+    h.sl_nfar.push_back(nf + ns);
   }
+}
+
+/// Cluster size for a sweep: one CTA when an average level fits one chunk
+/// (no handshakes), else a cluster of kMaxCluster CTAs, whose rings also keep
+/// the wide fine-level wavefronts resident (measured: tools/sweep_cluster.sh).
+int pick_cluster(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
+  if (const char* e = getenv(fwd ? "PSCU_WALK_CLUSTER_FWD" : "PSCU_WALK_CLUSTER_BWD"))
+    return std::max(1, std::min(kMaxCluster, atoi(e)));
+  if (const char* e = getenv("PSCU_WALK_CLUSTER")) return std::max(1, std::min(kMaxCluster, atoi(e)));
+  int nlev = 0;
+  const std::vector<int32_t> lvl = dag_levels(a, diag, fwd, nlev);
+  std::vector<int64_t> rows(nlev, 0), nz(nlev, 0);
+  for (int64_t i = 0; i < a.n; ++i) {
+    rows[lvl[i]]++;
+    nz[lvl[i]] += fwd ? diag[i] - a.h_row_ptr[i] : a.h_row_ptr[i + 1] - diag[i] - 1;
+  }
+  int64_t nr = 0, nq = 0, cnt = 0;
+  for (int l = 0; l < nlev; ++l)
+    if (rows[l] <= kWideRows) {
+      nr += rows[l];
+      nq += nz[l];
+      ++cnt;
+    }
+  if (!cnt) return 1;
+  return (2 * nr <= 3 * int64_t(kStageRows) * cnt && nq <= int64_t(kMaxNz) * cnt) ? 1 : kMaxCluster;
+}
+
+HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
+  HostPlan h;
+  const int C = pick_cluster(a, diag, fwd);
+  // the dataflow walker is correct but not yet faster than the level walker
+  const bool flow = C == 1 && getenv("PSCU_WALK_FLOW");
+  plan_sweep(a, diag, fwd, C, flow, h);
   return h;
 }
 
 void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   cudaStream_t st = c.stream;
   w.fwd = fwd;
+  w.C = h.C;
+  w.flow = h.flow;
   w.nsub = int(h.sl_k.size());
   w.npos = h.npos;
   w.segments.clear();
@@ -438,20 +894,29 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   w.sl_f.upload(h.sl_f, st);
   if (h.far.empty()) w.far.alloc(4);
   else w.far.upload(h.far, st);
+  w.sl_s.upload(h.sl_s, st);
+  w.h_sl_s = h.sl_s;
+  if (h.sfar.empty()) w.sfar.alloc(4);
+  else w.sfar.upload(h.sfar, st);
+  w.sfv.alloc(std::max<size_t>(4, h.sfar.size() / 2));
   w.sl_q.upload(h.sl_q, st);
   {
-    // {k0, rows, real entries, any global source}: one 16-byte bulk copy each
-    std::vector<int32_t> hdr(size_t(w.nsub) * 4, 0);
+    std::vector<int32_t> hdr(size_t(w.nsub) * 8, 0);
     for (int s = 0; s < w.nsub; ++s) {
-      hdr[size_t(s) * 4] = h.sl_k[s];
-      hdr[size_t(s) * 4 + 1] = h.sl_nr[s];
-      hdr[size_t(s) * 4 + 2] = h.sl_nq[s];
-      hdr[size_t(s) * 4 + 3] = h.sl_wide[s] ? 0 : h.sl_nfar[s];
+      hdr[size_t(s) * 8] = h.sl_k[s];
+      hdr[size_t(s) * 8 + 1] = h.sl_nr[s];
+      hdr[size_t(s) * 8 + 2] = h.sl_nq[s];
+      hdr[size_t(s) * 8 + 3] = h.sl_wide[s] ? 0 : h.sl_nfar[s];
+      hdr[size_t(s) * 8 + 4] = h.sl_r0[s];
+      hdr[size_t(s) * 8 + 5] = h.sl_nd[s];
+      hdr[size_t(s) * 8 + 6] = h.sl_d[s];
     }
     w.sl_hdr.upload(hdr, st);
   }
   w.rows.upload(h.rows, st);
   w.off.upload(h.off, st);
+  if (h.dp.empty()) w.dp.alloc(4);
+  else w.dp.upload(h.dp, st);
   w.src.upload(h.src, st);
   w.from.upload(h.from, st);
   w.val.alloc(h.from.size());
@@ -468,8 +933,8 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
 void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, WalkPlan& wf,
                 WalkPlan& wb) {
   if (a.n == 0) return;
-  const HostPlan hf = plan_sweep(a, diag, true);
-  const HostPlan hb = plan_sweep(a, diag, false);
+  const HostPlan hf = plan(a, diag, true);
+  const HostPlan hb = plan(a, diag, false);
   upload_plan(c, hf, true, wf);
   upload_plan(c, hb, false, wb);
   // forward results are written straight into backward position order
@@ -478,6 +943,13 @@ void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, Walk
     if (hf.rows[k] >= 0) opos[k] = hb.pos[hf.rows[k]];
   wf.opos.upload(opos, c.stream);
   wb.opos.alloc(4);
+  for (int dir = 0; dir < 2; ++dir) {
+    const HostPlan& h = dir ? hb : hf;
+    std::vector<int4> meta(h.rows.size());
+    for (size_t k = 0; k < h.rows.size(); ++k)
+      meta[k] = make_int4(h.off[k], h.rows[k] >= 0 ? h.rows[k] : 0, dir ? 0 : opos[k], 0);
+    (dir ? wb : wf).meta.upload(meta, c.stream);
+  }
   wf.scratch.alloc(size_t(hf.npos) + 8);  // rhs in forward position order
   wb.scratch.alloc(size_t(hb.npos) + 8);  // forward result in backward position order
   PSCU_CUDA(cudaMemsetAsync(wb.scratch.p, 0, sizeof(double) * (hb.npos + 8), c.stream));
@@ -486,11 +958,15 @@ void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, Walk
       int64_t ring = 0, far = 0;
       for (size_t q = 0; q < h->from.size(); ++q)
         if (h->from[q] >= 0) (h->src[q] >= 0 ? ring : far)++;
+      fprintf(stderr, "[walk %s] static out-of-ring %zu, in-segment out-of-ring %zu\n",
+              h == &hf ? "fwd" : "bwd", h->sfar.size() / 2, h->far.size() / 2);
       int nw = 0;
       for (auto x : h->sl_wide) nw += x;
-      fprintf(stderr, "[walk %s] n=%lld sublevels=%zu (wide %d) positions=%lld ring=%lld far=%lld\n",
-              h == &hf ? "fwd" : "bwd", (long long)a.n, h->sl_k.size(), nw, (long long)h->npos,
-              (long long)ring, (long long)far);
+      fprintf(stderr,
+              "[walk %s] n=%lld cluster=%d chunks=%zu (wide %d) positions=%lld ring=%lld "
+              "far=%lld\n",
+              h == &hf ? "fwd" : "bwd", (long long)a.n, h->C, h->sl_k.size(), nw,
+              (long long)h->npos, (long long)ring, (long long)far);
     }
   }
 }
@@ -508,28 +984,114 @@ void pack_walk(Context& c, const double* lu, WalkPlan& w) {
   }
 }
 
-static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y, double* yb) {
+size_t flow_smem() { return sizeof(ulonglong2) * kRing + kFlowStages * sizeof(Stage); }
+
+static void launch_flow(Context& c, bool fwd, const WalkArgs& a, int c0, int nch,
+                        const double* rhs, double* y, double* yb) {
   static bool attr = false;
   if (!attr) {
-    PSCU_CUDA(cudaFuncSetAttribute(walk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(walk_smem())));
-    PSCU_CUDA(cudaFuncSetAttribute(walk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(walk_smem())));
+    for (void* f : {(void*)flow_kernel<true>, (void*)flow_kernel<false>})
+      PSCU_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(flow_smem())));
     attr = true;
   }
-  const WalkArgs a = args_of(w);
-  static const int experiment = getenv("PSCU_WALK_EXPERIMENT") ? atoi(getenv("PSCU_WALK_EXPERIMENT")) : 0;
+  const unsigned threads = kWalkThreads + 64 * kFlowStages;
+  if (fwd) flow_kernel<true><<<1, threads, flow_smem(), c.stream>>>(a, c0, nch, rhs, y, yb);
+  else flow_kernel<false><<<1, threads, flow_smem(), c.stream>>>(a, c0, nch, rhs, y, yb);
+  PSCU_LAUNCHED(&c);
+}
+
+static void launch_walker(Context& c, bool fwd, const WalkArgs& a, int c0, int nsl, int C,
+                          const double* rhs, double* y, double* yb) {
+  static bool attr = false;
+  if (!attr) {
+    for (void* f : {(void*)walk_kernel<true>, (void*)walk_kernel<false>}) {
+      PSCU_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(walk_smem())));
+    }
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(C));
+  cfg.blockDim = dim3(kWalkThreads + kProducers);
+  cfg.dynamicSmemBytes = walk_smem();
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr_c[1];
+  attr_c[0].id = cudaLaunchAttributeClusterDimension;
+  attr_c[0].val.clusterDim.x = unsigned(C);
+  attr_c[0].val.clusterDim.y = 1;
+  attr_c[0].val.clusterDim.z = 1;
+  cfg.attrs = attr_c;
+  cfg.numAttrs = 1;
+  if (fwd) PSCU_CUDA(cudaLaunchKernelEx(&cfg, walk_kernel<true>, a, c0, nsl, C, rhs, y, yb));
+  else PSCU_CUDA(cudaLaunchKernelEx(&cfg, walk_kernel<false>, a, c0, nsl, C, rhs, y, yb));
+  PSCU_LAUNCHED(&c);
+}
+
+/// PSCU_WALK_TRACE=1: stamps of CTA 0 per sub-level, summarised on stderr
+/// after every walker launch (diagnostics only; synchronises the stream).
+static long long* trace_buffer() {
+  static long long* buf = [] {
+    long long* p = nullptr;
+    if (getenv("PSCU_WALK_TRACE")) cudaMalloc(&p, sizeof(long long) * kTraceSub * 16 * kMaxCluster);
+    return p;
+  }();
+  return buf;
+}
+
+static void trace_report(Context& c, bool fwd, int C, int nsl) {
+  const int ranks = C > 1 ? C : 1;
+  std::vector<long long> all(size_t(kTraceSub) * 16 * ranks);
+  PSCU_CUDA(cudaMemcpyAsync(all.data(), trace_buffer(), sizeof(long long) * all.size(),
+                            cudaMemcpyDeviceToHost, c.stream));
+  PSCU_CUDA(cudaStreamSynchronize(c.stream));
+  const int hi = std::min(nsl, kTraceSub) - 1;
+  if (hi <= 9) return;
+  for (int rk = 0; rk < ranks; ++rk) {
+    const long long* t = all.data() + size_t(rk) * kTraceSub * 16;
+    double d[8] = {0};
+    const int n = hi - 8;
+    for (int r = 8; r < hi; ++r) {
+      const long long* x = &t[size_t(r) * 16];
+      d[0] += x[1] - x[0];                  // consumer wait full
+      d[1] += x[2] - x[1];                  // products
+      d[2] += x[3] - x[2];                  // rows
+      d[3] += x[4] - x[3];                  // cluster handshake
+      d[4] += t[size_t(r + 1) * 16] - x[0];  // consumer loop
+      d[5] += x[9] - x[8];                  // producer wait empty
+      d[6] += x[10] - x[9];                 // TMA landing
+      d[7] += x[11] - x[10];                // out-of-ring products
+    }
+    fprintf(stderr,
+            "[walk trace %s C=%d rank=%d sub-levels=%d] cycles/sub-level: wait_full %.0f products "
+            "%.0f rows %.0f handshake %.0f | loop %.0f | producer: wait_empty %.0f landing %.0f "
+            "far %.0f\n",
+            fwd ? "fwd" : "bwd", C, rk, nsl, d[0] / n, d[1] / n, d[2] / n, d[3] / n, d[4] / n,
+            d[5] / n, d[6] / n, d[7] / n);
+  }
+}
+
+static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y, double* yb) {
+  WalkArgs a = args_of(w);
+  a.trace = trace_buffer();
   for (const WalkSeg& s : w.segments) {
     if (s.wide) {
       if (w.fwd) wide_kernel<true><<<148 * 4, 256, 0, c.stream>>>(a, s.s0, rhs, y, yb);
       else wide_kernel<false><<<148 * 4, 256, 0, c.stream>>>(a, s.s0, rhs, y, yb);
+      PSCU_LAUNCHED(&c);
     } else {
-      if (w.fwd)
-        walk_kernel<true><<<1, kWalkThreads + kProducers, walk_smem(), c.stream>>>(a, s.s0, s.s1, rhs, y, yb, experiment);
-      else
-        walk_kernel<false><<<1, kWalkThreads + kProducers, walk_smem(), c.stream>>>(a, s.s0, s.s1, rhs, y, yb, experiment);
+      // static out-of-ring sources of this launch: final now, gather them
+      const int64_t g0 = w.h_sl_s[s.s0], g1 = w.h_sl_s[s.s1];
+      if (g1 > g0) {
+        gather_static<<<grid1(g1 - g0), 256, 0, c.stream>>>(
+            g1 - g0, reinterpret_cast<const int2*>(w.sfar.p) + g0, y, w.sfv.p + g0);
+        PSCU_LAUNCHED(&c);
+      }
+      const int nch = s.s1 - s.s0;
+      if (w.flow) launch_flow(c, w.fwd, a, s.s0, nch, rhs, y, yb);
+      else launch_walker(c, w.fwd, a, s.s0, nch / w.C, w.C, rhs, y, yb);
+      if (a.trace) trace_report(c, w.fwd, w.flow ? 0 : w.C, w.flow ? nch : nch / w.C);
     }
-    PSCU_LAUNCHED(&c);
   }
 }
 
