@@ -114,6 +114,7 @@ struct WalkPlan {
   bool fwd = true;
   int C = 1;     // CTAs of the walker cluster (one chunk each per sub-level)
   bool flow = false;  // single-CTA dataflow walker
+  int S = 0;          // push walker: replicated ring slots per owner
   int nsub = 0;  // chunks
   int64_t npos = 0;
   std::vector<WalkSeg> segments;

@@ -228,40 +228,54 @@ __device__ __forceinline__ ulonglong2 ld_pair(const ulonglong2* p) {
 ///   kPairs true: {value bits, value bits ^ tag} in one relaxed 16-byte store.
 // two CTAs per SM (<= 128 registers) so up to 296 CTAs are co-resident:
 // n = 525k (the 256^2 coarse level) needs T = 65536 lanes = 256 CTAs
-template <bool kPairs>
-__global__ void __launch_bounds__(kStepThreads, 2)
-    arnoldi_step_kernel(int64_t n, int64_t T, int L, int epl, int j, double* __restrict__ wg,
+/// kL adjacent lanes per thread (the first tree level is then in-thread):
+/// kL = 2 halves the CTAs taking part in each grid-wide reduction.
+template <int kL>
+struct StepShape {
+  static constexpr int kE = kL == 1 ? kEpt : 10;  // elements per lane held in registers
+};
+
+template <int kL, bool kPairs>
+__global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
+    arnoldi_step_kernel(int64_t n, int64_t T, int epl, int j, double* __restrict__ wg,
                         double* V, int64_t ldv, double* __restrict__ hcol,
                         double* __restrict__ slot_v, unsigned long long* slot_tag,
                         unsigned long long tag_base) {
-  // one lane per thread (L == 1): w, v_{i-1} and v_i stay in registers and
-  // v_{i+1} is prefetched while the grid-wide reduction of pass i completes
+  // w, v_{i-1} and v_i stay in registers and v_{i+1} is prefetched while the
+  // grid-wide reduction of pass i completes
+  constexpr int kE = StepShape<kL>::kE;
   __shared__ double hsh;
   const int G = gridDim.x;
   const int tid = threadIdx.x;
-  const int64_t lane = int64_t(blockIdx.x) * kStepThreads + tid;
-  double w[kEpt], pv[kEpt], iv[kEpt];
+  const int64_t lane0 = (int64_t(blockIdx.x) * kStepThreads + tid) * kL;
+  double w[kL][kE], pv[kL][kE], iv[kL][kE];
 #pragma unroll
-  for (int k = 0; k < kEpt; ++k) {
-    const int64_t e = lane + int64_t(k) * T;
-    const bool ok = k < epl && e < n;
-    w[k] = ok ? wg[e] : 0.0;
-    iv[k] = ok ? __ldcg(V + e) : 0.0;  // v_0
-    pv[k] = 0.0;
-  }
+  for (int l = 0; l < kL; ++l)
+#pragma unroll
+    for (int k = 0; k < kE; ++k) {
+      const int64_t e = lane0 + l + int64_t(k) * T;
+      const bool ok = k < epl && e < n;
+      w[l][k] = ok ? wg[e] : 0.0;
+      iv[l][k] = ok ? __ldcg(V + e) : 0.0;  // v_0
+      pv[l][k] = 0.0;
+    }
   double hprev = 0.0;
   for (int i = 0; i <= j + 1; ++i) {
-    double acc = 0.0;
+    double acc[kL];
 #pragma unroll
-    for (int k = 0; k < kEpt; ++k) {
-      const int64_t e = lane + int64_t(k) * T;
-      if (k < epl && e < n) {
-        if (i > 0) w[k] = dsub(w[k], dmul(hprev, pv[k]));
-        const double o = i <= j ? iv[k] : w[k];
-        acc = dadd(acc, dmul(w[k], o));
+    for (int l = 0; l < kL; ++l) {
+      acc[l] = 0.0;
+#pragma unroll
+      for (int k = 0; k < kE; ++k) {
+        const int64_t e = lane0 + l + int64_t(k) * T;
+        if (k < epl && e < n) {
+          if (i > 0) w[l][k] = dsub(w[l][k], dmul(hprev, pv[l][k]));
+          const double o = i <= j ? iv[l][k] : w[l][k];
+          acc[l] = dadd(acc[l], dmul(w[l][k], o));
+        }
       }
     }
-    const double cta = block_tree(acc, kStepThreads);
+    const double cta = block_tree(kL == 1 ? acc[0] : dadd(acc[0], acc[kL - 1]), kStepThreads);
     const int par = i & 1;
     const unsigned long long want = tag_base + unsigned(i) + 1ull;
     if (tid == 0) {
@@ -277,14 +291,18 @@ __global__ void __launch_bounds__(kStepThreads, 2)
     if (i + 1 <= j) {
       const double* vn = V + int64_t(i + 1) * ldv;
 #pragma unroll
-      for (int k = 0; k < kEpt; ++k) {
-        const int64_t e = lane + int64_t(k) * T;
-        pv[k] = iv[k];
-        iv[k] = (k < epl && e < n) ? __ldcg(vn + e) : 0.0;
-      }
+      for (int l = 0; l < kL; ++l)
+#pragma unroll
+        for (int k = 0; k < kE; ++k) {
+          const int64_t e = lane0 + l + int64_t(k) * T;
+          pv[l][k] = iv[l][k];
+          iv[l][k] = (k < epl && e < n) ? __ldcg(vn + e) : 0.0;
+        }
     } else {
 #pragma unroll
-      for (int k = 0; k < kEpt; ++k) pv[k] = iv[k];
+      for (int l = 0; l < kL; ++l)
+#pragma unroll
+        for (int k = 0; k < kE; ++k) pv[l][k] = iv[l][k];
     }
     if (kPairs) {
       // relaxed 16-byte {value, value ^ tag} pairs: a pair is accepted only
@@ -346,10 +364,12 @@ __global__ void __launch_bounds__(kStepThreads, 2)
   // v_{j+1} = w / h, or 0 on a happy breakdown (gmres.hpp:66-67)
   double* vn = V + int64_t(j + 1) * ldv;
 #pragma unroll
-  for (int k = 0; k < kEpt; ++k) {
-    const int64_t e = lane + int64_t(k) * T;
-    if (k < epl && e < n) vn[e] = hprev > 0.0 ? __ddiv_rn(w[k], hprev) : 0.0;
-  }
+  for (int l = 0; l < kL; ++l)
+#pragma unroll
+    for (int k = 0; k < kE; ++k) {
+      const int64_t e = lane0 + l + int64_t(k) * T;
+      if (k < epl && e < n) vn[e] = hprev > 0.0 ? __ddiv_rn(w[l][k], hprev) : 0.0;
+    }
 }
 
 } // namespace
@@ -366,23 +386,31 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
   static int sm_count = 0;
   if (!sm_count)
     PSCU_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, c.device));
-  for (int L = 1; L <= 1; L <<= 1) {
+  static const bool pairs = [] {
+    const char* e = getenv("PSCU_MGS_PAIRS");
+    return e ? atoi(e) != 0 : true;
+  }();
+  static const int max_lanes = [] {
+    const char* e = getenv("PSCU_MGS_LANES");
+    return e ? atoi(e) : 2;
+  }();
+  // two lanes per thread when that keeps >= 64 CTAs (fewer participants per
+  // grid-wide reduction) and the elements fit the kL = 2 register budget
+  for (int L = (max_lanes >= 2 && T / (2 * kStepThreads) >= 64 && epl <= StepShape<2>::kE) ? 2 : 1;
+       L >= 1; L >>= 1) {
     const int64_t G = T / (int64_t(kStepThreads) * L);
     if (G < 1 || G > 1024) continue;
     const size_t smem = 0;
     int per_sm = 0;
-    static const bool pairs = [] {
-      const char* e = getenv("PSCU_MGS_PAIRS");
-      return e ? atoi(e) != 0 : true;
-    }();
-    void* fn = pairs ? (void*)arnoldi_step_kernel<true> : (void*)arnoldi_step_kernel<false>;
+    void* fn = L == 2 ? (pairs ? (void*)arnoldi_step_kernel<2, true> : (void*)arnoldi_step_kernel<2, false>)
+                      : (pairs ? (void*)arnoldi_step_kernel<1, true> : (void*)arnoldi_step_kernel<1, false>);
     PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kStepThreads, smem));
     if (int64_t(per_sm) * sm_count < G) continue;
     if (c.slot_tag.n < size_t(2 * G)) {
       c.slot_tag.alloc(2048);
       PSCU_CUDA(cudaMemsetAsync(c.slot_tag.p, 0, sizeof(unsigned long long) * 2048, c.stream));
     }
-    int Li = L, ei = epl, jj = j;
+    int ei = epl, jj = j;
     int64_t nn = n, TT = T, ld = ldv;
     double* pw = w;
     double* pV = V;
@@ -391,7 +419,7 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     unsigned long long* pt = c.slot_tag.p;
     unsigned long long base = c.pass_tag;
     c.pass_tag += unsigned(j + 2);
-    void* args[] = {&nn, &TT, &Li, &ei, &jj, &pw, &pV, &ld, &ph, &pv, &pt, &base};
+    void* args[] = {&nn, &TT, &ei, &jj, &pw, &pV, &ld, &ph, &pv, &pt, &base};
     PSCU_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(G)),
                                           dim3(kStepThreads), args, smem, c.stream));
     PSCU_LAUNCHED(&c);

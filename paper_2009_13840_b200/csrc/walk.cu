@@ -201,8 +201,8 @@ __device__ __forceinline__ void walk_products(Stage& st, double* ring, int rank)
 /// yb) after the sub-level's cluster handshake, whose release fence then
 /// never waits on these global stores.
 template <bool kFwd>
-__device__ __forceinline__ bool walk_rows(const Stage& st, double* ring, double& acc, int4& m) {
-  const int nr = st.hdr[1], r0 = st.hdr[4];
+__device__ __forceinline__ bool walk_rows(const Stage& st, double& acc, int4& m) {
+  const int nr = st.hdr[1];
   const int t = threadIdx.x;  // kStageRows == kWalkThreads: one row per thread
   if (t >= nr) return false;
   m = st.meta[t];
@@ -220,8 +220,66 @@ __device__ __forceinline__ bool walk_rows(const Stage& st, double* ring, double&
       if (u0 + u < len) acc = dsub(acc, v[u]);
   }
   if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
-  ring[(r0 + t) & (kRing - 1)] = acc;
   return true;
+}
+
+/// Producer side (warp-specialised): group g of kWarps warps owns stage slot
+/// g and stages sub-levels g, g + kS, ...: TMA bulk copies of the chunk, then
+/// the products of its out-of-ring entries (static sources gathered into sfv
+/// before the launch; in-segment ones >= 8 sub-levels old, complete since
+/// every CTA finished sub-level r - kS). Thread index relative to the first
+/// producer thread (kWalkThreads).
+template <bool kFwd, int kS, int kWarps>
+__device__ __forceinline__ void produce(const WalkArgs& a, int c0, int nsl, int C, unsigned rank,
+                                        Stage* stages, uint64_t* landed, uint64_t* full,
+                                        uint64_t* empty, const double* rhs, const double* y) {
+  constexpr int kGroup = 32 * kWarps;
+  const int pg = (threadIdx.x - kWalkThreads) / kGroup;
+  const int lane = (threadIdx.x - kWalkThreads) % kGroup;
+  const int slot = pg;
+  for (int r = pg; r < nsl; r += kS) {
+    const int ch = c0 + r * C + int(rank);
+    const unsigned ph = unsigned((r / kS) & 1);
+    WALK_TRACE(lane == 0, r, 8);
+    if (r >= kS) mbar_wait(&empty[slot], ph ^ 1u);
+    WALK_TRACE(lane == 0, r, 9);
+    if (lane == 0) issue<kFwd>(a, ch, stages[slot], &landed[slot], rhs);
+    const int64_t s0 = a.sl_s[ch], ns = a.sl_s[ch + 1] - s0;
+    const int64_t f0 = a.sl_f[ch], nf = a.sl_f[ch + 1] - f0;
+    double* val = stages[slot].val;
+    mbar_wait(&landed[slot], ph);
+    WALK_TRACE(lane == 0, r, 10);
+    for (int64_t base = 0; base < ns; base += 8 * kGroup) {
+      int off[8];
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t f = base + u * kGroup + lane;
+        off[u] = f < ns ? __ldg(&a.sfar[s0 + f].x) : -1;
+        v[u] = f < ns ? __ldg(a.sfv + s0 + f) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (off[u] >= 0) val[off[u]] = dmul(val[off[u]], v[u]);
+    }
+    for (int64_t base = 0; base < nf; base += 4 * kGroup) {
+      int2 e[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t f = base + u * kGroup + lane;
+        e[u] = f < nf ? __ldg(a.far + f0 + f) : make_int2(-1, 0);
+      }
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = e[u].x >= 0 ? __ldcg(y + e[u].y) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (e[u].x >= 0) val[e[u].x] = dmul(val[e[u].x], v[u]);
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(2 + pg), "n"(kGroup) : "memory");
+    WALK_TRACE(lane == 0, r, 11);
+    if (lane == 0) mbar_arrive(&full[slot]);
+  }
 }
 
 /// CTA `rank` of a C-CTA cluster walks chunks c0 + rank, c0 + rank + C, ...
@@ -250,57 +308,7 @@ __global__ void __launch_bounds__(kWalkThreads + kProducers, 1)
   if (C > 1) cluster_sync_all();
   else __syncthreads();
   if (threadIdx.x >= kWalkThreads) {
-    // producer group g (kProdWarps warps) owns slot g: sub-levels g, g + kStages, ...
-    constexpr int kGroup = 32 * kProdWarps;
-    const int pg = (threadIdx.x - kWalkThreads) / kGroup;
-    const int lane = (threadIdx.x - kWalkThreads) % kGroup;
-    const int slot = pg;
-    for (int r = pg; r < nsl; r += kStages) {
-      const int ch = c0 + r * C + int(rank);
-      const unsigned ph = unsigned((r / kStages) & 1);
-      WALK_TRACE(lane == 0, r, 8);
-      if (r >= kStages) mbar_wait(&empty[slot], ph ^ 1u);
-      WALK_TRACE(lane == 0, r, 9);
-      if (lane == 0) issue<kFwd>(a, ch, stages[slot], &landed[slot], rhs);
-      // out-of-ring sources: static ones (earlier launches) were gathered
-      // into sfv before this launch; in-segment ones are >= 8 sub-levels old,
-      // final since every CTA finished sub-level r - kStages
-      const int64_t s0 = a.sl_s[ch], ns = a.sl_s[ch + 1] - s0;
-      const int64_t f0 = a.sl_f[ch], nf = a.sl_f[ch + 1] - f0;
-      double* val = stages[slot].val;
-      mbar_wait(&landed[slot], ph);
-      WALK_TRACE(lane == 0, r, 10);
-      for (int64_t base = 0; base < ns; base += 8 * kGroup) {
-        int off[8];
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int64_t f = base + u * kGroup + lane;
-          off[u] = f < ns ? __ldg(&a.sfar[s0 + f].x) : -1;
-          v[u] = f < ns ? __ldg(a.sfv + s0 + f) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (off[u] >= 0) val[off[u]] = dmul(val[off[u]], v[u]);
-      }
-      for (int64_t base = 0; base < nf; base += 4 * kGroup) {
-        int2 e[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t f = base + u * kGroup + lane;
-          e[u] = f < nf ? __ldg(a.far + f0 + f) : make_int2(-1, 0);
-        }
-        double v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = e[u].x >= 0 ? __ldcg(y + e[u].y) : 0.0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (e[u].x >= 0) val[e[u].x] = dmul(val[e[u].x], v[u]);
-      }
-      asm volatile("bar.sync %0, %1;" ::"r"(2 + pg), "n"(kGroup) : "memory");
-      WALK_TRACE(lane == 0, r, 11);
-      if (lane == 0) mbar_arrive(&full[slot]);
-    }
+    produce<kFwd, kStages, kProdWarps>(a, c0, nsl, C, rank, stages, landed, full, empty, rhs, y);
   } else {
     for (int r = 0; r < nsl; ++r) {
       const int slot = r % kStages;
@@ -314,7 +322,8 @@ __global__ void __launch_bounds__(kWalkThreads + kProducers, 1)
       WALK_TRACE(threadIdx.x == 0, r, 2);
       double acc;
       int4 m;
-      const bool mine = walk_rows<kFwd>(st, ring, acc, m);
+      const bool mine = walk_rows<kFwd>(st, acc, m);
+      if (mine) ring[(st.hdr[4] + int(threadIdx.x)) & (kRing - 1)] = acc;
       asm volatile("bar.sync 1, %0;" ::"n"(kWalkThreads) : "memory");
       WALK_TRACE(threadIdx.x == 0, r, 3);
       if (C > 1) {
@@ -503,6 +512,129 @@ __global__ void __launch_bounds__(kWalkThreads + 64 * kFlowStages, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Push walker (cluster of C CTAs, sweeps without in-segment out-of-ring
+// sources): every CTA keeps a replica of all C rings (kRingTotal / C recent
+// positions per owner) and pushes each row it computes into every peer's
+// replica with st.async, completing the peer's per-sub-level mbarrier. A
+// sub-level then waits only for the bytes of the previous one to land: no
+// release fences, and every ring read is local.
+// ---------------------------------------------------------------------------
+
+constexpr int kRingTotal = 8192;  // replicated ring slots (all owners)
+constexpr int kSide = 2048;       // long-range slots: values read beyond the ring window
+constexpr int kPushStages = 3;
+constexpr int kPushProdWarps = 4;
+
+__device__ __forceinline__ void push_value(unsigned raddr, double v, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                   raddr),
+               "d"(v), "r"(rbar)
+               : "memory");
+}
+
+template <bool kFwd>
+__global__ void __launch_bounds__(kWalkThreads + 32 * kPushProdWarps * kPushStages, 1)
+    push_kernel(WalkArgs a, int c0, int nsl, int C, int S, const double* rhs, double* y,
+                double* yb) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t landed[kPushStages], full[kPushStages], empty[kPushStages],
+      recv[2];
+  double* ring = reinterpret_cast<double*>(smraw);  // kRingTotal ring + kSide long-range slots
+  Stage* stages = reinterpret_cast<Stage*>(smraw + sizeof(double) * (kRingTotal + kSide));
+  const unsigned rank = cluster_rank();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPushStages; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&landed[i])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[i])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&empty[i])) : "memory");
+    }
+    for (int i = 0; i < 2; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&recv[i])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster_sync_all();
+  if (threadIdx.x >= kWalkThreads) {
+    produce<kFwd, kPushStages, kPushProdWarps>(a, c0, nsl, C, rank, stages, landed, full, empty,
+                                               rhs, y);
+  } else {
+    const int t = threadIdx.x;
+    for (int r = 0; r < nsl; ++r) {
+      const int slot = r % kPushStages;
+      WALK_TRACE(t == 0, r, 0);
+      mbar_wait(&full[slot], unsigned((r / kPushStages) & 1));
+      Stage& st = stages[slot];
+      if (t == 0) {
+        // bytes the peers push during this sub-level (they may land first:
+        // the transaction count goes negative until this arrive)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         smem_addr(&recv[r & 1])),
+                     "r"(unsigned(st.hdr[7]))
+                     : "memory");
+      }
+      if (r > 0) mbar_wait(&recv[(r - 1) & 1], unsigned(((r - 1) >> 1) & 1));
+      WALK_TRACE(t == 0, r, 1);
+      {
+        constexpr int kPer = (kMaxNz + kWalkThreads - 1) / kWalkThreads;
+        const int nq = st.hdr[2];
+        int sv[kPer];
+        double pv[kPer], yv[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int q = t + u * kWalkThreads;
+          sv[u] = q < nq ? st.src[q] : -1;
+          pv[u] = q < nq ? st.val[q] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) yv[u] = ring[sv[u] >= 0 ? sv[u] : 0];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int q = t + u * kWalkThreads;
+          if (sv[u] >= 0) st.val[q] = dmul(pv[u], yv[u]);
+        }
+      }
+      // ring reads (generic proxy) before peers' st.async rewrite the slots
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kWalkThreads) : "memory");
+      WALK_TRACE(t == 0, r, 2);
+      double acc;
+      int4 m;
+      const bool mine = walk_rows<kFwd>(st, acc, m);
+      if (mine) {
+        const int pos = st.hdr[4] + t;
+        ring[int(rank) * S + (pos & (S - 1))] = acc;
+        const unsigned local = smem_addr(ring + int(rank) * S + (pos & (S - 1)));
+        // a value read beyond the ring window also goes to its long-range slot
+        const unsigned side = m.w ? smem_addr(ring + kRingTotal + m.w - 1) : 0u;
+        if (m.w) ring[kRingTotal + m.w - 1] = acc;
+        for (int o = 0; o < C; ++o) {
+          if (o == int(rank)) continue;
+          unsigned ra, rb;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(o));
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb)
+                       : "r"(smem_addr(&recv[r & 1])), "r"(o));
+          push_value(ra, acc, rb);
+          if (side) {
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(side), "r"(o));
+            push_value(ra, acc, rb);
+          }
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kWalkThreads) : "memory");
+      WALK_TRACE(t == 0, r, 3);
+      WALK_TRACE(t == 0, r, 4);
+      if (mine) {
+        y[m.y] = acc;
+        if (kFwd) yb[m.z] = acc;
+      }
+      if (t == 0) mbar_arrive(&empty[slot]);
+    }
+    // the last sub-level's pushes must land before any CTA leaves
+    if (nsl > 0) mbar_wait(&recv[(nsl - 1) & 1], unsigned(((nsl - 1) >> 1) & 1));
+  }
+  cluster_sync_all();
+}
+
 /// Row-parallel chunk (a level too wide for one CTA): global sources.
 template <bool kFwd>
 __global__ void wide_kernel(WalkArgs a, int ch, const double* rhs, double* y, double* yb) {
@@ -584,6 +716,9 @@ std::vector<int32_t> dag_levels(const Csr& a, const std::vector<int64_t>& diag, 
 struct HostPlan {
   int C = 1;
   bool flow = false;  // single-CTA dataflow walker (flow_kernel), chunks span levels
+  int S = 0;          // push walker: replicated ring slots per owner (0: classic walker)
+  bool push_ok = true;
+  std::vector<int32_t> side;  // push walker: long-range slot + 1 of a row (0: none), by row
   std::vector<int32_t> sl_k, sl_nr, sl_nq, sl_nfar, sl_r0, rows, off, src, pos;
   std::vector<int32_t> far, sfar;  // pairs {entry offset in chunk, source row}
   std::vector<int64_t> sl_f, sl_s, sl_q, from, dfrom;
@@ -594,7 +729,7 @@ struct HostPlan {
 
 /// Positions, chunks and packed operands of one sweep for a C-CTA walker.
 void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C, bool flow,
-                HostPlan& h) {
+                int S, HostPlan& h) {
   const int64_t n = a.n;
   const auto& rp = a.h_row_ptr;
   const auto& cols = a.h_cols;
@@ -615,6 +750,7 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
   h = HostPlan{};
   h.C = C;
   h.flow = flow;
+  h.S = S;
   h.pos.assign(n, -1);
   std::vector<int32_t> lpos(n, -1), chunk_of_row(n, -1);
   std::vector<int64_t> lcount(C, 0);  // per-CTA local positions (ring index)
@@ -762,6 +898,8 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
   // end of this chunk's sub-level
   h.sl_d.assign(nch, 0);
   h.sl_nd.assign(nch, 0);
+  if (S) h.side.assign(n, 0);
+  int side_seg = -1, side_next = 0;
   for (int c = 0; c < nch; ++c) {
     int nf = 0, ns = 0;
     const int sub = (c - seg_first[c]) / C;
@@ -803,7 +941,14 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
         const int cj = chunk_of_row[jr];
         bool in_ring = false;
         int owner = 0;
-        if (flow && !h.sl_wide[cj] && seg_of[cj] == seg_of[c]) {
+        if (S && !h.sl_wide[cj] && seg_of[cj] == seg_of[c]) {
+          // push walker: the owner's replica slot is rewritten once the owner
+          // runs past the next sub-level (peers are at most one ahead)
+          owner = (cj - seg_first[cj]) % C;
+          const int nx = sub_first + C + owner;
+          const int oc = (nx < nch && seg_of[nx] == seg_of[c]) ? nx : sub_first + owner;
+          in_ring = int64_t(h.sl_r0[oc]) + h.sl_nr[oc] - int64_t(lpos[jr]) <= S;
+        } else if (flow && !h.sl_wide[cj] && seg_of[cj] == seg_of[c]) {
           // dataflow: position s is overwritten by s + kRing, written no
           // earlier than chunk c + 2 (consumers run at most two chunks apart)
           const int cn = (c + 1 < nch && seg_of[c + 1] == seg_of[c]) ? c + 1 : c;
@@ -819,13 +964,28 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
         }
         if (in_ring) {
           // dataflow walker: the source's position (slot and readiness tag)
-          h.src[qq] = flow ? lpos[jr] : (owner << 12) | (lpos[jr] & (kRing - 1));
+          h.src[qq] = S      ? owner * S + (lpos[jr] & (S - 1))
+                      : flow ? lpos[jr]
+                             : (owner << 12) | (lpos[jr] & (kRing - 1));
         } else if (h.sl_wide[cj] || seg_of[cj] != seg_of[c]) {
           // final before this launch: gathered into sfv, product by a producer
           h.src[qq] = -1;
           h.sfar.push_back(int32_t(e));
           h.sfar.push_back(jr);
           ++ns;
+        } else if (S) {
+          // push walker: out of the ring window, read from the source's
+          // long-range slot (its owner pushes it there as well)
+          if (h.side[jr] == 0) {
+            const int seg_id = seg_of[c];
+            if (side_seg != seg_id) {
+              side_seg = seg_id;
+              side_next = 0;
+            }
+            if (side_next == kSide) h.push_ok = false;
+            else h.side[jr] = ++side_next;
+          }
+          h.src[qq] = kRingTotal + (h.side[jr] > 0 ? h.side[jr] - 1 : 0);
         } else {
           // out of the ring window: a producer forms this product from y
           h.src[qq] = -1;
@@ -842,9 +1002,9 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
   }
 }
 
-/// Cluster size for a sweep: one CTA when an average level fits one chunk
-/// (no handshakes), else a cluster of kMaxCluster CTAs, whose rings also keep
-/// the wide fine-level wavefronts resident (measured: tools/sweep_cluster.sh).
+/// Cluster size for a sweep (measured: tools/sweep_cluster.sh): two CTAs when
+/// an average level fits about one chunk, else kMaxCluster CTAs, whose rings
+/// also keep the wide fine-level wavefronts resident.
 int pick_cluster(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
   if (const char* e = getenv(fwd ? "PSCU_WALK_CLUSTER_FWD" : "PSCU_WALK_CLUSTER_BWD"))
     return std::max(1, std::min(kMaxCluster, atoi(e)));
@@ -864,15 +1024,22 @@ int pick_cluster(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
       ++cnt;
     }
   if (!cnt) return 1;
-  return (2 * nr <= 3 * int64_t(kStageRows) * cnt && nq <= int64_t(kMaxNz) * cnt) ? 1 : kMaxCluster;
+  // narrow sweeps (the coarse level): a pair of CTAs with the push walker
+  // (tools/sweep_cluster.sh at 256^2: 1.71 ms per coarse apply vs 2.24 ms
+  // for one CTA); wide sweeps: kMaxCluster
+  return (2 * nr <= 3 * int64_t(kStageRows) * cnt && nq <= int64_t(kMaxNz) * cnt) ? 2 : kMaxCluster;
 }
 
 HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
   HostPlan h;
   const int C = pick_cluster(a, diag, fwd);
+  if (C > 1 && !getenv("PSCU_WALK_NOPUSH")) {
+    plan_sweep(a, diag, fwd, C, false, kRingTotal / C, h);
+    if (h.push_ok) return h;
+  }
   // the dataflow walker is correct but not yet faster than the level walker
   const bool flow = C == 1 && getenv("PSCU_WALK_FLOW");
-  plan_sweep(a, diag, fwd, C, flow, h);
+  plan_sweep(a, diag, fwd, C, flow, 0, h);
   return h;
 }
 
@@ -881,6 +1048,7 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   w.fwd = fwd;
   w.C = h.C;
   w.flow = h.flow;
+  w.S = h.S;
   w.nsub = int(h.sl_k.size());
   w.npos = h.npos;
   w.segments.clear();
@@ -910,6 +1078,22 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
       hdr[size_t(s) * 8 + 4] = h.sl_r0[s];
       hdr[size_t(s) * 8 + 5] = h.sl_nd[s];
       hdr[size_t(s) * 8 + 6] = h.sl_d[s];
+      if (h.S && !h.sl_wide[s]) {
+        // bytes the peers of this chunk push during its sub-level
+        int first = s;
+        while (first > 0 && !h.sl_wide[first - 1]) --first;
+        const int sf = first + (s - first) / h.C * h.C;
+        int rows = 0;
+        for (int o = 0; o < h.C; ++o) {
+          if (sf + o == s) continue;
+          rows += h.sl_nr[sf + o];
+          for (int t = 0; t < h.sl_nr[sf + o]; ++t) {
+            const int32_t i = h.rows[h.sl_k[sf + o] + t];
+            if (h.side[i]) ++rows;  // long-range copy
+          }
+        }
+        hdr[size_t(s) * 8 + 7] = 8 * rows;
+      }
     }
     w.sl_hdr.upload(hdr, st);
   }
@@ -947,7 +1131,8 @@ void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, Walk
     const HostPlan& h = dir ? hb : hf;
     std::vector<int4> meta(h.rows.size());
     for (size_t k = 0; k < h.rows.size(); ++k)
-      meta[k] = make_int4(h.off[k], h.rows[k] >= 0 ? h.rows[k] : 0, dir ? 0 : opos[k], 0);
+      meta[k] = make_int4(h.off[k], h.rows[k] >= 0 ? h.rows[k] : 0, dir ? 0 : opos[k],
+                          h.S && h.rows[k] >= 0 ? h.side[h.rows[k]] : 0);
     (dir ? wb : wf).meta.upload(meta, c.stream);
   }
   wf.scratch.alloc(size_t(hf.npos) + 8);  // rhs in forward position order
@@ -963,9 +1148,10 @@ void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, Walk
       int nw = 0;
       for (auto x : h->sl_wide) nw += x;
       fprintf(stderr,
-              "[walk %s] n=%lld cluster=%d chunks=%zu (wide %d) positions=%lld ring=%lld "
+              "[walk %s] n=%lld cluster=%d %s chunks=%zu (wide %d) positions=%lld ring=%lld "
               "far=%lld\n",
-              h == &hf ? "fwd" : "bwd", (long long)a.n, h->C, h->sl_k.size(), nw,
+              h == &hf ? "fwd" : "bwd", (long long)a.n, h->C,
+              h->S ? "push" : (h->flow ? "flow" : "level"), h->sl_k.size(), nw,
               (long long)h->npos, (long long)ring, (long long)far);
     }
   }
@@ -998,6 +1184,36 @@ static void launch_flow(Context& c, bool fwd, const WalkArgs& a, int c0, int nch
   const unsigned threads = kWalkThreads + 64 * kFlowStages;
   if (fwd) flow_kernel<true><<<1, threads, flow_smem(), c.stream>>>(a, c0, nch, rhs, y, yb);
   else flow_kernel<false><<<1, threads, flow_smem(), c.stream>>>(a, c0, nch, rhs, y, yb);
+  PSCU_LAUNCHED(&c);
+}
+
+size_t push_smem() { return sizeof(double) * (kRingTotal + kSide) + kPushStages * sizeof(Stage); }
+
+static void launch_push(Context& c, bool fwd, const WalkArgs& a, int c0, int nsl, int C, int S,
+                        const double* rhs, double* y, double* yb) {
+  static bool attr = false;
+  if (!attr) {
+    for (void* f : {(void*)push_kernel<true>, (void*)push_kernel<false>}) {
+      PSCU_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(push_smem())));
+      PSCU_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(C));
+  cfg.blockDim = dim3(kWalkThreads + 32 * kPushProdWarps * kPushStages);
+  cfg.dynamicSmemBytes = push_smem();
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(C);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (fwd) PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<true>, a, c0, nsl, C, S, rhs, y, yb));
+  else PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<false>, a, c0, nsl, C, S, rhs, y, yb));
   PSCU_LAUNCHED(&c);
 }
 
@@ -1088,7 +1304,8 @@ static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y,
         PSCU_LAUNCHED(&c);
       }
       const int nch = s.s1 - s.s0;
-      if (w.flow) launch_flow(c, w.fwd, a, s.s0, nch, rhs, y, yb);
+      if (w.S) launch_push(c, w.fwd, a, s.s0, nch / w.C, w.C, w.S, rhs, y, yb);
+      else if (w.flow) launch_flow(c, w.fwd, a, s.s0, nch, rhs, y, yb);
       else launch_walker(c, w.fwd, a, s.s0, nch / w.C, w.C, rhs, y, yb);
       if (a.trace) trace_report(c, w.fwd, w.flow ? 0 : w.C, w.flow ? nch : nch / w.C);
     }
