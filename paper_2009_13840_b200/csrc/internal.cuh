@@ -131,6 +131,7 @@ struct Ilu {
   const Csr* a = nullptr;
   DevBuf<double> lu;
   DevBuf<int64_t> diag;
+  std::vector<int64_t> h_diag;   // diagonal positions (host, for the sweep plans)
   WalkPlan wfwd, wbwd;           // level walkers (application)
   std::vector<int32_t> flev_ptr; // forward DAG levels (factorisation launches)
   DevBuf<int32_t> flev_rows;
@@ -204,6 +205,10 @@ void upload_csr(Context& c, Csr& m, int64_t n, const int64_t* rp, const int32_t*
 
 // sptrsv.cu
 void ilu0_factor(Context& c, Ilu& ilu);
+/// ilu0_factor in two parts: pattern checks + factorisation launches, then
+/// (after the sweep plans are uploaded) the pivot check and value packing.
+void ilu0_factor_start(Context& c, Ilu& ilu);
+void ilu0_factor_finish(Context& c, Ilu& ilu);
 void ilu0_apply(Context& c, const Ilu& ilu, const double* x, double* y);
 
 // krylov.cu

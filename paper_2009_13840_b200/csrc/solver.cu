@@ -7,11 +7,15 @@
 // host with exactly the scalar code order of the reference (std::hypot is
 // not reproducible across libm and libdevice, so it stays on the host).
 #include <chrono>
+#include <exception>
+#include <thread>
+#include <cstdlib>
 #include <cmath>
 #include <memory>
 
 #include "internal.cuh"
 #include "solver.cuh"
+#include "walk.cuh"
 
 namespace pscu {
 
@@ -434,18 +438,59 @@ void Hierarchy::build(Context& c, const Csr* fine, const pscu_layout& lf, const 
     std::vector<int32_t> f2c(P.a->n, -1);
     for (int64_t i = 0; i < P.nc; ++i) f2c[c2f[i]] = int32_t(i);
     P.f2c.upload(f2c, c.stream);
+    const auto t0 = std::chrono::steady_clock::now();
     inherit(c, *P.a, c2f, L.own);
     L.a = &L.own;
+    if (getenv("PSCU_DEBUG"))
+      fprintf(stderr, "[setup] inherit level %d: %.3f s\n", l,
+              std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  }
+  // ILU(0) levels: factorisation launches first (device), then the sweep
+  // plans of all levels in parallel host threads, then uploads and checks
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<int> ilu_levels;
+  for (int l = 0; l < nlev; ++l) {
+    Level& L = *levels[l];
+    if (l + 1 == nlev && cfg.coarse == PSCU_COARSE_LU) {
+      L.dense_lu.factor(c, *L.a);
+    } else {
+      L.ilu.a = L.a;
+      ilu0_factor_start(c, L.ilu);
+      ilu_levels.push_back(l);
+    }
+  }
+  {
+    std::vector<std::shared_ptr<WalkBuild>> plans(ilu_levels.size());
+    std::vector<std::exception_ptr> errs(ilu_levels.size());
+    std::vector<std::thread> th;
+    for (size_t k = 0; k < ilu_levels.size(); ++k)
+      th.emplace_back([&, k] {
+        try {
+          const Level& L = *levels[ilu_levels[k]];
+          plans[k] = plan_walk(*L.a, L.ilu.h_diag);
+        } catch (...) {
+          errs[k] = std::current_exception();
+        }
+      });
+    for (auto& t : th) t.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+    if (getenv("PSCU_DEBUG"))
+      fprintf(stderr, "[setup] factor launches + sweep plans: %.3f s\n",
+              std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    for (size_t k = 0; k < ilu_levels.size(); ++k) {
+      Level& L = *levels[ilu_levels[k]];
+      upload_walk(c, *L.a, *plans[k], L.ilu.wfwd, L.ilu.wbwd);
+      plans[k].reset();
+      ilu0_factor_finish(c, L.ilu);
+    }
+    if (getenv("PSCU_DEBUG"))
+      fprintf(stderr, "[setup] ILU levels ready: %.3f s\n",
+              std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
   }
   for (int l = 0; l < nlev; ++l) {
     Level& L = *levels[l];
     const bool bottom = l + 1 == nlev;
-    if (bottom && cfg.coarse == PSCU_COARSE_LU) {
-      L.dense_lu.factor(c, *L.a);
-    } else {
-      L.ilu.a = L.a;
-      ilu0_factor(c, L.ilu);
-    }
     const int64_t n = L.a->n;
     L.w.alloc(n);
     if (!bottom) {

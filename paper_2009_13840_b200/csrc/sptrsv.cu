@@ -8,6 +8,9 @@
 // bit-identical. Application: the level walkers of walk.cu.
 #include <algorithm>
 
+#include <chrono>
+#include <cstdlib>
+
 #include "internal.cuh"
 #include "walk.cuh"
 
@@ -43,11 +46,12 @@ __global__ void ilu0_factor_level(int nrows, const int32_t* __restrict__ rows,
 
 } // namespace
 
-void ilu0_factor(Context& c, Ilu& ilu) {
+void ilu0_factor_start(Context& c, Ilu& ilu) {
   const Csr& a = *ilu.a;
   if (a.n == 0) return;
   const int64_t n = a.n;
-  std::vector<int64_t> diag(n);
+  std::vector<int64_t>& diag = ilu.h_diag;
+  diag.assign(n, 0);
   for (int64_t i = 0; i < n; ++i) {
     const auto b = a.h_cols.begin() + a.h_row_ptr[i];
     const auto e = a.h_cols.begin() + a.h_row_ptr[i + 1];
@@ -76,8 +80,6 @@ void ilu0_factor(Context& c, Ilu& ilu) {
     for (int64_t i = 0; i < n; ++i) rows[fill[lvl[i]]++] = int32_t(i);
   }
   ilu.flev_rows.upload(rows, c.stream);
-  build_walk(c, a, diag, ilu.wfwd, ilu.wbwd);
-
   ilu.lu.alloc(a.nnz);
   PSCU_CUDA(cudaMemcpyAsync(ilu.lu.p, a.vals.p, sizeof(double) * a.nnz, cudaMemcpyDeviceToDevice,
                             c.stream));
@@ -91,6 +93,11 @@ void ilu0_factor(Context& c, Ilu& ilu) {
                                                    c.err_flag.p);
     PSCU_LAUNCHED(&c);
   }
+}
+
+void ilu0_factor_finish(Context& c, Ilu& ilu) {
+  if (ilu.a->n == 0) return;
+  const int big = 0x7fffffff;
   int bad = 0;
   PSCU_CUDA(cudaMemcpyAsync(&bad, c.err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   PSCU_CUDA(cudaStreamSynchronize(c.stream));
@@ -99,6 +106,18 @@ void ilu0_factor(Context& c, Ilu& ilu) {
                                     "; a fill-reducing or pivot-friendly ordering is needed");
   pack_walk(c, ilu.lu.p, ilu.wfwd);
   pack_walk(c, ilu.lu.p, ilu.wbwd);
+}
+
+void ilu0_factor(Context& c, Ilu& ilu) {
+  ilu0_factor_start(c, ilu);
+  if (ilu.a->n == 0) return;
+  // host planning of the sweeps overlaps the factorisation launches
+  const auto tw = std::chrono::steady_clock::now();
+  build_walk(c, *ilu.a, ilu.h_diag, ilu.wfwd, ilu.wbwd);
+  if (getenv("PSCU_DEBUG"))
+    fprintf(stderr, "[setup] walk plans n=%lld: %.3f s\n", (long long)ilu.a->n,
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - tw).count());
+  ilu0_factor_finish(c, ilu);
 }
 
 void ilu0_apply(Context& c, const Ilu& ilu, const double* x, double* y) {

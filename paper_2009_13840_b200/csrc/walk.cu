@@ -28,6 +28,9 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <exception>
+#include <memory>
+#include <thread>
 
 #include <cooperative_groups.h>
 
@@ -533,9 +536,41 @@ __device__ __forceinline__ void push_value(unsigned raddr, double v, unsigned rb
                : "memory");
 }
 
+/// Single-pass row: acc = rhs - sum_u val_u * ring[src_u] (products formed
+/// in place; out-of-ring entries already hold theirs). Local ring only.
+template <bool kFwd>
+__device__ __forceinline__ bool fused_rows(const Stage& st, const double* ring, double& acc,
+                                           int4& m) {
+  const int t = threadIdx.x;
+  if (t >= st.hdr[1]) return false;
+  m = st.meta[t];
+  const int len = m.x;
+  acc = st.rhs[t];
+  for (int u0 = 0; u0 < len; u0 += 8) {
+    const int4 d0 = *reinterpret_cast<const int4*>(st.dptr + u0);
+    const int4 d1 = *reinterpret_cast<const int4*>(st.dptr + u0 + 4);
+    const int d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+    int sv[8];
+    double v[8], w[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool ok = u0 + u < len;
+      sv[u] = ok ? st.src[d[u] + t] : -1;
+      v[u] = ok ? st.val[d[u] + t] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) w[u] = ring[sv[u] >= 0 ? sv[u] : 0];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u0 + u < len) acc = dsub(acc, sv[u] >= 0 ? dmul(v[u], w[u]) : v[u]);
+  }
+  if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
+  return true;
+}
+
 template <bool kFwd>
 __global__ void __launch_bounds__(kWalkThreads + 32 * kPushProdWarps * kPushStages, 1)
-    push_kernel(WalkArgs a, int c0, int nsl, int C, int S, const double* rhs, double* y,
+    push_kernel(WalkArgs a, int c0, int nsl, int C, int S, int fused, const double* rhs, double* y,
                 double* yb) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ __align__(8) uint64_t landed[kPushStages], full[kPushStages], empty[kPushStages],
@@ -574,7 +609,15 @@ __global__ void __launch_bounds__(kWalkThreads + 32 * kPushProdWarps * kPushStag
       }
       if (r > 0) mbar_wait(&recv[(r - 1) & 1], unsigned(((r - 1) >> 1) & 1));
       WALK_TRACE(t == 0, r, 1);
-      {
+      double acc;
+      int4 m;
+      bool mine;
+      if (fused) {
+        mine = fused_rows<kFwd>(st, ring, acc, m);
+        // ring reads (generic proxy) before peers' st.async rewrite the slots
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        WALK_TRACE(t == 0, r, 2);
+      } else {
         constexpr int kPer = (kMaxNz + kWalkThreads - 1) / kWalkThreads;
         const int nq = st.hdr[2];
         int sv[kPer];
@@ -592,14 +635,12 @@ __global__ void __launch_bounds__(kWalkThreads + 32 * kPushProdWarps * kPushStag
           const int q = t + u * kWalkThreads;
           if (sv[u] >= 0) st.val[q] = dmul(pv[u], yv[u]);
         }
+        // ring reads (generic proxy) before peers' st.async rewrite the slots
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(kWalkThreads) : "memory");
+        WALK_TRACE(t == 0, r, 2);
+        mine = walk_rows<kFwd>(st, acc, m);
       }
-      // ring reads (generic proxy) before peers' st.async rewrite the slots
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync 1, %0;" ::"n"(kWalkThreads) : "memory");
-      WALK_TRACE(t == 0, r, 2);
-      double acc;
-      int4 m;
-      const bool mine = walk_rows<kFwd>(st, acc, m);
       if (mine) {
         const int pos = st.hdr[4] + t;
         ring[int(rank) * S + (pos & (S - 1))] = acc;
@@ -901,6 +942,7 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
   if (S) h.side.assign(n, 0);
   int side_seg = -1, side_next = 0;
   for (int c = 0; c < nch; ++c) {
+    if (S && !h.push_ok) return;  // infeasible for the push walker: stop early
     int nf = 0, ns = 0;
     const int sub = (c - seg_first[c]) / C;
     const int sub_first = seg_first[c] + sub * C;
@@ -1114,11 +1156,32 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
 
 } // namespace
 
-void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, WalkPlan& wf,
-                WalkPlan& wb) {
+struct WalkBuild {
+  HostPlan f, b;
+};
+
+std::shared_ptr<WalkBuild> plan_walk(const Csr& a, const std::vector<int64_t>& diag) {
+  auto wb = std::make_shared<WalkBuild>();
+  if (a.n == 0) return wb;
+  // the two sweeps are independent host work
+  std::exception_ptr err;
+  std::thread tb([&] {
+    try {
+      wb->b = plan(a, diag, false);
+    } catch (...) {
+      err = std::current_exception();
+    }
+  });
+  wb->f = plan(a, diag, true);
+  tb.join();
+  if (err) std::rethrow_exception(err);
+  return wb;
+}
+
+void upload_walk(Context& c, const Csr& a, const WalkBuild& b, WalkPlan& wf, WalkPlan& wb) {
   if (a.n == 0) return;
-  const HostPlan hf = plan(a, diag, true);
-  const HostPlan hb = plan(a, diag, false);
+  const HostPlan& hf = b.f;
+  const HostPlan& hb = b.b;
   upload_plan(c, hf, true, wf);
   upload_plan(c, hb, false, wb);
   // forward results are written straight into backward position order
@@ -1155,6 +1218,11 @@ void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, Walk
               (long long)h->npos, (long long)ring, (long long)far);
     }
   }
+}
+
+void build_walk(Context& c, const Csr& a, const std::vector<int64_t>& diag, WalkPlan& wf,
+                WalkPlan& wb) {
+  upload_walk(c, a, *plan_walk(a, diag), wf, wb);
 }
 
 void pack_walk(Context& c, const double* lu, WalkPlan& w) {
@@ -1212,8 +1280,14 @@ static void launch_push(Context& c, bool fwd, const WalkArgs& a, int c0, int nsl
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (fwd) PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<true>, a, c0, nsl, C, S, rhs, y, yb));
-  else PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<false>, a, c0, nsl, C, S, rhs, y, yb));
+  static const int fused = [] {
+    const char* e = getenv("PSCU_WALK_FUSED");
+    return e ? atoi(e) : 0;
+  }();
+  if (fwd)
+    PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<true>, a, c0, nsl, C, S, fused, rhs, y, yb));
+  else
+    PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<false>, a, c0, nsl, C, S, fused, rhs, y, yb));
   PSCU_LAUNCHED(&c);
 }
 
