@@ -43,9 +43,15 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_native(force: bool = False, verbose: bool = False) -> str:
+def build_native(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """Builds libpstokes_b200.so. trace=True builds the walker-instrumented
+    variant (-DPSCU_TRACE; PSCU_WALK_TRACE=1 at run time) into
+    tools/libpstokes_trace.so instead (diagnostics: PSCU_LIB=<that path>)."""
     nvcc = _nvcc()
-    os.makedirs(OBJ, exist_ok=True)
+    obj_dir = os.path.join(PKG, "_build_trace") if trace else OBJ
+    lib = os.path.join(ROOT, "tools", "libpstokes_trace.so") if trace else LIB
+    flags = NVCC_FLAGS + (["-DPSCU_TRACE"] if trace else [])
+    os.makedirs(obj_dir, exist_ok=True)
     sources = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "pstokes_cuda.h"))
@@ -53,10 +59,10 @@ def build_native(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in sources:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJ, src[:-3] + ".o")
+        o = os.path.join(obj_dir, src[:-3] + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            jobs.append([nvcc, *NVCC_FLAGS, "-c", s, "-o", o])
+            jobs.append([nvcc, *flags, "-c", s, "-o", o])
 
     def run(cmd):
         if verbose:
@@ -67,9 +73,9 @@ def build_native(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
-    if force or jobs or _stale(LIB, objs):
-        run([nvcc, "-shared", "-o", LIB, *objs, "-lcudart"])
-    return LIB
+    if force or jobs or _stale(lib, objs):
+        run([nvcc, "-shared", "-o", lib, *objs, "-lcudart"])
+    return lib
 
 
 def build_host(force: bool = False) -> str:

@@ -74,11 +74,18 @@ struct WalkArgs {
 };
 
 constexpr int kTraceSub = 4096;
+// per-sub-level clock stamps: only in the instrumented build (build.py trace=True)
+#ifdef PSCU_TRACE
 #define WALK_TRACE(cond, r, k)                                       \
   do {                                                               \
     if (a.trace && (cond) && (r) < kTraceSub)                        \
       a.trace[((rank) * kTraceSub + (r)) * 16 + (k)] = clock64();    \
   } while (0)
+#else
+#define WALK_TRACE(cond, r, k) \
+  do {                         \
+  } while (0)
+#endif
 
 struct alignas(16) Stage {
   double val[kMaxNz];
@@ -232,13 +239,13 @@ __device__ __forceinline__ bool walk_rows(const Stage& st, double& acc, int4& m)
 /// before the launch; in-segment ones >= 8 sub-levels old, complete since
 /// every CTA finished sub-level r - kS). Thread index relative to the first
 /// producer thread (kWalkThreads).
-template <bool kFwd, int kS, int kWarps>
+template <bool kFwd, int kS, int kWarps, int kFirst = kWalkThreads>
 __device__ __forceinline__ void produce(const WalkArgs& a, int c0, int nsl, int C, unsigned rank,
                                         Stage* stages, uint64_t* landed, uint64_t* full,
                                         uint64_t* empty, const double* rhs, const double* y) {
   constexpr int kGroup = 32 * kWarps;
-  const int pg = (threadIdx.x - kWalkThreads) / kGroup;
-  const int lane = (threadIdx.x - kWalkThreads) % kGroup;
+  const int pg = (threadIdx.x - kFirst) / kGroup;
+  const int lane = (threadIdx.x - kFirst) % kGroup;
   const int slot = pg;
   for (int r = pg; r < nsl; r += kS) {
     const int ch = c0 + r * C + int(rank);
@@ -536,41 +543,46 @@ __device__ __forceinline__ void push_value(unsigned raddr, double v, unsigned rb
                : "memory");
 }
 
-/// Single-pass row: acc = rhs - sum_u val_u * ring[src_u] (products formed
-/// in place; out-of-ring entries already hold theirs). Local ring only.
+constexpr int kPushConsumers = 256;  // each consumer thread folds up to two rows
+
+/// One row of the push walker: acc = rhs - sum_u val_u * y(src_u), u
+/// ascending (the reference's order and rounding), sources read from the
+/// local ring replica; out-of-ring entries (src -1) already hold their
+/// product (producers). Diagonal-major entries: unit-stride warp loads.
 template <bool kFwd>
-__device__ __forceinline__ bool fused_rows(const Stage& st, const double* ring, double& acc,
-                                           int4& m) {
-  const int t = threadIdx.x;
-  if (t >= st.hdr[1]) return false;
-  m = st.meta[t];
+__device__ __forceinline__ double push_row(const Stage& st, const double* ring, int row,
+                                           const int4& m) {
   const int len = m.x;
-  acc = st.rhs[t];
-  for (int u0 = 0; u0 < len; u0 += 8) {
-    const int4 d0 = *reinterpret_cast<const int4*>(st.dptr + u0);
-    const int4 d1 = *reinterpret_cast<const int4*>(st.dptr + u0 + 4);
-    const int d[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-    int sv[8];
-    double v[8], w[8];
+  double acc = st.rhs[row];
+  int u = 0;
+  for (; u + 4 <= len; u += 4) {
+    const int4 d = *reinterpret_cast<const int4*>(st.dptr + u);
+    const int e[4] = {d.x + row, d.y + row, d.z + row, d.w + row};
+    int sv[4];
+    double v[4], w[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const bool ok = u0 + u < len;
-      sv[u] = ok ? st.src[d[u] + t] : -1;
-      v[u] = ok ? st.val[d[u] + t] : 0.0;
+    for (int k = 0; k < 4; ++k) {
+      sv[k] = st.src[e[k]];
+      v[k] = st.val[e[k]];
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) w[u] = ring[sv[u] >= 0 ? sv[u] : 0];
+    for (int k = 0; k < 4; ++k) w[k] = ring[sv[k] >= 0 ? sv[k] : 0];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (u0 + u < len) acc = dsub(acc, sv[u] >= 0 ? dmul(v[u], w[u]) : v[u]);
+    for (int k = 0; k < 4; ++k) acc = dsub(acc, sv[k] >= 0 ? dmul(v[k], w[k]) : v[k]);
   }
-  if (!kFwd) acc = __ddiv_rn(acc, st.dv[t]);
-  return true;
+  for (; u < len; ++u) {
+    const int e = st.dptr[u] + row;
+    const int sv = st.src[e];
+    const double v = st.val[e];
+    acc = dsub(acc, sv >= 0 ? dmul(v, ring[sv]) : v);
+  }
+  if (!kFwd) acc = __ddiv_rn(acc, st.dv[row]);
+  return acc;
 }
 
 template <bool kFwd>
-__global__ void __launch_bounds__(kWalkThreads + 32 * kPushProdWarps * kPushStages, 1)
-    push_kernel(WalkArgs a, int c0, int nsl, int C, int S, int fused, const double* rhs, double* y,
+__global__ void __launch_bounds__(kPushConsumers + 32 * kPushProdWarps * kPushStages, 1)
+    push_kernel(WalkArgs a, int c0, int nsl, int C, int S, const double* rhs, double* y,
                 double* yb) {
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ __align__(8) uint64_t landed[kPushStages], full[kPushStages], empty[kPushStages],
@@ -589,16 +601,16 @@ __global__ void __launch_bounds__(kWalkThreads + 32 * kPushProdWarps * kPushStag
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cluster_sync_all();
-  if (threadIdx.x >= kWalkThreads) {
-    produce<kFwd, kPushStages, kPushProdWarps>(a, c0, nsl, C, rank, stages, landed, full, empty,
-                                               rhs, y);
+  if (threadIdx.x >= kPushConsumers) {
+    produce<kFwd, kPushStages, kPushProdWarps, kPushConsumers>(a, c0, nsl, C, rank, stages,
+                                                               landed, full, empty, rhs, y);
   } else {
     const int t = threadIdx.x;
     for (int r = 0; r < nsl; ++r) {
       const int slot = r % kPushStages;
       WALK_TRACE(t == 0, r, 0);
       mbar_wait(&full[slot], unsigned((r / kPushStages) & 1));
-      Stage& st = stages[slot];
+      const Stage& st = stages[slot];
       if (t == 0) {
         // bytes the peers push during this sub-level (they may land first:
         // the transaction count goes negative until this arrive)
@@ -609,65 +621,38 @@ __global__ void __launch_bounds__(kWalkThreads + 32 * kPushProdWarps * kPushStag
       }
       if (r > 0) mbar_wait(&recv[(r - 1) & 1], unsigned(((r - 1) >> 1) & 1));
       WALK_TRACE(t == 0, r, 1);
-      double acc;
-      int4 m;
-      bool mine;
-      if (fused) {
-        mine = fused_rows<kFwd>(st, ring, acc, m);
-        // ring reads (generic proxy) before peers' st.async rewrite the slots
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        WALK_TRACE(t == 0, r, 2);
-      } else {
-        constexpr int kPer = (kMaxNz + kWalkThreads - 1) / kWalkThreads;
-        const int nq = st.hdr[2];
-        int sv[kPer];
-        double pv[kPer], yv[kPer];
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-          const int q = t + u * kWalkThreads;
-          sv[u] = q < nq ? st.src[q] : -1;
-          pv[u] = q < nq ? st.val[q] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) yv[u] = ring[sv[u] >= 0 ? sv[u] : 0];
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-          const int q = t + u * kWalkThreads;
-          if (sv[u] >= 0) st.val[q] = dmul(pv[u], yv[u]);
-        }
-        // ring reads (generic proxy) before peers' st.async rewrite the slots
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("bar.sync 1, %0;" ::"n"(kWalkThreads) : "memory");
-        WALK_TRACE(t == 0, r, 2);
-        mine = walk_rows<kFwd>(st, acc, m);
-      }
-      if (mine) {
-        const int pos = st.hdr[4] + t;
-        ring[int(rank) * S + (pos & (S - 1))] = acc;
-        const unsigned local = smem_addr(ring + int(rank) * S + (pos & (S - 1)));
+      WALK_TRACE(t == 0, r, 2);
+      const int nr = st.hdr[1], r0 = st.hdr[4];
+      const unsigned rbar = smem_addr(&recv[r & 1]);
+      for (int row = t; row < nr; row += kPushConsumers) {
+        const int4 m = st.meta[row];
+        const double acc = push_row<kFwd>(st, ring, row, m);
+        const int pos = r0 + row;
+        double* own = ring + int(rank) * S + (pos & (S - 1));
+        *own = acc;
         // a value read beyond the ring window also goes to its long-range slot
-        const unsigned side = m.w ? smem_addr(ring + kRingTotal + m.w - 1) : 0u;
         if (m.w) ring[kRingTotal + m.w - 1] = acc;
         for (int o = 0; o < C; ++o) {
           if (o == int(rank)) continue;
           unsigned ra, rb;
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(local), "r"(o));
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb)
-                       : "r"(smem_addr(&recv[r & 1])), "r"(o));
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(own)), "r"(o));
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(rbar), "r"(o));
           push_value(ra, acc, rb);
-          if (side) {
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(side), "r"(o));
+          if (m.w) {
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra)
+                         : "r"(smem_addr(ring + kRingTotal + m.w - 1)), "r"(o));
             push_value(ra, acc, rb);
           }
         }
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(kWalkThreads) : "memory");
-      WALK_TRACE(t == 0, r, 3);
-      WALK_TRACE(t == 0, r, 4);
-      if (mine) {
         y[m.y] = acc;
         if (kFwd) yb[m.z] = acc;
       }
+      // ring reads (generic proxy) ordered before peers' st.async rewrite
+      // the slots; the sub-level's own ring writes visible to all consumers
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kPushConsumers) : "memory");
+      WALK_TRACE(t == 0, r, 3);
+      WALK_TRACE(t == 0, r, 4);
       if (t == 0) mbar_arrive(&empty[slot]);
     }
     // the last sub-level's pushes must land before any CTA leaves
@@ -1270,7 +1255,7 @@ static void launch_push(Context& c, bool fwd, const WalkArgs& a, int c0, int nsl
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(C));
-  cfg.blockDim = dim3(kWalkThreads + 32 * kPushProdWarps * kPushStages);
+  cfg.blockDim = dim3(kPushConsumers + 32 * kPushProdWarps * kPushStages);
   cfg.dynamicSmemBytes = push_smem();
   cfg.stream = c.stream;
   cudaLaunchAttribute at[1];
@@ -1280,14 +1265,8 @@ static void launch_push(Context& c, bool fwd, const WalkArgs& a, int c0, int nsl
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  static const int fused = [] {
-    const char* e = getenv("PSCU_WALK_FUSED");
-    return e ? atoi(e) : 0;
-  }();
-  if (fwd)
-    PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<true>, a, c0, nsl, C, S, fused, rhs, y, yb));
-  else
-    PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<false>, a, c0, nsl, C, S, fused, rhs, y, yb));
+  if (fwd) PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<true>, a, c0, nsl, C, S, rhs, y, yb));
+  else PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<false>, a, c0, nsl, C, S, rhs, y, yb));
   PSCU_LAUNCHED(&c);
 }
 
@@ -1381,7 +1360,9 @@ static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y,
       if (w.S) launch_push(c, w.fwd, a, s.s0, nch / w.C, w.C, w.S, rhs, y, yb);
       else if (w.flow) launch_flow(c, w.fwd, a, s.s0, nch, rhs, y, yb);
       else launch_walker(c, w.fwd, a, s.s0, nch / w.C, w.C, rhs, y, yb);
+#ifdef PSCU_TRACE
       if (a.trace) trace_report(c, w.fwd, w.flow ? 0 : w.C, w.flow ? nch : nch / w.C);
+#endif
     }
   }
 }
