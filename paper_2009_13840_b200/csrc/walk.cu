@@ -1029,7 +1029,7 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
   }
 }
 
-/// Cluster size for a sweep (measured: tools/sweep_cluster.sh): two CTAs when
+/// Cluster size for a sweep (measured: tools/sweep_cluster.sh): four CTAs when
 /// an average level fits about one chunk, else kMaxCluster CTAs, whose rings
 /// also keep the wide fine-level wavefronts resident.
 int pick_cluster(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
@@ -1051,16 +1051,16 @@ int pick_cluster(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
       ++cnt;
     }
   if (!cnt) return 1;
-  // narrow sweeps (the coarse level): a pair of CTAs with the push walker
-  // (tools/sweep_cluster.sh at 256^2: 1.71 ms per coarse apply vs 2.24 ms
-  // for one CTA); wide sweeps: kMaxCluster
-  return (2 * nr <= 3 * int64_t(kStageRows) * cnt && nq <= int64_t(kMaxNz) * cnt) ? 2 : kMaxCluster;
+  // narrow sweeps (the coarse level): four CTAs with the push walker
+  // (256^2 coarse apply: 1.49 ms with 4 CTAs, 1.54 ms with 2, 2.24 ms with
+  // one CTA of the level walker); wide sweeps: kMaxCluster
+  return (2 * nr <= 3 * int64_t(kStageRows) * cnt && nq <= int64_t(kMaxNz) * cnt) ? 4 : kMaxCluster;
 }
 
 HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
   HostPlan h;
   const int C = pick_cluster(a, diag, fwd);
-  if (C > 1 && !getenv("PSCU_WALK_NOPUSH")) {
+  if ((C > 1 || getenv("PSCU_WALK_PUSH1")) && !getenv("PSCU_WALK_NOPUSH")) {
     plan_sweep(a, diag, fwd, C, false, kRingTotal / C, h);
     if (h.push_ok) return h;
   }
