@@ -106,8 +106,9 @@ struct Csr {
 
 /// Level-walking sweep plan (walk.cu).
 struct WalkSeg {
-  bool wide;   // row-parallel launch of one chunk, else one walker cluster
+  bool wide;   // task-parallel launch of one chunk, else one walker cluster
   int s0, s1;  // chunk range
+  bool warp = false;  // wide: one warp per task (long tasks), else one thread
 };
 
 struct WalkPlan {
@@ -115,10 +116,11 @@ struct WalkPlan {
   int C = 1;     // CTAs of the walker cluster (one chunk each per sub-level)
   bool flow = false;  // single-CTA dataflow walker
   int S = 0;          // push walker: replicated ring slots per owner
+  bool levels = false;  // every task level is a task-parallel launch (no walker)
   int nsub = 0;  // chunks
   int64_t npos = 0;
   std::vector<WalkSeg> segments;
-  DevBuf<int32_t> sl_k, sl_nr, sl_hdr, rows, off, dp, opos, src, far, sfar;
+  DevBuf<int32_t> sl_k, sl_nr, sl_hdr, tt, rows, off, dp, opos, src, far, sfar;
   DevBuf<int64_t> sl_q, sl_f, sl_s, from, dfrom;
   DevBuf<double> val, dv;
   DevBuf<int4> meta;               // per position {length / offset, row, backward position, 0}

@@ -26,8 +26,11 @@
 // the reference's exact operation sequence, so the result is bit-identical
 // to Ilu0::apply.
 #include <algorithm>
+#include <queue>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <exception>
 #include <memory>
 #include <thread>
@@ -44,19 +47,24 @@ namespace {
 constexpr int kWalkThreads = 512;  // consumer threads per CTA (one row each)
 constexpr int kProdWarps = 4;      // producer warps per stage slot
 constexpr int kProducers = 32 * kProdWarps * 4;
-constexpr int kStageRows = kWalkThreads;  // rows of a chunk
-constexpr int kMaxNz = 2560;       // factor entries of a chunk (multiple of 4)
-constexpr int kStages = 4;         // chunks in flight per CTA
+constexpr int kStageRows = 640;   // rows of a push-walker chunk (level walker: kWalkThreads)
+constexpr int kMaxNz = 2048;       // factor entries of a chunk (multiple of 4)
+constexpr int kStages = 3;         // chunks in flight per CTA
 constexpr int kRing = 4096;        // per-CTA solution ring (local positions, power of 2)
 constexpr int kWideRows = 4096;    // levels with more rows run row-parallel
 constexpr int kMaxCluster = 8;
-constexpr int kMaxDiag = 128;      // longest row (factor entries) of a walker chunk
+constexpr int kMaxDiag = 128;      // longest task (factor entries) of a walker chunk
+constexpr int kHdr = 16;           // ints of a chunk header
+constexpr int kLevelMaxNz = 512;   // entries of a task of a level-launch plan (warp kernel buffer)
+constexpr int kLevelMaxRows = 32;  // rows of such a task
 
 struct WalkArgs {
   const int32_t* sl_k;    // chunk start position (multiple of 4)
   const int32_t* sl_nr;   // rows of the chunk
   const int64_t* sl_q;    // packed entry start (multiple of 4), nchunks + 1
-  const int32_t* sl_hdr;  // per chunk {k0, rows, entries, far, ring start, diagonals, dp start, 0}
+  const int32_t* sl_hdr;  // per chunk {k0, rows, entries, far, ring start, diagonals, dp start,
+                          //  push bytes, tasks, task table start, 0...} (kHdr ints)
+  const int32_t* tt;      // per chunk: first local row of every task, then the row count
   const int32_t* rows;    // row id per position (-1 padding)
   const int32_t* off;     // walker chunks: row length; wide chunks: row offset in the chunk
   const int32_t* dp;      // walker chunks: start of diagonal u within the chunk
@@ -94,7 +102,8 @@ struct alignas(16) Stage {
   double dv[kStageRows];
   int4 meta[kStageRows];
   int32_t dptr[kMaxDiag];
-  int32_t hdr[8];
+  int32_t tt[kStageRows + 4];
+  int32_t hdr[kHdr];
 };
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
@@ -158,14 +167,17 @@ __device__ void issue(const WalkArgs& a, int ch, Stage& st, uint64_t* bar, const
   const unsigned nr4 = unsigned((nr + 3) & ~3);
   const int64_t q0 = a.sl_q[ch];
   const unsigned nq = unsigned(a.sl_q[ch + 1] - q0);
-  const int* hd = a.sl_hdr + 8 * ch;
+  const int* hd = a.sl_hdr + kHdr * ch;
   const unsigned nd4 = unsigned((hd[5] + 3) & ~3);
-  const unsigned bytes = nq * 12u + nr4 * (8u + 16u) + (kFwd ? 0u : nr4 * 8u) + nd4 * 4u + 32u;
+  const unsigned nt4 = unsigned((hd[8] + 1 + 3) & ~3);
+  const unsigned bytes =
+      nq * 12u + nr4 * (8u + 16u) + (kFwd ? 0u : nr4 * 8u) + nd4 * 4u + nt4 * 4u + 4u * kHdr;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
                "r"(bytes)
                : "memory");
-  bulk_copy(st.hdr, a.sl_hdr + 8 * ch, 32u, bar);
+  bulk_copy(st.hdr, a.sl_hdr + kHdr * ch, 4u * kHdr, bar);
+  bulk_copy(st.tt, a.tt + hd[9], nt4 * 4u, bar);
   bulk_copy(st.val, a.val + q0, nq * 8u, bar);
   bulk_copy(st.src, a.src + q0, nq * 4u, bar);
   bulk_copy(st.rhs, rhs + k0, nr4 * 8u, bar);
@@ -213,7 +225,7 @@ __device__ __forceinline__ void walk_products(Stage& st, double* ring, int rank)
 template <bool kFwd>
 __device__ __forceinline__ bool walk_rows(const Stage& st, double& acc, int4& m) {
   const int nr = st.hdr[1];
-  const int t = threadIdx.x;  // kStageRows == kWalkThreads: one row per thread
+  const int t = threadIdx.x;  // level-walker chunks: at most kWalkThreads rows, one per thread
   if (t >= nr) return false;
   m = st.meta[t];
   const int len = m.x;
@@ -550,16 +562,17 @@ constexpr int kPushConsumers = 256;  // each consumer thread folds up to two row
 /// local ring replica; out-of-ring entries (src -1) already hold their
 /// product (producers). Diagonal-major entries: unit-stride warp loads.
 template <bool kFwd>
-__device__ __forceinline__ double push_row(const Stage& st, const double* ring, int row,
-                                           const int4& m) {
+__device__ __forceinline__ double push_row(const Stage& st, const double* ring, int task, int u0,
+                                           int row, const int4& m) {
   const int len = m.x;
+  const int32_t* dp = st.dptr + u0;
   double acc = st.rhs[row];
   int u = 0;
   for (; u + 4 <= len; u += 4) {
-    const int4 d = *reinterpret_cast<const int4*>(st.dptr + u);
-    const int e[4] = {d.x + row, d.y + row, d.z + row, d.w + row};
-    int sv[4];
+    int e[4], sv[4];
     double v[4], w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) e[k] = dp[u + k] + task;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       sv[k] = st.src[e[k]];
@@ -571,7 +584,7 @@ __device__ __forceinline__ double push_row(const Stage& st, const double* ring, 
     for (int k = 0; k < 4; ++k) acc = dsub(acc, sv[k] >= 0 ? dmul(v[k], w[k]) : v[k]);
   }
   for (; u < len; ++u) {
-    const int e = st.dptr[u] + row;
+    const int e = dp[u] + task;
     const int sv = st.src[e];
     const double v = st.val[e];
     acc = dsub(acc, sv >= 0 ? dmul(v, ring[sv]) : v);
@@ -622,30 +635,37 @@ __global__ void __launch_bounds__(kPushConsumers + 32 * kPushProdWarps * kPushSt
       if (r > 0) mbar_wait(&recv[(r - 1) & 1], unsigned(((r - 1) >> 1) & 1));
       WALK_TRACE(t == 0, r, 1);
       WALK_TRACE(t == 0, r, 2);
-      const int nr = st.hdr[1], r0 = st.hdr[4];
+      const int nt = st.hdr[8], r0 = st.hdr[4];
       const unsigned rbar = smem_addr(&recv[r & 1]);
-      for (int row = t; row < nr; row += kPushConsumers) {
-        const int4 m = st.meta[row];
-        const double acc = push_row<kFwd>(st, ring, row, m);
-        const int pos = r0 + row;
-        double* own = ring + int(rank) * S + (pos & (S - 1));
-        *own = acc;
-        // a value read beyond the ring window also goes to its long-range slot
-        if (m.w) ring[kRingTotal + m.w - 1] = acc;
-        for (int o = 0; o < C; ++o) {
-          if (o == int(rank)) continue;
-          unsigned ra, rb;
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(own)), "r"(o));
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(rbar), "r"(o));
-          push_value(ra, acc, rb);
-          if (m.w) {
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra)
-                         : "r"(smem_addr(ring + kRingTotal + m.w - 1)), "r"(o));
+      // one task (a chain of rows, folded in order) per thread; a row reads
+      // its task's earlier rows from this thread's own ring writes
+      for (int task = t; task < nt; task += kPushConsumers) {
+        const int re = st.tt[task + 1];
+        int u0 = 0;
+        for (int row = st.tt[task]; row < re; ++row) {
+          const int4 m = st.meta[row];
+          const double acc = push_row<kFwd>(st, ring, task, u0, row, m);
+          u0 += m.x;
+          const int pos = r0 + row;
+          double* own = ring + int(rank) * S + (pos & (S - 1));
+          *own = acc;
+          // a value read beyond the ring window also goes to its long-range slot
+          if (m.w) ring[kRingTotal + m.w - 1] = acc;
+          for (int o = 0; o < C; ++o) {
+            if (o == int(rank)) continue;
+            unsigned ra, rb;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(own)), "r"(o));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(rbar), "r"(o));
             push_value(ra, acc, rb);
+            if (m.w) {
+              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra)
+                           : "r"(smem_addr(ring + kRingTotal + m.w - 1)), "r"(o));
+              push_value(ra, acc, rb);
+            }
           }
+          y[m.y] = acc;
+          if (kFwd) yb[m.z] = acc;
         }
-        y[m.y] = acc;
-        if (kFwd) yb[m.z] = acc;
       }
       // ring reads (generic proxy) ordered before peers' st.async rewrite
       // the slots; the sub-level's own ring writes visible to all consumers
@@ -661,21 +681,91 @@ __global__ void __launch_bounds__(kPushConsumers + 32 * kPushProdWarps * kPushSt
   cluster_sync_all();
 }
 
-/// Row-parallel chunk (a level too wide for one CTA): global sources.
+/// Task-parallel chunk (a level too wide for one CTA): one thread per task
+/// (a chain of rows folded in order), global sources; a source inside the
+/// task (src >= 0: its index within the task) was written by this thread.
 template <bool kFwd>
 __global__ void wide_kernel(WalkArgs a, int ch, const double* rhs, double* y, double* yb) {
   const int k0 = a.sl_k[ch], nr = a.sl_nr[ch];
   const int64_t q0 = a.sl_q[ch];
-  const int nq = a.sl_hdr[8 * ch + 2];
-  for (int t = int(blockIdx.x * blockDim.x + threadIdx.x); t < nr; t += gridDim.x * blockDim.x) {
-    const int k = k0 + t;
-    const int64_t qa = q0 + a.off[k];
-    const int64_t qb = q0 + (t + 1 < nr ? a.off[k + 1] : nq);
-    double acc = rhs[k];
-    for (int64_t q = qa; q < qb; ++q) acc = dsub(acc, dmul(a.val[q], __ldcg(y + (-a.src[q] - 1))));
-    if (!kFwd) acc = __ddiv_rn(acc, a.dv[k]);
-    y[a.rows[k]] = acc;
-    if (kFwd) yb[a.opos[k]] = acc;
+  const int* hd = a.sl_hdr + kHdr * ch;
+  const int nq = hd[2], nt = hd[8];
+  const int32_t* tt = a.tt + hd[9];
+  for (int task = int(blockIdx.x * blockDim.x + threadIdx.x); task < nt;
+       task += gridDim.x * blockDim.x) {
+    const int r0 = tt[task], r1 = tt[task + 1];
+    for (int t = r0; t < r1; ++t) {
+      const int k = k0 + t;
+      const int64_t qa = q0 + a.off[k];
+      const int64_t qb = q0 + (t + 1 < nr ? a.off[k + 1] : nq);
+      double acc = rhs[k];
+      for (int64_t q = qa; q < qb; ++q) {
+        const int sv = a.src[q];
+        const int jr = sv < 0 ? -sv - 1 : a.rows[k0 + r0 + sv];
+        acc = dsub(acc, dmul(a.val[q], __ldcg(y + jr)));
+      }
+      if (!kFwd) acc = __ddiv_rn(acc, a.dv[k]);
+      y[a.rows[k]] = acc;
+      if (kFwd) yb[a.opos[k]] = acc;
+    }
+  }
+}
+
+/// The same with one warp per task (long chains of the fine levels): the
+/// lanes load the task's entries (row-contiguous, coalesced) and form every
+/// product whose source lies outside the task, then lane 0 folds the rows in
+/// order from shared memory (products of in-task sources use the values it
+/// just computed). Same rounded operations as ilu0.hpp:53-65.
+constexpr int kLevelWarps = 4;
+
+template <bool kFwd>
+__global__ void __launch_bounds__(32 * kLevelWarps)
+    level_kernel(WalkArgs a, int ch, const double* rhs, double* y, double* yb) {
+  __shared__ double pbuf[kLevelWarps][kLevelMaxNz];
+  __shared__ int32_t sbuf[kLevelWarps][kLevelMaxNz];
+  __shared__ double rb[kLevelWarps][kLevelMaxRows], dvb[kLevelWarps][kLevelMaxRows],
+      cv[kLevelWarps][kLevelMaxRows];
+  __shared__ int4 mb[kLevelWarps][kLevelMaxRows];
+  const int k0 = a.sl_k[ch], nr = a.sl_nr[ch];
+  const int64_t q0 = a.sl_q[ch];
+  const int* hd = a.sl_hdr + kHdr * ch;
+  const int nq = hd[2], nt = hd[8];
+  const int32_t* tt = a.tt + hd[9];
+  const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+  for (int task = int(blockIdx.x) * kLevelWarps + w; task < nt; task += gridDim.x * kLevelWarps) {
+    const int r0 = tt[task], r1 = tt[task + 1];
+    const int64_t qa = q0 + a.off[k0 + r0];
+    const int ne = int((r1 < nr ? q0 + a.off[k0 + r1] : q0 + nq) - qa);
+    if (lane < r1 - r0) {
+      const int k = k0 + r0 + lane;
+      const int len = int((r0 + lane + 1 < nr ? a.off[k + 1] : nq) - a.off[k]);
+      mb[w][lane] = make_int4(len, a.rows[k], kFwd ? a.opos[k] : 0, 0);
+      rb[w][lane] = rhs[k];
+      if (!kFwd) dvb[w][lane] = a.dv[k];
+    }
+    for (int e = lane; e < ne; e += 32) {
+      const int sv = a.src[qa + e];
+      const double v = a.val[qa + e];
+      sbuf[w][e] = sv;
+      pbuf[w][e] = sv < 0 ? dmul(v, __ldcg(y + (-sv - 1))) : v;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      int e = 0;
+      for (int r = 0; r < r1 - r0; ++r) {
+        const int4 m = mb[w][r];
+        double acc = rb[w][r];
+        for (const int e1 = e + m.x; e < e1; ++e) {
+          const int sv = sbuf[w][e];
+          acc = dsub(acc, sv < 0 ? pbuf[w][e] : dmul(pbuf[w][e], cv[w][sv]));
+        }
+        if (!kFwd) acc = __ddiv_rn(acc, dvb[w][r]);
+        cv[w][r] = acc;
+        y[m.y] = acc;
+        if (kFwd) yb[m.z] = acc;
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -707,7 +797,7 @@ __global__ void gather_vals(int64_t m, const int64_t* __restrict__ from,
 }
 
 WalkArgs args_of(const WalkPlan& w) {
-  return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_hdr.p, w.rows.p, w.off.p, w.dp.p, w.meta.p,
+  return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_hdr.p, w.tt.p, w.rows.p, w.off.p, w.dp.p, w.meta.p,
           w.opos.p, w.val.p,  w.src.p,  w.dv.p,     w.sl_f.p,
           reinterpret_cast<const int2*>(w.far.p), w.sl_s.p,
           reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr};
@@ -743,38 +833,124 @@ struct HostPlan {
   int C = 1;
   bool flow = false;  // single-CTA dataflow walker (flow_kernel), chunks span levels
   int S = 0;          // push walker: replicated ring slots per owner (0: classic walker)
+  bool levels = false;  // every task level is a wide chunk
   bool push_ok = true;
   std::vector<int32_t> side;  // push walker: long-range slot + 1 of a row (0: none), by row
   std::vector<int32_t> sl_k, sl_nr, sl_nq, sl_nfar, sl_r0, rows, off, src, pos;
   std::vector<int32_t> far, sfar;  // pairs {entry offset in chunk, source row}
   std::vector<int64_t> sl_f, sl_s, sl_q, from, dfrom;
   std::vector<int32_t> dp, sl_d, sl_nd;  // walker chunks: diagonal starts (padded to 4)
+  std::vector<int32_t> tt, sl_t, sl_nt;  // task tables (first local row per task, then the row
+                                         // count; 4-aligned starts) and task counts per chunk
   std::vector<uint8_t> sl_wide;
   int64_t npos = 0;
 };
 
 /// Positions, chunks and packed operands of one sweep for a C-CTA walker.
+/// Tasks of a sweep: chains of rows one thread folds in order. Row i (in
+/// processing order) joins the task holding its most recent source when that
+/// source is the task's last row, the task stays within `max_rows` rows and
+/// kMaxDiag entries, and every other source of i lies in a task of a strictly
+/// lower task level. Task levels are then a topological order of the task
+/// graph (every source of a task's row is in the task itself or in a lower
+/// level), and a level's tasks are independent. max_rows = 1 gives the row
+/// DAG levels. On the 256^2 config-2a hierarchy chains cut the sweep depth
+/// from 771 (k = 0) / 3090 (k = 3) levels to ~258 (one per mesh row).
+struct Tasks {
+  std::vector<int32_t> ptr, rows, lvl, nz;  // rows of task t: rows[ptr[t] .. ptr[t + 1])
+  int nlev = 0;
+};
+
+Tasks build_tasks(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int max_rows,
+                  int max_nz) {
+  const int64_t n = a.n;
+  const auto& rp = a.h_row_ptr;
+  const auto& cols = a.h_cols;
+  Tasks T;
+  T.lvl.reserve(n);
+  T.nz.reserve(n);
+  std::vector<int32_t> task(n, -1), tail, head, cnt, next(n, -1);
+  tail.reserve(n);
+  head.reserve(n);
+  cnt.reserve(n);
+  for (int64_t p = 0; p < n; ++p) {
+    const int64_t i = fwd ? p : n - 1 - p;
+    const int64_t q0 = fwd ? rp[i] : diag[i] + 1, q1 = fwd ? diag[i] : rp[i + 1];
+    const int len = int(q1 - q0);
+    int64_t latest = -1;
+    for (int64_t q = q0; q < q1; ++q)
+      if (latest < 0 || (fwd ? cols[q] > latest : cols[q] < latest)) latest = cols[q];
+    int join = -1;
+    if (latest >= 0 && max_rows > 1) {
+      const int t = task[latest];
+      bool ok = tail[t] == latest && cnt[t] < max_rows && T.nz[t] + len <= max_nz;
+      for (int64_t q = q0; q < q1 && ok; ++q) {
+        const int u = task[cols[q]];
+        if (u != t && T.lvl[u] >= T.lvl[t]) ok = false;
+      }
+      if (ok) join = t;
+    }
+    if (join < 0) {
+      int L = 0;
+      for (int64_t q = q0; q < q1; ++q) L = std::max(L, T.lvl[task[cols[q]]] + 1);
+      join = int(T.lvl.size());
+      T.lvl.push_back(L);
+      T.nz.push_back(0);
+      tail.push_back(-1);
+      head.push_back(int32_t(i));
+      cnt.push_back(0);
+      T.nlev = std::max(T.nlev, L + 1);
+    } else {
+      next[tail[join]] = int32_t(i);
+    }
+    task[i] = join;
+    tail[join] = int32_t(i);
+    T.nz[join] += len;
+    cnt[join]++;
+  }
+  const size_t nt = T.lvl.size();
+  T.ptr.assign(nt + 1, 0);
+  for (size_t t = 0; t < nt; ++t) T.ptr[t + 1] = T.ptr[t] + cnt[t];
+  T.rows.resize(n);
+  for (size_t t = 0; t < nt; ++t) {
+    int32_t m = T.ptr[t];
+    for (int32_t r = head[t]; r >= 0; r = next[r]) T.rows[m++] = r;
+  }
+  return T;
+}
+
+int chain_rows() {
+  if (const char* e = getenv("PSCU_CHAIN_ROWS")) return std::max(1, std::min(64, atoi(e)));
+  return 16;
+}
+
+/// Positions, chunks and packed operands of one sweep for a C-CTA walker.
+/// Chunks hold tasks (max_rows > 1 only for the push walker, whose
+/// consumers fold whole tasks).
 void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C, bool flow,
-                int S, HostPlan& h) {
+                int S, int max_rows, HostPlan& h, bool all_wide = false) {
   const int64_t n = a.n;
   const auto& rp = a.h_row_ptr;
   const auto& cols = a.h_cols;
   auto q_begin = [&](int64_t i) { return fwd ? rp[i] : diag[i] + 1; };
   auto q_end = [&](int64_t i) { return fwd ? diag[i] : rp[i + 1]; };
-  int nlev = 0;
-  const std::vector<int32_t> lvl = dag_levels(a, diag, fwd, nlev);
-  std::vector<int32_t> lvl_ptr(nlev + 1, 0), order(n);
-  for (int64_t i = 0; i < n; ++i) lvl_ptr[lvl[i] + 1]++;
+  const Tasks T = build_tasks(a, diag, fwd, max_rows, all_wide ? kLevelMaxNz : kMaxDiag);
+  std::vector<int32_t> task_of(n);
+  for (size_t t = 0; t + 1 < T.ptr.size(); ++t)
+    for (int32_t m = T.ptr[t]; m < T.ptr[t + 1]; ++m) task_of[T.rows[m]] = int32_t(t);
+  const int nlev = T.nlev;
+  const int ntask = int(T.lvl.size());
+  auto trows = [&](int t) { return T.ptr[t + 1] - T.ptr[t]; };
+  std::vector<int32_t> lvl_ptr(nlev + 1, 0), order(ntask);
+  for (int t = 0; t < ntask; ++t) lvl_ptr[T.lvl[t] + 1]++;
   for (int l = 0; l < nlev; ++l) lvl_ptr[l + 1] += lvl_ptr[l];
   {
     std::vector<int32_t> fill(lvl_ptr.begin(), lvl_ptr.end() - 1);
-    for (int64_t p = 0; p < n; ++p) {
-      const int64_t i = fwd ? p : n - 1 - p;
-      order[fill[lvl[i]]++] = int32_t(i);
-    }
+    for (int t = 0; t < ntask; ++t) order[fill[T.lvl[t]]++] = t;
   }
   h = HostPlan{};
   h.C = C;
+  h.levels = all_wide;
   h.flow = flow;
   h.S = S;
   h.pos.assign(n, -1);
@@ -791,41 +967,45 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
     h.sl_wide.push_back(wide ? 1 : 0);
     if (!wide) lcount[rank] = (lcount[rank] + 3) & ~int64_t(3);
     h.sl_r0.push_back(wide ? 0 : int32_t(lcount[rank] & 0x7fffffff));
+    while (h.tt.size() & 3) h.tt.push_back(0);
+    h.sl_t.push_back(int32_t(h.tt.size()));
+    h.sl_nt.push_back(0);
   };
-  // places the collected rows of the open chunk, longest first: diagonal u
-  // of a chunk is then a prefix of its rows, stored contiguously
-  std::vector<int32_t> members;
-  auto commit = [&](int rank) {
-    std::stable_sort(members.begin(), members.end(), [&](int32_t x, int32_t y2) {
-      return q_end(x) - q_begin(x) > q_end(y2) - q_begin(y2);
-    });
-    for (const int32_t i : members) {
+  auto place_task = [&](int t, bool wide, int rank) {
+    h.tt.push_back(h.sl_nr.back());
+    h.sl_nt.back()++;
+    for (int32_t m = T.ptr[t]; m < T.ptr[t + 1]; ++m) {
+      const int32_t i = T.rows[m];
       const int64_t nz = q_end(i) - q_begin(i);
-      if (nz > kMaxDiag) throw Error(PSCU_ECUDA, "walk plan: row exceeds the diagonal capacity");
+      if (!wide && nz > kMaxDiag) throw Error(PSCU_ECUDA, "walk plan: row exceeds the diagonal capacity");
       h.pos[i] = int32_t(k++);
-      lpos[i] = int32_t(lcount[rank]++);
+      if (!wide) lpos[i] = int32_t(lcount[rank]++);
       chunk_of_row[i] = int(h.sl_k.size()) - 1;
       h.sl_nr.back()++;
       h.sl_nq.back() += int32_t(nz);
       q += nz;
     }
+  };
+  auto close_chunk = [&]() { h.tt.push_back(h.sl_nr.back()); };
+  // places the collected tasks of the open chunk, longest first: diagonal u
+  // of a chunk is then a prefix of its tasks, stored contiguously
+  std::vector<int32_t> members;
+  auto commit = [&](int rank) {
+    std::stable_sort(members.begin(), members.end(),
+                     [&](int32_t x, int32_t y2) { return T.nz[x] > T.nz[y2]; });
+    for (const int32_t t : members) place_task(t, false, rank);
+    close_chunk();
     members.clear();
   };
   auto wide_level = [&](int l) {
     open_chunk(true, 0);
-    for (int j = lvl_ptr[l]; j < lvl_ptr[l + 1]; ++j) {
-      const int32_t i = order[j];
-      const int64_t nz = q_end(i) - q_begin(i);
-      h.pos[i] = int32_t(k++);
-      chunk_of_row[i] = int(h.sl_k.size()) - 1;
-      h.sl_nr.back()++;
-      h.sl_nq.back() += int32_t(nz);
-      q += nz;
-    }
+    for (int j = lvl_ptr[l]; j < lvl_ptr[l + 1]; ++j) place_task(order[j], true, 0);
+    close_chunk();
   };
   if (flow) {
     // dataflow chunks: consecutive rows in level order, across level
     // boundaries (rows wait on their own sources, not on levels)
+    if (max_rows != 1) throw Error(PSCU_ECUDA, "walk plan: the dataflow walker folds rows, not tasks");
     int64_t cnz = 0;
     bool open = false;
     for (int l = 0; l < nlev; ++l) {
@@ -836,9 +1016,8 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
         continue;
       }
       for (int j = lvl_ptr[l]; j < lvl_ptr[l + 1]; ++j) {
-        const int32_t i = order[j];
-        const int64_t nz = q_end(i) - q_begin(i);
-        if (open && (int(members.size()) == kStageRows || cnz + nz > kMaxNz - 8)) {
+        const int32_t t = order[j];
+        if (open && (int(members.size()) == kWalkThreads || cnz + T.nz[t] > kMaxNz - 8)) {
           commit(0);
           open = false;
         }
@@ -847,54 +1026,59 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
           open = true;
           cnz = 0;
         }
-        members.push_back(i);
-        cnz += nz;
+        members.push_back(t);
+        cnz += T.nz[t];
       }
     }
     if (open) commit(0);
   }
   for (int l = 0; l < nlev && !flow; ++l) {
-    const int nrl = lvl_ptr[l + 1] - lvl_ptr[l];
-    if (nrl > kWideRows) {
+    const int ntl = lvl_ptr[l + 1] - lvl_ptr[l];
+    if (ntl > kWideRows || all_wide) {
       wide_level(l);
       continue;
     }
-    // sub-levels of C chunks: row and entry budgets per chunk
-    const int row_cap = kStageRows;
+    // sub-levels of C chunks: row, task and entry budgets per chunk
+    const int row_cap = S ? kStageRows : kWalkThreads;
     const int64_t nz_cap = kMaxNz - 8;
-    int j = lvl_ptr[l];
-    while (j < lvl_ptr[l + 1]) {
-      // rows of this sub-level: up to C chunks; balance the entries
-      int64_t rem_nz = 0;
-      int jend = j, rows_left = 0;
-      for (int jj = j; jj < lvl_ptr[l + 1]; ++jj) {
-        const int64_t nz = q_end(order[jj]) - q_begin(order[jj]);
-        if (rows_left + 1 > C * row_cap || rem_nz + nz > C * nz_cap) break;
-        rem_nz += nz;
-        ++rows_left;
-        jend = jj + 1;
+    // tasks go, in order, to the least-loaded chunk (load: the larger of the
+    // row and entry fractions) that still has room; the rest start the next
+    // sub-level
+    std::vector<int32_t> rem(order.begin() + lvl_ptr[l], order.begin() + lvl_ptr[l + 1]), carry;
+    std::vector<std::vector<int32_t>> bins(C);
+    std::vector<int64_t> brows(C), bnz(C);
+    while (!rem.empty()) {
+      for (int r = 0; r < C; ++r) {
+        bins[r].clear();
+        brows[r] = bnz[r] = 0;
       }
-      if (jend == j) jend = j + 1;  // a single huge row still gets a chunk
-      const int64_t target = (rem_nz + C - 1) / C;
-      int jj = j;
+      carry.clear();
+      for (const int32_t t : rem) {
+        int best = -1;
+        double bl = 0;
+        for (int r = 0; r < C; ++r) {
+          if (brows[r] + trows(t) > row_cap || bnz[r] + T.nz[t] > nz_cap) continue;
+          const double ld = std::max(double(brows[r]) / row_cap, double(bnz[r]) / double(nz_cap));
+          if (best < 0 || ld < bl) {
+            best = r;
+            bl = ld;
+          }
+        }
+        if (best < 0 && brows[0] == 0) best = 0;  // a single huge task still gets a chunk
+        if (best < 0) {
+          carry.push_back(t);
+          continue;
+        }
+        bins[best].push_back(t);
+        brows[best] += trows(t);
+        bnz[best] += T.nz[t];
+      }
       for (int rank = 0; rank < C; ++rank) {
         open_chunk(false, rank);
-        int64_t cnz = 0;
-        members.clear();
-        while (jj < jend) {
-          const int32_t i = order[jj];
-          const int64_t nz = q_end(i) - q_begin(i);
-          const int cnt = int(members.size());
-          if (cnt > 0 && rank + 1 < C && (cnz + nz > target || cnt == row_cap)) break;
-          if (cnt > 0 && (cnt == row_cap || cnz + nz > nz_cap)) break;
-          members.push_back(i);
-          cnz += nz;
-          ++jj;
-        }
+        members = bins[rank];
         commit(rank);
       }
-      // rows the balancing left over start the next sub-level
-      j = jj;
+      rem.swap(carry);
     }
   }
   h.sl_q.push_back((q + 3) & ~int64_t(3));
@@ -925,22 +1109,75 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
   h.sl_d.assign(nch, 0);
   h.sl_nd.assign(nch, 0);
   if (S) h.side.assign(n, 0);
-  int side_seg = -1, side_next = 0;
+  {
+    // wide chunks (row-contiguous entries, global sources) are independent
+    // of each other and of the walker lists: filled by parallel host threads
+    std::vector<int> wide;
+    for (int c = 0; c < nch; ++c)
+      if (h.sl_wide[c]) wide.push_back(c);
+    std::atomic<size_t> next{0};
+    auto fill = [&] {
+      for (size_t w = next++; w < wide.size(); w = next++) {
+        const int c = wide[w];
+        int64_t roff = 0;
+        for (int t = 0; t < h.sl_nr[c]; ++t) {
+          const int64_t kp = h.sl_k[c] + t;
+          const int32_t i = h.rows[kp];
+          const int64_t qb = q_begin(i), len = q_end(i) - qb;
+          h.off[kp] = int32_t(roff);
+          h.dfrom[kp] = diag[i];
+          // a source in the row's own task: its index within the task (the
+          // same thread / warp computed it just before)
+          const int32_t ti = task_of[i], first = h.pos[T.rows[T.ptr[ti]]];
+          for (int64_t u = 0; u < len; ++u) {
+            const int64_t qq = h.sl_q[c] + roff + u;
+            const int32_t jr = cols[qb + u];
+            h.from[qq] = qb + u;
+            h.src[qq] = task_of[jr] == ti ? h.pos[jr] - first : -(jr + 1);
+          }
+          roff += len;
+        }
+      }
+    };
+    const int nth = int(std::min<size_t>(wide.size(), std::max(1u, std::min(8u, std::thread::hardware_concurrency()))));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nth; ++t) pool.emplace_back(fill);
+    fill();
+    for (auto& th : pool) th.join();
+  }
+  std::vector<std::pair<int64_t, int32_t>> side_q;  // {entry, source row} read from slots
+  std::vector<int32_t> last_read(S ? n : 0, -1);     // last reading sub-level (segment-local)
   for (int c = 0; c < nch; ++c) {
     if (S && !h.push_ok) return;  // infeasible for the push walker: stop early
+    if (h.sl_wide[c]) {
+      h.sl_f[c + 1] = h.sl_f[c];
+      h.sl_s[c + 1] = h.sl_s[c];
+      h.sl_nfar.push_back(0);
+      continue;
+    }
     int nf = 0, ns = 0;
     const int sub = (c - seg_first[c]) / C;
     const int sub_first = seg_first[c] + sub * C;
     const int nr = h.sl_nr[c];
     auto len_of = [&](int t) { return int(q_end(h.rows[h.sl_k[c] + t]) - q_begin(h.rows[h.sl_k[c] + t])); };
     // entry index of (row t, entry u): row-contiguous for wide chunks, else
-    // diagonal-major (rows sorted by length, descending)
-    std::vector<int32_t> dstart;
+    // diagonal-major over tasks (entry v of the concatenated rows of task i
+    // at dstart[v] + i; tasks sorted by entry count, descending)
+    std::vector<int32_t> dstart, ti(nr), uo(nr);
     if (!h.sl_wide[c]) {
-      const int nd = nr ? len_of(0) : 0;
+      const int nt = h.sl_nt[c];
+      const int32_t* tt = h.tt.data() + h.sl_t[c];
+      std::vector<int32_t> tlen(nt, 0);
+      for (int i = 0; i < nt; ++i)
+        for (int t = tt[i]; t < tt[i + 1]; ++t) {
+          ti[t] = i;
+          uo[t] = tlen[i];
+          tlen[i] += len_of(t);
+        }
+      const int nd = nt ? tlen[0] : 0;
       dstart.assign(nd + 1, 0);
-      for (int u = 0, t = nr; u < nd; ++u) {
-        while (t > 0 && len_of(t - 1) <= u) --t;
+      for (int u = 0, t = nt; u < nd; ++u) {
+        while (t > 0 && tlen[t - 1] <= u) --t;
         dstart[u + 1] = dstart[u] + t;
       }
       h.sl_d[c] = int32_t(h.dp.size());
@@ -957,12 +1194,16 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
       h.dfrom[kp] = diag[i];
       for (int u = 0; u < len; ++u) {
         const int64_t p = q_begin(i) + u;
-        const int64_t e = h.sl_wide[c] ? roff + u : int64_t(dstart[u]) + t;  // offset in chunk
+        const int64_t e = h.sl_wide[c] ? roff + u : int64_t(dstart[uo[t] + u]) + ti[t];  // in chunk
         const int64_t qq = h.sl_q[c] + e;
         const int32_t jr = cols[p];
         h.from[qq] = p;
         if (h.sl_wide[c]) {
-          h.src[qq] = -(jr + 1);  // wide launches read global memory directly
+          // wide launches read global memory directly; a source in the row's
+          // own task is its index within the task (the same thread / warp
+          // computed it just before)
+          h.src[qq] = task_of[jr] == task_of[i] ? h.pos[jr] - h.pos[T.rows[T.ptr[task_of[i]]]]
+                                                : -(jr + 1);
           continue;
         }
         const int cj = chunk_of_row[jr];
@@ -1002,17 +1243,11 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
           ++ns;
         } else if (S) {
           // push walker: out of the ring window, read from the source's
-          // long-range slot (its owner pushes it there as well)
-          if (h.side[jr] == 0) {
-            const int seg_id = seg_of[c];
-            if (side_seg != seg_id) {
-              side_seg = seg_id;
-              side_next = 0;
-            }
-            if (side_next == kSide) h.push_ok = false;
-            else h.side[jr] = ++side_next;
-          }
-          h.src[qq] = kRingTotal + (h.side[jr] > 0 ? h.side[jr] - 1 : 0);
+          // long-range slot (its owner pushes it there as well); slots are
+          // assigned below, once every reader is known
+          side_q.emplace_back(qq, jr);
+          const int sub_r = (c - seg_first[c]) / C;
+          if (last_read[jr] < sub_r) last_read[jr] = sub_r;
         } else {
           // out of the ring window: a producer forms this product from y
           h.src[qq] = -1;
@@ -1026,6 +1261,47 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
     h.sl_f[c + 1] = h.sl_f[c] + nf;
     h.sl_s[c + 1] = h.sl_s[c] + ns;
     h.sl_nfar.push_back(nf + ns);
+  }
+  if (S && !side_q.empty()) {
+    // long-range slots, recycled: a slot is written at its row's sub-level
+    // w and read up to sub-level r; peers run at most one sub-level ahead,
+    // so the next value may take the slot from sub-level r + 2 on. Slots
+    // are per walker launch (segment).
+    std::vector<int32_t> need;
+    for (int64_t i = 0; i < n; ++i)
+      if (last_read[i] >= 0) need.push_back(int32_t(i));
+    auto wsub = [&](int32_t i) {
+      const int cj = chunk_of_row[i];
+      return std::make_pair(seg_of[cj], (cj - seg_first[cj]) / C);
+    };
+    std::stable_sort(need.begin(), need.end(), [&](int32_t x, int32_t y2) { return wsub(x) < wsub(y2); });
+    // busy slots by the sub-level they become free; idle slots
+    std::priority_queue<std::pair<int, int>, std::vector<std::pair<int, int>>, std::greater<>> busy;
+    std::vector<int> idle;
+    int cur_seg = -1;
+    for (const int32_t i : need) {
+      const auto w = wsub(i);
+      if (w.first != cur_seg) {
+        cur_seg = w.first;
+        busy = {};
+        idle.clear();
+        for (int z = kSide - 1; z >= 0; --z) idle.push_back(z);
+      }
+      while (!busy.empty() && busy.top().first <= w.second) {
+        idle.push_back(busy.top().second);
+        busy.pop();
+      }
+      if (idle.empty()) {
+        h.push_ok = false;
+        if (getenv("PSCU_PLAN_DEBUG")) fprintf(stderr, "push plan: long-range slots exhausted\n");
+        return;
+      }
+      const int slot = idle.back();
+      idle.pop_back();
+      busy.emplace(last_read[i] + 2, slot);
+      h.side[i] = slot + 1;
+    }
+    for (const auto& e : side_q) h.src[e.first] = kRingTotal + h.side[e.second] - 1;
   }
 }
 
@@ -1059,14 +1335,35 @@ int pick_cluster(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
 
 HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
   HostPlan h;
+  const char* mode = getenv("PSCU_WALK_MODE");
+  if (mode && !strcmp(mode, "levels")) {
+    plan_sweep(a, diag, fwd, 1, false, 0, std::min(chain_rows(), kLevelMaxRows), h, true);
+    return h;
+  }
   const int C = pick_cluster(a, diag, fwd);
+  if (C == kMaxCluster && !mode) {
+    // wide sweeps (the fine levels): too much data per level for the rings
+    plan_sweep(a, diag, fwd, 1, false, 0, std::min(chain_rows(), kLevelMaxRows), h, true);
+    return h;
+  }
   if ((C > 1 || getenv("PSCU_WALK_PUSH1")) && !getenv("PSCU_WALK_NOPUSH")) {
-    plan_sweep(a, diag, fwd, C, false, kRingTotal / C, h);
+    const int g = chain_rows();
+    plan_sweep(a, diag, fwd, C, false, kRingTotal / C, g, h);
     if (h.push_ok) return h;
+    if (g > 1 && mode && !strcmp(mode, "push1")) {
+      plan_sweep(a, diag, fwd, C, false, kRingTotal / C, 1, h);
+      if (h.push_ok) return h;
+    }
+    if (!(mode && !strcmp(mode, "walker"))) {
+      // too much data per level for the rings: every task level becomes one
+      // task-parallel launch (the chains cut the fine-level depth ~12x)
+      plan_sweep(a, diag, fwd, 1, false, 0, std::min(g, kLevelMaxRows), h, true);
+      return h;
+    }
   }
   // the dataflow walker is correct but not yet faster than the level walker
   const bool flow = C == 1 && getenv("PSCU_WALK_FLOW");
-  plan_sweep(a, diag, fwd, C, flow, 0, h);
+  plan_sweep(a, diag, fwd, C, flow, 0, 1, h);
   return h;
 }
 
@@ -1080,8 +1377,13 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   w.npos = h.npos;
   w.segments.clear();
   for (int s = 0; s < w.nsub; ++s) {
-    if (h.sl_wide[s]) w.segments.push_back({true, s, s + 1});
-    else if (s == 0 || h.sl_wide[s - 1]) w.segments.push_back({false, s, s + 1});
+    if (h.sl_wide[s]) {
+      // one warp per task when the tasks are long chains
+      const bool warp = h.sl_nt[s] > 0 && h.sl_nq[s] >= 24 * int64_t(h.sl_nt[s]);
+      w.segments.push_back({true, s, s + 1, warp});
+    } else if (s == 0 || h.sl_wide[s - 1]) {
+      w.segments.push_back({false, s, s + 1});
+    }
     else w.segments.back().s1 = s + 1;
   }
   w.sl_k.upload(h.sl_k, st);
@@ -1096,15 +1398,17 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   w.sfv.alloc(std::max<size_t>(4, h.sfar.size() / 2));
   w.sl_q.upload(h.sl_q, st);
   {
-    std::vector<int32_t> hdr(size_t(w.nsub) * 8, 0);
+    std::vector<int32_t> hdr(size_t(w.nsub) * kHdr, 0);
     for (int s = 0; s < w.nsub; ++s) {
-      hdr[size_t(s) * 8] = h.sl_k[s];
-      hdr[size_t(s) * 8 + 1] = h.sl_nr[s];
-      hdr[size_t(s) * 8 + 2] = h.sl_nq[s];
-      hdr[size_t(s) * 8 + 3] = h.sl_wide[s] ? 0 : h.sl_nfar[s];
-      hdr[size_t(s) * 8 + 4] = h.sl_r0[s];
-      hdr[size_t(s) * 8 + 5] = h.sl_nd[s];
-      hdr[size_t(s) * 8 + 6] = h.sl_d[s];
+      hdr[size_t(s) * kHdr] = h.sl_k[s];
+      hdr[size_t(s) * kHdr + 1] = h.sl_nr[s];
+      hdr[size_t(s) * kHdr + 2] = h.sl_nq[s];
+      hdr[size_t(s) * kHdr + 3] = h.sl_wide[s] ? 0 : h.sl_nfar[s];
+      hdr[size_t(s) * kHdr + 4] = h.sl_r0[s];
+      hdr[size_t(s) * kHdr + 5] = h.sl_nd[s];
+      hdr[size_t(s) * kHdr + 6] = h.sl_d[s];
+      hdr[size_t(s) * kHdr + 8] = h.sl_nt[s];
+      hdr[size_t(s) * kHdr + 9] = h.sl_t[s];
       if (h.S && !h.sl_wide[s]) {
         // bytes the peers of this chunk push during its sub-level
         int first = s;
@@ -1119,10 +1423,15 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
             if (h.side[i]) ++rows;  // long-range copy
           }
         }
-        hdr[size_t(s) * 8 + 7] = 8 * rows;
+        hdr[size_t(s) * kHdr + 7] = 8 * rows;
       }
     }
     w.sl_hdr.upload(hdr, st);
+  }
+  {
+    std::vector<int32_t> tt(h.tt);
+    tt.resize((tt.size() + 8) & ~size_t(3), 0);  // whole 16-byte copies past the last table
+    w.tt.upload(tt, st);
   }
   w.rows.upload(h.rows, st);
   w.off.upload(h.off, st);
@@ -1344,7 +1653,11 @@ static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y,
   WalkArgs a = args_of(w);
   a.trace = trace_buffer();
   for (const WalkSeg& s : w.segments) {
-    if (s.wide) {
+    if (s.wide && s.warp) {
+      if (w.fwd) level_kernel<true><<<148 * 8, 32 * kLevelWarps, 0, c.stream>>>(a, s.s0, rhs, y, yb);
+      else level_kernel<false><<<148 * 8, 32 * kLevelWarps, 0, c.stream>>>(a, s.s0, rhs, y, yb);
+      PSCU_LAUNCHED(&c);
+    } else if (s.wide) {
       if (w.fwd) wide_kernel<true><<<148 * 4, 256, 0, c.stream>>>(a, s.s0, rhs, y, yb);
       else wide_kernel<false><<<148 * 4, 256, 0, c.stream>>>(a, s.s0, rhs, y, yb);
       PSCU_LAUNCHED(&c);
