@@ -108,6 +108,7 @@ struct VcycleOp : Op {
   int count = 0;
   VcycleOp(Hierarchy* hh, int64_t m) : h(hh), n(m) {}
   int64_t size() const override { return n; }
+  bool pure() const override { return false; }
   void apply(Context& c, const double* x, double* y) override {
     ++count;
     h->vcycle(c, 0, x, y);

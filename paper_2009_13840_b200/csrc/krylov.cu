@@ -235,7 +235,7 @@ struct StepShape {
   static constexpr int kE = kL == 1 ? kEpt : 10;  // elements per lane held in registers
 };
 
-template <int kL, bool kPairs>
+template <int kL, bool kPairs, bool kAll = false>
 __global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
     arnoldi_step_kernel(int64_t n, int64_t T, int epl, int j, double* __restrict__ wg,
                         double* V, int64_t ldv, double* __restrict__ hcol,
@@ -304,7 +304,28 @@ __global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
 #pragma unroll
         for (int k = 0; k < kE; ++k) pv[l][k] = iv[l][k];
     }
-    if (kPairs) {
+    if (kAll) {
+      // every CTA gathers all G pairs and rebuilds the same tree: one grid
+      // round trip per pass, no root. A slot of parity par is rewritten two
+      // passes later, after every CTA has published the pass in between,
+      // i.e. after every CTA finished reading it.
+      ulonglong2* pairs = reinterpret_cast<ulonglong2*>(slot_tag);
+      double v = 0.0;
+      if (tid < G) {
+        ulonglong2 p;
+        do {
+          p = ld_pair(pairs + par * G + tid);
+        } while ((p.x ^ p.y) != want);
+        v = __longlong_as_double(p.x);
+      }
+      __syncthreads();  // warp 0 finished reading block_tree's scratch of this pass
+      v = block_tree(v, G);
+      if (tid == 0) {
+        if (i == j + 1) v = __dsqrt_rn(v);
+        hsh = v;
+        if (blockIdx.x == 0) hcol[i] = v;
+      }
+    } else if (kPairs) {
       // relaxed 16-byte {value, value ^ tag} pairs: a pair is accepted only
       // when its two words agree on this pass's tag (a torn read never
       // passes), so neither side needs a fence: the value is the only datum
@@ -390,6 +411,10 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     const char* e = getenv("PSCU_MGS_PAIRS");
     return e ? atoi(e) != 0 : true;
   }();
+  static const bool all = [] {
+    const char* e = getenv("PSCU_MGS_ALL");
+    return e ? atoi(e) != 0 : true;
+  }();
   static const int max_lanes = [] {
     const char* e = getenv("PSCU_MGS_LANES");
     return e ? atoi(e) : 2;
@@ -402,8 +427,12 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     if (G < 1 || G > 1024) continue;
     const size_t smem = 0;
     int per_sm = 0;
-    void* fn = L == 2 ? (pairs ? (void*)arnoldi_step_kernel<2, true> : (void*)arnoldi_step_kernel<2, false>)
-                      : (pairs ? (void*)arnoldi_step_kernel<1, true> : (void*)arnoldi_step_kernel<1, false>);
+    void* fn = L == 2 ? (pairs ? (all && G <= kStepThreads ? (void*)arnoldi_step_kernel<2, true, true>
+                                                           : (void*)arnoldi_step_kernel<2, true>)
+                               : (void*)arnoldi_step_kernel<2, false>)
+                      : (pairs ? (all && G <= kStepThreads ? (void*)arnoldi_step_kernel<1, true, true>
+                                                           : (void*)arnoldi_step_kernel<1, true>)
+                               : (void*)arnoldi_step_kernel<1, false>);
     PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kStepThreads, smem));
     if (int64_t(per_sm) * sm_count < G) continue;
     if (c.slot_tag.n < size_t(2 * G)) {

@@ -81,7 +81,22 @@ void HostArnoldi::solve_y(int mm, std::vector<double>& y) const {
 // Krylov workspace and the device Arnoldi step
 // ---------------------------------------------------------------------------
 
+KrylovWs::~KrylovWs() {
+  if (hpin) cudaFreeHost(hpin);
+  for (auto& e : hev)
+    if (e) cudaEventDestroy(e);
+}
+
 void KrylovWs::ensure(int64_t n_, int m_, bool store_z_) {
+  if (!hev[0])
+    for (auto& e : hev) PSCU_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  if (m_ > hpin_m) {
+    if (hpin) PSCU_CUDA(cudaFreeHost(hpin));
+    hpin = nullptr;
+    PSCU_CUDA(cudaMallocHost(&hpin, sizeof(double) * 2 * size_t(m_ + 2)));
+    hpin_m = m_;
+  }
+  if (hcol.n < 2 * size_t(hpin_m + 2)) hcol.alloc(2 * size_t(hpin_m + 2));
   if (n_ == n && m_ <= m && (!store_z_ || store_z)) return;
   n = n_;
   m = m_;
@@ -93,31 +108,43 @@ void KrylovWs::ensure(int64_t n_, int m_, bool store_z_) {
   tmp.alloc(n);
   prhs.alloc(n);
   xs.alloc(n);
-  hcol.alloc(m + 2);
   ydev.alloc(m + 1);
   hcol_host.resize(m + 2);
 }
 
-/// ArnoldiWorkspace::step on the device (MGS passes) + host Givens.
-static double arnoldi_step(Context& c, KrylovWs& ws, HostArnoldi& ar, int j) {
+/// ArnoldiWorkspace::step on the device (MGS passes); the Hessenberg
+/// column goes to device slot `buf` and, asynchronously, to pinned host
+/// slot `buf` (event hev[buf]).
+static void arnoldi_launch(Context& c, KrylovWs& ws, int j, int buf) {
   const int64_t n = ws.n;
   double* V = ws.V.p;
+  double* hc = ws.hcol.p + size_t(buf) * size_t(ws.hpin_m + 2);
   {
     // algorithmic bytes of a fused MGS step: (j+1) 24 n + 16 n
     Context::Scope prof(&c, PROF_MGS, (double(j + 1) * 24.0 + 16.0) * double(n));
-    if (!arnoldi_step_fused(c, n, j, ws.w.p, V, n, ws.hcol.p)) {
-      mgs_launch(c, 0, n, ws.w.p, nullptr, nullptr, V, ws.hcol.p + 0);
+    if (!arnoldi_step_fused(c, n, j, ws.w.p, V, n, hc)) {
+      mgs_launch(c, 0, n, ws.w.p, nullptr, nullptr, V, hc + 0);
       for (int i = 1; i <= j; ++i)
-        mgs_launch(c, 1, n, ws.w.p, V + size_t(i - 1) * n, ws.hcol.p + (i - 1),
-                   V + size_t(i) * n, ws.hcol.p + i);
-      mgs_launch(c, 2, n, ws.w.p, V + size_t(j) * n, ws.hcol.p + j, nullptr, ws.hcol.p + j + 1);
-      scale_next_launch(c, n, ws.w.p, ws.hcol.p + j + 1, V + size_t(j + 1) * n);
+        mgs_launch(c, 1, n, ws.w.p, V + size_t(i - 1) * n, hc + (i - 1), V + size_t(i) * n,
+                   hc + i);
+      mgs_launch(c, 2, n, ws.w.p, V + size_t(j) * n, hc + j, nullptr, hc + j + 1);
+      scale_next_launch(c, n, ws.w.p, hc + j + 1, V + size_t(j + 1) * n);
     }
   }
-  PSCU_CUDA(cudaMemcpyAsync(ws.hcol_host.data(), ws.hcol.p, sizeof(double) * (j + 2),
-                            cudaMemcpyDeviceToHost, c.stream));
-  PSCU_CUDA(cudaStreamSynchronize(c.stream));
-  return ar.step(j, ws.hcol_host.data());
+  double* hp = ws.hpin + size_t(buf) * size_t(ws.hpin_m + 2);
+  PSCU_CUDA(cudaMemcpyAsync(hp, hc, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c.stream));
+  PSCU_CUDA(cudaEventRecord(ws.hev[buf], c.stream));
+}
+
+/// Host half of the step: Givens rotations on the column of slot `buf`.
+static double arnoldi_finish(KrylovWs& ws, HostArnoldi& ar, int j, int buf) {
+  PSCU_CUDA(cudaEventSynchronize(ws.hev[buf]));
+  return ar.step(j, ws.hpin + size_t(buf) * size_t(ws.hpin_m + 2));
+}
+
+static double arnoldi_step(Context& c, KrylovWs& ws, HostArnoldi& ar, int j) {
+  arnoldi_launch(c, ws, j, 0);
+  return arnoldi_finish(ws, ar, j, 0);
 }
 
 static double norm_dev(Context& c, const double* x, int64_t n) {
@@ -144,6 +171,7 @@ struct LeftOp : Op {
   double* tmp;
   LeftOp(Op* o, Op* p, double* t) : op(o), pc(p), tmp(t) {}
   int64_t size() const override { return op->size(); }
+  bool pure() const override { return op->pure() && pc->pure(); }
   void apply(Context& c, const double* x, double* y) override {
     op->apply(c, x, tmp);
     pc->apply(c, tmp, y);
@@ -190,7 +218,11 @@ KrylovResultDev gmres_dev(Context& c, Op& op, Op* pc, const double* rhs, const d
   ar.init(max_it, beta);
   scale_div_launch(c, n, ws.r0.p, beta, ws.V.p);
   int m = 0;
-  for (int j = 0; j < max_it; ++j) {
+  // step j's device work (preconditioner, operator, MGS) needs only device
+  // data, so step j + 1 is launched before the host reads column j: the host
+  // round trip and the launches overlap the device work. A step launched
+  // past convergence only writes scratch columns (V, Z, w) never used.
+  auto launch_step = [&](int j) {
     const double* vj = ws.V.p + size_t(j) * n;
     const double* zj = vj;
     if (pc) {
@@ -199,7 +231,14 @@ KrylovResultDev gmres_dev(Context& c, Op& op, Op* pc, const double* rhs, const d
       zj = zz;
     }
     op.apply(c, zj, ws.w.p);
-    const double est = arnoldi_step(c, ws, ar, j);
+    arnoldi_launch(c, ws, j, j & 1);
+  };
+  const bool ahead = op.pure() && (!pc || pc->pure());
+  if (max_it > 0 && ahead) launch_step(0);
+  for (int j = 0; j < max_it; ++j) {
+    if (!ahead) launch_step(j);
+    else if (j + 1 < max_it) launch_step(j + 1);
+    const double est = arnoldi_finish(ws, ar, j, j & 1);
     m = j + 1;
     res.rel_residual = est / beta;
     if (est <= rtol * beta) {

@@ -13,6 +13,9 @@ struct Op {
   virtual ~Op() = default;
   virtual int64_t size() const = 0;
   virtual void apply(Context& c, const double* x, double* y) = 0;
+  /// false when an apply has effects beyond y (counters): such operators
+  /// are never applied speculatively
+  virtual bool pure() const { return true; }
 };
 
 struct KrylovResultDev {
@@ -41,7 +44,15 @@ struct KrylovWs {
   bool store_z = false;
   DevBuf<double> V, Z, w, r0, tmp, prhs, xs, hcol, ydev;
   std::vector<double> hcol_host;
+  // pinned, double-buffered Hessenberg columns of the look-ahead Arnoldi loop
+  double* hpin = nullptr;
+  int hpin_m = -1;
+  cudaEvent_t hev[2] = {nullptr, nullptr};
   void ensure(int64_t n, int m, bool store_z);
+  KrylovWs() = default;
+  KrylovWs(const KrylovWs&) = delete;
+  KrylovWs& operator=(const KrylovWs&) = delete;
+  ~KrylovWs();
 };
 
 KrylovResultDev gmres_dev(Context& c, Op& op, Op* pc, const double* rhs, const double* x0,

@@ -291,3 +291,31 @@ def test_condensation_singular_block_raises(S):
     mats[1, 0, 0] = 0.0  # eliminated dof 0 has a zero pivot on element 1
     with pytest.raises(RuntimeError, match="element 1"):
         S.condense_elements(mats, np.ones((2, n)), [0])
+
+
+# Sweep-plan variants (walk.cu): the push walker over row chains (default on
+# narrow sweeps), task-level launches (default on wide sweeps; warp- and
+# thread-per-task kernels), the level walker and row (chain-free) plans.
+# Every variant must reproduce Ilu0::apply bitwise.
+PLAN_MODES = [("default", "16"), ("default", "3"), ("default", "1"), ("levels", "16"),
+              ("levels", "1"), ("walker", "1"), ("push1", "16")]
+PLAN_CASES = [dict(mesh="unit-tri", n=12, jitter=0.2, seed=0, side="top", scheme="hho-dp",
+                   strategy="v-cond", k=3, data="sincos"),
+              dict(mesh="unit-tri", n=16, jitter=0.2, seed=0, side="top", scheme="hho-dp",
+                   strategy="v-cond", k=0, data="sincos"),
+              dict(family="trapz", n=6, scheme="hho-dp", strategy="vp-cond", k=2)]
+
+
+@pytest.mark.parametrize("mode,rows", PLAN_MODES, ids=[f"{m}-g{r}" for m, r in PLAN_MODES])
+@pytest.mark.parametrize("ci", range(len(PLAN_CASES)))
+def test_ilu0_plan_variants_bitwise(S, monkeypatch, mode, rows, ci):
+    if mode != "default":
+        monkeypatch.setenv("PSCU_WALK_MODE", mode)
+    monkeypatch.setenv("PSCU_CHAIN_ROWS", rows)
+    s = O.RefSystem(**PLAN_CASES[ci])
+    a = s.csr()
+    ri = O.RefIlu(O.RefCsr(a))
+    ilu = S.Ilu0(S.CsrMatrix(a.row_ptr, a.cols, a.vals))
+    for seed in range(2):
+        x = np.random.default_rng(seed).standard_normal(a.n)
+        assert same(ilu.apply(x), ri.apply(x))
