@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -127,6 +128,17 @@ struct WalkPlan {
   mutable DevBuf<double> sfv;      // per-apply values of the static out-of-ring sources
   std::vector<int64_t> h_sl_s;     // static list start per chunk (host copy)
   mutable DevBuf<double> scratch;  // per-apply right-hand sides in position order
+  // level-launch plans: both sweeps captured once as a CUDA graph working on
+  // fixed buffers (ybuf); the apply copies the result out
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    long long kernels = 0;
+    ~Graph() {
+      if (exec) cudaGraphExecDestroy(exec);
+    }
+  };
+  mutable std::shared_ptr<Graph> graph;
+  mutable DevBuf<double> ybuf;
 };
 
 struct Ilu {

@@ -1493,6 +1493,7 @@ void upload_walk(Context& c, const Csr& a, const WalkBuild& b, WalkPlan& wf, Wal
     (dir ? wb : wf).meta.upload(meta, c.stream);
   }
   wf.scratch.alloc(size_t(hf.npos) + 8);  // rhs in forward position order
+  if (hf.levels || hb.levels) wf.ybuf.alloc(size_t(a.n));
   wb.scratch.alloc(size_t(hb.npos) + 8);  // forward result in backward position order
   PSCU_CUDA(cudaMemsetAsync(wb.scratch.p, 0, sizeof(double) * (hb.npos + 8), c.stream));
   if (getenv("PSCU_DEBUG")) {
@@ -1685,6 +1686,40 @@ void run_walk(Context& c, const WalkPlan& wf, const WalkPlan& wb, const double* 
   // result into backward position order), backward sweep in place on y
   gather_rhs<<<grid1(wf.npos), 256, 0, c.stream>>>(wf.npos, wf.rows.p, x, wf.scratch.p);
   PSCU_LAUNCHED(&c);
+  static const bool graphs = [] {
+    const char* e = getenv("PSCU_WALK_GRAPH");
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (graphs && (wf.levels || wb.levels) && wf.segments.size() + wb.segments.size() > 16) {
+    // hundreds of task-level launches: replay them as one captured graph on
+    // fixed buffers (the launch rate no longer bounds the sweep)
+    const int64_t n = int64_t(wf.ybuf.n);
+    if (!wf.graph) {
+      auto g = std::make_shared<WalkPlan::Graph>();
+      const long long before = c.launches;
+      cudaGraph_t graph = nullptr;
+      PSCU_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        run_one(c, wf, wf.scratch.p, wf.ybuf.p, wb.scratch.p);
+        run_one(c, wb, wb.scratch.p, wf.ybuf.p, nullptr);
+      } catch (...) {
+        cudaStreamEndCapture(c.stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      PSCU_CUDA(cudaStreamEndCapture(c.stream, &graph));
+      const cudaError_t e = cudaGraphInstantiate(&g->exec, graph, 0);
+      cudaGraphDestroy(graph);
+      PSCU_CUDA(e);
+      g->kernels = c.launches - before;
+      c.launches = before;
+      wf.graph = g;
+    }
+    PSCU_CUDA(cudaGraphLaunch(wf.graph->exec, c.stream));
+    c.launches += wf.graph->kernels;
+    PSCU_CUDA(cudaMemcpyAsync(y, wf.ybuf.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+    return;
+  }
   run_one(c, wf, wf.scratch.p, y, wb.scratch.p);
   run_one(c, wb, wb.scratch.p, y, nullptr);
 }
