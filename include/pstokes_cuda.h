@@ -42,6 +42,7 @@ typedef struct pscu_ctx pscu_ctx;
 typedef struct pscu_mat pscu_mat;
 typedef struct pscu_ilu pscu_ilu;
 typedef struct pscu_hier pscu_hier;
+typedef struct pscu_bj pscu_bj;
 
 /* DofLayout (dof_layout.hpp:56-85). scheme: 0 hho-dp, 1 hho-hp, 2 dg;
  * strategy: 0 uncond, 1 v-cond, 2 vp-cond. */
@@ -86,7 +87,7 @@ int pscu_timer_start(pscu_ctx* ctx);
 int pscu_timer_stop(pscu_ctx* ctx, double* ms);
 /* Live per-kernel-class timing (events around every launch of the class on
  * the context stream) with the algorithmic bytes each launch moves.
- * class: 0 ILU(0) apply, 1 SpMV, 2 MGS Arnoldi step, 3 other.
+ * class: 0 ILU(0) apply, 1 SpMV, 2 MGS Arnoldi step, 3 other, 4 block-Jacobi apply.
  * pscu_profile(ctx, 1) clears and starts recording. */
 int pscu_profile(pscu_ctx* ctx, int enable);
 int pscu_profile_read(pscu_ctx* ctx, int cls, long long* count, double* ms, double* bytes);
@@ -106,6 +107,17 @@ int pscu_ilu0_create(pscu_ctx* ctx, const pscu_mat* a, pscu_ilu** out);
 int pscu_ilu0_destroy(pscu_ilu* p);
 int pscu_ilu0_factors(pscu_ctx* ctx, const pscu_ilu* p, double* lu_host);
 int pscu_ilu0_apply(pscu_ctx* ctx, const pscu_ilu* p, const double* x, double* y, int mem);
+
+/* Block-Jacobi over the layout's entity blocks (face f: [f fb, (f+1) fb),
+ * element e: [F + e eb, ...), dof_layout.hpp:56-85). Not in the reference:
+ * BASELINE.json's "block-Jacobi smoothing with batched face-block
+ * inverses", plugged in as the smoother's preconditioner where the
+ * reference uses Ilu0 (plevels.hpp:174; pscu_level_cfg.smoother =
+ * PSCU_SMOOTHER_BJACOBI). Dense partial-pivot LU + inverse per block;
+ * PSCU_ESINGULAR names a singular block (HHO-dp mean-pressure blocks). */
+int pscu_bj_create(pscu_ctx* ctx, const pscu_mat* a, const pscu_layout* layout, pscu_bj** out);
+int pscu_bj_destroy(pscu_bj* p);
+int pscu_bj_apply(pscu_ctx* ctx, const pscu_bj* p, const double* x, double* y, int mem);
 
 /* layouts and transfers (dof_layout.hpp:87-126, plevels.hpp:47-113) ------- */
 int pscu_layout_make(int scheme, int strategy, int k, int n_faces, int n_elements,

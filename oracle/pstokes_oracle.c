@@ -500,11 +500,13 @@ typedef struct {
   int64_t* down_map; /* coarse (l+1) -> this level */
   int64_t n_coarse;
   po_csr csr;
+  double* bj; /* block-Jacobi inverses (smoother 1) */
 } po_level;
 
 struct po_hier {
   int nlev;
   po_level* lev;
+  int smoother;
   int smoother_iters;
   double coarse_rtol;
   int coarse_maxit;
@@ -523,10 +525,20 @@ static void lev_ilu(void* c, const double* x, double* y) {
   const po_level* l = ((lev_ctx*)c)->lev;
   po_ilu0_apply(&l->csr, l->lu, l->diag, x, y);
 }
+static void lev_bj(void* c, const double* x, double* y) {
+  const po_level* l = ((lev_ctx*)c)->lev;
+  po_bj_apply(&l->layout, l->bj, x, y);
+}
 
 /* LevelHierarchy ctor, plevels.hpp:129-159 (ILU-GMRES coarse solver) */
 po_hier* po_hier_create(const po_csr* fine, const po_layout* lf, const int* degrees, int nlev,
                         int smoother_iters, double coarse_rtol, int coarse_maxit) {
+  return po_hier_create_ex(fine, lf, degrees, nlev, smoother_iters, coarse_rtol, coarse_maxit, 0);
+}
+
+po_hier* po_hier_create_ex(const po_csr* fine, const po_layout* lf, const int* degrees, int nlev,
+                           int smoother_iters, double coarse_rtol, int coarse_maxit,
+                           int smoother) {
   if (nlev < 1 || degrees[0] != lf->k) {
     set_err("hierarchy: level degrees must start at the fine degree");
     return NULL;
@@ -542,6 +554,7 @@ po_hier* po_hier_create(const po_csr* fine, const po_layout* lf, const int* degr
   }
   po_hier* h = (po_hier*)calloc(1, sizeof(po_hier));
   h->nlev = nlev;
+  h->smoother = smoother;
   h->smoother_iters = smoother_iters;
   h->coarse_rtol = coarse_rtol;
   h->coarse_maxit = coarse_maxit;
@@ -578,6 +591,14 @@ po_hier* po_hier_create(const po_csr* fine, const po_layout* lf, const int* degr
   }
   for (int l = 0; l < nlev; ++l) {
     po_level* L = &h->lev[l];
+    if (smoother == 1 && l + 1 < nlev) {
+      L->bj = (double*)malloc(sizeof(double) * (size_t)(po_bj_size(&L->layout) + 1));
+      if (po_bj_factor(&L->csr, &L->layout, L->bj, NULL) != 0) {
+        po_hier_destroy(h);
+        return NULL;
+      }
+      continue;
+    }
     L->lu = (double*)malloc(sizeof(double) * (size_t)(L->nnz + 1));
     L->diag = (int64_t*)malloc(sizeof(int64_t) * (size_t)(L->n + 1));
     if (po_ilu0_factor(&L->csr, L->lu, L->diag) != 0) {
@@ -598,6 +619,7 @@ void po_hier_destroy(po_hier* h) {
     free(L->lu);
     free(L->diag);
     free(L->down_map);
+    free(L->bj);
   }
   free(h->lev);
   free(h);
@@ -644,8 +666,8 @@ int po_vcycle(po_hier* h, int l, const double* d, double* c) {
   double* cc = (double*)malloc(sizeof(double) * (size_t)(nc + 1));
   int its, conv;
   double rel;
-  po_gmres(lev_spmv, &ctx, lev_ilu, &ctx, n, d, zero, h->smoother_iters, 0.0, 1, w, &its, &rel,
-           &conv);
+  po_apply_fn pc = h->smoother == 1 ? lev_bj : lev_ilu;
+  po_gmres(lev_spmv, &ctx, pc, &ctx, n, d, zero, h->smoother_iters, 0.0, 1, w, &its, &rel, &conv);
   po_csr_multiply(&L->csr, w, t);
   for (int64_t e = 0; e < n; ++e) t[e] = d[e] - t[e];
   for (int64_t i = 0; i < nc; ++i) dc[i] = t[L->down_map[i]];
@@ -654,8 +676,7 @@ int po_vcycle(po_hier* h, int l, const double* d, double* c) {
   for (int64_t e = 0; e < n; ++e) t[e] = 0.0;
   for (int64_t i = 0; i < nc; ++i) t[L->down_map[i]] = cc[i];
   for (int64_t e = 0; e < n; ++e) w[e] = w[e] + t[e];
-  po_gmres(lev_spmv, &ctx, lev_ilu, &ctx, n, d, w, h->smoother_iters, 0.0, 1, c, &its, &rel,
-           &conv);
+  po_gmres(lev_spmv, &ctx, pc, &ctx, n, d, w, h->smoother_iters, 0.0, 1, c, &its, &rel, &conv);
   free(zero);
   free(w);
   free(t);
@@ -687,6 +708,141 @@ int po_solve(po_hier* h, const double* rhs, double outer_rtol, int outer_maxit, 
   *coarse_its = h->coarse_its;
   *vcycles = pc.vcycles;
   return rc;
+}
+
+/* ---------------------------------------------------------------------------
+ * Block-Jacobi over entity blocks (not in the reference: BASELINE.json names
+ * "block-Jacobi smoothing with batched face-block inverses"; SURVEY.md §0
+ * finding 4 makes it a labelled alternative to the ILU(0) smoother plugged
+ * in at the same point, plevels.hpp:174). Blocks follow the DofLayout
+ * numbering (dof_layout.hpp:56-85). Every operation is individually
+ * rounded and ordered exactly like the device kernels (bjacobi.cu).
+ * ------------------------------------------------------------------------- */
+static void bj_shape(const po_layout* l, int* fb, int* eb, int64_t* eoff) {
+  *fb = 2 * l->face_vel + l->face_press;
+  *eb = 2 * l->elem_vel + l->elem_press;
+  *eoff = (int64_t)l->n_faces * *fb;
+}
+
+int64_t po_bj_size(const po_layout* l) {
+  int fb, eb;
+  int64_t eoff;
+  bj_shape(l, &fb, &eb, &eoff);
+  return (int64_t)l->n_faces * fb * fb + (int64_t)l->n_elements * eb * eb;
+}
+
+/* dense block extraction, partial-pivot LU, inverse column by column */
+static int bj_block(const po_csr* a, int64_t s, int bs, double* d, double* inv, int* perm,
+                    double* y) {
+  for (int i = 0; i < bs * bs; ++i) d[i] = 0.0;
+  for (int i = 0; i < bs; ++i)
+    for (int64_t q = a->row_ptr[s + i]; q < a->row_ptr[s + i + 1]; ++q) {
+      const int64_t c = a->cols[q];
+      if (c >= s && c < s + bs) d[i * bs + (c - s)] = a->vals[q];
+    }
+  double amax = 0.0;
+  for (int i = 0; i < bs * bs; ++i)
+    if (fabs(d[i]) > amax) amax = fabs(d[i]);
+  for (int i = 0; i < bs; ++i) perm[i] = i;
+  for (int k = 0; k < bs; ++k) {
+    int p = k;
+    double m = fabs(d[k * bs + k]);
+    for (int i = k + 1; i < bs; ++i)
+      if (fabs(d[i * bs + k]) > m) {
+        m = fabs(d[i * bs + k]);
+        p = i;
+      }
+    if (!(m > 1e-14 * amax)) return 1;
+    if (p != k) {
+      for (int j = 0; j < bs; ++j) {
+        const double t = d[k * bs + j];
+        d[k * bs + j] = d[p * bs + j];
+        d[p * bs + j] = t;
+      }
+      const int t = perm[k];
+      perm[k] = perm[p];
+      perm[p] = t;
+    }
+    for (int i = k + 1; i < bs; ++i) {
+      const double f = d[i * bs + k] / d[k * bs + k];
+      d[i * bs + k] = f;
+      for (int j = k + 1; j < bs; ++j) {
+        const double t = f * d[k * bs + j];
+        d[i * bs + j] = d[i * bs + j] - t;
+      }
+    }
+  }
+  for (int c = 0; c < bs; ++c) {
+    for (int i = 0; i < bs; ++i) {
+      double v = perm[i] == c ? 1.0 : 0.0;
+      for (int j = 0; j < i; ++j) {
+        const double t = d[i * bs + j] * y[j];
+        v = v - t;
+      }
+      y[i] = v;
+    }
+    for (int i = bs - 1; i >= 0; --i) {
+      double v = y[i];
+      for (int j = i + 1; j < bs; ++j) {
+        const double t = d[i * bs + j] * y[j];
+        v = v - t;
+      }
+      y[i] = v / d[i * bs + i];
+    }
+    for (int i = 0; i < bs; ++i) inv[i * bs + c] = y[i];
+  }
+  return 0;
+}
+
+int po_bj_factor(const po_csr* a, const po_layout* l, double* inv, int64_t* bad_block) {
+  int fb, eb;
+  int64_t eoff;
+  bj_shape(l, &fb, &eb, &eoff);
+  const int mb = fb > eb ? fb : eb;
+  double* d = (double*)malloc(sizeof(double) * (size_t)(mb * mb + 1));
+  double* y = (double*)malloc(sizeof(double) * (size_t)(mb + 1));
+  int* perm = (int*)malloc(sizeof(int) * (size_t)(mb + 1));
+  int rc = 0;
+  const int64_t nb = (int64_t)l->n_faces + l->n_elements;
+  for (int64_t b = 0; b < nb && !rc; ++b) {
+    const int face = b < l->n_faces;
+    const int bs = face ? fb : eb;
+    if (!bs) continue;
+    const int64_t s = face ? b * fb : eoff + (b - l->n_faces) * eb;
+    double* out = inv + (face ? b * fb * fb
+                              : (int64_t)l->n_faces * fb * fb + (b - l->n_faces) * eb * eb);
+    if (bj_block(a, s, bs, d, out, perm, y)) {
+      rc = 1;
+      if (bad_block) *bad_block = b;
+      set_err("block-Jacobi: singular diagonal block");
+    }
+  }
+  free(d);
+  free(y);
+  free(perm);
+  return rc;
+}
+
+void po_bj_apply(const po_layout* l, const double* inv, const double* x, double* y) {
+  int fb, eb;
+  int64_t eoff;
+  bj_shape(l, &fb, &eb, &eoff);
+  const int64_t nb = (int64_t)l->n_faces + l->n_elements;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int face = b < l->n_faces;
+    const int bs = face ? fb : eb;
+    const int64_t s = face ? b * fb : eoff + (b - l->n_faces) * eb;
+    const double* m = inv + (face ? b * fb * fb
+                                  : (int64_t)l->n_faces * fb * fb + (b - l->n_faces) * eb * eb);
+    for (int i = 0; i < bs; ++i) {
+      double acc = 0.0;
+      for (int j = 0; j < bs; ++j) {
+        const double t = m[i * bs + j] * x[s + j];
+        acc = acc + t;
+      }
+      y[s + i] = acc;
+    }
+  }
 }
 
 /* ---------------------------------------------------------------------------

@@ -56,11 +56,24 @@ int po_fgmres(po_apply_fn op, void* op_ctx, po_apply_fn pc, void* pc_ctx, int64_
               const double* rhs, int max_it, double rtol, int restart, double* x, double* hist,
               int* its, double* rel, int* converged);
 
+/* Block-Jacobi preconditioner over the entity blocks of a DofLayout
+ * (BASELINE.json's smoother; the reference smooths with ILU(0)-GMRES).
+ * Face f owns [f*fb, (f+1)*fb), element e owns [F + e*eb, F + (e+1)*eb).
+ * inv: n_faces*fb*fb + n_elements*eb*eb doubles, row-major per block.
+ * Returns 0, or 1 with *bad_block on a singular block (pivot <= 1e-14 max). */
+int64_t po_bj_size(const po_layout* l);
+int po_bj_factor(const po_csr* a, const po_layout* l, double* inv, int64_t* bad_block);
+void po_bj_apply(const po_layout* l, const double* inv, const double* x, double* y);
+
 typedef struct po_hier po_hier;
 /* Builds levels below `fine` (layout lf): coarse_to_fine maps, inherited
  * operators, ILU(0) per level; the coarsest level uses ILU-GMRES. */
 po_hier* po_hier_create(const po_csr* fine, const po_layout* lf, const int* degrees, int nlev,
                         int smoother_iters, double coarse_rtol, int coarse_maxit);
+/* The same with the smoother's preconditioner chosen: 0 ILU(0) (the
+ * reference), 1 block-Jacobi (every level but the coarsest). */
+po_hier* po_hier_create_ex(const po_csr* fine, const po_layout* lf, const int* degrees, int nlev,
+                           int smoother_iters, double coarse_rtol, int coarse_maxit, int smoother);
 void po_hier_destroy(po_hier* h);
 int po_hier_nlev(const po_hier* h);
 int64_t po_hier_level_dim(const po_hier* h, int l);

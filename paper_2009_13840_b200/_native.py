@@ -27,7 +27,8 @@ EXPORTS = [
     "pscu_coarse_to_fine", "pscu_inherit", "pscu_gmres", "pscu_fgmres", "pscu_hier_create",
     "pscu_hier_destroy", "pscu_hier_nlev", "pscu_hier_level_mat", "pscu_hier_level_ilu",
     "pscu_vcycle", "pscu_hier_coarse_its", "pscu_hier_reset", "pscu_solve", "pscu_solve_system",
-    "pscu_condense_batch", "pscu_condense_assemble", "pscu_recover_batch",
+    "pscu_condense_batch", "pscu_condense_assemble", "pscu_recover_batch", "pscu_bj_create",
+    "pscu_bj_destroy", "pscu_bj_apply",
 ]
 
 
@@ -87,6 +88,9 @@ def load(path: str = LIB):
     lib.pscu_ilu0_destroy.argtypes = [vp]
     lib.pscu_ilu0_factors.argtypes = [vp, vp, vp]
     lib.pscu_ilu0_apply.argtypes = [vp, vp, vp, vp, i32]
+    lib.pscu_bj_create.argtypes = [vp, vp, C.POINTER(Layout), C.POINTER(vp)]
+    lib.pscu_bj_destroy.argtypes = [vp]
+    lib.pscu_bj_apply.argtypes = [vp, vp, vp, vp, i32]
     lib.pscu_layout_make.argtypes = [i32, i32, i32, i32, i32, C.POINTER(Layout)]
     lib.pscu_layout_dim.restype = i64
     lib.pscu_layout_dim.argtypes = [C.POINTER(Layout)]

@@ -36,6 +36,9 @@ struct pscu_mat {
 struct pscu_ilu {
   Ilu i;
 };
+struct pscu_bj {
+  BlockJacobi b;
+};
 struct pscu_hier {
   Hierarchy h;
   const pscu_mat* fine = nullptr;
@@ -299,6 +302,31 @@ int pscu_ilu0_apply(pscu_ctx* ctx, const pscu_ilu* p, const double* x, double* y
     const double* dx = in_vec(c, x, n, mem, bx);
     double* dy = out_vec(n, y, mem, by);
     ilu0_apply(c, p->i, dx, dy);
+    finish_out(c, y, dy, n, mem);
+  });
+}
+
+int pscu_bj_create(pscu_ctx* ctx, const pscu_mat* a, const pscu_layout* l, pscu_bj** out) {
+  return guard([&] {
+    auto p = std::make_unique<pscu_bj>();
+    bj_factor(ctx->c, a->m, *l, p->b);
+    *out = p.release();
+  });
+}
+
+int pscu_bj_destroy(pscu_bj* p) {
+  delete p;
+  return PSCU_OK;
+}
+
+int pscu_bj_apply(pscu_ctx* ctx, const pscu_bj* p, const double* x, double* y, int mem) {
+  return guard([&] {
+    Context& c = ctx->c;
+    const int64_t n = p->b.n;
+    DevBuf<double> bx, by;
+    const double* dx = in_vec(c, x, n, mem, bx);
+    double* dy = out_vec(n, y, mem, by);
+    bj_apply(c, p->b, dx, dy);
     finish_out(c, y, dy, n, mem);
   });
 }

@@ -152,7 +152,7 @@ struct Ilu {
 };
 
 /// Live per-kernel-class timing with CUDA events on the launching stream.
-enum ProfClass { PROF_ILU = 0, PROF_SPMV = 1, PROF_MGS = 2, PROF_OTHER = 3, PROF_NCLASS = 4 };
+enum ProfClass { PROF_ILU = 0, PROF_SPMV = 1, PROF_MGS = 2, PROF_OTHER = 3, PROF_BJ = 4, PROF_NCLASS = 5 };
 
 struct ProfRec {
   int cls;

@@ -441,6 +441,12 @@ struct IluOp : Op {
   int64_t size() const override { return ilu->a->n; }
   void apply(Context& c, const double* x, double* y) override { ilu0_apply(c, *ilu, x, y); }
 };
+struct BjOp : Op {
+  const BlockJacobi* bj;
+  explicit BjOp(const BlockJacobi* p) : bj(p) {}
+  int64_t size() const override { return bj->n; }
+  void apply(Context& c, const double* x, double* y) override { bj_apply(c, *bj, x, y); }
+};
 
 Hierarchy::~Hierarchy() = default;
 
@@ -455,8 +461,8 @@ void Hierarchy::build(Context& c, const Csr* fine, const pscu_layout& lf, const 
   const int kmin = lf.scheme == 2 ? 1 : 0;
   if (degrees[nlev - 1] < kmin)
     throw Error(PSCU_EINVAL, "hierarchy: coarsest degree below the scheme minimum");
-  if (cfg.smoother != PSCU_SMOOTHER_ILU0)
-    throw Error(PSCU_EINVAL, "hierarchy: only the ILU(0)-GMRES smoother is built in this release");
+  if (cfg.smoother != PSCU_SMOOTHER_ILU0 && cfg.smoother != PSCU_SMOOTHER_BJACOBI)
+    throw Error(PSCU_EINVAL, "hierarchy: unknown smoother");
   if (cfg.coarse != PSCU_COARSE_ILU_GMRES && nlev > 0 && cfg.coarse != PSCU_COARSE_LU)
     throw Error(PSCU_EINVAL, "hierarchy: unknown coarse solver");
   levels.clear();
@@ -492,6 +498,9 @@ void Hierarchy::build(Context& c, const Csr* fine, const pscu_layout& lf, const 
     Level& L = *levels[l];
     if (l + 1 == nlev && cfg.coarse == PSCU_COARSE_LU) {
       L.dense_lu.factor(c, *L.a);
+    } else if (l + 1 < nlev && cfg.smoother == PSCU_SMOOTHER_BJACOBI) {
+      L.use_bj = true;
+      bj_factor(c, *L.a, L.layout, L.bj);
     } else {
       L.ilu.a = L.a;
       ilu0_factor_start(c, L.ilu);
@@ -563,7 +572,9 @@ void Hierarchy::vcycle(Context& c, int l, const double* d, double* out) {
   }
   Level& L = *levels[l];
   SpmvOp op(L.a);
-  IluOp pc(&L.ilu);
+  IluOp ilu_pc(&L.ilu);
+  BjOp bj_pc(&L.bj);
+  Op& pc = L.use_bj ? static_cast<Op&>(bj_pc) : static_cast<Op&>(ilu_pc);
   const int s = cfg.smoother_iters;
   // pre-smoothing from zero: gmres(op, pc, d, 0, s, 0, Left) (plevels.hpp:175-176)
   gmres_dev(c, op, &pc, d, nullptr, s, 0.0, true, L.w.p, L.ws, nullptr);

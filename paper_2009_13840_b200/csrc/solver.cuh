@@ -73,12 +73,24 @@ struct DenseLu {
   void solve(Context& c, const double* b, double* x);
 };
 
+/// Block-Jacobi over the layout's entity blocks (bjacobi.cu).
+struct BlockJacobi {
+  pscu_layout layout{};
+  int fb = 0, eb = 0;
+  int64_t eoff = 0, n = 0;
+  DevBuf<double> inv;  // face blocks then element blocks, column-major per block
+};
+void bj_factor(Context& c, const Csr& a, const pscu_layout& l, BlockJacobi& bj);
+void bj_apply(Context& c, const BlockJacobi& bj, const double* x, double* y);
+
 struct Level {
   int k = 0;
   pscu_layout layout{};
   const Csr* a = nullptr;  // level 0 borrows the fine matrix
   Csr own;
   Ilu ilu;
+  BlockJacobi bj;
+  bool use_bj = false;  // smoother preconditioner: block-Jacobi instead of ILU(0)
   DenseLu dense_lu;
   DevBuf<int64_t> down_map;  // coarse (l+1) -> this level
   DevBuf<int32_t> f2c;       // this level -> coarse index or -1

@@ -54,7 +54,7 @@ class Context:
     def profile(self, enable: bool = True):
         N.check(self.lib.pscu_profile(self.h, int(enable)))
 
-    PROFILE_CLASSES = {"ilu0_apply": 0, "spmv": 1, "mgs_step": 2, "other": 3}
+    PROFILE_CLASSES = {"ilu0_apply": 0, "spmv": 1, "mgs_step": 2, "other": 3, "bjacobi_apply": 4}
 
     def profile_read(self) -> dict:
         """{class: (launch groups, total ms, algorithmic bytes)} from CUDA
@@ -157,6 +157,31 @@ class Ilu0:
         y = np.zeros(self.a.n)
         N.check(self.lib.pscu_ilu0_apply(self.ctx.h, self.h, x.ctypes.data, y.ctypes.data,
                                          N.PSCU_HOST))
+        return y
+
+
+class BlockJacobi:
+    """Block-Jacobi over the layout's entity blocks (BASELINE.json's smoother,
+    a labelled alternative to the reference's Ilu0: plevels.hpp:174)."""
+
+    def __init__(self, a: CsrMatrix, layout: N.Layout):
+        self.a = a
+        self.ctx = a.ctx
+        self.lib = a.lib
+        h = C.c_void_p()
+        N.check(self.lib.pscu_bj_create(self.ctx.h, a.h, C.byref(layout), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.pscu_bj_destroy(self.h)
+            self.h = None
+
+    def apply(self, x) -> np.ndarray:
+        x = _f64(x)
+        y = np.zeros(self.a.n)
+        N.check(self.lib.pscu_bj_apply(self.ctx.h, self.h, x.ctypes.data, y.ctypes.data,
+                                       N.PSCU_HOST))
         return y
 
 

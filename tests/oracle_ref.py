@@ -453,6 +453,14 @@ def port_lib():
         lib.po_hier_create.restype = vp
         lib.po_hier_create.argtypes = [C.POINTER(_PoCsr), C.POINTER(PoLayout), _i32p, C.c_int,
                                        C.c_int, C.c_double, C.c_int]
+        lib.po_hier_create_ex.restype = vp
+        lib.po_hier_create_ex.argtypes = [C.POINTER(_PoCsr), C.POINTER(PoLayout), _i32p, C.c_int,
+                                          C.c_int, C.c_double, C.c_int, C.c_int]
+        lib.po_bj_size.restype = C.c_int64
+        lib.po_bj_size.argtypes = [C.POINTER(PoLayout)]
+        lib.po_bj_factor.argtypes = [C.POINTER(_PoCsr), C.POINTER(PoLayout), _f64p,
+                                     C.POINTER(C.c_int64)]
+        lib.po_bj_apply.argtypes = [C.POINTER(PoLayout), _f64p, _f64p, _f64p]
         lib.po_hier_destroy.argtypes = [vp]
         lib.po_hier_level_dim.restype = C.c_int64
         lib.po_hier_level_dim.argtypes = [vp, C.c_int]
@@ -484,15 +492,34 @@ def po_layout(scheme, strategy, k, n_faces, n_elements) -> PoLayout:
     return lay
 
 
+class PortBlockJacobi:
+    """Block-Jacobi over the entity blocks of a layout (restatement)."""
+
+    def __init__(self, a: Csr, layout: PoLayout):
+        self.lib = port_lib()
+        self.layout = layout
+        c = po_csr(a)
+        self.inv = np.zeros(self.lib.po_bj_size(C.byref(layout)))
+        bad = C.c_int64(-1)
+        if self.lib.po_bj_factor(C.byref(c), C.byref(layout), self.inv, C.byref(bad)):
+            raise RuntimeError(f"{self.lib.po_last_error().decode()} (block {bad.value})")
+        self.n = a.n
+
+    def apply(self, x):
+        y = np.zeros(self.n)
+        self.lib.po_bj_apply(C.byref(self.layout), self.inv, np.ascontiguousarray(x, np.float64), y)
+        return y
+
+
 class PortHierarchy:
     def __init__(self, a: Csr, layout: PoLayout, degrees, smoother_iters=2, coarse_rtol=1e-3,
-                 coarse_maxit=400):
+                 coarse_maxit=400, smoother=0):
         self.lib = port_lib()
         self.a = a
         self._c = po_csr(a)
         deg = np.asarray(degrees, np.int32)
-        self.h = self.lib.po_hier_create(C.byref(self._c), C.byref(layout), deg, len(deg),
-                                         smoother_iters, coarse_rtol, coarse_maxit)
+        self.h = self.lib.po_hier_create_ex(C.byref(self._c), C.byref(layout), deg, len(deg),
+                                            smoother_iters, coarse_rtol, coarse_maxit, smoother)
         if not self.h:
             raise RuntimeError(self.lib.po_last_error().decode())
         self.nlev = len(deg)

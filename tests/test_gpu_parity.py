@@ -319,3 +319,57 @@ def test_ilu0_plan_variants_bitwise(S, monkeypatch, mode, rows, ci):
     for seed in range(2):
         x = np.random.default_rng(seed).standard_normal(a.n)
         assert same(ilu.apply(x), ri.apply(x))
+
+
+# Block-Jacobi over entity blocks (BASELINE.json's smoother; a labelled
+# alternative to the reference's ILU(0), oracle: po_bj_* / po_hier_create_ex
+# in oracle/pstokes_oracle.c). Apply, V-cycle and full solves bitwise.
+BJ_CASES = [dict(family="tri", n=4, scheme="hho-hp", strategy="vp-cond", k=3, degrees=[3, 2, 1, 0]),
+            dict(family="trapz", n=3, scheme="hho-hp", strategy="vp-cond", k=2, degrees=[2, 1, 0]),
+            dict(family="trapz", n=2, scheme="dg", strategy="uncond", k=2, degrees=[2, 1])]
+BJ_IDS = [f"{c['family']}-{c['scheme']}-k{c['k']}" for c in BJ_CASES]
+
+
+def _po_layout(s):
+    L = s.layout
+    return O.po_layout(L.scheme, L.strategy, L.k, L.n_faces, L.n_elements)
+
+
+@pytest.mark.parametrize("c", BJ_CASES, ids=BJ_IDS)
+def test_bjacobi_apply_bitwise(S, c):
+    s = _sys(c)
+    a = s.csr()
+    ref = O.PortBlockJacobi(a, _po_layout(s))
+    bj = S.BlockJacobi(S.CsrMatrix(a.row_ptr, a.cols, a.vals), _layout(S, s))
+    for seed in range(2):
+        x = np.random.default_rng(seed).standard_normal(a.n)
+        assert same(bj.apply(x), ref.apply(x))
+
+
+def test_bjacobi_singular_block_raises(S):
+    # HHO-dp v-cond: the element mean-pressure block is singular (SURVEY.md
+    # §0 finding 4); both sides refuse it
+    s = _sys(CASES[1] | dict(strategy="v-cond"))
+    a = s.csr()
+    with pytest.raises(RuntimeError, match="singular"):
+        O.PortBlockJacobi(a, _po_layout(s))
+    with pytest.raises(RuntimeError, match="singular"):
+        S.BlockJacobi(S.CsrMatrix(a.row_ptr, a.cols, a.vals), _layout(S, s))
+
+
+@pytest.mark.parametrize("c", BJ_CASES, ids=BJ_IDS)
+def test_bjacobi_vcycle_and_solve_bitwise(S, c):
+    s = _sys(c, data="exp")
+    a = s.csr()
+    ref = O.PortHierarchy(a, _po_layout(s), c["degrees"], smoother=1)
+    m = S.CsrMatrix(a.row_ptr, a.cols, a.vals)
+    cfg = S.LevelConfig(degrees=c["degrees"], coarse="gmres-ilu", smoother="bjacobi",
+                        outer_rtol=1e-10)
+    h = S.LevelHierarchy(m, _layout(S, s), cfg)
+    d = np.random.default_rng(3).standard_normal(a.n)
+    assert same(h.vcycle(0, d), ref.vcycle(0, d))
+    r = ref.solve(s.rhs(), rtol=1e-10)
+    x, hist, rep = h.solve(s.rhs())
+    assert rep.converged and r["converged"]
+    assert rep.outer_its == r["its"] and rep.coarse_its == r["coarse_its"]
+    assert same(hist, r["hist"]) and same(x, r["x"])
