@@ -104,6 +104,8 @@ def build_oracle(force: bool = False) -> None:
     targets = ["restatement"]
     if os.path.isdir("/root/reference/proj/include"):
         targets.append(os.path.join(oracle, "_ref", "libpstokes_ref.so"))
+        if os.path.exists(LIB):
+            targets.append("dropin")  # links the solver library
     cmd = ["make", "-C", oracle, *targets]
     if force:
         cmd.insert(1, "-B")
