@@ -6,6 +6,7 @@
 // rotations, the convergence test and the small triangular solve run on the
 // host with exactly the scalar code order of the reference (std::hypot is
 // not reproducible across libm and libdevice, so it stays on the host).
+#include <algorithm>
 #include <chrono>
 #include <exception>
 #include <thread>
@@ -397,28 +398,51 @@ void coarse_to_fine(const pscu_layout& f, const pscu_layout& c, int64_t* map) {
 /// inherit_matrix (plevels.hpp:93-113): the coarse pattern and the source
 /// position of every coarse entry come from the host copy of the fine
 /// pattern (setup bookkeeping); the values are gathered on the device.
+/// Runs f(lo, hi) over [0, n) in parallel host threads.
+template <typename F>
+static void parallel_ranges(int64_t n, F f) {
+  const int nth = int(std::max<int64_t>(1, std::min<int64_t>(
+      std::min(16u, std::max(1u, std::thread::hardware_concurrency())), n / 65536)));
+  std::vector<std::thread> th;
+  for (int t = 1; t < nth; ++t) th.emplace_back([&, t] { f(n * t / nth, n * (t + 1) / nth); });
+  f(0, n / nth);
+  for (auto& x : th) x.join();
+}
+
+/// inherit_matrix (plevels.hpp:93-113): the coarse pattern and the source
+/// position of every coarse entry on the host (row-parallel: count, prefix,
+/// fill), then the value gather on the device.
 void inherit(Context& c, const Csr& fine, const std::vector<int64_t>& c2f, Csr& out) {
   const int64_t nf = fine.n, nc = int64_t(c2f.size());
   std::vector<int64_t> f2c(nf, -1);
   for (int64_t i = 0; i < nc; ++i) f2c[c2f[i]] = i;
   out.n = nc;
   out.h_row_ptr.assign(nc + 1, 0);
-  out.h_cols.clear();
-  std::vector<int64_t> src;
-  src.reserve(size_t(fine.nnz * (double(nc) / double(nf > 0 ? nf : 1)) * 0.8) + 16);
-  out.h_cols.reserve(src.capacity());
-  for (int64_t ic = 0; ic < nc; ++ic) {
-    const int64_t r = c2f[ic];
-    for (int64_t p = fine.h_row_ptr[r]; p < fine.h_row_ptr[r + 1]; ++p) {
-      const int64_t jc = f2c[fine.h_cols[p]];
-      if (jc >= 0) {
-        out.h_cols.push_back(int32_t(jc));
-        src.push_back(p);
+  parallel_ranges(nc, [&](int64_t lo, int64_t hi) {
+    for (int64_t ic = lo; ic < hi; ++ic) {
+      const int64_t r = c2f[ic];
+      int64_t k = 0;
+      for (int64_t p = fine.h_row_ptr[r]; p < fine.h_row_ptr[r + 1]; ++p) k += f2c[fine.h_cols[p]] >= 0;
+      out.h_row_ptr[ic + 1] = k;
+    }
+  });
+  for (int64_t ic = 0; ic < nc; ++ic) out.h_row_ptr[ic + 1] += out.h_row_ptr[ic];
+  out.nnz = out.h_row_ptr[nc];
+  out.h_cols.resize(size_t(out.nnz));
+  std::vector<int64_t> src(size_t(out.nnz));
+  parallel_ranges(nc, [&](int64_t lo, int64_t hi) {
+    for (int64_t ic = lo; ic < hi; ++ic) {
+      const int64_t r = c2f[ic];
+      int64_t k = out.h_row_ptr[ic];
+      for (int64_t p = fine.h_row_ptr[r]; p < fine.h_row_ptr[r + 1]; ++p) {
+        const int64_t jc = f2c[fine.h_cols[p]];
+        if (jc >= 0) {
+          out.h_cols[k] = int32_t(jc);
+          src[k++] = p;
+        }
       }
     }
-    out.h_row_ptr[ic + 1] = int64_t(out.h_cols.size());
-  }
-  out.nnz = int64_t(out.h_cols.size());
+  });
   out.row_ptr.upload(out.h_row_ptr, c.stream);
   out.cols.upload(out.h_cols, c.stream);
   out.vals.alloc(out.nnz);
