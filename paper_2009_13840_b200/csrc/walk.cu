@@ -555,7 +555,7 @@ __device__ __forceinline__ void push_value(unsigned raddr, double v, unsigned rb
                : "memory");
 }
 
-constexpr int kPushConsumers = 256;  // each consumer thread folds up to two rows
+constexpr int kPushConsumers = 256;  // consumer threads (default; 512 selectable)
 
 /// One row of the push walker: acc = rhs - sum_u val_u * y(src_u), u
 /// ascending (the reference's order and rounding), sources read from the
@@ -593,8 +593,8 @@ __device__ __forceinline__ double push_row(const Stage& st, const double* ring, 
   return acc;
 }
 
-template <bool kFwd>
-__global__ void __launch_bounds__(kPushConsumers + 32 * kPushProdWarps * kPushStages, 1)
+template <bool kFwd, int kCons = kPushConsumers>
+__global__ void __launch_bounds__(kCons + 32 * kPushProdWarps * kPushStages, 1)
     push_kernel(WalkArgs a, int c0, int nsl, int C, int S, const double* rhs, double* y,
                 double* yb) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -614,8 +614,8 @@ __global__ void __launch_bounds__(kPushConsumers + 32 * kPushProdWarps * kPushSt
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cluster_sync_all();
-  if (threadIdx.x >= kPushConsumers) {
-    produce<kFwd, kPushStages, kPushProdWarps, kPushConsumers>(a, c0, nsl, C, rank, stages,
+  if (threadIdx.x >= kCons) {
+    produce<kFwd, kPushStages, kPushProdWarps, kCons>(a, c0, nsl, C, rank, stages,
                                                                landed, full, empty, rhs, y);
   } else {
     const int t = threadIdx.x;
@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(kPushConsumers + 32 * kPushProdWarps * kPushSt
       const unsigned rbar = smem_addr(&recv[r & 1]);
       // one task (a chain of rows, folded in order) per thread; a row reads
       // its task's earlier rows from this thread's own ring writes
-      for (int task = t; task < nt; task += kPushConsumers) {
+      for (int task = t; task < nt; task += kCons) {
         const int re = st.tt[task + 1];
         int u0 = 0;
         for (int row = st.tt[task]; row < re; ++row) {
@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(kPushConsumers + 32 * kPushProdWarps * kPushSt
       // ring reads (generic proxy) ordered before peers' st.async rewrite
       // the slots; the sub-level's own ring writes visible to all consumers
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync 1, %0;" ::"n"(kPushConsumers) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory");
       WALK_TRACE(t == 0, r, 3);
       WALK_TRACE(t == 0, r, 4);
       if (t == 0) mbar_arrive(&empty[slot]);
@@ -1552,11 +1552,20 @@ static void launch_flow(Context& c, bool fwd, const WalkArgs& a, int c0, int nch
 
 size_t push_smem() { return sizeof(double) * (kRingTotal + kSide) + kPushStages * sizeof(Stage); }
 
-static void launch_push(Context& c, bool fwd, const WalkArgs& a, int c0, int nsl, int C, int S,
-                        const double* rhs, double* y, double* yb) {
+static int push_consumers() {
+  static const int v = [] {
+    const char* e = getenv("PSCU_PUSH_CONSUMERS");
+    return e && atoi(e) == 512 ? 512 : kPushConsumers;
+  }();
+  return v;
+}
+
+template <int kCons>
+static void launch_push_t(Context& c, bool fwd, const WalkArgs& a, int c0, int nsl, int C, int S,
+                          const double* rhs, double* y, double* yb) {
   static bool attr = false;
   if (!attr) {
-    for (void* f : {(void*)push_kernel<true>, (void*)push_kernel<false>}) {
+    for (void* f : {(void*)push_kernel<true, kCons>, (void*)push_kernel<false, kCons>}) {
       PSCU_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(push_smem())));
       PSCU_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -1565,7 +1574,7 @@ static void launch_push(Context& c, bool fwd, const WalkArgs& a, int c0, int nsl
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(unsigned(C));
-  cfg.blockDim = dim3(kPushConsumers + 32 * kPushProdWarps * kPushStages);
+  cfg.blockDim = dim3(kCons + 32 * kPushProdWarps * kPushStages);
   cfg.dynamicSmemBytes = push_smem();
   cfg.stream = c.stream;
   cudaLaunchAttribute at[1];
@@ -1575,9 +1584,15 @@ static void launch_push(Context& c, bool fwd, const WalkArgs& a, int c0, int nsl
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (fwd) PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<true>, a, c0, nsl, C, S, rhs, y, yb));
-  else PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<false>, a, c0, nsl, C, S, rhs, y, yb));
+  if (fwd) PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<true, kCons>, a, c0, nsl, C, S, rhs, y, yb));
+  else PSCU_CUDA(cudaLaunchKernelEx(&cfg, push_kernel<false, kCons>, a, c0, nsl, C, S, rhs, y, yb));
   PSCU_LAUNCHED(&c);
+}
+
+static void launch_push(Context& c, bool fwd, const WalkArgs& a, int c0, int nsl, int C, int S,
+                        const double* rhs, double* y, double* yb) {
+  if (push_consumers() == 512) launch_push_t<512>(c, fwd, a, c0, nsl, C, S, rhs, y, yb);
+  else launch_push_t<kPushConsumers>(c, fwd, a, c0, nsl, C, S, rhs, y, yb);
 }
 
 static void launch_walker(Context& c, bool fwd, const WalkArgs& a, int c0, int nsl, int C,

@@ -6,6 +6,7 @@ set -x
 PSCU_DEBUG=1 timeout 600 python tools/probe_ilu.py 256 20 > gpurun_out/probe_default.log 2>&1; grep -E "level|setup|walk " gpurun_out/probe_default.log | tail -24
 PSCU_WALK_MODE=push1 PSCU_WALK_CLUSTER_BWD=8 timeout 600 python tools/probe_ilu.py 256 20 3 > gpurun_out/probe_c8.log 2>&1; grep -E "level" gpurun_out/probe_c8.log | tail -2
 PSCU_WALK_MODE=push1 PSCU_WALK_CLUSTER=8 timeout 600 python tools/probe_ilu.py 256 20 3 > gpurun_out/probe_c88.log 2>&1; grep -E "level" gpurun_out/probe_c88.log | tail -2
+PSCU_PUSH_CONSUMERS=512 timeout 600 python tools/probe_ilu.py 256 20 3 > gpurun_out/probe_c512.log 2>&1; grep -E "level" gpurun_out/probe_c512.log | tail -2
 PSCU_WALK_GRAPH=0 timeout 600 python tools/probe_ilu.py 256 20 0,1,2 > gpurun_out/probe_nograph.log 2>&1; grep -E "level" gpurun_out/probe_nograph.log | tail -3
 PSCU_CHAIN_ROWS=1 PSCU_WALK_MODE=walker timeout 600 python tools/probe_ilu.py 256 20 > gpurun_out/probe_rows.log 2>&1; grep -E "level|setup" gpurun_out/probe_rows.log | tail -6
 timeout 600 python tools/probe_gmres.py 256 > gpurun_out/probe_gmres.log 2>&1; tail -2 gpurun_out/probe_gmres.log
