@@ -121,7 +121,7 @@ struct WalkPlan {
   int nsub = 0;  // chunks
   int64_t npos = 0;
   std::vector<WalkSeg> segments;
-  DevBuf<int32_t> sl_k, sl_nr, sl_hdr, tt, rows, off, dp, opos, src, far, sfar;
+  DevBuf<int32_t> sl_k, sl_nr, sl_hdr, tt, tq, rows, off, dp, opos, src, far, sfar;
   DevBuf<int64_t> sl_q, sl_f, sl_s, from, dfrom;
   DevBuf<double> val, dv;
   DevBuf<int4> meta;               // per position {length / offset, row, backward position, 0}

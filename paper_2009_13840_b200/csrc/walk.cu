@@ -65,6 +65,7 @@ struct WalkArgs {
   const int32_t* sl_hdr;  // per chunk {k0, rows, entries, far, ring start, diagonals, dp start,
                           //  push bytes, tasks, task table start, 0...} (kHdr ints)
   const int32_t* tt;      // per chunk: first local row of every task, then the row count
+  const int32_t* tq;      // wide chunks: entry offset of every task in the chunk, then the total
   const int32_t* rows;    // row id per position (-1 padding)
   const int32_t* off;     // walker chunks: row length; wide chunks: row offset in the chunk
   const int32_t* dp;      // walker chunks: start of diagonal u within the chunk
@@ -721,6 +722,7 @@ constexpr int kLevelWarps = 4;
 template <bool kFwd>
 __global__ void __launch_bounds__(32 * kLevelWarps)
     level_kernel(WalkArgs a, int ch, const double* rhs, double* y, double* yb) {
+  constexpr int kPer = kLevelMaxNz / 32;  // entries per lane
   __shared__ double pbuf[kLevelWarps][kLevelMaxNz];
   __shared__ int32_t sbuf[kLevelWarps][kLevelMaxNz];
   __shared__ double rb[kLevelWarps][kLevelMaxRows], dvb[kLevelWarps][kLevelMaxRows],
@@ -731,11 +733,22 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
   const int* hd = a.sl_hdr + kHdr * ch;
   const int nq = hd[2], nt = hd[8];
   const int32_t* tt = a.tt + hd[9];
+  const int32_t* tq = a.tq + hd[9];
   const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
   for (int task = int(blockIdx.x) * kLevelWarps + w; task < nt; task += gridDim.x * kLevelWarps) {
+    // one round trip for the task record, one for its rows and entries,
+    // one for the sources outside the task
     const int r0 = tt[task], r1 = tt[task + 1];
-    const int64_t qa = q0 + a.off[k0 + r0];
-    const int ne = int((r1 < nr ? q0 + a.off[k0 + r1] : q0 + nq) - qa);
+    const int e0 = tq[task], ne = tq[task + 1] - e0;
+    const int64_t qa = q0 + e0;
+    int sv[kPer];
+    double v[kPer], yv[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = lane + 32 * u;
+      sv[u] = e < ne ? __ldg(a.src + qa + e) : 0;
+      v[u] = e < ne ? __ldg(a.val + qa + e) : 0.0;
+    }
     if (lane < r1 - r0) {
       const int k = k0 + r0 + lane;
       const int len = int((r0 + lane + 1 < nr ? a.off[k + 1] : nq) - a.off[k]);
@@ -743,11 +756,18 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
       rb[w][lane] = rhs[k];
       if (!kFwd) dvb[w][lane] = a.dv[k];
     }
-    for (int e = lane; e < ne; e += 32) {
-      const int sv = a.src[qa + e];
-      const double v = a.val[qa + e];
-      sbuf[w][e] = sv;
-      pbuf[w][e] = sv < 0 ? dmul(v, __ldcg(y + (-sv - 1))) : v;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = lane + 32 * u;
+      yv[u] = (e < ne && sv[u] < 0) ? __ldcg(y + (-sv[u] - 1)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = lane + 32 * u;
+      if (e < ne) {
+        sbuf[w][e] = sv[u];
+        pbuf[w][e] = sv[u] < 0 ? dmul(v[u], yv[u]) : v[u];
+      }
     }
     __syncwarp();
     if (lane == 0) {
@@ -756,8 +776,8 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
         const int4 m = mb[w][r];
         double acc = rb[w][r];
         for (const int e1 = e + m.x; e < e1; ++e) {
-          const int sv = sbuf[w][e];
-          acc = dsub(acc, sv < 0 ? pbuf[w][e] : dmul(pbuf[w][e], cv[w][sv]));
+          const int s = sbuf[w][e];
+          acc = dsub(acc, s < 0 ? pbuf[w][e] : dmul(pbuf[w][e], cv[w][s]));
         }
         if (!kFwd) acc = __ddiv_rn(acc, dvb[w][r]);
         cv[w][r] = acc;
@@ -797,7 +817,7 @@ __global__ void gather_vals(int64_t m, const int64_t* __restrict__ from,
 }
 
 WalkArgs args_of(const WalkPlan& w) {
-  return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_hdr.p, w.tt.p, w.rows.p, w.off.p, w.dp.p, w.meta.p,
+  return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_hdr.p, w.tt.p, w.tq.p, w.rows.p, w.off.p, w.dp.p, w.meta.p,
           w.opos.p, w.val.p,  w.src.p,  w.dv.p,     w.sl_f.p,
           reinterpret_cast<const int2*>(w.far.p), w.sl_s.p,
           reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr};
@@ -840,6 +860,7 @@ struct HostPlan {
   std::vector<int32_t> far, sfar;  // pairs {entry offset in chunk, source row}
   std::vector<int64_t> sl_f, sl_s, sl_q, from, dfrom;
   std::vector<int32_t> dp, sl_d, sl_nd;  // walker chunks: diagonal starts (padded to 4)
+  std::vector<int32_t> tq;               // wide chunks: entry offset per task (+ total)
   std::vector<int32_t> tt, sl_t, sl_nt;  // task tables (first local row per task, then the row
                                          // count; 4-aligned starts) and task counts per chunk
   std::vector<uint8_t> sl_wide;
@@ -919,8 +940,18 @@ Tasks build_tasks(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int 
   return T;
 }
 
+/// Rows per chain. Push walker: a consumer thread folds its chain's rows
+/// back to back (~0.5-1k cycles of dependent latency per row, measured), so
+/// long chains cost more than the sub-level handshakes they save: 1 unless
+/// PSCU_CHAIN_ROWS says otherwise. Task-level launches (one warp per task,
+/// ~5 us per launch): chains of up to 16 rows cut the fine-level depth 12x.
 int chain_rows() {
   if (const char* e = getenv("PSCU_CHAIN_ROWS")) return std::max(1, std::min(64, atoi(e)));
+  return 1;
+}
+
+int level_chain_rows() {
+  if (const char* e = getenv("PSCU_LEVEL_CHAIN_ROWS")) return std::max(1, std::min(kLevelMaxRows, atoi(e)));
   return 16;
 }
 
@@ -1116,10 +1147,21 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
     for (int c = 0; c < nch; ++c)
       if (h.sl_wide[c]) wide.push_back(c);
     std::atomic<size_t> next{0};
+    h.tq.assign(h.tt.size(), 0);
     auto fill = [&] {
       for (size_t w = next++; w < wide.size(); w = next++) {
         const int c = wide[w];
         int64_t roff = 0;
+        {
+          // entry offset of every task (rows of a task are consecutive)
+          const int32_t* tt = h.tt.data() + h.sl_t[c];
+          int64_t o = 0;
+          for (int i = 0, t = 0; i < h.sl_nt[c]; ++i) {
+            for (; t < tt[i]; ++t) o += q_end(h.rows[h.sl_k[c] + t]) - q_begin(h.rows[h.sl_k[c] + t]);
+            h.tq[h.sl_t[c] + i] = int32_t(o);
+          }
+          h.tq[h.sl_t[c] + h.sl_nt[c]] = h.sl_nq[c];
+        }
         for (int t = 0; t < h.sl_nr[c]; ++t) {
           const int64_t kp = h.sl_k[c] + t;
           const int32_t i = h.rows[kp];
@@ -1337,13 +1379,13 @@ HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
   HostPlan h;
   const char* mode = getenv("PSCU_WALK_MODE");
   if (mode && !strcmp(mode, "levels")) {
-    plan_sweep(a, diag, fwd, 1, false, 0, std::min(chain_rows(), kLevelMaxRows), h, true);
+    plan_sweep(a, diag, fwd, 1, false, 0, level_chain_rows(), h, true);
     return h;
   }
   const int C = pick_cluster(a, diag, fwd);
   if (C == kMaxCluster && !mode) {
     // wide sweeps (the fine levels): too much data per level for the rings
-    plan_sweep(a, diag, fwd, 1, false, 0, std::min(chain_rows(), kLevelMaxRows), h, true);
+    plan_sweep(a, diag, fwd, 1, false, 0, level_chain_rows(), h, true);
     return h;
   }
   if ((C > 1 || getenv("PSCU_WALK_PUSH1")) && !getenv("PSCU_WALK_NOPUSH")) {
@@ -1357,7 +1399,7 @@ HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
     if (!(mode && !strcmp(mode, "walker"))) {
       // too much data per level for the rings: every task level becomes one
       // task-parallel launch (the chains cut the fine-level depth ~12x)
-      plan_sweep(a, diag, fwd, 1, false, 0, std::min(g, kLevelMaxRows), h, true);
+      plan_sweep(a, diag, fwd, 1, false, 0, level_chain_rows(), h, true);
       return h;
     }
   }
@@ -1432,6 +1474,9 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
     std::vector<int32_t> tt(h.tt);
     tt.resize((tt.size() + 8) & ~size_t(3), 0);  // whole 16-byte copies past the last table
     w.tt.upload(tt, st);
+    std::vector<int32_t> tq(h.tq);
+    tq.resize(tt.size(), 0);
+    w.tq.upload(tq, st);
   }
   w.rows.upload(h.rows, st);
   w.off.upload(h.off, st);

@@ -312,6 +312,7 @@ def test_ilu0_plan_variants_bitwise(S, monkeypatch, mode, rows, ci):
     if mode != "default":
         monkeypatch.setenv("PSCU_WALK_MODE", mode)
     monkeypatch.setenv("PSCU_CHAIN_ROWS", rows)
+    monkeypatch.setenv("PSCU_LEVEL_CHAIN_ROWS", rows)
     s = O.RefSystem(**PLAN_CASES[ci])
     a = s.csr()
     ri = O.RefIlu(O.RefCsr(a))

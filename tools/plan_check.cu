@@ -76,6 +76,9 @@ int main(int argc, char** argv) {
         for (int task = 0; task < nt; ++task)
           for (int t = tt[task]; t < tt[task + 1]; ++t) {
             const int64_t k = h.sl_k[ch] + t;
+            if (t == tt[task] && h.tq[h.sl_t[ch] + task] != h.off[k]) {
+              if (bad++ < 5) fprintf(stderr, "task entry offset mismatch\n");
+            }
             const int64_t qa = h.sl_q[ch] + h.off[k];
             const int64_t qb = h.sl_q[ch] + (t + 1 < h.sl_nr[ch] ? h.off[k + 1] : h.sl_nq[ch]);
             double acc = x[h.rows[k]];
