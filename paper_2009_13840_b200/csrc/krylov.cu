@@ -9,6 +9,7 @@
 // subtree with warp shuffles (offsets 1,2,4,8,16 = adjacent pairs) and
 // shared memory, and the last CTA to finish reduces the per-CTA results,
 // so each MGS pass is one kernel with no host round trip.
+#include <algorithm>
 #include <cstdlib>
 
 #include "internal.cuh"
@@ -393,6 +394,154 @@ __global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// The same Arnoldi step with the basis vectors streamed through shared
+// memory: CTA b's lanes [b*512, b*512+512) read, per vector, epl contiguous
+// 4 KB segments (element e = lane + k*T), staged kVStages passes ahead by
+// TMA bulk copies on an mbarrier per stage. A pass then waits on HBM only
+// when the reductions outrun the copies, w stays in registers, v_{i-1} is
+// re-read from its stage for the w update. Same arithmetic and tree as
+// arnoldi_step_kernel<2, true, true>.
+// ---------------------------------------------------------------------------
+
+constexpr int kVStages = 3;
+constexpr int kVLanes = 2 * kStepThreads;  // lanes per CTA
+
+__device__ __forceinline__ unsigned sa(const void* p) {
+  return unsigned(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void stage_vector(double* dst, const double* v, int64_t n, int64_t T,
+                                             int epl, int64_t lane_base, uint64_t* bar) {
+  unsigned bytes = 0;
+  for (int k = 0; k < epl; ++k) {
+    const int64_t s0 = lane_base + int64_t(k) * T;
+    const int64_t cnt = s0 < n ? (n - s0 < kVLanes ? n - s0 : kVLanes) : 0;
+    bytes += unsigned(cnt) * 8u;
+  }
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(bar)), "r"(bytes)
+               : "memory");
+  for (int k = 0; k < epl; ++k) {
+    const int64_t s0 = lane_base + int64_t(k) * T;
+    const int64_t cnt = s0 < n ? (n - s0 < kVLanes ? n - s0 : kVLanes) : 0;
+    if (cnt > 0)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(sa(dst + k * kVLanes)),
+          "l"(v + s0), "r"(unsigned(cnt) * 8u), "r"(sa(bar))
+          : "memory");
+  }
+}
+
+__device__ __forceinline__ void wait_stage(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(sa(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kStepThreads, 1)
+    arnoldi_tma_kernel(int64_t n, int64_t T, int epl, int j, double* __restrict__ wg,
+                       const double* V, int64_t ldv, double* __restrict__ hcol,
+                       unsigned long long* slot_tag, unsigned long long tag_base, double* vout) {
+  extern __shared__ __align__(16) double vst[];  // kVStages x epl x kVLanes
+  __shared__ __align__(8) uint64_t bar[kVStages];
+  __shared__ double hsh;
+  const int G = gridDim.x;
+  const int tid = threadIdx.x;
+  const int64_t lane_base = int64_t(blockIdx.x) * kVLanes;
+  const int64_t lane0 = lane_base + 2 * tid;
+  const size_t sstride = size_t(epl) * kVLanes;
+  if (tid == 0) {
+    for (int s = 0; s < kVStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bar[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // vectors v_0 .. v_{kVStages-2} in flight before the first pass
+  if (tid == 0)
+    for (int s = 0; s < kVStages - 1 && s <= j; ++s)
+      stage_vector(vst + s * sstride, V + int64_t(s) * ldv, n, T, epl, lane_base, &bar[s]);
+  double w[2][kEpt];
+#pragma unroll
+  for (int l = 0; l < 2; ++l)
+#pragma unroll
+    for (int k = 0; k < kEpt; ++k) {
+      const int64_t e = lane0 + l + int64_t(k) * T;
+      w[l][k] = (k < epl && e < n) ? wg[e] : 0.0;
+    }
+  ulonglong2* pairs = reinterpret_cast<ulonglong2*>(slot_tag);
+  double hprev = 0.0;
+  for (int i = 0; i <= j + 1; ++i) {
+    if (i <= j) wait_stage(&bar[i % kVStages], unsigned((i / kVStages) & 1));
+    const double* vi = vst + (i % kVStages) * sstride;
+    const double* vp = vst + ((i + kVStages - 1) % kVStages) * sstride;
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < kEpt; ++k) {
+      if (k >= epl) break;
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        const int64_t e = lane0 + l + int64_t(k) * T;
+        if (e < n) {
+          if (i > 0) w[l][k] = dsub(w[l][k], dmul(hprev, vp[k * kVLanes + 2 * tid + l]));
+          const double o = i <= j ? vi[k * kVLanes + 2 * tid + l] : w[l][k];
+          acc[l] = dadd(acc[l], dmul(w[l][k], o));
+        }
+      }
+    }
+    const double cta = block_tree(dadd(acc[0], acc[1]), kStepThreads);
+    // block_tree's __syncthreads: every thread is done with stage (i-1):
+    // refill it with v_{i+kVStages-1}
+    if (tid == 0 && i >= 1 && i + kVStages - 1 <= j) {
+      const int s = (i + kVStages - 1) % kVStages;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      stage_vector(vst + s * sstride, V + int64_t(i + kVStages - 1) * ldv, n, T, epl, lane_base,
+                   &bar[s]);
+    }
+    if (tid == 0 && i == 0 && kVStages - 1 <= j) {
+      const int s = kVStages - 1;
+      stage_vector(vst + s * sstride, V + int64_t(kVStages - 1) * ldv, n, T, epl, lane_base,
+                   &bar[s]);
+    }
+    const int par = i & 1;
+    const unsigned long long want = tag_base + unsigned(i) + 1ull;
+    if (tid == 0) {
+      const unsigned long long bits = __double_as_longlong(cta);
+      st_pair(pairs + par * G + blockIdx.x, bits, bits ^ want);
+    }
+    double v = 0.0;
+    if (tid < G) {
+      ulonglong2 p;
+      do {
+        p = ld_pair(pairs + par * G + tid);
+      } while ((p.x ^ p.y) != want);
+      v = __longlong_as_double(p.x);
+    }
+    __syncthreads();  // warp 0 finished reading block_tree's scratch of this pass
+    v = block_tree(v, G);
+    if (tid == 0) {
+      if (i == j + 1) v = __dsqrt_rn(v);
+      hsh = v;
+      if (blockIdx.x == 0) hcol[i] = v;
+    }
+    __syncthreads();
+    hprev = hsh;
+  }
+  // v_{j+1} = w / h, or 0 on a happy breakdown (gmres.hpp:66-67)
+#pragma unroll
+  for (int l = 0; l < 2; ++l)
+#pragma unroll
+    for (int k = 0; k < kEpt; ++k) {
+      const int64_t e = lane0 + l + int64_t(k) * T;
+      if (k < epl && e < n) vout[e] = hprev > 0.0 ? __ddiv_rn(w[l][k], hprev) : 0.0;
+    }
+}
+
 } // namespace
 
 /// Cooperative single-launch Arnoldi step; returns false when the problem
@@ -415,6 +564,45 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     const char* e = getenv("PSCU_MGS_ALL");
     return e ? atoi(e) != 0 : true;
   }();
+  const char* te = getenv("PSCU_MGS_TMA");
+  const bool tma = te ? atoi(te) != 0 : true;
+  // TMA staging once >= 64 CTAs share the stream (PSCU_MGS_TMA_MIN_G: tests)
+  const char* mg = getenv("PSCU_MGS_TMA_MIN_G");
+  const int64_t min_g = mg ? std::max(1, atoi(mg)) : 64;
+  if (tma && (n % 2) == 0 && (ldv % 2) == 0 && T % kVLanes == 0 && T / kVLanes >= min_g &&
+      T / kVLanes <= kStepThreads) {
+    const int64_t G = T / kVLanes;
+    const size_t smem = sizeof(double) * kVStages * size_t(epl) * kVLanes;
+    static size_t attr_smem = 0;
+    if (smem > attr_smem) {
+      PSCU_CUDA(cudaFuncSetAttribute(arnoldi_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem)));
+      attr_smem = smem;
+    }
+    int per_sm = 0;
+    PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_tma_kernel,
+                                                            kStepThreads, smem));
+    if (int64_t(per_sm) * sm_count >= G) {
+      if (c.slot_tag.n < size_t(2 * G)) {
+        c.slot_tag.alloc(2048);
+        PSCU_CUDA(cudaMemsetAsync(c.slot_tag.p, 0, sizeof(unsigned long long) * 2048, c.stream));
+      }
+      int ei = epl, jj = j;
+      int64_t nn = n, TT = T, ld = ldv;
+      double* pw = w;
+      const double* pV = V;
+      double* ph = hcol;
+      unsigned long long* pt = c.slot_tag.p;
+      unsigned long long base = c.pass_tag;
+      double* vo = V + int64_t(j + 1) * ldv;
+      c.pass_tag += unsigned(j + 2);
+      void* args[] = {&nn, &TT, &ei, &jj, &pw, &pV, &ld, &ph, &pt, &base, &vo};
+      PSCU_CUDA(cudaLaunchCooperativeKernel((void*)arnoldi_tma_kernel, dim3(unsigned(G)),
+                                            dim3(kStepThreads), args, smem, c.stream));
+      PSCU_LAUNCHED(&c);
+      return true;
+    }
+  }
   static const int max_lanes = [] {
     const char* e = getenv("PSCU_MGS_LANES");
     return e ? atoi(e) : 2;

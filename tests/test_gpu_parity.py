@@ -374,3 +374,26 @@ def test_bjacobi_vcycle_and_solve_bitwise(S, c):
     assert rep.converged and r["converged"]
     assert rep.outer_its == r["its"] and rep.coarse_its == r["coarse_its"]
     assert same(hist, r["hist"]) and same(x, r["x"])
+
+
+@pytest.mark.parametrize("tma", ["0", "1"])
+@pytest.mark.parametrize("side", ["right", "left"])
+def test_gmres_mgs_variants_bitwise(S, monkeypatch, tma, side):
+    """The fused Arnoldi step with the basis streamed through shared memory
+    by TMA (arnoldi_tma_kernel; forced at small sizes) and without it."""
+    monkeypatch.setenv("PSCU_MGS_TMA_MIN_G", "1")
+    monkeypatch.setenv("PSCU_MGS_TMA", tma)
+    s = O.RefSystem(**PLAN_CASES[0])
+    a = s.csr()
+    ra = O.RefCsr(a)
+    ri = O.RefIlu(ra)
+    m = S.CsrMatrix(a.row_ptr, a.cols, a.vals)
+    ilu = S.Ilu0(m)
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal(a.n)
+    x0 = rng.standard_normal(a.n)
+    for (maxit, rtol) in [(3, 0.0), (60, 1e-9)]:
+        r = O.ref_gmres(ra, ri, b, x0, maxit, rtol, left=side == "left")
+        g = S.gmres(m, ilu, b, x0, maxit, rtol, side=side)
+        assert g.iterations == r["its"] and g.converged == r["converged"]
+        assert same(g.x, r["x"])
