@@ -110,6 +110,7 @@ struct WalkSeg {
   bool wide;   // task-parallel launch of one chunk, else one walker cluster
   int s0, s1;  // chunk range
   bool warp = false;  // wide: one warp per task (long tasks), else one thread
+  int tasks = 0;      // wide: tasks of the chunk
 };
 
 struct WalkPlan {

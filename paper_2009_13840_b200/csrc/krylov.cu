@@ -495,24 +495,25 @@ __global__ void __launch_bounds__(kStepThreads, 1)
       }
     }
     const double cta = block_tree(dadd(acc[0], acc[1]), kStepThreads);
-    // block_tree's __syncthreads: every thread is done with stage (i-1):
-    // refill it with v_{i+kVStages-1}
-    if (tid == 0 && i >= 1 && i + kVStages - 1 <= j) {
-      const int s = (i + kVStages - 1) % kVStages;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      stage_vector(vst + s * sstride, V + int64_t(i + kVStages - 1) * ldv, n, T, epl, lane_base,
-                   &bar[s]);
-    }
-    if (tid == 0 && i == 0 && kVStages - 1 <= j) {
-      const int s = kVStages - 1;
-      stage_vector(vst + s * sstride, V + int64_t(kVStages - 1) * ldv, n, T, epl, lane_base,
-                   &bar[s]);
-    }
     const int par = i & 1;
     const unsigned long long want = tag_base + unsigned(i) + 1ull;
     if (tid == 0) {
       const unsigned long long bits = __double_as_longlong(cta);
       st_pair(pairs + par * G + blockIdx.x, bits, bits ^ want);
+    }
+    if (tid == kStepThreads - 1) {
+      // the last warp refills stage (i-1) with v_{i+kVStages-1} while the
+      // reduction completes (block_tree's __syncthreads: every thread is
+      // done with that stage)
+      if (i >= 1 && i + kVStages - 1 <= j) {
+        const int s = (i + kVStages - 1) % kVStages;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        stage_vector(vst + s * sstride, V + int64_t(i + kVStages - 1) * ldv, n, T, epl,
+                     lane_base, &bar[s]);
+      }
+      if (i == 0 && kVStages - 1 <= j)
+        stage_vector(vst + (kVStages - 1) * sstride, V + int64_t(kVStages - 1) * ldv, n, T, epl,
+                     lane_base, &bar[kVStages - 1]);
     }
     double v = 0.0;
     if (tid < G) {
@@ -564,8 +565,10 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     const char* e = getenv("PSCU_MGS_ALL");
     return e ? atoi(e) != 0 : true;
   }();
+  // TMA-staged basis: correct, but measured slower than the register-
+  // prefetch kernel at the 256^2 coarse level (766 vs 567 us per step)
   const char* te = getenv("PSCU_MGS_TMA");
-  const bool tma = te ? atoi(te) != 0 : true;
+  const bool tma = te ? atoi(te) != 0 : false;
   // TMA staging once >= 64 CTAs share the stream (PSCU_MGS_TMA_MIN_G: tests)
   const char* mg = getenv("PSCU_MGS_TMA_MIN_G");
   const int64_t min_g = mg ? std::max(1, atoi(mg)) : 64;

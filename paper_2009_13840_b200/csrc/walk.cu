@@ -738,6 +738,10 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
   for (int task = int(blockIdx.x) * kLevelWarps + w; task < nt; task += gridDim.x * kLevelWarps) {
     // one round trip for the task record, one for its rows and entries,
     // one for the sources outside the task
+#ifdef PSCU_TRACE
+    const bool tr = a.trace && task == 0 && lane == 0 && ch < kTraceSub;
+    if (tr) a.trace[size_t(ch) * 16 + 0] = clock64();
+#endif
     const int r0 = tt[task], r1 = tt[task + 1];
     const int e0 = tq[task], ne = tq[task + 1] - e0;
     const int64_t qa = q0 + e0;
@@ -770,12 +774,34 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
       }
     }
     __syncwarp();
+#ifdef PSCU_TRACE
+    if (tr) {
+      a.trace[size_t(ch) * 16 + 1] = clock64();
+      a.trace[size_t(ch) * 16 + 3] = ne;
+      a.trace[size_t(ch) * 16 + 4] = r1 - r0;
+    }
+#endif
     if (lane == 0) {
       int e = 0;
       for (int r = 0; r < r1 - r0; ++r) {
         const int4 m = mb[w][r];
         double acc = rb[w][r];
-        for (const int e1 = e + m.x; e < e1; ++e) {
+        const int e1 = e + m.x;
+        // operands of 8 entries loaded before their dependent subtractions
+        for (; e + 8 <= e1; e += 8) {
+          int s8[8];
+          double p8[8], c8[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            s8[k] = sbuf[w][e + k];
+            p8[k] = pbuf[w][e + k];
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) c8[k] = s8[k] < 0 ? 0.0 : cv[w][s8[k]];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc = dsub(acc, s8[k] < 0 ? p8[k] : dmul(p8[k], c8[k]));
+        }
+        for (; e < e1; ++e) {
           const int s = sbuf[w][e];
           acc = dsub(acc, s < 0 ? pbuf[w][e] : dmul(pbuf[w][e], cv[w][s]));
         }
@@ -784,6 +810,9 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
         y[m.y] = acc;
         if (kFwd) yb[m.z] = acc;
       }
+#ifdef PSCU_TRACE
+      if (tr) a.trace[size_t(ch) * 16 + 2] = clock64();
+#endif
     }
     __syncwarp();
   }
@@ -942,12 +971,11 @@ Tasks build_tasks(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int 
 
 /// Rows per chain. Push walker: a consumer thread folds its chain's rows
 /// back to back (~0.5-1k cycles of dependent latency per row, measured), so
-/// long chains cost more than the sub-level handshakes they save: 1 unless
-/// PSCU_CHAIN_ROWS says otherwise. Task-level launches (one warp per task,
+/// long chains cost more than the sub-level handshakes they save. Task-level launches (one warp per task,
 /// ~5 us per launch): chains of up to 16 rows cut the fine-level depth 12x.
 int chain_rows() {
   if (const char* e = getenv("PSCU_CHAIN_ROWS")) return std::max(1, std::min(64, atoi(e)));
-  return 1;
+  return 3;  // 256^2 coarse apply: 1.43 ms (1), 1.61 (2), 1.28 (3), 3.8 (16)
 }
 
 int level_chain_rows() {
@@ -1413,6 +1441,7 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   cudaStream_t st = c.stream;
   w.fwd = fwd;
   w.C = h.C;
+  w.levels = h.levels;
   w.flow = h.flow;
   w.S = h.S;
   w.nsub = int(h.sl_k.size());
@@ -1422,7 +1451,7 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
     if (h.sl_wide[s]) {
       // one warp per task when the tasks are long chains
       const bool warp = h.sl_nt[s] > 0 && h.sl_nq[s] >= 24 * int64_t(h.sl_nt[s]);
-      w.segments.push_back({true, s, s + 1, warp});
+      w.segments.push_back({true, s, s + 1, warp, h.sl_nt[s]});
     } else if (s == 0 || h.sl_wide[s - 1]) {
       w.segments.push_back({false, s, s + 1});
     }
@@ -1710,13 +1739,35 @@ static void trace_report(Context& c, bool fwd, int C, int nsl) {
   }
 }
 
+static void level_trace_report(Context& c, const WalkPlan& w) {
+  std::vector<long long> all(size_t(kTraceSub) * 16);
+  PSCU_CUDA(cudaMemcpyAsync(all.data(), trace_buffer(), sizeof(long long) * all.size(),
+                            cudaMemcpyDeviceToHost, c.stream));
+  PSCU_CUDA(cudaStreamSynchronize(c.stream));
+  double ld = 0, fold = 0, ne = 0, nr = 0;
+  int cnt = 0;
+  for (int ch = 1; ch < std::min(w.nsub, kTraceSub); ++ch) {
+    const long long* t = &all[size_t(ch) * 16];
+    if (t[2] <= t[0]) continue;
+    ld += double(t[1] - t[0]);
+    fold += double(t[2] - t[1]);
+    ne += double(t[3]);
+    nr += double(t[4]);
+    ++cnt;
+  }
+  if (cnt)
+    fprintf(stderr, "[level trace %s] tasks sampled %d: loads %.0f cycles, fold %.0f cycles, entries %.0f, rows %.1f\n",
+            w.fwd ? "fwd" : "bwd", cnt, ld / cnt, fold / cnt, ne / cnt, nr / cnt);
+}
+
 static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y, double* yb) {
   WalkArgs a = args_of(w);
   a.trace = trace_buffer();
   for (const WalkSeg& s : w.segments) {
     if (s.wide && s.warp) {
-      if (w.fwd) level_kernel<true><<<148 * 8, 32 * kLevelWarps, 0, c.stream>>>(a, s.s0, rhs, y, yb);
-      else level_kernel<false><<<148 * 8, 32 * kLevelWarps, 0, c.stream>>>(a, s.s0, rhs, y, yb);
+      const unsigned g = unsigned(std::max(1, std::min(148 * 8, (s.tasks + kLevelWarps - 1) / kLevelWarps)));
+      if (w.fwd) level_kernel<true><<<g, 32 * kLevelWarps, 0, c.stream>>>(a, s.s0, rhs, y, yb);
+      else level_kernel<false><<<g, 32 * kLevelWarps, 0, c.stream>>>(a, s.s0, rhs, y, yb);
       PSCU_LAUNCHED(&c);
     } else if (s.wide) {
       if (w.fwd) wide_kernel<true><<<148 * 4, 256, 0, c.stream>>>(a, s.s0, rhs, y, yb);
@@ -1739,6 +1790,9 @@ static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y,
 #endif
     }
   }
+#ifdef PSCU_TRACE
+  if (a.trace && w.levels) level_trace_report(c, w);
+#endif
 }
 
 void run_walk(Context& c, const WalkPlan& wf, const WalkPlan& wb, const double* x, double* y) {

@@ -60,8 +60,16 @@ int main(int argc, char** argv) {
     }
     if (getenv("PLAN_DUMP"))
       for (int c = 0; c < std::min<int>(h.sl_k.size(), 40); ++c)
-        fprintf(stderr, "chunk %d wide %d rows %d tasks %d entries %d\n", c, h.sl_wide[c], h.sl_nr[c],
-                h.sl_nt[c], h.sl_nq[c]);
+      {
+        int maxe = 0, maxr = 0;
+        if (h.sl_wide[c] && !h.tq.empty())
+          for (int i = 0; i < h.sl_nt[c]; ++i) {
+            maxe = std::max(maxe, h.tq[h.sl_t[c] + i + 1] - h.tq[h.sl_t[c] + i]);
+            maxr = std::max(maxr, h.tt[h.sl_t[c] + i + 1] - h.tt[h.sl_t[c] + i]);
+          }
+        fprintf(stderr, "chunk %d wide %d rows %d tasks %d entries %d max task entries %d rows %d\n", c,
+                h.sl_wide[c], h.sl_nr[c], h.sl_nt[c], h.sl_nq[c], maxe, maxr);
+      }
     // emulation
     const int nch = int(h.sl_k.size());
     const int C = h.C;
