@@ -556,6 +556,20 @@ __device__ __forceinline__ void push_value(unsigned raddr, double v, unsigned rb
                : "memory");
 }
 
+#ifndef PSCU_BULK_PUSH
+#define PSCU_BULK_PUSH 1
+#endif
+constexpr bool kBulkPush = PSCU_BULK_PUSH != 0;
+
+/// smem -> peer smem bulk copy completing the peer's mbarrier.
+__device__ __forceinline__ void bulk_dsmem(unsigned dst, unsigned src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "r"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
 constexpr int kPushConsumers = 256;  // consumer threads (default; 512 selectable)
 
 /// One row of the push walker: acc = rhs - sum_u val_u * y(src_u), u
@@ -646,32 +660,64 @@ __global__ void __launch_bounds__(kCons + 32 * kPushProdWarps * kPushStages, 1)
         for (int row = st.tt[task]; row < re; ++row) {
           const int4 m = st.meta[row];
           const double acc = push_row<kFwd>(st, ring, task, u0, row, m);
+          WALK_TRACE(t == 0 && row == st.tt[0], r, 5);
           u0 += m.x;
           const int pos = r0 + row;
           double* own = ring + int(rank) * S + (pos & (S - 1));
           *own = acc;
           // a value read beyond the ring window also goes to its long-range slot
           if (m.w) ring[kRingTotal + m.w - 1] = acc;
-          for (int o = 0; o < C; ++o) {
-            if (o == int(rank)) continue;
-            unsigned ra, rb;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(own)), "r"(o));
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(rbar), "r"(o));
-            push_value(ra, acc, rb);
-            if (m.w) {
-              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra)
-                           : "r"(smem_addr(ring + kRingTotal + m.w - 1)), "r"(o));
+          if (kBulkPush) {
+            // ring slots reach the peers in one bulk copy per peer after the
+            // sub-level barrier; only long-range copies go out per row
+            if (m.w)
+              for (int o = 0; o < C; ++o) {
+                if (o == int(rank)) continue;
+                unsigned ra, rb;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra)
+                             : "r"(smem_addr(ring + kRingTotal + m.w - 1)), "r"(o));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(rbar), "r"(o));
+                push_value(ra, acc, rb);
+              }
+          } else {
+            for (int o = 0; o < C; ++o) {
+              if (o == int(rank)) continue;
+              unsigned ra, rb;
+              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(own)), "r"(o));
+              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(rbar), "r"(o));
               push_value(ra, acc, rb);
+              if (m.w) {
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra)
+                             : "r"(smem_addr(ring + kRingTotal + m.w - 1)), "r"(o));
+                push_value(ra, acc, rb);
+              }
             }
           }
+          WALK_TRACE(t == 0 && row == st.tt[0], r, 6);
           y[m.y] = acc;
           if (kFwd) yb[m.z] = acc;
         }
       }
+      WALK_TRACE(t == 0, r, 7);
       // ring reads (generic proxy) ordered before peers' st.async rewrite
       // the slots; the sub-level's own ring writes visible to all consumers
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync 1, %0;" ::"n"(kCons) : "memory");
+      if (kBulkPush && t < C && t != int(rank)) {
+        // this sub-level's ring slots [r0, r0 + nr) of this owner, rounded to
+        // whole 16-byte pairs (positions are 4-aligned; the pad slot is never
+        // read), to peer t's replica: one or two bulk DSMEM copies
+        const int nr = st.hdr[1];
+        const int b0 = r0 & (S - 1);
+        const int n2 = (nr + 1) & ~1;
+        const int first = b0 + n2 <= S ? n2 : S - b0;
+        const unsigned rb = map_rank(&recv[r & 1], unsigned(t));
+        const double* src = ring + int(rank) * S;
+        if (first > 0)
+          bulk_dsmem(map_rank(src + b0, unsigned(t)), smem_addr(src + b0), unsigned(first) * 8u, rb);
+        if (n2 > first)
+          bulk_dsmem(map_rank(src, unsigned(t)), smem_addr(src), unsigned(n2 - first) * 8u, rb);
+      }
       WALK_TRACE(t == 0, r, 3);
       WALK_TRACE(t == 0, r, 4);
       if (t == 0) mbar_arrive(&empty[slot]);
@@ -1285,7 +1331,8 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
           owner = (cj - seg_first[cj]) % C;
           const int nx = sub_first + C + owner;
           const int oc = (nx < nch && seg_of[nx] == seg_of[c]) ? nx : sub_first + owner;
-          in_ring = int64_t(h.sl_r0[oc]) + h.sl_nr[oc] - int64_t(lpos[jr]) <= S;
+          // (S - 2: the bulk push also rewrites one pad slot past the chunk)
+          in_ring = int64_t(h.sl_r0[oc]) + h.sl_nr[oc] - int64_t(lpos[jr]) <= S - 2;
         } else if (flow && !h.sl_wide[cj] && seg_of[cj] == seg_of[c]) {
           // dataflow: position s is overwritten by s + kRing, written no
           // earlier than chunk c + 2 (consumers run at most two chunks apart)
@@ -1488,7 +1535,8 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
         int rows = 0;
         for (int o = 0; o < h.C; ++o) {
           if (sf + o == s) continue;
-          rows += h.sl_nr[sf + o];
+          // ring slice, whole 16-byte pairs (bulk copy) or one slot per row
+          rows += kBulkPush ? (h.sl_nr[sf + o] + 1) & ~1 : h.sl_nr[sf + o];
           for (int t = 0; t < h.sl_nr[sf + o]; ++t) {
             const int32_t i = h.rows[h.sl_k[sf + o] + t];
             if (h.side[i]) ++rows;  // long-range copy
@@ -1717,10 +1765,15 @@ static void trace_report(Context& c, bool fwd, int C, int nsl) {
   if (hi <= 9) return;
   for (int rk = 0; rk < ranks; ++rk) {
     const long long* t = all.data() + size_t(rk) * kTraceSub * 16;
-    double d[8] = {0};
+    double d[8] = {0}, e3[3] = {0};
     const int n = hi - 8;
     for (int r = 8; r < hi; ++r) {
       const long long* x = &t[size_t(r) * 16];
+      if (x[5] > x[2] && x[6] >= x[5] && x[7] >= x[6]) {
+        e3[0] += x[5] - x[2];  // thread 0: first row folded
+        e3[1] += x[6] - x[5];  // its ring writes + pushes
+        e3[2] += x[3] - x[7];  // thread 0 done -> sub-level barrier passed
+      }
       d[0] += x[1] - x[0];                  // consumer wait full
       d[1] += x[2] - x[1];                  // products
       d[2] += x[3] - x[2];                  // rows
@@ -1736,6 +1789,8 @@ static void trace_report(Context& c, bool fwd, int C, int nsl) {
             "far %.0f\n",
             fwd ? "fwd" : "bwd", C, rk, nsl, d[0] / n, d[1] / n, d[2] / n, d[3] / n, d[4] / n,
             d[5] / n, d[6] / n, d[7] / n);
+    fprintf(stderr, "    thread 0: fold %.0f, push %.0f, wait at barrier %.0f\n", e3[0] / n, e3[1] / n,
+            e3[2] / n);
   }
 }
 
