@@ -11,6 +11,7 @@
 // so each MGS pass is one kernel with no host round trip.
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -207,6 +208,19 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+#ifdef PSCU_TRACE
+__device__ long long* g_mgs_trace = nullptr;  // per-pass clock64 stamps of CTA 0 thread 0
+#define MGS_STAMP(i, k)                                                          \
+  do {                                                                           \
+    if (g_mgs_trace && blockIdx.x == 0 && threadIdx.x == 0 && (i) < 1024)        \
+      g_mgs_trace[(i) * 4 + (k)] = clock64();                                    \
+  } while (0)
+#else
+#define MGS_STAMP(i, k) \
+  do {                  \
+  } while (0)
+#endif
+
 constexpr int kEpt = 16;  // elements per lane (repro_lanes guarantees <= 16 up to n = 2^22)
 
 __device__ __forceinline__ void st_pair(ulonglong2* p, unsigned long long a, unsigned long long b) {
@@ -262,6 +276,7 @@ __global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
     }
   double hprev = 0.0;
   for (int i = 0; i <= j + 1; ++i) {
+    MGS_STAMP(i, 0);
     double acc[kL];
 #pragma unroll
     for (int l = 0; l < kL; ++l) {
@@ -277,6 +292,7 @@ __global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
       }
     }
     const double cta = block_tree(kL == 1 ? acc[0] : dadd(acc[0], acc[kL - 1]), kStepThreads);
+    MGS_STAMP(i, 1);
     const int par = i & 1;
     const unsigned long long want = tag_base + unsigned(i) + 1ull;
     if (tid == 0) {
@@ -320,6 +336,7 @@ __global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
         v = __longlong_as_double(p.x);
       }
       __syncthreads();  // warp 0 finished reading block_tree's scratch of this pass
+      MGS_STAMP(i, 2);
       v = block_tree(v, G);
       if (tid == 0) {
         if (i == j + 1) v = __dsqrt_rn(v);
@@ -381,6 +398,7 @@ __global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
     }
     __syncthreads();
     hprev = hsh;
+    MGS_STAMP(i, 3);
     __syncthreads();
   }
   // v_{j+1} = w / h, or 0 on a happy breakdown (gmres.hpp:66-67)
@@ -640,9 +658,35 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     unsigned long long base = c.pass_tag;
     c.pass_tag += unsigned(j + 2);
     void* args[] = {&nn, &TT, &ei, &jj, &pw, &pV, &ld, &ph, &pv, &pt, &base};
+#ifdef PSCU_TRACE
+    static long long* tbuf = nullptr;
+    if (getenv("PSCU_MGS_TRACE") && !tbuf) {
+      PSCU_CUDA(cudaMalloc(&tbuf, sizeof(long long) * 4096));
+      PSCU_CUDA(cudaMemcpyToSymbol(g_mgs_trace, &tbuf, sizeof(tbuf)));
+    }
+#endif
     PSCU_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(G)),
                                           dim3(kStepThreads), args, smem, c.stream));
     PSCU_LAUNCHED(&c);
+#ifdef PSCU_TRACE
+    if (tbuf && j >= 100 && j % 100 == 0) {
+      std::vector<long long> h(4096);
+      PSCU_CUDA(cudaMemcpyAsync(h.data(), tbuf, sizeof(long long) * 4096, cudaMemcpyDeviceToHost,
+                                c.stream));
+      PSCU_CUDA(cudaStreamSynchronize(c.stream));
+      double d[4] = {0, 0, 0, 0};
+      int cnt = 0;
+      for (int i = 1; i + 1 <= j && i < 1000; ++i, ++cnt) {
+        const long long* t = &h[size_t(i) * 4];
+        d[0] += double(t[1] - t[0]);   // local compute + CTA tree
+        d[1] += double(t[2] - t[1]);   // publish + gather all pairs
+        d[2] += double(t[3] - t[2]);   // second tree + broadcast
+        d[3] += double(h[size_t(i + 1) * 4] - t[0]);  // whole pass
+      }
+      fprintf(stderr, "[mgs trace j=%d L=%d] cycles/pass: compute+tree %.0f gather %.0f tree2 %.0f | pass %.0f\n",
+              j, L, d[0] / cnt, d[1] / cnt, d[2] / cnt, d[3] / cnt);
+    }
+#endif
     return true;
   }
   return false;

@@ -26,6 +26,7 @@
 // the reference's exact operation sequence, so the result is bit-identical
 // to Ilu0::apply.
 #include <algorithm>
+#include <chrono>
 #include <queue>
 #include <atomic>
 #include <cstdio>
@@ -924,6 +925,25 @@ std::vector<int32_t> dag_levels(const Csr& a, const std::vector<int64_t>& diag, 
   return lvl;
 }
 
+/// Allocator that leaves new elements uninitialised (the big per-entry plan
+/// arrays are filled by parallel host threads, which then also take the
+/// first-touch page faults).
+template <typename T>
+struct UninitAlloc : std::allocator<T> {
+  template <typename U>
+  struct rebind {
+    using other = UninitAlloc<U>;
+  };
+  UninitAlloc() = default;
+  template <typename U>
+  UninitAlloc(const UninitAlloc<U>&) {}
+  template <typename U, typename... Args>
+  void construct(U* p, Args&&... args) {
+    if constexpr (sizeof...(Args) > 0) ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+    else ::new (static_cast<void*>(p)) U;
+  }
+};
+
 struct HostPlan {
   int C = 1;
   bool flow = false;  // single-CTA dataflow walker (flow_kernel), chunks span levels
@@ -931,9 +951,11 @@ struct HostPlan {
   bool levels = false;  // every task level is a wide chunk
   bool push_ok = true;
   std::vector<int32_t> side;  // push walker: long-range slot + 1 of a row (0: none), by row
-  std::vector<int32_t> sl_k, sl_nr, sl_nq, sl_nfar, sl_r0, rows, off, src, pos;
+  std::vector<int32_t> sl_k, sl_nr, sl_nq, sl_nfar, sl_r0, rows, off, pos;
+  std::vector<int32_t, UninitAlloc<int32_t>> src;   // per packed entry
+  std::vector<int64_t, UninitAlloc<int64_t>> from;  // per packed entry: factor position or -1
   std::vector<int32_t> far, sfar;  // pairs {entry offset in chunk, source row}
-  std::vector<int64_t> sl_f, sl_s, sl_q, from, dfrom;
+  std::vector<int64_t> sl_f, sl_s, sl_q, dfrom;
   std::vector<int32_t> dp, sl_d, sl_nd;  // walker chunks: diagonal starts (padded to 4)
   std::vector<int32_t> tq;               // wide chunks: entry offset per task (+ total)
   std::vector<int32_t> tt, sl_t, sl_nt;  // task tables (first local row per task, then the row
@@ -1033,13 +1055,23 @@ int level_chain_rows() {
 /// Chunks hold tasks (max_rows > 1 only for the push walker, whose
 /// consumers fold whole tasks).
 void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C, bool flow,
-                int S, int max_rows, HostPlan& h, bool all_wide = false) {
+                int S, int max_rows, HostPlan& h, bool all_wide = false,
+                const Tasks* pre = nullptr) {
   const int64_t n = a.n;
   const auto& rp = a.h_row_ptr;
   const auto& cols = a.h_cols;
   auto q_begin = [&](int64_t i) { return fwd ? rp[i] : diag[i] + 1; };
   auto q_end = [&](int64_t i) { return fwd ? diag[i] : rp[i + 1]; };
-  const Tasks T = build_tasks(a, diag, fwd, max_rows, all_wide ? kLevelMaxNz : kMaxDiag);
+  const auto tp0 = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (getenv("PSCU_PLAN_DEBUG"))
+      fprintf(stderr, "[plan %s n=%lld] %s %.3f s\n", fwd ? "fwd" : "bwd", (long long)a.n, what,
+              std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count());
+  };
+  Tasks own;
+  if (!pre) own = build_tasks(a, diag, fwd, max_rows, all_wide ? kLevelMaxNz : kMaxDiag);
+  const Tasks& T = pre ? *pre : own;
+  tick("tasks");
   std::vector<int32_t> task_of(n);
   for (size_t t = 0; t + 1 < T.ptr.size(); ++t)
     for (int32_t m = T.ptr[t]; m < T.ptr[t + 1]; ++m) task_of[T.rows[m]] = int32_t(t);
@@ -1186,6 +1218,7 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
       rem.swap(carry);
     }
   }
+  tick("chunks");
   h.sl_q.push_back((q + 3) & ~int64_t(3));
   h.npos = (k + 3) & ~int64_t(3);
   const int nch = int(h.sl_k.size());
@@ -1201,8 +1234,19 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
   h.off.assign(h.npos + 4, 0);
   h.dfrom.assign(h.npos + 4, -1);
   const int64_t total = h.sl_q.back() + 8;
-  h.from.assign(total, -1);
-  h.src.assign(total, 0);
+  h.from.resize(total);  // uninitialised: every entry is written below
+  h.src.resize(total);
+  {
+    // padding entries (chunk alignment, tail): no factor value, no source
+    auto pad = [&](int64_t q0, int64_t q1) {
+      for (int64_t q = q0; q < q1; ++q) {
+        h.from[q] = -1;
+        h.src[q] = 0;
+      }
+    };
+    for (int c = 0; c < nch; ++c) pad(h.sl_q[c] + h.sl_nq[c], h.sl_q[c + 1]);
+    pad(h.sl_q[nch], total);
+  }
   for (int64_t i = 0; i < n; ++i) h.rows[h.pos[i]] = int32_t(i);
   h.sl_f.assign(nch + 1, 0);
   h.sl_s.assign(nch + 1, 0);
@@ -1214,6 +1258,7 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
   h.sl_d.assign(nch, 0);
   h.sl_nd.assign(nch, 0);
   if (S) h.side.assign(n, 0);
+  tick("arrays");
   {
     // wide chunks (row-contiguous entries, global sources) are independent
     // of each other and of the walker lists: filled by parallel host threads
@@ -1261,6 +1306,7 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
     fill();
     for (auto& th : pool) th.join();
   }
+  tick("wide fill");
   std::vector<std::pair<int64_t, int32_t>> side_q;  // {entry, source row} read from slots
   std::vector<int32_t> last_read(S ? n : 0, -1);     // last reading sub-level (segment-local)
   for (int c = 0; c < nch; ++c) {
@@ -1457,6 +1503,22 @@ HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
     plan_sweep(a, diag, fwd, 1, false, 0, level_chain_rows(), h, true);
     return h;
   }
+  if (!mode && !getenv("PSCU_WALK_CLUSTER") && !getenv("PSCU_WALK_CLUSTER_FWD") &&
+      !getenv("PSCU_WALK_CLUSTER_BWD")) {
+    // wide sweeps (the fine levels: thousands of rows per task level) are
+    // too much data per level for the rings: task-level launches. Narrow
+    // ones (the coarse level, ~2 k rows per task level at 256^2): the push
+    // walker on four CTAs (1.05 ms per 256^2 coarse apply; 1.01 ms on 8).
+    const Tasks T = build_tasks(a, diag, fwd, level_chain_rows(), kLevelMaxNz);
+    if (a.n >= int64_t(3000) * std::max(1, T.nlev)) {
+      plan_sweep(a, diag, fwd, 1, false, 0, level_chain_rows(), h, true, &T);
+      return h;
+    }
+    plan_sweep(a, diag, fwd, 4, false, kRingTotal / 4, chain_rows(), h);
+    if (h.push_ok) return h;
+    plan_sweep(a, diag, fwd, 1, false, 0, level_chain_rows(), h, true, &T);
+    return h;
+  }
   const int C = pick_cluster(a, diag, fwd);
   if (C == kMaxCluster && !mode) {
     // wide sweeps (the fine levels): too much data per level for the rings
@@ -1559,8 +1621,8 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   w.off.upload(h.off, st);
   if (h.dp.empty()) w.dp.alloc(4);
   else w.dp.upload(h.dp, st);
-  w.src.upload(h.src, st);
-  w.from.upload(h.from, st);
+  w.src.upload(h.src.data(), h.src.size(), st);
+  w.from.upload(h.from.data(), h.from.size(), st);
   w.val.alloc(h.from.size());
   if (!fwd) {
     w.dfrom.upload(h.dfrom, st);
