@@ -397,3 +397,21 @@ def test_gmres_mgs_variants_bitwise(S, monkeypatch, tma, side):
         g = S.gmres(m, ilu, b, x0, maxit, rtol, side=side)
         assert g.iterations == r["its"] and g.converged == r["converged"]
         assert same(g.x, r["x"])
+
+
+def test_gmres_wide_grid_reduction_bitwise(S):
+    """A size where the fused Arnoldi step's grid reduction runs over 64 CTAs
+    (warp 0 of every CTA gathers two CTA partials per lane): 128^2 tris, k=0."""
+    s = O.RefSystem(mesh="unit-tri", n=128, jitter=0.2, seed=0, side="top", scheme="hho-dp",
+                    strategy="v-cond", k=0, data="sincos")
+    a = s.csr()
+    assert a.n > 16 * 256 * 32
+    ra = O.RefCsr(a)
+    ri = O.RefIlu(ra)
+    m = S.CsrMatrix(a.row_ptr, a.cols, a.vals)
+    ilu = S.Ilu0(m)
+    b = np.random.default_rng(7).standard_normal(a.n)
+    x0 = np.zeros(a.n)
+    r = O.ref_gmres(ra, ri, b, x0, 25, 0.0, left=False)
+    g = S.gmres(m, ilu, b, x0, 25, 0.0, side="right")
+    assert g.iterations == r["its"] and same(g.x, r["x"])
