@@ -571,8 +571,6 @@ __device__ __forceinline__ void bulk_dsmem(unsigned dst, unsigned src, unsigned 
       : "memory");
 }
 
-constexpr int kFastRows = 4;   // push walker: tasks folded from registers (rows,
-constexpr int kFastNz = 16;    //   factor entries)
 constexpr int kPushConsumers = 256;  // consumer threads (default; 512 selectable)
 
 /// One row of the push walker: acc = rhs - sum_u val_u * y(src_u), u
@@ -657,108 +655,48 @@ __global__ void __launch_bounds__(kCons + 32 * kPushProdWarps * kPushStages, 1)
       const unsigned rbar = smem_addr(&recv[r & 1]);
       // one task (a chain of rows, folded in order) per thread; a row reads
       // its task's earlier rows from this thread's own ring writes
-      // one row done: own ring slot, long-range slot (+ peers), y / yb
-      auto emit = [&](const int4& m, int row, double acc) {
-        ring[int(rank) * S + ((r0 + row) & (S - 1))] = acc;
-        if (m.w) {
-          ring[kRingTotal + m.w - 1] = acc;
-          for (int o = 0; o < C; ++o) {
-            if (o == int(rank)) continue;
-            unsigned ra, rb2;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra)
-                         : "r"(smem_addr(ring + kRingTotal + m.w - 1)), "r"(o));
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb2) : "r"(rbar), "r"(o));
-            push_value(ra, acc, rb2);
-          }
-        }
-        y[m.y] = acc;
-        if (kFwd) yb[m.z] = acc;
-      };
       for (int task = t; task < nt; task += kCons) {
-        const int rbeg = st.tt[task], re = st.tt[task + 1], nrow = re - rbeg;
-        if (kBulkPush && nrow <= kFastRows) {
-          // short task: every operand loaded up front (no load waits behind
-          // this thread's own ring stores), in-task sources taken from
-          // registers
-          int4 mm[kFastRows];
-          int beg[kFastRows + 1];
-          beg[0] = 0;
-#pragma unroll
-          for (int k = 0; k < kFastRows; ++k) {
-            mm[k] = k < nrow ? st.meta[rbeg + k] : make_int4(0, 0, 0, 0);
-            beg[k + 1] = beg[k] + mm[k].x;
-          }
-          if (beg[kFastRows] <= kFastNz) {
-            const int tot = beg[kFastRows];
-            const int slot0 = (r0 + rbeg) & (S - 1);
-            int cl[kFastNz];
-            double pv[kFastNz];
-#pragma unroll
-            for (int v = 0; v < kFastNz; ++v) {
-              const bool ok = v < tot;
-              const int e = ok ? st.dptr[v] + task : 0;
-              const int sv = ok ? st.src[e] : -1;
-              const double val = ok ? st.val[e] : 0.0;
-              const int rel = sv - int(rank) * S;
-              const int kk = (rel - slot0) & (S - 1);
-              cl[v] = (sv >= 0 && rel >= 0 && rel < S && kk < nrow) ? kk : -1;
-              pv[v] = (sv >= 0 && cl[v] < 0) ? dmul(val, ring[sv]) : val;
-            }
-            double rv[kFastRows];
-#pragma unroll
-            for (int k = 0; k < kFastRows; ++k) {
-              rv[k] = 0.0;
-              if (k < nrow) {
-                double acc = st.rhs[rbeg + k];
-#pragma unroll
-                for (int v = 0; v < kFastNz; ++v) {
-                  if (v >= beg[k] && v < beg[k + 1]) {
-                    double src = rv[0];
-#pragma unroll
-                    for (int q = 1; q < kFastRows; ++q)
-                      if (cl[v] == q) src = rv[q];
-                    acc = dsub(acc, cl[v] >= 0 ? dmul(pv[v], src) : pv[v]);
-                  }
-                }
-                if (!kFwd) acc = __ddiv_rn(acc, st.dv[rbeg + k]);
-                rv[k] = acc;
-                emit(mm[k], rbeg + k, acc);
-              }
-            }
-            WALK_TRACE(t == 0 && task == 0, r, 5);
-            WALK_TRACE(t == 0 && task == 0, r, 6);
-            continue;
-          }
-        }
+        const int re = st.tt[task + 1];
         int u0 = 0;
-        for (int row = rbeg; row < re; ++row) {
+        for (int row = st.tt[task]; row < re; ++row) {
           const int4 m = st.meta[row];
           const double acc = push_row<kFwd>(st, ring, task, u0, row, m);
           WALK_TRACE(t == 0 && row == st.tt[0], r, 5);
           u0 += m.x;
+          const int pos = r0 + row;
+          double* own = ring + int(rank) * S + (pos & (S - 1));
+          *own = acc;
+          // a value read beyond the ring window also goes to its long-range slot
+          if (m.w) ring[kRingTotal + m.w - 1] = acc;
           if (kBulkPush) {
-            emit(m, row, acc);
+            // ring slots reach the peers in one bulk copy per peer after the
+            // sub-level barrier; only long-range copies go out per row
+            if (m.w)
+              for (int o = 0; o < C; ++o) {
+                if (o == int(rank)) continue;
+                unsigned ra, rb;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra)
+                             : "r"(smem_addr(ring + kRingTotal + m.w - 1)), "r"(o));
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(rbar), "r"(o));
+                push_value(ra, acc, rb);
+              }
           } else {
-            const int pos = r0 + row;
-            double* own = ring + int(rank) * S + (pos & (S - 1));
-            *own = acc;
-            if (m.w) ring[kRingTotal + m.w - 1] = acc;
             for (int o = 0; o < C; ++o) {
               if (o == int(rank)) continue;
-              unsigned ra, rb2;
+              unsigned ra, rb;
               asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(own)), "r"(o));
-              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb2) : "r"(rbar), "r"(o));
-              push_value(ra, acc, rb2);
+              asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(rbar), "r"(o));
+              push_value(ra, acc, rb);
               if (m.w) {
                 asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra)
                              : "r"(smem_addr(ring + kRingTotal + m.w - 1)), "r"(o));
-                push_value(ra, acc, rb2);
+                push_value(ra, acc, rb);
               }
             }
-            y[m.y] = acc;
-            if (kFwd) yb[m.z] = acc;
           }
           WALK_TRACE(t == 0 && row == st.tt[0], r, 6);
+          y[m.y] = acc;
+          if (kFwd) yb[m.z] = acc;
         }
       }
       WALK_TRACE(t == 0, r, 7);
