@@ -326,45 +326,22 @@ __global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
       // round trip per pass, no root. A slot of parity par is rewritten two
       // passes later, after every CTA has published the pass in between,
       // i.e. after every CTA finished reading it.
-      // Warp 0 alone gathers the G pairs: lane l holds the contiguous block
-      // [l per, (l+1) per) (a subtree of the adjacent-pair tree), reduces it
-      // in-lane, then the shuffle tree over the lanes completes the same
-      // tree; no barrier until the broadcast below.
       ulonglong2* pairs = reinterpret_cast<ulonglong2*>(slot_tag);
-      if (tid < 32) {
-        const int per = G > 32 ? G / 32 : 1;
-        const int lanes = G > 32 ? 32 : G;
-        double v = 0.0;
-        if (tid < lanes) {
-          double b[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            b[q] = 0.0;
-            if (q < per) {
-              ulonglong2 p;
-              do {
-                p = ld_pair(pairs + par * G + tid * per + q);
-              } while ((p.x ^ p.y) != want);
-              b[q] = __longlong_as_double(p.x);
-            }
-          }
-#pragma unroll
-          for (int wdt = 8; wdt > 1; wdt >>= 1)
-            if (wdt <= per)
-#pragma unroll
-              for (int q = 0; q < wdt / 2; ++q) b[q] = dadd(b[2 * q], b[2 * q + 1]);
-          v = b[0];
-        }
-        MGS_STAMP(i, 2);
-        for (int off = 1; off < lanes; off <<= 1) {
-          const double o = __shfl_down_sync(0xffffffffu, v, off);
-          if ((tid & (2 * off - 1)) == 0) v = dadd(v, o);
-        }
-        if (tid == 0) {
-          if (i == j + 1) v = __dsqrt_rn(v);
-          hsh = v;
-          if (blockIdx.x == 0) hcol[i] = v;
-        }
+      double v = 0.0;
+      if (tid < G) {
+        ulonglong2 p;
+        do {
+          p = ld_pair(pairs + par * G + tid);
+        } while ((p.x ^ p.y) != want);
+        v = __longlong_as_double(p.x);
+      }
+      __syncthreads();  // warp 0 finished reading block_tree's scratch of this pass
+      MGS_STAMP(i, 2);
+      v = block_tree(v, G);
+      if (tid == 0) {
+        if (i == j + 1) v = __dsqrt_rn(v);
+        hsh = v;
+        if (blockIdx.x == 0) hcol[i] = v;
       }
     } else if (kPairs) {
       // relaxed 16-byte {value, value ^ tag} pairs: a pair is accepted only
