@@ -123,7 +123,8 @@ struct WalkPlan {
   int64_t npos = 0;
   std::vector<WalkSeg> segments;
   DevBuf<int32_t> sl_k, sl_nr, sl_hdr, tt, tq, rows, off, dp, opos, src, far, sfar;
-  DevBuf<int64_t> sl_q, sl_f, sl_s, from, dfrom;
+  DevBuf<int64_t> sl_q, sl_f, sl_s, dfrom;
+  DevBuf<int32_t> from;  // factor position of every packed entry (-1: padding)
   DevBuf<double> val, dv;
   DevBuf<int4> meta;               // per position {length / offset, row, backward position, 0}
   mutable DevBuf<double> sfv;      // per-apply values of the static out-of-ring sources

@@ -30,7 +30,7 @@ void combine_launch(Context& c, int64_t n, int m, const double* x0, const double
                     const double* z, int64_t ldz, double* x);
 void sub_launch(Context& c, int64_t n, const double* a, const double* b, double* r);
 void prolong_add_launch(Context& c, int64_t n, const int32_t* f2c, const double* cc, double* w);
-void inherit_gather_launch(Context& c, int64_t nnz, const int64_t* src, const double* fine,
+void inherit_gather_launch(Context& c, int64_t nnz, const int32_t* src, const double* fine,
                            double* out);
 
 // ---------------------------------------------------------------------------
@@ -429,7 +429,9 @@ void inherit(Context& c, const Csr& fine, const std::vector<int64_t>& c2f, Csr& 
   for (int64_t ic = 0; ic < nc; ++ic) out.h_row_ptr[ic + 1] += out.h_row_ptr[ic];
   out.nnz = out.h_row_ptr[nc];
   out.h_cols.resize(size_t(out.nnz));
-  std::vector<int64_t> src(size_t(out.nnz));
+  if (fine.nnz >= (int64_t(1) << 31))
+    throw Error(PSCU_EINVAL, "inherit: more than 2^31 fine entries are not supported");
+  std::vector<int32_t> src(size_t(out.nnz));
   parallel_ranges(nc, [&](int64_t lo, int64_t hi) {
     for (int64_t ic = lo; ic < hi; ++ic) {
       const int64_t r = c2f[ic];
@@ -438,7 +440,7 @@ void inherit(Context& c, const Csr& fine, const std::vector<int64_t>& c2f, Csr& 
         const int64_t jc = f2c[fine.h_cols[p]];
         if (jc >= 0) {
           out.h_cols[k] = int32_t(jc);
-          src[k++] = p;
+          src[k++] = int32_t(p);
         }
       }
     }
@@ -446,7 +448,7 @@ void inherit(Context& c, const Csr& fine, const std::vector<int64_t>& c2f, Csr& 
   out.row_ptr.upload(out.h_row_ptr, c.stream);
   out.cols.upload(out.h_cols, c.stream);
   out.vals.alloc(out.nnz);
-  DevBuf<int64_t> dsrc;
+  DevBuf<int32_t> dsrc;
   dsrc.upload(src, c.stream);
   inherit_gather_launch(c, out.nnz, dsrc.p, fine.vals.p, out.vals.p);
   PSCU_CUDA(cudaStreamSynchronize(c.stream));
@@ -626,7 +628,7 @@ __global__ void prolong_add(int64_t n, const int32_t* __restrict__ f2c,
   }
 }
 
-__global__ void gather_kernel(int64_t nnz, const int64_t* __restrict__ src,
+__global__ void gather_kernel(int64_t nnz, const int32_t* __restrict__ src,
                               const double* __restrict__ fine, double* __restrict__ out) {
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nnz;
        q += int64_t(gridDim.x) * blockDim.x)
@@ -645,7 +647,7 @@ void prolong_add_launch(Context& c, int64_t n, const int32_t* f2c, const double*
   PSCU_LAUNCHED(&c);
 }
 
-void inherit_gather_launch(Context& c, int64_t nnz, const int64_t* src, const double* fine,
+void inherit_gather_launch(Context& c, int64_t nnz, const int32_t* src, const double* fine,
                            double* out) {
   if (!nnz) return;
   gather_kernel<<<grid1d(nnz), 256, 0, c.stream>>>(nnz, src, fine, out);

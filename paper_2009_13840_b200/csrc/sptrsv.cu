@@ -44,12 +44,69 @@ __global__ void ilu0_factor_level(int nrows, const int32_t* __restrict__ rows,
   }
 }
 
+/// The same with one warp per row: row i sits in shared memory; for each k
+/// of its lower part (ascending, as the reference) the lanes take row k's
+/// upper entries 32 at a time, find their column in row i by binary search
+/// and apply lu[r] -= l_ik * lu[q] (distinct r per k, so the updates of an
+/// entry still arrive in k order, individually rounded: bit-identical).
+/// Global loads are one round per k instead of one per merge step.
+constexpr int kFacWarps = 4;
+constexpr int kFacMaxRow = 256;
+
+__global__ void __launch_bounds__(32 * kFacWarps)
+    ilu0_factor_level_warp(int nrows, const int32_t* __restrict__ rows,
+                           const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                           double* lu, const int64_t* __restrict__ diag, int* err) {
+  __shared__ int32_t sc[kFacWarps][kFacMaxRow];
+  __shared__ double sv[kFacWarps][kFacMaxRow];
+  const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+  for (int t = int(blockIdx.x) * kFacWarps + w; t < nrows; t += gridDim.x * kFacWarps) {
+    const int i = rows[t];
+    const int64_t r0 = rp[i];
+    const int len = int(rp[i + 1] - r0), di = int(diag[i] - r0);
+    for (int e = lane; e < len; e += 32) {
+      sc[w][e] = cols[r0 + e];
+      sv[w][e] = lu[r0 + e];
+    }
+    __syncwarp();
+    for (int p = 0; p < di; ++p) {
+      const int k = sc[w][p];
+      const int64_t dk = diag[k], qe = rp[k + 1];
+      const double piv = lu[dk];
+      if (piv == 0.0 && lane == 0) atomicMin(err, k);
+      const double lik = __ddiv_rn(sv[w][p], piv);
+      __syncwarp();
+      if (lane == 0) sv[w][p] = lik;
+      for (int64_t q0 = dk + 1; q0 < qe; q0 += 32) {
+        const int64_t q = q0 + lane;
+        if (q < qe) {
+          const int cq = cols[q];
+          const double lq = lu[q];
+          int lo = p + 1, hi = len;  // first entry of row i with column >= cq
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sc[w][mid] < cq) lo = mid + 1;
+            else hi = mid;
+          }
+          if (lo < len && sc[w][lo] == cq) sv[w][lo] = dsub(sv[w][lo], dmul(lik, lq));
+        }
+      }
+      __syncwarp();
+    }
+    for (int e = lane; e < len; e += 32) lu[r0 + e] = sv[w][e];
+    if (lane == 0 && sv[w][di] == 0.0) atomicMin(err, i);
+    __syncwarp();
+  }
+}
+
 } // namespace
 
 void ilu0_factor_start(Context& c, Ilu& ilu) {
   const Csr& a = *ilu.a;
   if (a.n == 0) return;
   const int64_t n = a.n;
+  const bool dbg = getenv("PSCU_DEBUG") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   std::vector<int64_t>& diag = ilu.h_diag;
   diag.assign(n, 0);
   for (int64_t i = 0; i < n; ++i) {
@@ -85,13 +142,42 @@ void ilu0_factor_start(Context& c, Ilu& ilu) {
                             c.stream));
   const int big = 0x7fffffff;
   PSCU_CUDA(cudaMemcpyAsync(c.err_flag.p, &big, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (dbg) {
+    PSCU_CUDA(cudaEventCreate(&e0));
+    PSCU_CUDA(cudaEventCreate(&e1));
+    PSCU_CUDA(cudaEventRecord(e0, c.stream));
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  int64_t maxrow = 0;
+  for (int64_t i = 0; i < n; ++i) maxrow = std::max(maxrow, a.h_row_ptr[i + 1] - a.h_row_ptr[i]);
+  const bool warp_rows = maxrow <= kFacMaxRow && !getenv("PSCU_FACTOR_THREAD");
   for (int l = 0; l < nlev; ++l) {
     const int nr = ilu.flev_ptr[l + 1] - ilu.flev_ptr[l];
-    const int grid = std::min((nr + 127) / 128, 148 * 8);
-    ilu0_factor_level<<<grid, 128, 0, c.stream>>>(nr, ilu.flev_rows.p + ilu.flev_ptr[l],
-                                                   a.row_ptr.p, a.cols.p, ilu.lu.p, ilu.diag.p,
-                                                   c.err_flag.p);
+    if (warp_rows) {
+      const int grid = std::min((nr + kFacWarps - 1) / kFacWarps, 148 * 16);
+      ilu0_factor_level_warp<<<grid, 32 * kFacWarps, 0, c.stream>>>(
+          nr, ilu.flev_rows.p + ilu.flev_ptr[l], a.row_ptr.p, a.cols.p, ilu.lu.p, ilu.diag.p,
+          c.err_flag.p);
+    } else {
+      const int grid = std::min((nr + 127) / 128, 148 * 8);
+      ilu0_factor_level<<<grid, 128, 0, c.stream>>>(nr, ilu.flev_rows.p + ilu.flev_ptr[l],
+                                                     a.row_ptr.p, a.cols.p, ilu.lu.p, ilu.diag.p,
+                                                     c.err_flag.p);
+    }
     PSCU_LAUNCHED(&c);
+  }
+  if (dbg) {
+    PSCU_CUDA(cudaEventRecord(e1, c.stream));
+    const auto t2 = std::chrono::steady_clock::now();
+    PSCU_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    PSCU_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    fprintf(stderr, "[setup] ilu0 factor n=%lld: host prep %.3f s, %d level launches issued in %.3f s, device %.3f s\n",
+            (long long)n, std::chrono::duration<double>(t1 - t0).count(), nlev,
+            std::chrono::duration<double>(t2 - t1).count(), ms / 1e3);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   }
 }
 

@@ -883,7 +883,8 @@ __global__ void gather_rhs(int64_t npos, const int32_t* __restrict__ rows,
   }
 }
 
-__global__ void gather_vals(int64_t m, const int64_t* __restrict__ from,
+template <typename I>
+__global__ void gather_vals(int64_t m, const I* __restrict__ from,
                             const double* __restrict__ lu, double* __restrict__ out) {
   for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < m;
        q += int64_t(gridDim.x) * blockDim.x) {
@@ -953,7 +954,7 @@ struct HostPlan {
   std::vector<int32_t> side;  // push walker: long-range slot + 1 of a row (0: none), by row
   std::vector<int32_t> sl_k, sl_nr, sl_nq, sl_nfar, sl_r0, rows, off, pos;
   std::vector<int32_t, UninitAlloc<int32_t>> src;   // per packed entry
-  std::vector<int64_t, UninitAlloc<int64_t>> from;  // per packed entry: factor position or -1
+  std::vector<int32_t, UninitAlloc<int32_t>> from;  // per packed entry: factor position or -1
   std::vector<int32_t> far, sfar;  // pairs {entry offset in chunk, source row}
   std::vector<int64_t> sl_f, sl_s, sl_q, dfrom;
   std::vector<int32_t> dp, sl_d, sl_nd;  // walker chunks: diagonal starts (padded to 4)
@@ -1293,7 +1294,7 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
           for (int64_t u = 0; u < len; ++u) {
             const int64_t qq = h.sl_q[c] + roff + u;
             const int32_t jr = cols[qb + u];
-            h.from[qq] = qb + u;
+            h.from[qq] = int32_t(qb + u);
             h.src[qq] = task_of[jr] == ti ? h.pos[jr] - first : -(jr + 1);
           }
           roff += len;
@@ -1359,7 +1360,7 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
         const int64_t e = h.sl_wide[c] ? roff + u : int64_t(dstart[uo[t] + u]) + ti[t];  // in chunk
         const int64_t qq = h.sl_q[c] + e;
         const int32_t jr = cols[p];
-        h.from[qq] = p;
+        h.from[qq] = int32_t(p);
         if (h.sl_wide[c]) {
           // wide launches read global memory directly; a source in the row's
           // own task is its index within the task (the same thread / warp
@@ -1498,6 +1499,8 @@ int pick_cluster(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
 
 HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
   HostPlan h;
+  if (a.nnz >= (int64_t(1) << 31))
+    throw Error(PSCU_EINVAL, "walk plan: more than 2^31 factor entries per level are not supported");
   const char* mode = getenv("PSCU_WALK_MODE");
   if (mode && !strcmp(mode, "levels")) {
     plan_sweep(a, diag, fwd, 1, false, 0, level_chain_rows(), h, true);

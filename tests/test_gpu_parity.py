@@ -415,3 +415,17 @@ def test_gmres_wide_grid_reduction_bitwise(S):
     r = O.ref_gmres(ra, ri, b, x0, 25, 0.0, left=False)
     g = S.gmres(m, ilu, b, x0, 25, 0.0, side="right")
     assert g.iterations == r["its"] and same(g.x, r["x"])
+
+
+@pytest.mark.parametrize("thread_rows", ["0", "1"])
+@pytest.mark.parametrize("ci", range(len(PLAN_CASES)))
+def test_ilu0_factor_variants_bitwise(S, monkeypatch, thread_rows, ci):
+    """ILU(0) factorisation with one warp per row (default) and one thread
+    per row (PSCU_FACTOR_THREAD): factors bit-identical to ilu0.hpp."""
+    if thread_rows == "1":
+        monkeypatch.setenv("PSCU_FACTOR_THREAD", "1")
+    s = O.RefSystem(**PLAN_CASES[ci])
+    a = s.csr()
+    ri = O.RefIlu(O.RefCsr(a))
+    ilu = S.Ilu0(S.CsrMatrix(a.row_ptr, a.cols, a.vals))
+    assert same(ilu.factors(), ri.factors())
