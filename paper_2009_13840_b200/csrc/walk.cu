@@ -782,12 +782,21 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
   const int32_t* tt = a.tt + hd[9];
   const int32_t* tq = a.tq + hd[9];
   const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+  // programmatic dependent launch: the next level's grid may start now; it
+  // loads its static plan data while this level finishes, then waits for
+  // this grid (griddepcontrol.wait) before touching right-hand sides and y
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  bool waited = false;
   for (int task = int(blockIdx.x) * kLevelWarps + w; task < nt; task += gridDim.x * kLevelWarps) {
-    // one round trip for the task record, one for its rows and entries,
-    // one for the sources outside the task
+    // one round trip for the task record, one for its rows and entries
+    // (both static), one for the sources outside the task
 #ifdef PSCU_TRACE
     const bool tr = a.trace && task == 0 && lane == 0 && ch < kTraceSub;
     if (tr) a.trace[size_t(ch) * 16 + 0] = clock64();
+    // every task of chunk 100: globaltimer at start and end (spread of a level)
+    const bool tr2 = a.trace && ch == 100 && lane == 0 && task < 8192;
+    unsigned long long gt0 = 0;
+    if (tr2) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
 #endif
     const int r0 = tt[task], r1 = tt[task + 1];
     const int e0 = tq[task], ne = tq[task + 1] - e0;
@@ -804,9 +813,13 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
       const int k = k0 + r0 + lane;
       const int len = int((r0 + lane + 1 < nr ? a.off[k + 1] : nq) - a.off[k]);
       mb[w][lane] = make_int4(len, a.rows[k], kFwd ? a.opos[k] : 0, 0);
-      rb[w][lane] = rhs[k];
       if (!kFwd) dvb[w][lane] = a.dv[k];
     }
+    if (!waited) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      waited = true;
+    }
+    if (lane < r1 - r0) rb[w][lane] = __ldcg(rhs + k0 + r0 + lane);
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int e = lane + 32 * u;
@@ -859,6 +872,12 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
       }
 #ifdef PSCU_TRACE
       if (tr) a.trace[size_t(ch) * 16 + 2] = clock64();
+      if (tr2) {
+        unsigned long long gt1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+        a.trace[size_t(kTraceSub) * 16 + size_t(task) * 2] = (long long)gt0;
+        a.trace[size_t(kTraceSub) * 16 + size_t(task) * 2 + 1] = (long long)gt1;
+      }
 #endif
     }
     __syncwarp();
@@ -1047,6 +1066,13 @@ int chain_rows() {
   return 3;  // 256^2 coarse apply: 1.43 ms (1), 1.61 (2), 1.28 (3), 3.8 (16)
 }
 
+/// Entry cap of a level-plan task: the slowest task's serial fold sets a
+/// level's time (~76 cycles per entry measured), so long chains are cut.
+int level_chain_nz() {
+  if (const char* e = getenv("PSCU_LEVEL_CHAIN_NZ")) return std::max(16, std::min(kLevelMaxNz, atoi(e)));
+  return kLevelMaxNz;
+}
+
 int level_chain_rows() {
   if (const char* e = getenv("PSCU_LEVEL_CHAIN_ROWS")) return std::max(1, std::min(kLevelMaxRows, atoi(e)));
   return 16;
@@ -1070,7 +1096,7 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
               std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count());
   };
   Tasks own;
-  if (!pre) own = build_tasks(a, diag, fwd, max_rows, all_wide ? kLevelMaxNz : kMaxDiag);
+  if (!pre) own = build_tasks(a, diag, fwd, max_rows, all_wide ? level_chain_nz() : kMaxDiag);
   const Tasks& T = pre ? *pre : own;
   tick("tasks");
   std::vector<int32_t> task_of(n);
@@ -1512,7 +1538,7 @@ HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
     // too much data per level for the rings: task-level launches. Narrow
     // ones (the coarse level, ~2 k rows per task level at 256^2): the push
     // walker on four CTAs (1.05 ms per 256^2 coarse apply; 1.01 ms on 8).
-    const Tasks T = build_tasks(a, diag, fwd, level_chain_rows(), kLevelMaxNz);
+    const Tasks T = build_tasks(a, diag, fwd, level_chain_rows(), level_chain_nz());
     if (a.n >= int64_t(3000) * std::max(1, T.nlev)) {
       plan_sweep(a, diag, fwd, 1, false, 0, level_chain_rows(), h, true, &T);
       return h;
@@ -1814,7 +1840,10 @@ static void launch_walker(Context& c, bool fwd, const WalkArgs& a, int c0, int n
 static long long* trace_buffer() {
   static long long* buf = [] {
     long long* p = nullptr;
-    if (getenv("PSCU_WALK_TRACE")) cudaMalloc(&p, sizeof(long long) * kTraceSub * 16 * kMaxCluster);
+    if (getenv("PSCU_WALK_TRACE")) {
+      cudaMalloc(&p, sizeof(long long) * kTraceSub * 16 * kMaxCluster);
+      cudaMemset(p, 0, sizeof(long long) * kTraceSub * 16 * kMaxCluster);
+    }
     return p;
   }();
   return buf;
@@ -1878,6 +1907,28 @@ static void level_trace_report(Context& c, const WalkPlan& w) {
   if (cnt)
     fprintf(stderr, "[level trace %s] tasks sampled %d: loads %.0f cycles, fold %.0f cycles, entries %.0f, rows %.1f\n",
             w.fwd ? "fwd" : "bwd", cnt, ld / cnt, fold / cnt, ne / cnt, nr / cnt);
+  {
+    std::vector<long long> g(8192 * 2);
+    PSCU_CUDA(cudaMemcpy(g.data(), trace_buffer() + size_t(kTraceSub) * 16, sizeof(long long) * g.size(),
+                         cudaMemcpyDeviceToHost));
+    long long mn = -1, mx = 0, dmax = 0, smax = 0;
+    std::vector<long long> d;
+    for (int t = 0; t < 8192; ++t) {
+      if (g[2 * t] <= 0 || g[2 * t + 1] < g[2 * t]) continue;
+      if (mn < 0 || g[2 * t] < mn) mn = g[2 * t];
+      mx = std::max(mx, g[2 * t + 1]);
+      d.push_back(g[2 * t + 1] - g[2 * t]);
+    }
+    if (!d.empty()) {
+      std::sort(d.begin(), d.end());
+      for (int t = 0; t < 8192; ++t)
+        if (g[2 * t] > 0) smax = std::max(smax, g[2 * t] - mn);
+      dmax = d.back();
+      fprintf(stderr, "[level trace %s] chunk 100: %zu tasks, span %.1f us, task median %.1f us max %.1f us, last start +%.1f us\n",
+              w.fwd ? "fwd" : "bwd", d.size(), (mx - mn) / 1e3, d[d.size() / 2] / 1e3, dmax / 1e3, smax / 1e3);
+    }
+    PSCU_CUDA(cudaMemset(trace_buffer() + size_t(kTraceSub) * 16, 0, sizeof(long long) * g.size()));
+  }
 }
 
 static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y, double* yb) {
@@ -1886,8 +1937,22 @@ static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y,
   for (const WalkSeg& s : w.segments) {
     if (s.wide && s.warp) {
       const unsigned g = unsigned(std::max(1, std::min(148 * 8, (s.tasks + kLevelWarps - 1) / kLevelWarps)));
-      if (w.fwd) level_kernel<true><<<g, 32 * kLevelWarps, 0, c.stream>>>(a, s.s0, rhs, y, yb);
-      else level_kernel<false><<<g, 32 * kLevelWarps, 0, c.stream>>>(a, s.s0, rhs, y, yb);
+      static const bool pdl = [] {
+        const char* e = getenv("PSCU_LEVEL_PDL");
+        return e ? atoi(e) != 0 : true;
+      }();
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(g);
+      cfg.blockDim = dim3(32 * kLevelWarps);
+      cfg.stream = c.stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = pdl ? 1 : 0;
+      const int s0 = s.s0;
+      if (w.fwd) PSCU_CUDA(cudaLaunchKernelEx(&cfg, level_kernel<true>, a, s0, rhs, y, yb));
+      else PSCU_CUDA(cudaLaunchKernelEx(&cfg, level_kernel<false>, a, s0, rhs, y, yb));
       PSCU_LAUNCHED(&c);
     } else if (s.wide) {
       if (w.fwd) wide_kernel<true><<<148 * 4, 256, 0, c.stream>>>(a, s.s0, rhs, y, yb);
