@@ -1061,7 +1061,9 @@ Tasks build_tasks(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int 
 /// back to back (~0.5-1k cycles of dependent latency per row, measured), so
 /// long chains cost more than the sub-level handshakes they save. Task-level launches (one warp per task,
 /// ~5 us per launch): chains of up to 16 rows cut the fine-level depth 12x.
-int chain_rows() {
+int chain_rows(bool fwd = true) {
+  if (const char* e = getenv(fwd ? "PSCU_CHAIN_ROWS_FWD" : "PSCU_CHAIN_ROWS_BWD"))
+    return std::max(1, std::min(64, atoi(e)));
   if (const char* e = getenv("PSCU_CHAIN_ROWS")) return std::max(1, std::min(64, atoi(e)));
   return 3;  // 256^2 coarse apply: 1.43 ms (1), 1.61 (2), 1.28 (3), 3.8 (16)
 }
@@ -1543,7 +1545,12 @@ HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
       plan_sweep(a, diag, fwd, 1, false, 0, level_chain_rows(), h, true, &T);
       return h;
     }
-    plan_sweep(a, diag, fwd, 4, false, kRingTotal / 4, chain_rows(), h);
+    const int pc = [] {
+      const char* e = getenv("PSCU_PUSH_CTAS");
+      const int v = e ? atoi(e) : 4;
+      return v == 2 || v == 8 ? v : 4;
+    }();
+    plan_sweep(a, diag, fwd, pc, false, kRingTotal / pc, chain_rows(fwd), h);
     if (h.push_ok) return h;
     plan_sweep(a, diag, fwd, 1, false, 0, level_chain_rows(), h, true, &T);
     return h;
