@@ -260,7 +260,6 @@ __global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
   // grid-wide reduction of pass i completes
   constexpr int kE = StepShape<kL>::kE;
   __shared__ double hsh;
-  __shared__ double gpart[2][kStepThreads / 32];
   const int G = gridDim.x;
   const int tid = threadIdx.x;
   const int64_t lane0 = (int64_t(blockIdx.x) * kStepThreads + tid) * kL;
@@ -326,10 +325,7 @@ __global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
       // every CTA gathers all G pairs and rebuilds the same tree: one grid
       // round trip per pass, no root. A slot of parity par is rewritten two
       // passes later, after every CTA has published the pass in between,
-      // i.e. after every CTA finished reading it. Warps 0..G/32-1 reduce
-      // their lanes with shuffles (adjacent pairs), the warp partials go
-      // through shared memory (double-buffered by parity) and every thread
-      // finishes the tree itself: one barrier, no broadcast step.
+      // i.e. after every CTA finished reading it.
       ulonglong2* pairs = reinterpret_cast<ulonglong2*>(slot_tag);
       double v = 0.0;
       if (tid < G) {
@@ -339,29 +335,14 @@ __global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
         } while ((p.x ^ p.y) != want);
         v = __longlong_as_double(p.x);
       }
+      __syncthreads();  // warp 0 finished reading block_tree's scratch of this pass
       MGS_STAMP(i, 2);
-      const int nl = G < 32 ? G : 32, nw = G < 32 ? 1 : G / 32;
-      const int lane = tid & 31, wid = tid >> 5;
-      for (int off = 1; off < nl; off <<= 1) {
-        const double o = __shfl_down_sync(0xffffffffu, v, off);
-        if ((lane & (2 * off - 1)) == 0) v = dadd(v, o);
+      v = block_tree(v, G);
+      if (tid == 0) {
+        if (i == j + 1) v = __dsqrt_rn(v);
+        hsh = v;
+        if (blockIdx.x == 0) hcol[i] = v;
       }
-      if (lane == 0 && wid < nw) gpart[par][wid] = v;
-      __syncthreads();
-      double t[kStepThreads / 32];
-#pragma unroll
-      for (int q = 0; q < kStepThreads / 32; ++q) t[q] = q < nw ? gpart[par][q] : 0.0;
-#pragma unroll
-      for (int wdt = kStepThreads / 32; wdt > 1; wdt >>= 1)
-        if (wdt <= nw)
-#pragma unroll
-          for (int q = 0; q < wdt / 2; ++q) t[q] = dadd(t[2 * q], t[2 * q + 1]);
-      double hs = t[0];
-      if (i == j + 1) hs = __dsqrt_rn(hs);
-      if (blockIdx.x == 0 && tid == 0) hcol[i] = hs;
-      hprev = hs;
-      MGS_STAMP(i, 3);
-      continue;
     } else if (kPairs) {
       // relaxed 16-byte {value, value ^ tag} pairs: a pair is accepted only
       // when its two words agree on this pass's tag (a torn read never
