@@ -259,8 +259,12 @@ def run_ours(args, cfg):
                          restart=RESTART)
     dofs = A.n
 
+    setup_s = []
+
     def step():
+        t_h = time.perf_counter()
         h = S.LevelHierarchy(A, lay, lcfg)
+        setup_s.append(time.perf_counter() - t_h)
         x, hist, rep = h.solve(b)
         del h
         return rep
@@ -341,6 +345,7 @@ def run_ours(args, cfg):
             "restart": RESTART, "step": "hierarchy setup + FGMRES (reference t_solve)",
             "l2": "inputs larger than L2 (fine operator %.2f GB)" % ((12 * A.nnz) / 1e9),
             "assembly_s_untimed": round(t_asm, 3), "parallelism": f"replicas x{ws}",
+            "hierarchy_setup_s_in_step": round(setup_s[-1], 3),
         },
         "e2e": {"value": dofs * ws / t_e2e, "unit": "DoF/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
