@@ -141,6 +141,8 @@ struct WalkPlan {
   };
   mutable std::shared_ptr<Graph> graph;
   mutable DevBuf<double> ybuf;
+  mutable DevBuf<unsigned long long> barrier;  // persistent task-level kernel
+  int persist_grid = 0;                        // its grid (0: per-level launches)
 };
 
 struct Ilu {

@@ -766,9 +766,9 @@ __global__ void wide_kernel(WalkArgs a, int ch, const double* rhs, double* y, do
 /// just computed). Same rounded operations as ilu0.hpp:53-65.
 constexpr int kLevelWarps = 4;
 
-template <bool kFwd>
-__global__ void __launch_bounds__(32 * kLevelWarps)
-    level_kernel(WalkArgs a, int ch, const double* rhs, double* y, double* yb) {
+template <bool kFwd, bool kPdl>
+__device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const double* rhs, double* y,
+                                            double* yb) {
   constexpr int kPer = kLevelMaxNz / 32;  // entries per lane
   __shared__ double pbuf[kLevelWarps][kLevelMaxNz];
   __shared__ int32_t sbuf[kLevelWarps][kLevelMaxNz];
@@ -785,8 +785,8 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
   // programmatic dependent launch: the next level's grid may start now; it
   // loads its static plan data while this level finishes, then waits for
   // this grid (griddepcontrol.wait) before touching right-hand sides and y
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  bool waited = false;
+  if (kPdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  bool waited = !kPdl;
   for (int task = int(blockIdx.x) * kLevelWarps + w; task < nt; task += gridDim.x * kLevelWarps) {
     // one round trip for the task record, one for its rows and entries
     // (both static), one for the sources outside the task
@@ -881,6 +881,40 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
 #endif
     }
     __syncwarp();
+  }
+}
+
+template <bool kFwd>
+__global__ void __launch_bounds__(32 * kLevelWarps)
+    level_kernel(WalkArgs a, int ch, const double* rhs, double* y, double* yb) {
+  level_chunk<kFwd, true>(a, ch, rhs, y, yb);
+}
+
+/// Grid-wide barrier for the persistent task-level kernel: a monotone
+/// arrival counter (zeroed before the launch), target = levels x CTAs.
+__device__ __forceinline__ void level_barrier(unsigned long long* cnt, unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(cnt, 1ull);
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+/// All task levels of a level-plan sweep in one cooperative launch: a grid
+/// barrier replaces the kernel boundary between levels.
+template <bool kFwd>
+__global__ void __launch_bounds__(32 * kLevelWarps)
+    level_persist_kernel(WalkArgs a, int c0, int c1, const double* rhs, double* y, double* yb,
+                         unsigned long long* cnt) {
+  for (int ch = c0; ch < c1; ++ch) {
+    level_chunk<kFwd, false>(a, ch, rhs, y, yb);
+    if (ch + 1 < c1) level_barrier(cnt, (unsigned long long)(ch - c0 + 1) * gridDim.x);
   }
 }
 
@@ -1582,11 +1616,32 @@ HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
   return h;
 }
 
+static bool level_persist() {
+  static const bool v = [] {
+    const char* e = getenv("PSCU_LEVEL_PERSIST");
+    return e ? atoi(e) != 0 : false;
+  }();
+  return v;
+}
+
 void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   cudaStream_t st = c.stream;
   w.fwd = fwd;
   w.C = h.C;
   w.levels = h.levels;
+  w.persist_grid = 0;
+  if (h.levels && level_persist()) {
+    int per_sm = 0, sms = 0, dev = 0;
+    PSCU_CUDA(cudaGetDevice(&dev));
+    PSCU_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    void* fn = fwd ? (void*)level_persist_kernel<true> : (void*)level_persist_kernel<false>;
+    PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kLevelWarps, 0));
+    int most = 0;
+    for (size_t s = 0; s < h.sl_nt.size(); ++s) most = std::max(most, h.sl_nt[s]);
+    const int want = (std::min(most, 4096) + kLevelWarps - 1) / kLevelWarps;
+    w.persist_grid = std::max(1, std::min(want, per_sm * sms));
+    w.barrier.alloc(1);
+  }
   w.flow = h.flow;
   w.S = h.S;
   w.nsub = int(h.sl_k.size());
@@ -1941,6 +1996,17 @@ static void level_trace_report(Context& c, const WalkPlan& w) {
 static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y, double* yb) {
   WalkArgs a = args_of(w);
   a.trace = trace_buffer();
+  if (w.levels && w.persist_grid > 0 && !a.trace) {
+    // every task level of the sweep in one cooperative launch
+    PSCU_CUDA(cudaMemsetAsync(w.barrier.p, 0, sizeof(unsigned long long), c.stream));
+    int c0 = 0, c1 = w.nsub;
+    void* args[] = {&a, &c0, &c1, (void*)&rhs, (void*)&y, (void*)&yb, (void*)&w.barrier.p};
+    void* fn = w.fwd ? (void*)level_persist_kernel<true> : (void*)level_persist_kernel<false>;
+    PSCU_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(w.persist_grid)), dim3(32 * kLevelWarps),
+                                          args, 0, c.stream));
+    PSCU_LAUNCHED(&c);
+    return;
+  }
   for (const WalkSeg& s : w.segments) {
     if (s.wide && s.warp) {
       const unsigned g = unsigned(std::max(1, std::min(148 * 8, (s.tasks + kLevelWarps - 1) / kLevelWarps)));
@@ -1997,7 +2063,8 @@ void run_walk(Context& c, const WalkPlan& wf, const WalkPlan& wb, const double* 
     const char* e = getenv("PSCU_WALK_GRAPH");
     return e ? atoi(e) != 0 : true;
   }();
-  if (graphs && (wf.levels || wb.levels) && wf.segments.size() + wb.segments.size() > 16) {
+  if (graphs && (wf.levels || wb.levels) && wf.persist_grid == 0 && wb.persist_grid == 0 &&
+      wf.segments.size() + wb.segments.size() > 16) {
     // hundreds of task-level launches: replay them as one captured graph on
     // fixed buffers (the launch rate no longer bounds the sweep)
     const int64_t n = int64_t(wf.ybuf.n);

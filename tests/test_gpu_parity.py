@@ -429,3 +429,28 @@ def test_ilu0_factor_variants_bitwise(S, monkeypatch, thread_rows, ci):
     ri = O.RefIlu(O.RefCsr(a))
     ilu = S.Ilu0(S.CsrMatrix(a.row_ptr, a.cols, a.vals))
     assert same(ilu.factors(), ri.factors())
+
+
+def test_ilu0_persistent_levels_bitwise(S, monkeypatch):
+    """Task-level plans swept by one cooperative launch per sweep (grid
+    barrier between task levels, PSCU_LEVEL_PERSIST) in a fresh process."""
+    import subprocess, sys, os
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+import oracle_ref as O
+from paper_2009_13840_b200 import solver as S
+for c in [dict(mesh="unit-tri", n=12, jitter=0.2, seed=0, side="top", scheme="hho-dp", strategy="v-cond", k=3, data="sincos"),
+          dict(family="trapz", n=6, scheme="hho-dp", strategy="vp-cond", k=2)]:
+    s = O.RefSystem(**c); a = s.csr(); ri = O.RefIlu(O.RefCsr(a))
+    ilu = S.Ilu0(S.CsrMatrix(a.row_ptr, a.cols, a.vals))
+    for seed in range(2):
+        x = np.random.default_rng(seed).standard_normal(a.n)
+        assert np.all(ilu.apply(x) == ri.apply(x))
+print("persistent ok")
+'''
+    env = dict(os.environ, PSCU_LEVEL_PERSIST="1", PSCU_WALK_MODE="levels")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "persistent ok" in r.stdout, r.stdout + r.stderr
