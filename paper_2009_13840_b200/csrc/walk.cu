@@ -1633,7 +1633,8 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   w.C = h.C;
   w.levels = h.levels;
   w.persist_grid = 0;
-  if (h.levels && level_persist()) {
+  // (k=1 at 256^2, 1.2 M rows: per-level launches measured faster, 4.8 vs 5.2 ms)
+  if (h.levels && level_persist() && h.npos >= 1500000) {
     int per_sm = 0, sms = 0, dev = 0;
     PSCU_CUDA(cudaGetDevice(&dev));
     PSCU_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
