@@ -1634,7 +1634,8 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   w.levels = h.levels;
   w.persist_grid = 0;
   // (k=1 at 256^2, 1.2 M rows: per-level launches measured faster, 4.8 vs 5.2 ms)
-  if (h.levels && level_persist() && h.npos >= 1500000) {
+  const char* pm = getenv("PSCU_LEVEL_PERSIST_MIN_ROWS");
+  if (h.levels && level_persist() && h.npos >= (pm ? atoll(pm) : 1500000)) {
     int per_sm = 0, sms = 0, dev = 0;
     PSCU_CUDA(cudaGetDevice(&dev));
     PSCU_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

@@ -449,7 +449,8 @@ for c in [dict(mesh="unit-tri", n=12, jitter=0.2, seed=0, side="top", scheme="hh
         assert np.all(ilu.apply(x) == ri.apply(x))
 print("persistent ok")
 '''
-    env = dict(os.environ, PSCU_LEVEL_PERSIST="1", PSCU_WALK_MODE="levels")
+    env = dict(os.environ, PSCU_LEVEL_PERSIST="1", PSCU_WALK_MODE="levels",
+               PSCU_LEVEL_PERSIST_MIN_ROWS="0")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                        text=True, timeout=600)
