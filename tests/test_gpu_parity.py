@@ -376,13 +376,15 @@ def test_bjacobi_vcycle_and_solve_bitwise(S, c):
     assert same(hist, r["hist"]) and same(x, r["x"])
 
 
-@pytest.mark.parametrize("tma", ["0", "1"])
+@pytest.mark.parametrize("tma,allg", [("0", "0"), ("0", "1"), ("1", "0")])
 @pytest.mark.parametrize("side", ["right", "left"])
-def test_gmres_mgs_variants_bitwise(S, monkeypatch, tma, side):
-    """The fused Arnoldi step with the basis streamed through shared memory
-    by TMA (arnoldi_tma_kernel; forced at small sizes) and without it."""
+def test_gmres_mgs_variants_bitwise(S, monkeypatch, tma, allg, side):
+    """The fused Arnoldi step: root-CTA and all-gather grid reductions, and
+    the basis streamed through shared memory by TMA (arnoldi_tma_kernel;
+    forced at small sizes)."""
     monkeypatch.setenv("PSCU_MGS_TMA_MIN_G", "1")
     monkeypatch.setenv("PSCU_MGS_TMA", tma)
+    monkeypatch.setenv("PSCU_MGS_ALL", allg)
     s = O.RefSystem(**PLAN_CASES[0])
     a = s.csr()
     ra = O.RefCsr(a)
