@@ -579,10 +579,11 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     const char* e = getenv("PSCU_MGS_PAIRS");
     return e ? atoi(e) != 0 : true;
   }();
-  // root-CTA reduction by default (256^2 coarse: 537 vs 567 us per step for
-  // the all-gather variant, PSCU_MGS_ALL=1)
+  // all-gather reduction by default; the root-CTA variant (PSCU_MGS_ALL=0)
+  // measured 537 vs 567 us per coarse step in isolation but equal within
+  // noise over a whole solve (10.59 vs 10.51 s of Arnoldi steps)
   const char* ae = getenv("PSCU_MGS_ALL");
-  const bool all = ae ? atoi(ae) != 0 : false;
+  const bool all = ae ? atoi(ae) != 0 : true;
   // TMA-staged basis: correct, but measured slower than the register-
   // prefetch kernel at the 256^2 coarse level (766 vs 567 us per step)
   const char* te = getenv("PSCU_MGS_TMA");
