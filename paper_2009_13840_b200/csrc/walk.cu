@@ -58,6 +58,7 @@ constexpr int kMaxDiag = 128;      // longest task (factor entries) of a walker 
 constexpr int kHdr = 16;           // ints of a chunk header
 constexpr int kLevelMaxNz = 512;   // entries of a task of a level-launch plan (warp kernel buffer)
 constexpr int kLevelMaxRows = 32;  // rows of such a task
+constexpr int kPadSrc = int(0x80000000);  // level plans: pad entry (product 0; acc - 0.0 == acc)
 
 struct WalkArgs {
   const int32_t* sl_k;    // chunk start position (multiple of 4)
@@ -749,6 +750,7 @@ __global__ void wide_kernel(WalkArgs a, int ch, const double* rhs, double* y, do
       double acc = rhs[k];
       for (int64_t q = qa; q < qb; ++q) {
         const int sv = a.src[q];
+        if (sv == kPadSrc) continue;  // pad entry: acc - 0.0 == acc
         const int jr = sv < 0 ? -sv - 1 : a.rows[k0 + r0 + sv];
         acc = dsub(acc, dmul(a.val[q], __ldcg(y + jr)));
       }
@@ -823,14 +825,14 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int e = lane + 32 * u;
-      yv[u] = (e < ne && sv[u] < 0) ? __ldcg(y + (-sv[u] - 1)) : 0.0;
+      yv[u] = (e < ne && sv[u] < 0 && sv[u] != kPadSrc) ? __ldcg(y + (-sv[u] - 1)) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int e = lane + 32 * u;
       if (e < ne) {
         sbuf[w][e] = sv[u];
-        pbuf[w][e] = sv[u] < 0 ? dmul(v[u], yv[u]) : v[u];
+        pbuf[w][e] = sv[u] == kPadSrc ? 0.0 : (sv[u] < 0 ? dmul(v[u], yv[u]) : v[u]);
       }
     }
     __syncwarp();
@@ -1034,7 +1036,7 @@ struct Tasks {
 };
 
 Tasks build_tasks(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int max_rows,
-                  int max_nz) {
+                  int max_nz, int pad = 1) {
   const int64_t n = a.n;
   const auto& rp = a.h_row_ptr;
   const auto& cols = a.h_cols;
@@ -1048,7 +1050,7 @@ Tasks build_tasks(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int 
   for (int64_t p = 0; p < n; ++p) {
     const int64_t i = fwd ? p : n - 1 - p;
     const int64_t q0 = fwd ? rp[i] : diag[i] + 1, q1 = fwd ? diag[i] : rp[i + 1];
-    const int len = int(q1 - q0);
+    const int len = int((q1 - q0 + pad - 1) / pad * pad);  // entries incl. padding
     int64_t latest = -1;
     for (int64_t q = q0; q < q1; ++q)
       if (latest < 0 || (fwd ? cols[q] > latest : cols[q] < latest)) latest = cols[q];
@@ -1109,6 +1111,17 @@ int level_chain_nz() {
   return kLevelMaxNz;
 }
 
+/// Level plans pad every row to whole 8-entry blocks with zero products
+/// (acc - 0.0 == acc in IEEE arithmetic, so the fold is unchanged bit for
+/// bit) so the warp kernel's fold never takes its scalar remainder loop.
+int level_pad() {
+  static const int v = [] {
+    const char* e = getenv("PSCU_LEVEL_PAD");
+    return e ? (atoi(e) != 0 ? 8 : 1) : 8;
+  }();
+  return v;
+}
+
 int level_chain_rows() {
   if (const char* e = getenv("PSCU_LEVEL_CHAIN_ROWS")) return std::max(1, std::min(kLevelMaxRows, atoi(e)));
   return 16;
@@ -1131,8 +1144,9 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
       fprintf(stderr, "[plan %s n=%lld] %s %.3f s\n", fwd ? "fwd" : "bwd", (long long)a.n, what,
               std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count());
   };
+  const int pad = all_wide ? level_pad() : 1;
   Tasks own;
-  if (!pre) own = build_tasks(a, diag, fwd, max_rows, all_wide ? level_chain_nz() : kMaxDiag);
+  if (!pre) own = build_tasks(a, diag, fwd, max_rows, all_wide ? level_chain_nz() : kMaxDiag, pad);
   const Tasks& T = pre ? *pre : own;
   tick("tasks");
   std::vector<int32_t> task_of(n);
@@ -1176,7 +1190,7 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
     h.sl_nt.back()++;
     for (int32_t m = T.ptr[t]; m < T.ptr[t + 1]; ++m) {
       const int32_t i = T.rows[m];
-      const int64_t nz = q_end(i) - q_begin(i);
+      const int64_t nz = wide ? (q_end(i) - q_begin(i) + pad - 1) / pad * pad : q_end(i) - q_begin(i);
       if (!wide && nz > kMaxDiag) throw Error(PSCU_ECUDA, "walk plan: row exceeds the diagonal capacity");
       h.pos[i] = int32_t(k++);
       if (!wide) lpos[i] = int32_t(lcount[rank]++);
@@ -1339,7 +1353,8 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
           const int32_t* tt = h.tt.data() + h.sl_t[c];
           int64_t o = 0;
           for (int i = 0, t = 0; i < h.sl_nt[c]; ++i) {
-            for (; t < tt[i]; ++t) o += q_end(h.rows[h.sl_k[c] + t]) - q_begin(h.rows[h.sl_k[c] + t]);
+            for (; t < tt[i]; ++t)
+              o += (q_end(h.rows[h.sl_k[c] + t]) - q_begin(h.rows[h.sl_k[c] + t]) + pad - 1) / pad * pad;
             h.tq[h.sl_t[c] + i] = int32_t(o);
           }
           h.tq[h.sl_t[c] + h.sl_nt[c]] = h.sl_nq[c];
@@ -1348,8 +1363,13 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
           const int64_t kp = h.sl_k[c] + t;
           const int32_t i = h.rows[kp];
           const int64_t qb = q_begin(i), len = q_end(i) - qb;
+          const int64_t plen = (len + pad - 1) / pad * pad;
           h.off[kp] = int32_t(roff);
           h.dfrom[kp] = diag[i];
+          for (int64_t u = len; u < plen; ++u) {
+            h.from[h.sl_q[c] + roff + u] = -1;
+            h.src[h.sl_q[c] + roff + u] = kPadSrc;
+          }
           // a source in the row's own task: its index within the task (the
           // same thread / warp computed it just before)
           const int32_t ti = task_of[i], first = h.pos[T.rows[T.ptr[ti]]];
@@ -1359,7 +1379,7 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
             h.from[qq] = int32_t(qb + u);
             h.src[qq] = task_of[jr] == ti ? h.pos[jr] - first : -(jr + 1);
           }
-          roff += len;
+          roff += plen;
         }
       }
     };
@@ -1574,7 +1594,7 @@ HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
     // too much data per level for the rings: task-level launches. Narrow
     // ones (the coarse level, ~2 k rows per task level at 256^2): the push
     // walker on four CTAs (1.05 ms per 256^2 coarse apply; 1.01 ms on 8).
-    const Tasks T = build_tasks(a, diag, fwd, level_chain_rows(), level_chain_nz());
+    const Tasks T = build_tasks(a, diag, fwd, level_chain_rows(), level_chain_nz(), level_pad());
     if (a.n >= int64_t(3000) * std::max(1, T.nlev)) {
       plan_sweep(a, diag, fwd, 1, false, 0, level_chain_rows(), h, true, &T);
       return h;

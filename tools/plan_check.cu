@@ -92,6 +92,7 @@ int main(int argc, char** argv) {
             double acc = x[h.rows[k]];
             for (int64_t q = qa; q < qb; ++q) {
               const int sv = h.src[q];
+              if (sv == kPadSrc) continue;
               const int jr = sv < 0 ? -sv - 1 : h.rows[h.sl_k[ch] + tt[task] + sv];
               acc -= lu[h.from[q]] * y[jr];
             }
