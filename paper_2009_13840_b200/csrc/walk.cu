@@ -772,8 +772,9 @@ template <bool kFwd, bool kPdl>
 __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const double* rhs, double* y,
                                             double* yb) {
   constexpr int kPer = kLevelMaxNz / 32;  // entries per lane
-  __shared__ double pbuf[kLevelWarps][kLevelMaxNz];
-  __shared__ int32_t sbuf[kLevelWarps][kLevelMaxNz];
+  // per entry {product or factor value, in-task source index or < 0}: one
+  // 16-byte shared-memory load per entry in the fold
+  __shared__ double2 rec[kLevelWarps][kLevelMaxNz];
   __shared__ double rb[kLevelWarps][kLevelMaxRows], dvb[kLevelWarps][kLevelMaxRows],
       cv[kLevelWarps][kLevelMaxRows];
   __shared__ int4 mb[kLevelWarps][kLevelMaxRows];
@@ -831,8 +832,8 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
     for (int u = 0; u < kPer; ++u) {
       const int e = lane + 32 * u;
       if (e < ne) {
-        sbuf[w][e] = sv[u];
-        pbuf[w][e] = sv[u] == kPadSrc ? 0.0 : (sv[u] < 0 ? dmul(v[u], yv[u]) : v[u]);
+        rec[w][e] = make_double2(sv[u] == kPadSrc ? 0.0 : (sv[u] < 0 ? dmul(v[u], yv[u]) : v[u]),
+                                 __longlong_as_double((long long)sv[u]));
       }
     }
     __syncwarp();
@@ -855,8 +856,9 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
           double p8[8], c8[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            s8[k] = sbuf[w][e + k];
-            p8[k] = pbuf[w][e + k];
+            const double2 r2 = rec[w][e + k];
+            s8[k] = int(__double_as_longlong(r2.y));
+            p8[k] = r2.x;
           }
 #pragma unroll
           for (int k = 0; k < 8; ++k) c8[k] = s8[k] < 0 ? 0.0 : cv[w][s8[k]];
@@ -864,8 +866,9 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
           for (int k = 0; k < 8; ++k) acc = dsub(acc, s8[k] < 0 ? p8[k] : dmul(p8[k], c8[k]));
         }
         for (; e < e1; ++e) {
-          const int s = sbuf[w][e];
-          acc = dsub(acc, s < 0 ? pbuf[w][e] : dmul(pbuf[w][e], cv[w][s]));
+          const double2 r2 = rec[w][e];
+          const int s = int(__double_as_longlong(r2.y));
+          acc = dsub(acc, s < 0 ? r2.x : dmul(r2.x, cv[w][s]));
         }
         if (!kFwd) acc = __ddiv_rn(acc, dvb[w][r]);
         cv[w][r] = acc;
