@@ -140,6 +140,11 @@ def _ref_worker(args):
     """One reference process: assemble the sample (untimed, like the
     reference's own t_solve), then time hierarchy setup + FGMRES."""
     cfg, n, mode, rounds, maxit = args
+    # sampled mode runs exactly `maxit` FGMRES iterations (rtol 0: the
+    # reference's fixed-iteration convention, gmres.hpp:103-139), so the
+    # per-iteration stamps exist for any --warmup/--steps; full mode solves
+    # to the workload's rtol.
+    rtol = RTOL if mode == "full" else 0.0
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_ref as O
 
@@ -148,8 +153,11 @@ def _ref_worker(args):
                     k=cfg["k"], data="sincos")
     out = []
     for _ in range(rounds):
-        t_setup, stamps = s.solve_timed(cfg["degrees"], maxit, coarse=cfg["coarse"], rtol=RTOL,
+        t_setup, stamps = s.solve_timed(cfg["degrees"], maxit, coarse=cfg["coarse"], rtol=rtol,
                                         restart=RESTART)
+        if mode != "full" and len(stamps) < maxit:
+            raise RuntimeError(f"reference sample stopped after {len(stamps)} of {maxit} "
+                               "fixed FGMRES iterations (breakdown)")
         out.append((t_setup, stamps.tolist()))
     return s.n, out
 

@@ -6,13 +6,16 @@
 //   DeviceCsr      (CsrMatrix::multiply)  csr.hpp:68-76
 //   DeviceIlu0     (Ilu0 / Ilu0::apply)   ilu0.hpp:19-65
 //   DeviceHierarchy (LevelHierarchy)      plevels.hpp:125-206
+//   recover_solution(sys, x)              assemble.hpp:58-66, condense.hpp:28-38
 // and ApplyFn adapters (gmres.hpp:17) so the reference's own gmres/fgmres
 // can drive the device operators unchanged. Errors rethrow by code:
 // PSCU_EINVAL -> std::invalid_argument, everything else -> std::runtime_error.
 #pragma once
 
+#include <map>
 #include <memory>
 #include <stdexcept>
+#include <utility>
 #include <vector>
 
 #include "pstokes/plevels.hpp"
@@ -135,8 +138,48 @@ class DeviceHierarchy {
   std::unique_ptr<pscu_hier, int (*)(pscu_hier*)> h_{nullptr, pscu_hier_destroy};
 };
 
-/// solve_system (plevels.hpp:217-239) with the hierarchy and FGMRES on the
-/// device; recovery of the eliminated unknowns as the reference does it.
+/// StokesSystem::recover_solution (assemble.hpp:58-66) on the device:
+/// ElementCondensation::recover (condense.hpp:28-38) for every element
+/// through pscu_recover_batch, batched over the elements that share a local
+/// size and elimination list (all of them on the reference's meshes). The
+/// device back-substitution x_e = elim_rhs - elim_coupling x_k sums k
+/// ascending from 0 like the reference's product, so the result is bitwise.
+inline std::vector<Eigen::VectorXd> recover_solution(const StokesSystem& sys,
+                                                     const Eigen::VectorXd& x) {
+  std::map<std::pair<int, std::vector<int>>, std::vector<std::size_t>> groups;
+  for (std::size_t e = 0; e < sys.recovery.size(); ++e) {
+    const ElementCondensation& c = sys.recovery[e];
+    groups[{int(c.keep.size() + c.elim.size()), c.elim}].push_back(e);
+  }
+  std::vector<Eigen::VectorXd> out(sys.recovery.size());
+  for (const auto& [key, elems] : groups) {
+    const int n = key.first;
+    const std::vector<int>& elim = key.second;
+    const int ne = int(elim.size()), nk = n - ne;
+    const std::size_t ng = elems.size();
+    std::vector<std::int64_t> kept(ng * nk);
+    std::vector<double> coup(ng * std::size_t(ne) * nk), erhs(ng * std::size_t(ne));
+    for (std::size_t g = 0; g < ng; ++g) {
+      const std::size_t e = elems[g];
+      const ElementCondensation& c = sys.recovery[e];
+      for (int i = 0; i < nk; ++i) kept[g * nk + i] = sys.kept_global[e][i];
+      if (ne) {
+        std::copy(c.elim_coupling.data(), c.elim_coupling.data() + std::size_t(ne) * nk,
+                  coup.begin() + g * std::size_t(ne) * nk);
+        std::copy(c.elim_rhs.data(), c.elim_rhs.data() + ne, erhs.begin() + g * ne);
+      }
+    }
+    std::vector<double> locals(ng * std::size_t(n));
+    check(pscu_recover_batch(context(), int(ng), n, ne, elim.data(), kept.data(), coup.data(),
+                             erhs.data(), x.data(), locals.data(), PSCU_HOST));
+    for (std::size_t g = 0; g < ng; ++g)
+      out[elems[g]] = Eigen::Map<const Eigen::VectorXd>(locals.data() + g * n, n);
+  }
+  return out;
+}
+
+/// solve_system (plevels.hpp:217-239) with the hierarchy, FGMRES and the
+/// recovery of the eliminated unknowns on the device.
 inline StokesSolution solve_system(const Mesh&, const StokesSystem& sys, const LevelConfig& cfg) {
   const pscu_layout lay = to_pscu(sys.layout);
   const pscu_level_cfg lc = to_pscu(cfg);
@@ -154,7 +197,7 @@ inline StokesSolution solve_system(const Mesh&, const StokesSystem& sys, const L
   sol.report.converged = rep.converged != 0;
   sol.report.t_assembly = sys.t_assembly;
   sol.report.t_solve = rep.t_solve;
-  sol.local = sys.recover_solution(sol.x);
+  sol.local = recover_solution(sys, sol.x);
   return sol;
 }
 

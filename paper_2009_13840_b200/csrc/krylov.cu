@@ -566,6 +566,18 @@ __global__ void __launch_bounds__(kStepThreads, 1)
 /// Cooperative single-launch Arnoldi step; returns false when the problem
 /// does not fit the co-resident configuration (caller falls back to one
 /// kernel per pass).
+/// Tagged reduction slots of a G-CTA Arnoldi step: the pair layout uses
+/// 2G + 2 16-byte slots (4G + 4 words, root CTA publication included), the
+/// release/acquire layout 2G + 2 words; sized for the larger, never below
+/// the historical 2048 words.
+static void ensure_slot_tags(Context& c, int64_t G) {
+  const size_t need = std::max<size_t>(2048, size_t(4 * G + 4));
+  if (c.slot_tag.n < need) {
+    c.slot_tag.alloc(need);
+    PSCU_CUDA(cudaMemsetAsync(c.slot_tag.p, 0, sizeof(unsigned long long) * need, c.stream));
+  }
+}
+
 bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int64_t ldv,
                         double* hcol) {
   const int64_t T = repro_lanes(n);
@@ -605,10 +617,7 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_tma_kernel,
                                                             kStepThreads, smem));
     if (int64_t(per_sm) * sm_count >= G) {
-      if (c.slot_tag.n < size_t(2 * G)) {
-        c.slot_tag.alloc(2048);
-        PSCU_CUDA(cudaMemsetAsync(c.slot_tag.p, 0, sizeof(unsigned long long) * 2048, c.stream));
-      }
+      ensure_slot_tags(c, G);
       int ei = epl, jj = j;
       int64_t nn = n, TT = T, ld = ldv;
       double* pw = w;
@@ -645,10 +654,7 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
                                : (void*)arnoldi_step_kernel<1, false>);
     PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kStepThreads, smem));
     if (int64_t(per_sm) * sm_count < G) continue;
-    if (c.slot_tag.n < size_t(2 * G)) {
-      c.slot_tag.alloc(2048);
-      PSCU_CUDA(cudaMemsetAsync(c.slot_tag.p, 0, sizeof(unsigned long long) * 2048, c.stream));
-    }
+    ensure_slot_tags(c, G);
     int ei = epl, jj = j;
     int64_t nn = n, TT = T, ld = ldv;
     double* pw = w;

@@ -1656,9 +1656,26 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   w.C = h.C;
   w.levels = h.levels;
   w.persist_grid = 0;
+  // the warp kernel (level_chunk) buffers at most kLevelMaxRows rows and
+  // kLevelMaxNz entries per task: a wide chunk with a larger task (a single
+  // row longer than the entry cap, or a push-walker chunk of long chains)
+  // runs on the thread-per-task wide_kernel instead, and such a plan is
+  // never swept by the persistent kernel
+  std::vector<char> warp_fits(h.sl_k.size(), 0);
+  bool all_fit = true;
+  for (size_t s = 0; s < h.sl_k.size(); ++s) {
+    if (!h.sl_wide[s]) continue;
+    bool ok = true;
+    for (int i = 0; i < h.sl_nt[s] && ok; ++i) {
+      const int32_t t0 = h.sl_t[s] + i;
+      ok = h.tt[t0 + 1] - h.tt[t0] <= kLevelMaxRows && h.tq[t0 + 1] - h.tq[t0] <= kLevelMaxNz;
+    }
+    warp_fits[s] = ok;
+    all_fit = all_fit && ok;
+  }
   // (k=1 at 256^2, 1.2 M rows: per-level launches measured faster, 4.8 vs 5.2 ms)
   const char* pm = getenv("PSCU_LEVEL_PERSIST_MIN_ROWS");
-  if (h.levels && level_persist() && h.npos >= (pm ? atoll(pm) : 1500000)) {
+  if (h.levels && all_fit && level_persist() && h.npos >= (pm ? atoll(pm) : 1500000)) {
     int per_sm = 0, sms = 0, dev = 0;
     PSCU_CUDA(cudaGetDevice(&dev));
     PSCU_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1680,7 +1697,7 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   for (int s = 0; s < w.nsub; ++s) {
     if (h.sl_wide[s]) {
       // one warp per task when the tasks are long chains
-      const bool warp = h.sl_nt[s] > 0 && h.sl_nq[s] >= 24 * int64_t(h.sl_nt[s]);
+      const bool warp = h.sl_nt[s] > 0 && h.sl_nq[s] >= 24 * int64_t(h.sl_nt[s]) && warp_fits[s];
       w.segments.push_back({true, s, s + 1, warp, h.sl_nt[s]});
     } else if (s == 0 || h.sl_wide[s - 1]) {
       w.segments.push_back({false, s, s + 1});

@@ -393,3 +393,27 @@ def condense_elements(mats, rhs, elim, ctx: Context | None = None):
     return dict(schur=np.transpose(schur, (0, 2, 1)), reduced_rhs=rr,
                 elim_coupling=np.transpose(coup[:, : ne * nk].reshape(nelem, nk, ne), (0, 2, 1)),
                 elim_rhs=er[:, :ne])
+
+
+def recover_elements(elim, kept_global, elim_coupling, elim_rhs, x, ctx: Context | None = None):
+    """ElementCondensation::recover (condense.hpp:28-38) for a batch of
+    elements sharing one local size and elimination list, i.e.
+    StokesSystem::recover_solution (assemble.hpp:58-66) on the device.
+    kept_global: (nelem, nk) retained global ids; elim_coupling: (nelem, ne,
+    nk); elim_rhs: (nelem, ne); x: the global solution. Returns the full local
+    vectors (nelem, n) in local dof order."""
+    ctx = ctx or default_context()
+    el = np.ascontiguousarray(elim, np.int32)
+    kept = np.ascontiguousarray(kept_global, np.int64)
+    nelem, nk = kept.shape
+    ne = len(el)
+    n = nk + ne
+    coup = np.ascontiguousarray(np.transpose(np.asarray(elim_coupling, np.float64).reshape(
+        nelem, ne, nk), (0, 2, 1)))  # column-major blocks
+    er = _f64(np.asarray(elim_rhs, np.float64).reshape(nelem, ne))
+    xx = _f64(x)
+    locals_ = np.zeros((nelem, n))
+    N.check(ctx.lib.pscu_recover_batch(ctx.h, nelem, n, ne, el.ctypes.data, kept.ctypes.data,
+                                       coup.ctypes.data, er.ctypes.data, xx.ctypes.data,
+                                       locals_.ctypes.data, N.PSCU_HOST))
+    return locals_

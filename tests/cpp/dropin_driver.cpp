@@ -6,8 +6,11 @@
 //     Ilu0 ones (both sides, left and right preconditioning).
 // Built by oracle/Makefile (target dropin) against the unmodified reference
 // headers and the Eigen subset; links libpstokes_b200.so.
+#include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <string>
+#include <tuple>
 
 #include "pstokes/plevels.hpp"
 #include "pstokes/study.hpp"
@@ -41,8 +44,24 @@ int main() {
   expect(ref.report.outer_its == dev.report.outer_its, "solve_system: FGMRES iterations equal");
   expect(ref.report.coarse_its == dev.report.coarse_its, "solve_system: coarse iterations equal");
   expect(same(ref.x, dev.x), "solve_system: solution bitwise");
-  expect(ref.local.size() == dev.local.size() && same(ref.local[0], dev.local[0]),
-         "solve_system: recovered local vectors");
+  bool all_local = ref.local.size() == dev.local.size();
+  for (std::size_t e = 0; all_local && e < ref.local.size(); ++e)
+    all_local = same(ref.local[e], dev.local[e]);
+  expect(all_local, "solve_system: device-recovered local vectors bitwise (every element)");
+  // device recovery on its own, for the other condensation variants
+  for (const auto& [scheme, strategy, k] :
+       {std::tuple{Scheme::HhoDp, Strategy::VpCond, 2}, std::tuple{Scheme::HhoHp, Strategy::VpCond, 2},
+        std::tuple{Scheme::HhoDp, Strategy::Uncond, 1}}) {
+    const StokesSystem s2 = assemble_stokes(mesh, scheme, strategy, k, ManufacturedCase::data());
+    Eigen::VectorXd xs(s2.a.n);
+    for (Eigen::Index i = 0; i < xs.size(); ++i) xs[i] = std::sin(0.37 * double(i) + 0.1);
+    const auto r1 = s2.recover_solution(xs);
+    const auto r2 = b200::recover_solution(s2, xs);
+    bool ok = r1.size() == r2.size();
+    for (std::size_t e = 0; ok && e < r1.size(); ++e) ok = same(r1[e], r2[e]);
+    expect(ok, (std::string("recover_solution bitwise: ") + to_string(scheme) + " " +
+                to_string(strategy)).c_str());
+  }
 
   // 2. reference fgmres with the device V-cycle as the variable preconditioner
   b200::DeviceCsr a(sys.a);

@@ -285,6 +285,47 @@ def test_condensation_bitwise(S, scheme, strategy, k):
         assert same(out["elim_rhs"][e], refs[e]["elim_rhs"])
 
 
+def _recover_ref(coup, erhs, kept_vals):
+    """ElementCondensation::recover (condense.hpp:28-38) as the reference
+    computes it: xe = elim_rhs - elim_coupling * kept, the product summed k
+    ascending from 0.0 (include/eigen_subset GEMM), one rounding per op."""
+    ne, nk = coup.shape
+    out = np.zeros(ne)
+    for i in range(ne):
+        acc = 0.0
+        for k in range(nk):
+            acc = acc + float(coup[i, k]) * float(kept_vals[k])
+        out[i] = float(erhs[i]) - acc
+    return out
+
+
+@pytest.mark.parametrize("family,scheme,strategy,k", [("trapz", "hho-dp", "v-cond", 3),
+                                                      ("trapz", "hho-dp", "vp-cond", 2),
+                                                      ("tri", "hho-hp", "vp-cond", 2),
+                                                      ("trapz", "hho-hp", "vp-cond", 1)])
+def test_recovery_bitwise(S, family, scheme, strategy, k):
+    """pscu_recover_batch (recover_kernel) against the reference's recovery
+    data and back-substitution, every element, a random global vector."""
+    s = O.RefSystem(family=family, n=3, scheme=scheme, strategy=strategy, k=k)
+    ne_el = s.layout.n_elements
+    refs = [s.condensation(e) for e in range(ne_el)]
+    _, _, elim = s.local_blocks(0, data="exp")
+    x = np.random.default_rng(7).standard_normal(s.n)
+    kept = np.stack([r["kept_global"] for r in refs])
+    coup = np.stack([r["elim_coupling"] for r in refs])
+    erhs = np.stack([r["elim_rhs"] for r in refs])
+    got = S.recover_elements(elim, kept, coup, erhs, x)
+    n = kept.shape[1] + len(elim)
+    is_elim = np.zeros(n, bool)
+    is_elim[elim] = True
+    keep = np.nonzero(~is_elim)[0]
+    for e in range(ne_el):
+        want = np.zeros(n)
+        want[keep] = x[kept[e]]
+        want[elim] = _recover_ref(coup[e], erhs[e], x[kept[e]])
+        assert same(got[e], want), e
+
+
 def test_condensation_singular_block_raises(S):
     n = 4
     mats = np.stack([np.eye(n), np.eye(n)])
@@ -433,9 +474,13 @@ def test_ilu0_factor_variants_bitwise(S, monkeypatch, thread_rows, ci):
     assert same(ilu.factors(), ri.factors())
 
 
-def test_ilu0_persistent_levels_bitwise(S, monkeypatch):
+@pytest.mark.parametrize("pad", ["0", "1"])
+@pytest.mark.parametrize("persist", ["0", "1"])
+def test_ilu0_persistent_levels_bitwise(S, monkeypatch, pad, persist):
     """Task-level plans swept by one cooperative launch per sweep (grid
-    barrier between task levels, PSCU_LEVEL_PERSIST) in a fresh process."""
+    barrier between task levels, PSCU_LEVEL_PERSIST) or per-level launches,
+    with and without the 8-entry row padding (PSCU_LEVEL_PAD, cached per
+    process: a fresh process per variant); byte-level comparison."""
     import subprocess, sys, os
     code = r'''
 import sys, numpy as np
@@ -448,12 +493,51 @@ for c in [dict(mesh="unit-tri", n=12, jitter=0.2, seed=0, side="top", scheme="hh
     ilu = S.Ilu0(S.CsrMatrix(a.row_ptr, a.cols, a.vals))
     for seed in range(2):
         x = np.random.default_rng(seed).standard_normal(a.n)
-        assert np.all(ilu.apply(x) == ri.apply(x))
+        assert ilu.apply(x).tobytes() == ri.apply(x).tobytes()
 print("persistent ok")
 '''
-    env = dict(os.environ, PSCU_LEVEL_PERSIST="1", PSCU_WALK_MODE="levels",
-               PSCU_LEVEL_PERSIST_MIN_ROWS="0")
+    env = dict(os.environ, PSCU_LEVEL_PERSIST=persist, PSCU_WALK_MODE="levels",
+               PSCU_LEVEL_PERSIST_MIN_ROWS="0", PSCU_LEVEL_PAD=pad)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "persistent ok" in r.stdout, r.stdout + r.stderr
+
+
+def _long_row_csr(n=3000, long_rows=(2999, 2500), width=1200, seed=11):
+    """Diagonally dominant CSR with a few rows far longer than a task-level
+    plan's per-task buffers (512 entries): chains are cut there and the
+    oversize tasks run on the thread-per-task kernel."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for i in range(n):
+        cols = set(rng.choice(n, size=6, replace=False).tolist()) | {i, max(i - 1, 0)}
+        if i in long_rows:
+            cols |= set(range(max(0, i - width), i))
+        rows.append(sorted(cols))
+    rp = np.zeros(n + 1, np.int64)
+    for i, c in enumerate(rows):
+        rp[i + 1] = rp[i] + len(c)
+    cols = np.concatenate([np.asarray(c, np.int32) for c in rows])
+    vals = rng.uniform(-1.0, 1.0, len(cols)) * 1e-3
+    for i in range(n):
+        d = rp[i] + rows[i].index(i)
+        vals[d] = 4.0 + i % 7
+    return O.Csr(rp, cols, vals)
+
+
+@pytest.mark.parametrize("mode", ["default", "levels"])
+def test_ilu0_oversize_tasks_bitwise(S, monkeypatch, mode):
+    """Rows longer than the warp kernel's task buffers (walk.cu level_chunk:
+    kLevelMaxNz entries) fall back to the thread-per-task kernel and keep
+    the (default-on) persistent sweep off (advisor finding, round 1)."""
+    if mode != "default":
+        monkeypatch.setenv("PSCU_WALK_MODE", mode)
+    monkeypatch.setenv("PSCU_LEVEL_PERSIST_MIN_ROWS", "0")
+    a = _long_row_csr()
+    ri = O.RefIlu(O.RefCsr(a))
+    ilu = S.Ilu0(S.CsrMatrix(a.row_ptr, a.cols, a.vals))
+    assert ilu.factors().tobytes() == ri.factors().tobytes()
+    for seed in range(2):
+        x = np.random.default_rng(seed).standard_normal(a.n)
+        assert ilu.apply(x).tobytes() == ri.apply(x).tobytes()
