@@ -62,6 +62,44 @@ const int64_t* psh_row_ptr(const psh_system* s);    /* dim + 1 */
 const int32_t* psh_cols(const psh_system* s);       /* nnz */
 double psh_build_seconds(const psh_system* s);
 
+/* ---- 3D (BASELINE.json configs 3 and 5; not in the reference, which is
+ * 2D only: mesh.hpp:21). The 3D generalisation of the
+ * reference's discretisation, documented in host/pstokes_host3d.cpp. ---- */
+typedef struct psh_mesh3 psh_mesh3;
+enum { PSH3_DATA_ZERO = 0, PSH3_DATA_RANDOM = 3, PSH3_DATA_MANUFACTURED = 4 };
+
+const char* psh3_last_error(void);
+/* Unit cube, n^3 hexahedra, interior vertices jittered by
+ * frac*(1/n)*SplitMix64(seed).sym() (x, y, z; l outer, j, i inner); faces
+ * numbered first-seen over the element loop (local faces x-, x+, y-, y+,
+ * z-, z+); Neumann on z = 1 when neumann_top, Dirichlet elsewhere. */
+int psh_mesh_unit_cube(int n, double frac, uint64_t seed, int neumann_top, psh_mesh3** out);
+void psh_mesh3_destroy(psh_mesh3* m);
+/* out[0..2] = vertices, elements, faces */
+void psh_mesh3_counts(const psh_mesh3* m, int64_t* out);
+/* 7 ints per face: 4 vertices (oriented out of left), left, right, tag */
+void psh_mesh3_faces(const psh_mesh3* m, int32_t* faces);
+/* 6 face ids per element (local order x-, x+, y-, y+, z-, z+) */
+void psh_mesh3_element_faces(const psh_mesh3* m, int32_t* ef);
+void psh_mesh3_vertices(const psh_mesh3* m, double* xyz);
+/* HHO-hp vp-cond at face degree k: info[0..7] = n_local, n_elim, n_keep,
+ * face_vel, face_press, face_block, faces per element (6), element velocity
+ * modes per component. */
+int psh3_hp_info(int k, int32_t* info);
+int psh3_hp_elim(int k, int32_t* elim);         /* n_elim local ids (condense.hpp:44-55 order) */
+int psh3_hp_keep_pos(int k, int32_t* pos);      /* n_keep x (local face, offset in face block) */
+/* Local blocks of elements [e0, e1) (column-major n x n) and loads;
+ * data: PSH3_DATA_*, seed for the random body force; eta <= 0: 3(k+1)^2. */
+int psh3_local_blocks(const psh_mesh3* m, int k, int data, uint64_t seed, double eta, int e0,
+                      int e1, int nthreads, double* mats, double* rhs);
+/* Face-block pattern of the condensed operator (block row f: faces of the
+ * elements holding f, ascending). Returns the block count; arrays nullable. */
+int64_t psh3_block_pattern(const psh_mesh3* m, int64_t* brow_ptr, int32_t* bcols);
+/* Face L2 projections of the manufactured solution (n_faces x 4 nf). */
+int psh3_face_projection(const psh_mesh3* m, int k, double* out);
+/* nelem volumes, then nelem closure norms |sum_F int_F n dA|. */
+int psh3_geometry(const psh_mesh3* m, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1166,6 +1166,22 @@ void plan_sweep(const Csr& a, const std::vector<int64_t>& diag, bool fwd, int C,
     for (int t = 0; t < ntask; ++t) order[fill[T.lvl[t]]++] = t;
   }
   h = HostPlan{};
+  // a walker chunk stages at most kMaxDiag entries per task: a narrow level
+  // holding a longer task (a row longer than that) cannot be walked — the
+  // push walker reports it infeasible (the caller falls back to task-level
+  // launches), the explicit walker modes refuse the pattern
+  if (!all_wide && !flow)
+    for (int l = 0; l < nlev; ++l) {
+      if (lvl_ptr[l + 1] - lvl_ptr[l] > kWideRows) continue;
+      for (int j = lvl_ptr[l]; j < lvl_ptr[l + 1]; ++j)
+        if (T.nz[order[j]] > kMaxDiag) {
+          if (S) {
+            h.push_ok = false;
+            return;
+          }
+          throw Error(PSCU_EINVAL, "walk plan: row exceeds the walker's diagonal capacity");
+        }
+    }
   h.C = C;
   h.levels = all_wide;
   h.flow = flow;
@@ -1788,8 +1804,14 @@ std::shared_ptr<WalkBuild> plan_walk(const Csr& a, const std::vector<int64_t>& d
       err = std::current_exception();
     }
   });
-  wb->f = plan(a, diag, true);
-  tb.join();
+  std::exception_ptr err_f;
+  try {
+    wb->f = plan(a, diag, true);
+  } catch (...) {
+    err_f = std::current_exception();
+  }
+  tb.join();  // never unwind past a joinable thread (std::terminate)
+  if (err_f) std::rethrow_exception(err_f);
   if (err) std::rethrow_exception(err);
   return wb;
 }

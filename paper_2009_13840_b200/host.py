@@ -167,3 +167,129 @@ def assemble_stokes(local: LocalSystem, ctx=None):
     m = S.CsrMatrix(None, None, None, ctx=ctx, _handle=h.value)
     m._owned = True
     return m, rhs
+
+
+# ---------------------------------------------------------------------------
+# 3D (BASELINE.json configs 3 and 5): hexahedral unit cube, HHO-hp vp-cond
+# ---------------------------------------------------------------------------
+
+DATA3 = {"zero": 0, "random": 3, "manufactured": 4}
+
+
+def load3():
+    lib = load()
+    if not getattr(lib, "_psh3", False):
+        vp = C.c_void_p
+        lib.psh3_last_error.restype = C.c_char_p
+        lib.psh_mesh_unit_cube.argtypes = [C.c_int, C.c_double, C.c_uint64, C.c_int, C.POINTER(vp)]
+        lib.psh_mesh3_destroy.argtypes = [vp]
+        for f in ("psh_mesh3_counts", "psh_mesh3_faces", "psh_mesh3_element_faces",
+                  "psh_mesh3_vertices"):
+            getattr(lib, f).argtypes = [vp, vp]
+        lib.psh3_hp_info.argtypes = [C.c_int, vp]
+        lib.psh3_hp_elim.argtypes = [C.c_int, vp]
+        lib.psh3_hp_keep_pos.argtypes = [C.c_int, vp]
+        lib.psh3_local_blocks.argtypes = [vp, C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_int,
+                                          C.c_int, C.c_int, vp, vp]
+        lib.psh3_block_pattern.restype = C.c_int64
+        lib.psh3_block_pattern.argtypes = [vp, vp, vp]
+        lib.psh3_face_projection.argtypes = [vp, C.c_int, vp]
+        lib.psh3_geometry.argtypes = [vp, vp]
+        lib._psh3 = True
+    return lib
+
+
+def _check3(rc):
+    if rc:
+        msg = load3().psh3_last_error().decode()
+        raise ValueError(msg) if rc == 1 else RuntimeError(msg)
+
+
+class Mesh3:
+    """Hexahedral unit-cube mesh (3D generalisation of mesh.hpp; see
+    host/pstokes_host3d.cpp for the recipe and the non-planar-face choice)."""
+
+    def __init__(self, n: int, jitter: float = 0.0, seed: int = 0, neumann_top: bool = True):
+        self.lib = load3()
+        h = C.c_void_p()
+        _check3(self.lib.psh_mesh_unit_cube(n, jitter, seed, int(neumann_top), C.byref(h)))
+        self.h = h
+        self.n = n
+        c = np.zeros(3, np.int64)
+        self.lib.psh_mesh3_counts(h, c.ctypes.data)
+        self.n_vertices, self.n_elements, self.n_faces = (int(v) for v in c)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.psh_mesh3_destroy(self.h)
+            self.h = None
+
+    def faces(self) -> np.ndarray:
+        f = np.zeros(7 * self.n_faces, np.int32)
+        self.lib.psh_mesh3_faces(self.h, f.ctypes.data)
+        return f.reshape(-1, 7)
+
+    def element_faces(self) -> np.ndarray:
+        f = np.zeros(6 * self.n_elements, np.int32)
+        self.lib.psh_mesh3_element_faces(self.h, f.ctypes.data)
+        return f.reshape(-1, 6)
+
+    def vertices(self) -> np.ndarray:
+        v = np.zeros(3 * self.n_vertices)
+        self.lib.psh_mesh3_vertices(self.h, v.ctypes.data)
+        return v.reshape(-1, 3)
+
+    def geometry(self):
+        out = np.zeros(2 * self.n_elements)
+        _check3(self.lib.psh3_geometry(self.h, out.ctypes.data))
+        return out[: self.n_elements], out[self.n_elements:]
+
+    def block_pattern(self):
+        lib = self.lib
+        nb = lib.psh3_block_pattern(self.h, None, None)
+        rp = np.zeros(self.n_faces + 1, np.int64)
+        cols = np.zeros(nb, np.int32)
+        lib.psh3_block_pattern(self.h, rp.ctypes.data, cols.ctypes.data)
+        return rp, cols
+
+    def face_projection(self, k: int) -> np.ndarray:
+        nf = (k + 1) * (k + 2) // 2
+        out = np.zeros(self.n_faces * 4 * nf)
+        _check3(self.lib.psh3_face_projection(self.h, k, out.ctypes.data))
+        return out
+
+
+class HpLocal3:
+    """HHO-hp vp-cond local structure at face degree k (3D): sizes, the
+    eliminated local dofs and the face-block position of every retained dof."""
+
+    def __init__(self, k: int):
+        lib = load3()
+        self.k = k
+        info = np.zeros(8, np.int32)
+        _check3(lib.psh3_hp_info(k, info.ctypes.data))
+        (self.n_local, self.n_elim, self.n_keep, self.face_vel, self.face_press, self.face_block,
+         self.nfaces, self.ne) = (int(v) for v in info)
+        self.elim = np.zeros(self.n_elim, np.int32)
+        _check3(lib.psh3_hp_elim(k, self.elim.ctypes.data))
+        pos = np.zeros(2 * self.n_keep, np.int32)
+        _check3(lib.psh3_hp_keep_pos(k, pos.ctypes.data))
+        self.keep_pos = pos.reshape(-1, 2)
+
+    def kept_global(self, element_faces: np.ndarray) -> np.ndarray:
+        """Retained global ids per element (nelem x n_keep)."""
+        ef = np.asarray(element_faces, np.int64)
+        return ef[:, self.keep_pos[:, 0]] * self.face_block + self.keep_pos[:, 1][None, :]
+
+    def local_blocks(self, mesh: Mesh3, e0: int, e1: int, data: str = "random", seed: int = 0,
+                     eta: float = 0.0, nthreads: int = 0, out=None):
+        n = self.n_local
+        m = e1 - e0
+        if out is None:
+            mats = np.zeros(m * n * n)
+            rhs = np.zeros(m * n)
+        else:
+            mats, rhs = out
+        _check3(load3().psh3_local_blocks(mesh.h, self.k, DATA3[data], seed, eta, e0, e1, nthreads,
+                                          N.ptr(mats), N.ptr(rhs)))
+        return mats, rhs

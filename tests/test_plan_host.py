@@ -60,3 +60,21 @@ def test_plans_emulate_bitwise(checker, tmp_path, ci):
                            timeout=300)
         assert r.returncode == 0, (m, r.stdout, r.stderr)
         assert r.stdout.count("mismatches 0") == 2, (m, r.stdout)
+
+
+def test_plans_long_rows_fall_back(checker, tmp_path):
+    """Rows longer than a walker chunk's diagonal capacity: the push plan is
+    reported infeasible and the sweep falls back to task-level launches
+    (no exception escapes the planner threads); emulation still bitwise."""
+    import synthetic
+    a = synthetic.long_row_csr()
+    rp, cl = tmp_path / "rp.bin", tmp_path / "c.bin"
+    a.row_ptr.astype(np.int64).tofile(rp)
+    a.cols.astype(np.int32).tofile(cl)
+    for m in MODES[:4]:
+        env = {k: v for k, v in os.environ.items() if not k.startswith("PSCU_")}
+        env.update(m)
+        r = subprocess.run([checker, str(rp), str(cl)], capture_output=True, text=True, env=env,
+                           timeout=300)
+        assert r.returncode == 0, (m, r.stdout, r.stderr)
+        assert r.stdout.count("mismatches 0") == 2, (m, r.stdout)
