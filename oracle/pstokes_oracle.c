@@ -36,6 +36,7 @@ int po_make_layout(int scheme, int strategy, int k, int n_faces, int n_elements,
   l->k = k;
   l->n_faces = n_faces;
   l->n_elements = n_elements;
+  l->dim = 2;
   const int nf = dim_p1(k), np = dim_p2(k);
   const int ne = dim_p2(scheme == 1 ? k + 1 : k);
   switch (scheme) {
@@ -62,8 +63,32 @@ int po_make_layout(int scheme, int strategy, int k, int n_faces, int n_elements,
   return 0;
 }
 
-static int64_t face_block(const po_layout* l) { return 2 * l->face_vel + l->face_press; }
-static int64_t elem_block(const po_layout* l) { return 2 * l->elem_vel + l->elem_press; }
+static int ncomp(const po_layout* l) { return l->dim == 3 ? 3 : 2; }
+static int64_t face_block(const po_layout* l) { return ncomp(l) * l->face_vel + l->face_press; }
+static int64_t elem_block(const po_layout* l) { return ncomp(l) * l->elem_vel + l->elem_press; }
+
+/* 3D: hho-hp vp-cond only (the configs that need it); P^k on a face has
+ * (k+1)(k+2)/2 modes */
+int po_make_layout3(int scheme, int strategy, int k, int n_faces, int n_elements, po_layout* l) {
+  if (k < 0) return set_err("layout: k must be >= 0");
+  if (scheme != 1 || strategy != 2) return set_err("3D layout: hho-hp vp-cond only");
+  memset(l, 0, sizeof *l);
+  l->scheme = scheme;
+  l->strategy = strategy;
+  l->k = k;
+  l->n_faces = n_faces;
+  l->n_elements = n_elements;
+  l->face_vel = dim_p2(k);
+  l->face_press = dim_p2(k);
+  l->dim = 3;
+  return 0;
+}
+
+/* the layout of the same scheme at another degree */
+static int layout_at(const po_layout* lf, int k, po_layout* out) {
+  if (lf->dim == 3) return po_make_layout3(lf->scheme, lf->strategy, k, lf->n_faces, lf->n_elements, out);
+  return po_make_layout(lf->scheme, lf->strategy, k, lf->n_faces, lf->n_elements, out);
+}
 
 int64_t po_layout_dim(const po_layout* l) {
   return (int64_t)l->n_faces * face_block(l) + (int64_t)l->n_elements * elem_block(l);
@@ -78,18 +103,20 @@ int po_coarse_to_fine_map(const po_layout* f, const po_layout* c, int64_t* map) 
     return set_err("transfer: coarse layout is not nested in the fine one");
   for (int64_t fc = 0; fc < c->n_faces; ++fc) {
     const int64_t cb = fc * face_block(c), fb = fc * face_block(f);
-    for (int comp = 0; comp < 2; ++comp)
+    for (int comp = 0; comp < ncomp(c); ++comp)
       for (int m = 0; m < c->face_vel; ++m)
         map[cb + comp * c->face_vel + m] = fb + comp * f->face_vel + m;
-    for (int m = 0; m < c->face_press; ++m) map[cb + 2 * c->face_vel + m] = fb + 2 * f->face_vel + m;
+    for (int m = 0; m < c->face_press; ++m)
+      map[cb + ncomp(c) * c->face_vel + m] = fb + ncomp(f) * f->face_vel + m;
   }
   const int64_t cfo = (int64_t)c->n_faces * face_block(c), ffo = (int64_t)f->n_faces * face_block(f);
   for (int64_t e = 0; e < c->n_elements; ++e) {
     const int64_t cb = cfo + e * elem_block(c), fb = ffo + e * elem_block(f);
-    for (int comp = 0; comp < 2; ++comp)
+    for (int comp = 0; comp < ncomp(c); ++comp)
       for (int m = 0; m < c->elem_vel; ++m)
         map[cb + comp * c->elem_vel + m] = fb + comp * f->elem_vel + m;
-    for (int m = 0; m < c->elem_press; ++m) map[cb + 2 * c->elem_vel + m] = fb + 2 * f->elem_vel + m;
+    for (int m = 0; m < c->elem_press; ++m)
+      map[cb + ncomp(c) * c->elem_vel + m] = fb + ncomp(f) * f->elem_vel + m;
   }
   return 0;
 }
@@ -573,7 +600,7 @@ po_hier* po_hier_create_ex(const po_csr* fine, const po_layout* lf, const int* d
     po_level* L = &h->lev[l];
     if (l > 0) {
       po_level* P = &h->lev[l - 1];
-      po_make_layout(lf->scheme, lf->strategy, degrees[l], lf->n_faces, lf->n_elements, &L->layout);
+      layout_at(lf, degrees[l], &L->layout);
       L->n = po_layout_dim(&L->layout);
       P->down_map = (int64_t*)malloc(sizeof(int64_t) * (size_t)(L->n + 1));
       P->n_coarse = L->n;
@@ -719,8 +746,8 @@ int po_solve(po_hier* h, const double* rhs, double outer_rtol, int outer_maxit, 
  * rounded and ordered exactly like the device kernels (bjacobi.cu).
  * ------------------------------------------------------------------------- */
 static void bj_shape(const po_layout* l, int* fb, int* eb, int64_t* eoff) {
-  *fb = 2 * l->face_vel + l->face_press;
-  *eb = 2 * l->elem_vel + l->elem_press;
+  *fb = (int)face_block(l);
+  *eb = (int)elem_block(l);
   *eoff = (int64_t)l->n_faces * *fb;
 }
 
@@ -985,4 +1012,77 @@ int po_condense(int n, const double* mat, const double* rhs, int ne, const int* 
   free(perm);
   free(sol);
   return 0;
+}
+
+/* dof_kind / structurally_coupled (assemble.hpp:25-46) with the layout's
+ * component count: kinds 0..ncomp-1 velocity components, ncomp pressure */
+static int dof_kind(const po_layout* l, int64_t g) {
+  const int nc = ncomp(l);
+  const int64_t fsz = (int64_t)l->n_faces * face_block(l);
+  int within, nvel;
+  if (g < fsz) {
+    within = (int)(g % face_block(l));
+    nvel = l->face_vel;
+  } else {
+    within = (int)((g - fsz) % elem_block(l));
+    nvel = l->elem_vel;
+  }
+  return nvel > 0 && within < nc * nvel ? within / nvel : nc;
+}
+
+static int coupled(const po_layout* l, int ka, int kb) {
+  const int nc = ncomp(l);
+  const int av = ka != nc, bv = kb != nc;
+  if (av && bv && ka != kb) return l->strategy == 2;
+  if (!av && !bv) return l->strategy != 0;
+  return 1;
+}
+
+int po_condense_assemble(int nelem, int n, const double* mats, const double* rhs, int ne,
+                         const int* elim, const int64_t* kept, const po_layout* layout,
+                         const po_csr* pat, double* vals, double* rhs_out) {
+  const int nk = n - ne;
+  double* schur = (double*)malloc(sizeof(double) * (size_t)nk * nk);
+  double* rr = (double*)malloc(sizeof(double) * (size_t)nk);
+  double* coup = (double*)malloc(sizeof(double) * (size_t)(ne > 0 ? ne : 1) * nk);
+  double* er = (double*)malloc(sizeof(double) * (size_t)(ne > 0 ? ne : 1));
+  int* kinds = (int*)malloc(sizeof(int) * (size_t)nk);
+  int rc = 0;
+  memset(vals, 0, sizeof(double) * (size_t)pat->row_ptr[pat->n]);
+  memset(rhs_out, 0, sizeof(double) * (size_t)pat->n);
+  for (int e = 0; e < nelem && !rc; ++e) {
+    if (po_condense(n, mats + (size_t)e * n * n, rhs + (size_t)e * n, ne, elim, schur, rr, coup,
+                    er)) {
+      snprintf(g_err, sizeof g_err, "condense: near-singular eliminated block on element %d", e);
+      rc = -1;
+      break;
+    }
+    const int64_t* g = kept + (size_t)e * nk;
+    for (int i = 0; i < nk; ++i) kinds[i] = dof_kind(layout, g[i]);
+    for (int i = 0; i < nk && !rc; ++i)
+      for (int j = 0; j < nk; ++j) {
+        if (g[i] != g[j] && !coupled(layout, kinds[i], kinds[j])) continue;
+        const double v = schur[i + (size_t)j * nk];
+        if (!(v != 0.0 || g[i] == g[j])) continue;
+        /* CsrMatrix::add: binary search in the sorted row (csr.hpp:47-61) */
+        int64_t lo = pat->row_ptr[g[i]], hi = pat->row_ptr[g[i] + 1];
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) / 2;
+          if (pat->cols[mid] < g[j]) lo = mid + 1;
+          else hi = mid;
+        }
+        if (lo == pat->row_ptr[g[i] + 1] || pat->cols[lo] != g[j]) {
+          rc = set_err("CsrMatrix::add: entry outside the sparsity pattern");
+          break;
+        }
+        vals[lo] += v;
+      }
+    for (int i = 0; i < nk; ++i) rhs_out[g[i]] += rr[i];
+  }
+  free(schur);
+  free(rr);
+  free(coup);
+  free(er);
+  free(kinds);
+  return rc;
 }

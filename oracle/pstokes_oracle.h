@@ -30,6 +30,7 @@ typedef struct {
   int k;
   int n_faces, n_elements;
   int face_vel, face_press, elem_vel, elem_press;
+  int dim;      /* space dimension: 2 (the reference; 0 reads as 2) or 3 */
 } po_layout;
 
 typedef void (*po_apply_fn)(void* ctx, const double* x, double* y);
@@ -37,6 +38,10 @@ typedef void (*po_apply_fn)(void* ctx, const double* x, double* y);
 const char* po_last_error(void);
 
 int po_make_layout(int scheme, int strategy, int k, int n_faces, int n_elements, po_layout* out);
+/* 3D generalisation (BASELINE.json configs 3/5; no reference): hho-hp
+ * vp-cond, face blocks [vx | vy | vz | p] of dim P^k(F) = (k+1)(k+2)/2
+ * modes each, no element unknowns. */
+int po_make_layout3(int scheme, int strategy, int k, int n_faces, int n_elements, po_layout* out);
 int64_t po_layout_dim(const po_layout* l);
 int po_coarse_to_fine_map(const po_layout* fine, const po_layout* coarse, int64_t* map);
 
@@ -85,6 +90,16 @@ long long po_hier_coarse_its(const po_hier* h);
 int po_solve(po_hier* h, const double* rhs, double outer_rtol, int outer_maxit, int restart,
              double* x, double* hist, int* its, long long* coarse_its, int* vcycles, double* rel,
              int* converged);
+
+/* assemble_hho's value pass (assemble.hpp:121-131,164-169) over all
+ * elements: condense_element per element (po_condense), then the Schur
+ * scatter into the structural CSR pattern in element order (exact zeros
+ * skipped except on the diagonal) and the reduced-load accumulation.
+ * kept: nelem x nk retained global ids in local keep order. Returns 0, or
+ * -1 with po_last_error (a singular block or an entry outside the pattern). */
+int po_condense_assemble(int nelem, int n, const double* mats, const double* rhs, int n_elim,
+                         const int* elim, const int64_t* kept, const po_layout* layout,
+                         const po_csr* pattern, double* vals, double* rhs_out);
 
 /* condense_element (condense.hpp:57-97) on one column-major n x n block. */
 int po_condense(int n, const double* mat, const double* rhs, int n_elim, const int* elim,

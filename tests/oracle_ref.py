@@ -430,7 +430,8 @@ class _PoCsr(C.Structure):
 
 class PoLayout(C.Structure):
     _fields_ = [(f, C.c_int) for f in ("scheme", "strategy", "k", "n_faces", "n_elements",
-                                       "face_vel", "face_press", "elem_vel", "elem_press")]
+                                       "face_vel", "face_press", "elem_vel", "elem_press",
+                                       "dim")]
 
 
 def port_lib():
@@ -440,6 +441,9 @@ def port_lib():
         vp = C.c_void_p
         lib.po_last_error.restype = C.c_char_p
         lib.po_make_layout.argtypes = [C.c_int] * 5 + [C.POINTER(PoLayout)]
+        lib.po_make_layout3.argtypes = [C.c_int] * 5 + [C.POINTER(PoLayout)]
+        lib.po_condense_assemble.argtypes = [C.c_int, C.c_int, vp, vp, C.c_int, vp, vp,
+                                             C.POINTER(PoLayout), C.POINTER(_PoCsr), vp, vp]
         lib.po_layout_dim.restype = C.c_int64
         lib.po_layout_dim.argtypes = [C.POINTER(PoLayout)]
         lib.po_coarse_to_fine_map.argtypes = [C.POINTER(PoLayout), C.POINTER(PoLayout), _i64p]
@@ -484,12 +488,51 @@ def po_csr(a: Csr) -> _PoCsr:
     return _PoCsr(a.n, a.row_ptr.ctypes.data, a.cols.ctypes.data, a.vals.ctypes.data)
 
 
-def po_layout(scheme, strategy, k, n_faces, n_elements) -> PoLayout:
+def po_layout(scheme, strategy, k, n_faces, n_elements, dim=2) -> PoLayout:
     lib = port_lib()
     lay = PoLayout()
-    if lib.po_make_layout(scheme, strategy, k, n_faces, n_elements, C.byref(lay)):
+    make = lib.po_make_layout3 if dim == 3 else lib.po_make_layout
+    if make(scheme, strategy, k, n_faces, n_elements, C.byref(lay)):
         raise ValueError(lib.po_last_error().decode())
     return lay
+
+
+def bsr_to_csr_pattern(brow_ptr, bcols, bs):
+    """CSR pattern of a dense-block face pattern: row f*bs + r holds the
+    columns g*bs + c of every block column g of block row f, ascending."""
+    nb = len(brow_ptr) - 1
+    cnt = np.diff(brow_ptr) * bs
+    rp = np.zeros(nb * bs + 1, np.int64)
+    rp[1:] = np.cumsum(np.repeat(cnt, bs))
+    cols = np.empty(int(rp[-1]), np.int32)
+    for f in range(nb):
+        blk = (np.asarray(bcols[brow_ptr[f]:brow_ptr[f + 1]], np.int64)[:, None] * bs
+               + np.arange(bs)[None, :]).ravel().astype(np.int32)
+        for r in range(bs):
+            i = f * bs + r
+            cols[rp[i]:rp[i + 1]] = blk
+    return rp, cols
+
+
+def port_condense_assemble(mats, rhs, n, elim, kept, layout: PoLayout, row_ptr, cols):
+    """po_condense_assemble: element condensation + element-order scatter
+    into the given structural pattern (assemble.hpp:136-172)."""
+    lib = port_lib()
+    nelem = len(rhs) // n
+    mats = np.ascontiguousarray(mats, np.float64)
+    rhs = np.ascontiguousarray(rhs, np.float64)
+    el = np.ascontiguousarray(elim, np.int32)
+    kept = np.ascontiguousarray(kept, np.int64)
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cl = np.ascontiguousarray(cols, np.int32)
+    vals = np.zeros(len(cl))
+    b = np.zeros(len(rp) - 1)
+    pat = _PoCsr(len(rp) - 1, rp.ctypes.data, cl.ctypes.data, vals.ctypes.data)
+    if lib.po_condense_assemble(nelem, n, mats.ctypes.data, rhs.ctypes.data, len(el),
+                                el.ctypes.data, kept.ctypes.data, C.byref(layout), C.byref(pat),
+                                vals.ctypes.data, b.ctypes.data):
+        raise RuntimeError(lib.po_last_error().decode())
+    return Csr(rp, cl, vals), b
 
 
 class PortBlockJacobi:
