@@ -45,11 +45,14 @@ typedef struct pscu_hier pscu_hier;
 typedef struct pscu_bj pscu_bj;
 
 /* DofLayout (dof_layout.hpp:56-85). scheme: 0 hho-dp, 1 hho-hp, 2 dg;
- * strategy: 0 uncond, 1 v-cond, 2 vp-cond. */
+ * strategy: 0 uncond, 1 v-cond, 2 vp-cond. dim: space dimension, 2 (the
+ * reference; 0 also reads as 2) or 3 (BASELINE.json configs 3/5: velocity
+ * blocks have three components, face modes dim P^k(F) = (k+1)(k+2)/2). */
 typedef struct {
   int scheme, strategy, k;
   int n_faces, n_elements;
   int face_vel, face_press, elem_vel, elem_press;
+  int dim;
 } pscu_layout;
 
 /* LevelConfig (plevels.hpp:23-42) minus the degrees, plus the smoother kind. */
@@ -99,6 +102,16 @@ int pscu_mat_destroy(pscu_mat* m);
 int pscu_mat_dims(const pscu_mat* m, int64_t* n, int64_t* nnz);
 int pscu_mat_download(pscu_ctx* ctx, const pscu_mat* m, int64_t* row_ptr, int32_t* cols,
                       double* vals);
+/* Dense face-block storage of the same CsrMatrix (operators whose structural
+ * pattern is made of dense bs x bs blocks: 3D HHO-hp vp-cond). Block row f
+ * covers rows [f bs, (f+1) bs); bcols ascending per block row; vals holds the
+ * blocks column-major (entry (r, c) of block q at q bs^2 + c bs + r). Every
+ * operation on a pscu_mat accepts either storage; results are identical to
+ * the CSR expansion (pscu_mat_download returns it), bit for bit. */
+int pscu_bsr_create(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow_ptr,
+                    const int32_t* bcols, const double* vals, int mem, pscu_mat** out);
+/* 0 for CSR storage, else the block size. */
+int pscu_mat_block_size(const pscu_mat* m);
 /* CsrMatrix::multiply (csr.hpp:68-74): y = A x, per-row sequential sums. */
 int pscu_spmv(pscu_ctx* ctx, const pscu_mat* a, const double* x, double* y, int mem);
 
@@ -122,6 +135,10 @@ int pscu_bj_apply(pscu_ctx* ctx, const pscu_bj* p, const double* x, double* y, i
 /* layouts and transfers (dof_layout.hpp:87-126, plevels.hpp:47-113) ------- */
 int pscu_layout_make(int scheme, int strategy, int k, int n_faces, int n_elements,
                      pscu_layout* out);
+/* 3D generalisation of make_layout (no reference: mesh.hpp is 2D): hho-hp
+ * vp-cond only, face blocks [vx | vy | vz | p], no element unknowns. */
+int pscu_layout_make3(int scheme, int strategy, int k, int n_faces, int n_elements,
+                      pscu_layout* out);
 int64_t pscu_layout_dim(const pscu_layout* l);
 int pscu_coarse_to_fine(const pscu_layout* fine, const pscu_layout* coarse, int64_t* map);
 /* inherit_matrix (plevels.hpp:93-113) as a device gather. */
@@ -181,6 +198,30 @@ int pscu_condense_assemble(pscu_ctx* ctx, int nelem, int n, const double* mats,
                            const int32_t* cols, const pscu_layout* layout, int mem,
                            pscu_mat** out, double* rhs_out, double* elim_coupling,
                            double* elim_rhs);
+/* assemble_hho into face-block storage, streamed over element batches
+ * (3D: the local blocks of all elements do not fit in memory at once):
+ * begin allocates the zero operator over the block pattern and a zero load;
+ * each add condenses a batch (condense_element, bitwise in the order of the
+ * reference's PartialPivLU / GEMM) and scatters the Schur blocks and reduced
+ * loads (assemble.hpp:121-131, 164-169; two-term sums, order-free).
+ * efaces: nelem x nfe global face ids of the batch; keep_pos: n_keep x
+ * (local face, offset in the face block) of the retained local dofs. e0 is
+ * the global id of the batch's first element (error messages). Recovery data
+ * (elim_coupling nelem x ne x nk, elim_rhs nelem x ne) is optional. */
+int pscu_assembly_begin(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow_ptr,
+                        const int32_t* bcols, pscu_mat** out);
+int pscu_assembly_add(pscu_ctx* ctx, pscu_mat* m, int e0, int nelem, int n, const double* mats,
+                      const double* rhs, int n_elim, const int* elim, const int32_t* efaces,
+                      int nfe, const int32_t* keep_pos, double* elim_coupling, double* elim_rhs,
+                      int mem);
+int pscu_assembly_rhs(pscu_ctx* ctx, const pscu_mat* m, double* rhs, int mem);
+/* pscu_solve_system on a face-block operator (host buffers, copies timed). */
+int pscu_solve_system_bsr(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow_ptr,
+                          const int32_t* bcols, const double* vals, const double* rhs,
+                          const pscu_layout* lf, const int* degrees, int nlev,
+                          const pscu_level_cfg* cfg, double rtol, int maxit, int restart,
+                          double* x, double* hist, pscu_report* rep);
+
 /* ElementCondensation::recover (condense.hpp:28-38) for all elements:
  * locals[e] (n) from global x through kept_global (nelem x nk). */
 int pscu_recover_batch(pscu_ctx* ctx, int nelem, int n, int n_elim, const int* elim,

@@ -28,13 +28,16 @@ EXPORTS = [
     "pscu_hier_destroy", "pscu_hier_nlev", "pscu_hier_level_mat", "pscu_hier_level_ilu",
     "pscu_vcycle", "pscu_hier_coarse_its", "pscu_hier_reset", "pscu_solve", "pscu_solve_system",
     "pscu_condense_batch", "pscu_condense_assemble", "pscu_recover_batch", "pscu_bj_create",
-    "pscu_bj_destroy", "pscu_bj_apply",
+    "pscu_bj_destroy", "pscu_bj_apply", "pscu_layout_make3", "pscu_bsr_create",
+    "pscu_mat_block_size", "pscu_assembly_begin", "pscu_assembly_add", "pscu_assembly_rhs",
+    "pscu_solve_system_bsr",
 ]
 
 
 class Layout(C.Structure):
     _fields_ = [(f, C.c_int) for f in ("scheme", "strategy", "k", "n_faces", "n_elements",
-                                       "face_vel", "face_press", "elem_vel", "elem_press")]
+                                       "face_vel", "face_press", "elem_vel", "elem_press",
+                                       "dim")]
 
 
 class LevelCfg(C.Structure):
@@ -118,6 +121,16 @@ def load(path: str = LIB):
     lib.pscu_condense_assemble.argtypes = [vp, i32, i32, vp, vp, i32, vp, vp, i64, vp, vp,
                                            C.POINTER(Layout), i32, C.POINTER(vp), vp, vp, vp]
     lib.pscu_recover_batch.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32]
+    lib.pscu_layout_make3.argtypes = [i32, i32, i32, i32, i32, C.POINTER(Layout)]
+    lib.pscu_bsr_create.argtypes = [vp, i64, i32, vp, vp, vp, i32, C.POINTER(vp)]
+    lib.pscu_mat_block_size.argtypes = [vp]
+    lib.pscu_assembly_begin.argtypes = [vp, i64, i32, vp, vp, C.POINTER(vp)]
+    lib.pscu_assembly_add.argtypes = [vp, vp, i32, i32, i32, vp, vp, i32, vp, vp, i32, vp, vp,
+                                      vp, i32]
+    lib.pscu_assembly_rhs.argtypes = [vp, vp, vp, i32]
+    lib.pscu_solve_system_bsr.argtypes = [vp, i64, i32, vp, vp, vp, vp, C.POINTER(Layout), vp,
+                                          i32, C.POINTER(LevelCfg), f64, i32, i32, vp, vp,
+                                          C.POINTER(Report)]
     _lib = lib
     return lib
 

@@ -24,6 +24,10 @@ namespace pscu {
 
 namespace {
 
+/// kBsr: the operator is in dense-block storage (bsr.cu) with this block
+/// size; the diagonal block of block row b is copied directly (rp / cols
+/// are then the block row pointer / block columns).
+template <bool kBsr>
 __global__ void bj_factor_kernel(int64_t nb, int bs, int64_t s0, int64_t b0,
                                  const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
                                  const double* __restrict__ vals, double* __restrict__ inv,
@@ -36,12 +40,20 @@ __global__ void bj_factor_kernel(int64_t nb, int bs, int64_t s0, int64_t b0,
     double* y = work + nb * bs * bs + b * bs;
     int* perm = perm_ws + b * bs;
     double* out = inv + b * bs * bs;  // column-major
-    for (int i = 0; i < bs * bs; ++i) d[i] = 0.0;
-    for (int i = 0; i < bs; ++i)
-      for (int64_t q = rp[s + i]; q < rp[s + i + 1]; ++q) {
-        const int64_t c = cols[q];
-        if (c >= s && c < s + bs) d[i * bs + (c - s)] = vals[q];
-      }
+    if (kBsr) {
+      int64_t q = rp[b];
+      while (q < rp[b + 1] && cols[q] != b) ++q;
+      const double* blk = vals + q * bs * bs;
+      for (int i = 0; i < bs; ++i)
+        for (int c = 0; c < bs; ++c) d[i * bs + c] = q < rp[b + 1] ? blk[c * bs + i] : 0.0;
+    } else {
+      for (int i = 0; i < bs * bs; ++i) d[i] = 0.0;
+      for (int i = 0; i < bs; ++i)
+        for (int64_t q = rp[s + i]; q < rp[s + i + 1]; ++q) {
+          const int64_t c = cols[q];
+          if (c >= s && c < s + bs) d[i * bs + (c - s)] = vals[q];
+        }
+    }
     double amax = 0.0;
     for (int i = 0; i < bs * bs; ++i) amax = fmax(amax, fabs(d[i]));
     for (int i = 0; i < bs; ++i) perm[i] = i;
@@ -134,6 +146,7 @@ void apply_batch(Context& c, int64_t rows, int bs, int64_t s0, const double* inv
     case 9: bj_apply_kernel<9><<<g, 256, 0, c.stream>>>(rows, bs, s0, inv, x, y); break;
     case 10: bj_apply_kernel<10><<<g, 256, 0, c.stream>>>(rows, bs, s0, inv, x, y); break;
     case 12: bj_apply_kernel<12><<<g, 256, 0, c.stream>>>(rows, bs, s0, inv, x, y); break;
+    case 24: bj_apply_kernel<24><<<g, 256, 0, c.stream>>>(rows, bs, s0, inv, x, y); break;
     default:
       if (bs > 64) throw Error(PSCU_EINVAL, "block-Jacobi: blocks larger than 64 unsupported");
       bj_apply_kernel<0><<<g, 256, 0, c.stream>>>(rows, bs, s0, inv, x, y);
@@ -145,8 +158,10 @@ void apply_batch(Context& c, int64_t rows, int bs, int64_t s0, const double* inv
 
 void bj_factor(Context& c, const Csr& a, const pscu_layout& l, BlockJacobi& bj) {
   bj.layout = l;
-  bj.fb = 2 * l.face_vel + l.face_press;
-  bj.eb = 2 * l.elem_vel + l.elem_press;
+  bj.fb = ncomp(l) * l.face_vel + l.face_press;
+  bj.eb = ncomp(l) * l.elem_vel + l.elem_press;
+  if (a.bs && (bj.eb != 0 || bj.fb != a.bs))
+    throw Error(PSCU_EINVAL, "block-Jacobi: block storage must match the layout's face blocks");
   bj.eoff = int64_t(l.n_faces) * bj.fb;
   bj.n = a.n;
   if (layout_dim(l) != a.n) throw Error(PSCU_EINVAL, "block-Jacobi: layout/matrix size mismatch");
@@ -166,9 +181,14 @@ void bj_factor(Context& c, const Csr& a, const pscu_layout& l, BlockJacobi& bj) 
     if (!nb || !bs) continue;
     DevBuf<double> work(size_t(nb) * bs * (bs + 1));
     DevBuf<int> perm(size_t(nb) * bs);
-    bj_factor_kernel<<<grid_rows(nb), 256, 0, c.stream>>>(nb, bs, s0[t], t ? nf : 0, a.row_ptr.p,
-                                                         a.cols.p, a.vals.p, bj.inv.p + off[t],
-                                                         work.p, perm.p, bad.p);
+    if (a.bs)
+      bj_factor_kernel<true><<<grid_rows(nb), 256, 0, c.stream>>>(
+          nb, bs, s0[t], t ? nf : 0, a.brow_ptr.p, a.bcols.p, a.vals.p, bj.inv.p + off[t], work.p,
+          perm.p, bad.p);
+    else
+      bj_factor_kernel<false><<<grid_rows(nb), 256, 0, c.stream>>>(
+          nb, bs, s0[t], t ? nf : 0, a.row_ptr.p, a.cols.p, a.vals.p, bj.inv.p + off[t], work.p,
+          perm.p, bad.p);
     PSCU_LAUNCHED(&c);
     PSCU_CUDA(cudaStreamSynchronize(c.stream));  // scratch freed at scope end
   }

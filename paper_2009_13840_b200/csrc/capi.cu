@@ -15,6 +15,10 @@ void recover_batch(Context& c, int nelem, int n, int ne, const int* elim_host,
                    const double* x, double* locals);
 void assemble_values(Context& c, int nelem, int nk, const int64_t* kept, const double* schur,
                      const double* rrhs, const pscu_layout& l, Csr& a, double* rhs);
+void condense_scatter_bsr(Context& c, Csr& a, int e0, int nelem, int n, const double* mats,
+                          const double* rhs, int ne, const int* elim_host, const int32_t* efaces,
+                          int nfe, const int32_t* keep_pos_host, double* rhs_acc,
+                          double* coupling, double* erhs);
 
 Context::~Context() {
   for (auto e : ev_pool) cudaEventDestroy(e);
@@ -31,10 +35,12 @@ struct pscu_ctx {
   Context c;
 };
 struct pscu_mat {
-  Csr m;
+  Csr m;                     // first member: hierarchy levels are viewed as pscu_mat
+  DevBuf<double> rhs_acc;    // reduced load of a streamed assembly (pscu_assembly_*)
 };
 struct pscu_ilu {
   Ilu i;
+  Csr own;  // CSR copy of a block-stored operator (ILU(0) works on CSR)
 };
 struct pscu_bj {
   BlockJacobi b;
@@ -242,10 +248,16 @@ int pscu_mat_dims(const pscu_mat* m, int64_t* n, int64_t* nnz) {
   return PSCU_OK;
 }
 
-int pscu_mat_download(pscu_ctx* ctx, const pscu_mat* m, int64_t* row_ptr, int32_t* cols,
+int pscu_mat_download(pscu_ctx* ctx, const pscu_mat* mm, int64_t* row_ptr, int32_t* cols,
                       double* vals) {
   return guard([&] {
     Context& c = ctx->c;
+    Csr expanded;
+    if (mm->m.bs) bsr_to_csr(c, mm->m, expanded);  // CSR view of block storage
+    struct {
+      const Csr& m;
+    } view{mm->m.bs ? expanded : mm->m};
+    const auto* m = &view;
     if (row_ptr)
       PSCU_CUDA(cudaMemcpyAsync(row_ptr, m->m.row_ptr.p, sizeof(int64_t) * (m->m.n + 1),
                                 cudaMemcpyDeviceToHost, c.stream));
@@ -274,6 +286,10 @@ int pscu_ilu0_create(pscu_ctx* ctx, const pscu_mat* a, pscu_ilu** out) {
   return guard([&] {
     auto p = std::make_unique<pscu_ilu>();
     p->i.a = &a->m;
+    if (a->m.bs) {
+      bsr_to_csr(ctx->c, a->m, p->own);
+      p->i.a = &p->own;
+    }
     ilu0_factor(ctx->c, p->i);
     *out = p.release();
   });
@@ -336,6 +352,11 @@ int pscu_layout_make(int scheme, int strategy, int k, int n_faces, int n_element
   return guard([&] { make_layout(scheme, strategy, k, n_faces, n_elements, *out); });
 }
 
+int pscu_layout_make3(int scheme, int strategy, int k, int n_faces, int n_elements,
+                      pscu_layout* out) {
+  return guard([&] { make_layout3(scheme, strategy, k, n_faces, n_elements, *out); });
+}
+
 int64_t pscu_layout_dim(const pscu_layout* l) { return layout_dim(*l); }
 
 int pscu_coarse_to_fine(const pscu_layout* fine, const pscu_layout* coarse, int64_t* map) {
@@ -350,7 +371,16 @@ int pscu_inherit(pscu_ctx* ctx, const pscu_mat* fine, const pscu_layout* lf,
     std::vector<int64_t> c2f(layout_dim(*lc));
     coarse_to_fine(*lf, *lc, c2f.data());
     auto m = std::make_unique<pscu_mat>();
-    inherit(ctx->c, fine->m, c2f, m->m);
+    if (fine->m.bs) {
+      const int fbc = ncomp(*lc) * lc->face_vel + lc->face_press;
+      if (lc->elem_vel || lc->elem_press)
+        throw Error(PSCU_EINVAL, "inherit: block storage needs face-only layouts");
+      std::vector<int32_t> in_block(c2f.begin(), c2f.begin() + fbc);
+      inherit_bsr(ctx->c, fine->m, in_block, m->m);
+      PSCU_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    } else {
+      inherit(ctx->c, fine->m, c2f, m->m);
+    }
     *out = m.release();
   });
 }
@@ -504,6 +534,94 @@ int pscu_solve_system(pscu_ctx* ctx, int64_t n, const int64_t* row_ptr, const in
     r.t_setup = std::chrono::duration<double>(t1 - t0).count();
     r.t_solve = std::chrono::duration<double>(t2 - t0).count();
     if (rep) *rep = r;
+  });
+}
+
+int pscu_solve_system_bsr(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow_ptr,
+                          const int32_t* bcols, const double* vals, const double* rhs,
+                          const pscu_layout* lf, const int* degrees, int nlev,
+                          const pscu_level_cfg* cfg, double rtol, int maxit, int restart,
+                          double* x, double* hist, pscu_report* rep) {
+  return guard([&] {
+    Context& c = ctx->c;
+    const auto t0 = std::chrono::steady_clock::now();
+    pscu_mat fine;
+    upload_bsr(c, fine.m, nb, bs, brow_ptr, bcols, vals, PSCU_HOST);
+    if (layout_dim(*lf) != fine.m.n) throw Error(PSCU_EINVAL, "solve: layout/matrix mismatch");
+    pscu_hier h;
+    h.fine = &fine;
+    h.h.build(c, &fine.m, *lf, degrees, nlev, *cfg);
+    PSCU_CUDA(cudaStreamSynchronize(c.stream));
+    const auto t1 = std::chrono::steady_clock::now();
+    pscu_report r{};
+    const int rc = pscu_solve(ctx, &h, rhs, rtol, maxit, restart, x, hist, &r, PSCU_HOST);
+    if (rc) throw Error(rc, g_err);
+    const auto t2 = std::chrono::steady_clock::now();
+    r.t_setup = std::chrono::duration<double>(t1 - t0).count();
+    r.t_solve = std::chrono::duration<double>(t2 - t0).count();
+    if (rep) *rep = r;
+  });
+}
+
+int pscu_bsr_create(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow_ptr,
+                    const int32_t* bcols, const double* vals, int mem, pscu_mat** out) {
+  return guard([&] {
+    if (nb < 0) throw Error(PSCU_EINVAL, "pscu_bsr_create: negative dimension");
+    auto m = std::make_unique<pscu_mat>();
+    upload_bsr(ctx->c, m->m, nb, bs, brow_ptr, bcols, vals, mem);
+    PSCU_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    *out = m.release();
+  });
+}
+
+int pscu_mat_block_size(const pscu_mat* m) { return m->m.bs; }
+
+int pscu_assembly_begin(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow_ptr,
+                        const int32_t* bcols, pscu_mat** out) {
+  return guard([&] {
+    auto m = std::make_unique<pscu_mat>();
+    alloc_bsr(ctx->c, m->m, nb, bs, brow_ptr, bcols);
+    m->rhs_acc.alloc(size_t(std::max<int64_t>(1, m->m.n)));
+    PSCU_CUDA(cudaMemsetAsync(m->rhs_acc.p, 0, sizeof(double) * size_t(m->m.n), ctx->c.stream));
+    PSCU_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    *out = m.release();
+  });
+}
+
+int pscu_assembly_add(pscu_ctx* ctx, pscu_mat* m, int e0, int nelem, int n, const double* mats,
+                      const double* rhs, int n_elim, const int* elim, const int32_t* efaces,
+                      int nfe, const int32_t* keep_pos, double* elim_coupling, double* elim_rhs,
+                      int mem) {
+  return guard([&] {
+    Context& c = ctx->c;
+    if (!m->rhs_acc.p) throw Error(PSCU_EINVAL, "assembly_add: not an assembly target");
+    const int nk = n - n_elim;
+    DevBuf<double> bm, br, bc, be;
+    DevBuf<int32_t> bf;
+    const double* dm = in_vec(c, mats, int64_t(nelem) * n * n, mem, bm);
+    const double* dr = in_vec(c, rhs, int64_t(nelem) * n, mem, br);
+    const int32_t* df = efaces;
+    if (mem == PSCU_HOST) {
+      bf.upload(efaces, size_t(nelem) * nfe, c.stream);
+      df = bf.p;
+    }
+    double* dc = elim_coupling ? out_vec(int64_t(nelem) * n_elim * nk, elim_coupling, mem, bc) : nullptr;
+    double* de = elim_rhs ? out_vec(int64_t(nelem) * n_elim, elim_rhs, mem, be) : nullptr;
+    condense_scatter_bsr(c, m->m, e0, nelem, n, dm, dr, n_elim, elim, df, nfe, keep_pos,
+                         m->rhs_acc.p, dc, de);
+    if (elim_coupling) finish_out(c, elim_coupling, dc, int64_t(nelem) * n_elim * nk, mem);
+    if (elim_rhs) finish_out(c, elim_rhs, de, int64_t(nelem) * n_elim, mem);
+    PSCU_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pscu_assembly_rhs(pscu_ctx* ctx, const pscu_mat* m, double* rhs, int mem) {
+  return guard([&] {
+    if (!m->rhs_acc.p) throw Error(PSCU_EINVAL, "assembly_rhs: not an assembly target");
+    PSCU_CUDA(cudaMemcpyAsync(rhs, m->rhs_acc.p, sizeof(double) * size_t(m->m.n),
+                              mem == PSCU_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                              ctx->c.stream));
+    PSCU_CUDA(cudaStreamSynchronize(ctx->c.stream));
   });
 }
 

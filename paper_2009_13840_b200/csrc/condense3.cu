@@ -1,0 +1,309 @@
+// Batched static condensation of large element blocks (the 3D HHO-hp
+// vp-cond blocks: n = 214, 70 eliminated, 144 retained at k = 2) fused with
+// the value scatter into face-block (BSR) storage: condense_element
+// (condense.hpp:57-97) + scatter_block / the reduced-load accumulation of
+// assemble_hho (assemble.hpp:121-131, 164-169) in one kernel.
+//
+// One CTA per element. Shared memory holds the eliminated block's LU
+// (ne^2), the solutions X = A_ee^-1 [A_ek | b_e] (ne (nk+1)) and A_ke
+// (nk ne); the local block itself stays in global memory and is read once
+// per entry used. Every entry receives its operations in the order of
+// include/eigen_subset's PartialPivLU / GEMM, which oracle/pstokes_oracle.c
+// (po_condense) restates, so the Schur complement and the assembled
+// operator are bitwise equal to the oracle's:
+//  * LU: pivot = first largest |a_ik|, full-row swap, a_ik /= a_kk, then
+//    a_ij -= a_ik a_kj for j > k with a_kj != 0;
+//  * solves: one thread per right-hand-side column, forward then backward
+//    substitution with the sums j ascending;
+//  * Schur: s = 0, s += A_ke(i,k) X(k,j) for k ascending, S = A_kk - s,
+//    each thread folding a 2 x 2 register tile (four independent chains).
+// The FP64 tensor pipe (DMMA) would reorder these sums, so it is not used:
+// B200's FP64 DMMA and FP64 FFMA peaks are equal, and condensation is < 1%
+// of a solve.
+//
+// The Schur entries are scattered straight from registers: retained dof i of
+// the element is (local face lf_i, offset o_i in the face block), so entry
+// (i, j) lands in block (face(lf_i), face(lf_j)) at column-major position
+// (o_j, o_i). A face-pair block receives one element's contribution
+// (distinct hexahedral faces share at most one element) and a diagonal
+// block two; a two-term sum from 0.0 is order-independent, so the atomics
+// reproduce the reference's element-order sums bit for bit. Exact zeros are
+// skipped except on the diagonal, like scatter_block.
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace pscu {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxFacesPerElem = 8;
+
+struct ScatterArgs {
+  const int64_t* brp;
+  const int32_t* bcols;
+  double* vals;  // BSR values (column-major blocks)
+  double* rhs;   // assembled reduced load
+  int bs;
+  const int32_t* efaces;  // nelem x nfe global face ids
+  int nfe;
+  const int2* keep_pos;   // nk x (local face, offset in the face block)
+};
+
+__global__ void __launch_bounds__(kThreads)
+    condense_bsr_kernel(int e0, int nelem, int n, const double* __restrict__ mats,
+                        const double* __restrict__ rhs, int ne, const int* __restrict__ elim,
+                        const int* __restrict__ keep, ScatterArgs sa,
+                        double* __restrict__ coupling, double* __restrict__ erhs, int* bad) {
+  extern __shared__ double sm[];
+  const int nk = n - ne;
+  double* LU = sm;                         // ne x ne, column-major
+  double* X = LU + size_t(ne) * ne;        // ne x (nk + 1)
+  double* AKE = X + size_t(ne) * (nk + 1); // nk x ne
+  __shared__ int perm[128];
+  __shared__ int piv_row, singular;
+  __shared__ int64_t qpair[kMaxFacesPerElem * kMaxFacesPerElem];
+  __shared__ double colnorm[128];
+  for (int le = blockIdx.x; le < nelem; le += gridDim.x) {
+    const int e = e0 + le;
+    const double* M = mats + size_t(le) * n * n;
+    const double* b = rhs + size_t(le) * n;
+    for (int t = threadIdx.x; t < ne * ne; t += blockDim.x) {
+      const int i = t % ne, j = t / ne;
+      LU[t] = M[elim[i] + size_t(elim[j]) * n];
+    }
+    for (int t = threadIdx.x; t < nk * ne; t += blockDim.x) {
+      const int i = t % nk, k = t / nk;
+      AKE[t] = M[keep[i] + size_t(elim[k]) * n];
+    }
+    for (int t = threadIdx.x; t < ne; t += blockDim.x) perm[t] = t;
+    // block position of every (local face, local face) pair of this element
+    for (int t = threadIdx.x; t < sa.nfe * sa.nfe; t += blockDim.x) {
+      const int F = sa.efaces[size_t(le) * sa.nfe + t / sa.nfe];
+      const int G = sa.efaces[size_t(le) * sa.nfe + t % sa.nfe];
+      int64_t q = sa.brp[F];
+      const int64_t q1 = sa.brp[F + 1];
+      while (q < q1 && sa.bcols[q] != G) ++q;
+      qpair[t] = q < q1 ? q : -1;
+    }
+    if (threadIdx.x == 0) singular = 0;
+    __syncthreads();
+    // partial-pivot LU (PartialPivLU::compute of include/eigen_subset)
+    for (int k = 0; k < ne; ++k) {
+      if (threadIdx.x < 32) {
+        // first largest |a_ik|, i >= k: warp arg-max, ties to the lower row
+        double best = -1.0;
+        int bi = k;
+        for (int i = k + int(threadIdx.x); i < ne; i += 32) {
+          const double v = fabs(LU[i + k * ne]);
+          if (v > best) {
+            best = v;
+            bi = i;
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_down_sync(0xffffffffu, best, o);
+          const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+          if (ov > best || (ov == best && oi < bi)) {
+            best = ov;
+            bi = oi;
+          }
+        }
+        if (threadIdx.x == 0) {
+          piv_row = bi;
+          if (bi != k) {
+            const int t = perm[k];
+            perm[k] = perm[bi];
+            perm[bi] = t;
+          }
+        }
+      }
+      __syncthreads();
+      const int p = piv_row;
+      if (p != k)
+        for (int j = threadIdx.x; j < ne; j += blockDim.x) {
+          const double t = LU[k + j * ne];
+          LU[k + j * ne] = LU[p + j * ne];
+          LU[p + j * ne] = t;
+        }
+      __syncthreads();
+      const double piv = LU[k + k * ne];
+      if (piv != 0.0) {
+        for (int i = k + 1 + threadIdx.x; i < ne; i += blockDim.x)
+          LU[i + k * ne] = __ddiv_rn(LU[i + k * ne], piv);
+        __syncthreads();
+        const int m = ne - k - 1;
+        for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+          const int i = k + 1 + t % m, j = k + 1 + t / m;
+          const double ukj = LU[k + j * ne];
+          if (ukj != 0.0) LU[i + j * ne] = dsub(LU[i + j * ne], dmul(LU[i + k * ne], ukj));
+        }
+      }
+      __syncthreads();
+    }
+    // solves (one thread per column of [A_ek | b_e]) and, on the remaining
+    // threads, the inverse columns of the rcond guard
+    const int ncol = nk + 1;
+    for (int col = threadIdx.x; col < ncol + ne; col += blockDim.x) {
+      if (col < ncol) {
+        double* x = X + size_t(col) * ne;
+        const double* src = col < nk ? M + size_t(keep[col]) * n : b;
+        for (int i = 0; i < ne; ++i) x[i] = src[elim[perm[i]]];
+        for (int i = 0; i < ne; ++i) {
+          double s = x[i];
+          for (int j = 0; j < i; ++j) s = dsub(s, dmul(LU[i + j * ne], x[j]));
+          x[i] = s;
+        }
+        for (int i = ne - 1; i >= 0; --i) {
+          double s = x[i];
+          for (int j = i + 1; j < ne; ++j) s = dsub(s, dmul(LU[i + j * ne], x[j]));
+          x[i] = __ddiv_rn(s, LU[i + i * ne]);
+        }
+      } else {
+        // column cidx of A_ee^-1 (exact inverse 1-norm for rcond)
+        const int cidx = col - ncol;
+        double xc[128];
+        for (int i = 0; i < ne; ++i) xc[i] = perm[i] == cidx ? 1.0 : 0.0;
+        for (int i = 0; i < ne; ++i) {
+          double t = xc[i];
+          for (int j = 0; j < i; ++j) t = t - LU[i + j * ne] * xc[j];
+          xc[i] = t;
+        }
+        for (int i = ne - 1; i >= 0; --i) {
+          double t = xc[i];
+          for (int j = i + 1; j < ne; ++j) t = t - LU[i + j * ne] * xc[j];
+          xc[i] = t / LU[i + i * ne];
+        }
+        double s = 0.0;
+        for (int i = 0; i < ne; ++i) s += fabs(xc[i]);
+        colnorm[cidx] = s;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bool sing = false;
+      for (int i = 0; i < ne; ++i) sing = sing || LU[i + i * ne] == 0.0;
+      if (!sing) {
+        double an = 0.0, inorm = 0.0;
+        for (int j = 0; j < ne; ++j) {
+          double s = 0.0;
+          for (int i = 0; i < ne; ++i) s += fabs(M[elim[i] + size_t(elim[j]) * n]);
+          an = fmax(an, s);
+          inorm = fmax(inorm, colnorm[j]);
+        }
+        const double rc = (an > 0.0 && inorm > 0.0 && isfinite(inorm)) ? (1.0 / an) / inorm : 0.0;
+        sing = rc < 1e-14;
+      }
+      if (sing) {
+        singular = 1;
+        atomicMin(bad, e);
+      }
+    }
+    __syncthreads();
+    if (!singular) {
+      if (coupling)
+        for (int t = threadIdx.x; t < ne * nk; t += blockDim.x)
+          coupling[size_t(le) * ne * nk + t] = X[t];
+      if (erhs)
+        for (int t = threadIdx.x; t < ne; t += blockDim.x)
+          erhs[size_t(le) * ne + t] = X[size_t(nk) * ne + t];
+      // Schur complement + reduced load, 2 x 2 tiles, scattered from registers
+      const int ti = (nk + 1) / 2, tj = (ncol + 1) / 2;
+      const int64_t bs2 = int64_t(sa.bs) * sa.bs;
+      for (int t = threadIdx.x; t < ti * tj; t += blockDim.x) {
+        const int i0 = 2 * (t % ti), j0 = 2 * (t / ti);
+        const int i1 = min(i0 + 1, nk - 1), j1 = min(j0 + 1, ncol - 1);
+        double s00 = 0.0, s01 = 0.0, s10 = 0.0, s11 = 0.0;
+        for (int k = 0; k < ne; ++k) {
+          const double a0 = AKE[i0 + k * nk], a1 = AKE[i1 + k * nk];
+          const double x0 = X[k + size_t(j0) * ne], x1 = X[k + size_t(j1) * ne];
+          s00 = dadd(s00, dmul(a0, x0));
+          s01 = dadd(s01, dmul(a0, x1));
+          s10 = dadd(s10, dmul(a1, x0));
+          s11 = dadd(s11, dmul(a1, x1));
+        }
+        const double sv[2][2] = {{s00, s01}, {s10, s11}};
+        for (int di = 0; di < 2; ++di)
+          for (int dj = 0; dj < 2; ++dj) {
+            const int i = di ? i1 : i0, j = dj ? j1 : j0;
+            if ((di && i1 == i0) || (dj && j1 == j0)) continue;
+            const double* src = j < nk ? M + size_t(keep[j]) * n : b;
+            const double v = dsub(src[keep[i]], sv[di][dj]);
+            const int2 pi = sa.keep_pos[i];
+            if (j == nk) {
+              atomicAdd(sa.rhs + int64_t(sa.efaces[size_t(le) * sa.nfe + pi.x]) * sa.bs + pi.y, v);
+              continue;
+            }
+            const int2 pj = sa.keep_pos[j];
+            const bool diag = pi.x == pj.x && pi.y == pj.y;
+            if (v == 0.0 && !diag) continue;
+            const int64_t q = qpair[pi.x * sa.nfe + pj.x];
+            if (q < 0) {
+              atomicExch(bad, -2);
+              continue;
+            }
+            atomicAdd(sa.vals + q * bs2 + int64_t(pj.y) * sa.bs + pi.y, v);
+          }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+} // namespace
+
+void condense_scatter_bsr(Context& c, Csr& a, int e0, int nelem, int n, const double* mats,
+                          const double* rhs, int ne, const int* elim_host, const int32_t* efaces,
+                          int nfe, const int32_t* keep_pos_host, double* rhs_acc,
+                          double* coupling, double* erhs) {
+  if (!a.bs) throw Error(PSCU_EINVAL, "condense_scatter: the operator must use block storage");
+  if (n > 256 || ne > 128 || ne < 1 || nfe > kMaxFacesPerElem)
+    throw Error(PSCU_EINVAL, "condense_scatter: local block too large for the kernel");
+  std::vector<int> is_elim(n, 0), keep;
+  for (int i = 0; i < ne; ++i) {
+    if (elim_host[i] < 0 || elim_host[i] >= n) throw Error(PSCU_EINVAL, "condense: bad elim index");
+    is_elim[elim_host[i]] = 1;
+  }
+  for (int i = 0; i < n; ++i)
+    if (!is_elim[i]) keep.push_back(i);
+  const int nk = int(keep.size());
+  std::vector<int2> kp(nk);
+  for (int i = 0; i < nk; ++i) {
+    kp[i] = make_int2(keep_pos_host[2 * i], keep_pos_host[2 * i + 1]);
+    if (kp[i].x < 0 || kp[i].x >= nfe || kp[i].y < 0 || kp[i].y >= a.bs)
+      throw Error(PSCU_EINVAL, "condense_scatter: retained dof outside the face blocks");
+  }
+  DevBuf<int> d_elim, d_keep;
+  DevBuf<int2> d_kp;
+  d_elim.upload(elim_host, ne, c.stream);
+  d_keep.upload(keep, c.stream);
+  d_kp.upload(kp, c.stream);
+  const int big = 0x7fffffff;
+  PSCU_CUDA(cudaMemcpyAsync(c.err_flag.p, &big, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+  const size_t smem = sizeof(double) * (size_t(ne) * ne + size_t(ne) * (nk + 1) + size_t(nk) * ne);
+  if (smem > 227 * 1024) throw Error(PSCU_EINVAL, "condense_scatter: block too large for shared memory");
+  static size_t attr = 0;
+  if (smem > attr) {
+    PSCU_CUDA(cudaFuncSetAttribute(condense_bsr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+    attr = smem;
+  }
+  ScatterArgs sa{a.brow_ptr.p, a.bcols.p, a.vals.p, rhs_acc, a.bs, efaces, nfe, d_kp.p};
+  int per_sm = 1;
+  PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, condense_bsr_kernel, kThreads, smem));
+  const int grid = std::max(1, std::min(nelem, 148 * std::max(1, per_sm)));
+  condense_bsr_kernel<<<grid, kThreads, smem, c.stream>>>(e0, nelem, n, mats, rhs, ne, d_elim.p,
+                                                          d_keep.p, sa, coupling, erhs,
+                                                          c.err_flag.p);
+  PSCU_LAUNCHED(&c);
+  int bad = big;
+  PSCU_CUDA(cudaMemcpyAsync(&bad, c.err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  PSCU_CUDA(cudaStreamSynchronize(c.stream));
+  if (bad == -2) throw Error(PSCU_EINVAL, "CsrMatrix::add: entry outside the sparsity pattern");
+  if (bad != big)
+    throw Error(PSCU_ESINGULAR,
+                "condense: near-singular eliminated block on element " + std::to_string(bad));
+}
+
+} // namespace pscu

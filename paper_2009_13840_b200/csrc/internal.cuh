@@ -94,6 +94,9 @@ inline int64_t repro_lanes(int64_t n) {
 
 struct Context;
 
+/// Velocity components of a layout (dof_layout.hpp:68-69 has 2; dim 3 adds z).
+inline int ncomp(const pscu_layout& l) { return l.dim == 3 ? 3 : 2; }
+
 /// Device CSR (csr.hpp:19-24) plus a host copy of the pattern for schedule
 /// construction.
 struct Csr {
@@ -103,6 +106,18 @@ struct Csr {
   DevBuf<double> vals;
   std::vector<int64_t> h_row_ptr;
   std::vector<int32_t> h_cols;
+  // Dense-block storage (bsr.cu) of operators whose structural pattern is
+  // made of dense bs x bs face blocks (3D HHO-hp vp-cond): bs > 0 means
+  // row_ptr / cols are unused and vals holds nblk blocks, column-major per
+  // block, in block-row order with block columns ascending (the CSR order of
+  // csr.hpp:30-44 is block column, then column within the block). n = nb bs,
+  // nnz = nblk bs^2 structural entries.
+  int bs = 0;
+  int64_t nb = 0, nblk = 0;
+  DevBuf<int64_t> brow_ptr;
+  DevBuf<int32_t> bcols, brow_of;  // block columns, block row of every block
+  std::vector<int64_t> h_brow_ptr;
+  std::vector<int32_t> h_bcols;
 };
 
 /// Level-walking sweep plan (walk.cu).
@@ -220,6 +235,21 @@ void residual_restrict(Context& c, const Csr& a, const double* d, const double* 
                        const int64_t* map, int64_t nc, double* rc);
 void upload_csr(Context& c, Csr& m, int64_t n, const int64_t* rp, const int32_t* cols,
                 const double* vals, int mem);
+
+// bsr.cu
+void upload_bsr(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brow_ptr,
+                const int32_t* bcols, const double* vals, int mem);
+/// Zero-valued block matrix over a block pattern (host arrays).
+void alloc_bsr(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brow_ptr,
+               const int32_t* bcols);
+/// The same operator in CSR storage (pattern on the host too: ILU plans).
+void bsr_to_csr(Context& c, const Csr& b, Csr& out);
+/// inherit_matrix (plevels.hpp:93-113) between face-block operators: every
+/// block keeps its position, its entries are the in-block map's rows/cols.
+void inherit_bsr(Context& c, const Csr& fine, const std::vector<int32_t>& in_block, Csr& out);
+void spmv_bsr(Context& c, const Csr& a, const double* x, double* y);
+void residual_restrict_bsr(Context& c, const Csr& a, const double* d, const double* w,
+                           const int64_t* map, int64_t nc, double* rc);
 
 // sptrsv.cu
 void ilu0_factor(Context& c, Ilu& ilu);

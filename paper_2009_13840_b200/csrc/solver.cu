@@ -324,8 +324,26 @@ KrylovResultDev fgmres_dev(Context& c, Op& op, Op& pc, const double* rhs, int ma
 // ---------------------------------------------------------------------------
 
 int64_t layout_dim(const pscu_layout& l) {
-  return int64_t(l.n_faces) * (2 * l.face_vel + l.face_press) +
-         int64_t(l.n_elements) * (2 * l.elem_vel + l.elem_press);
+  return int64_t(l.n_faces) * (ncomp(l) * l.face_vel + l.face_press) +
+         int64_t(l.n_elements) * (ncomp(l) * l.elem_vel + l.elem_press);
+}
+
+void make_layout3(int scheme, int strategy, int k, int n_faces, int n_elements, pscu_layout& l) {
+  if (k < 0) throw Error(PSCU_EINVAL, "layout: k must be >= 0");
+  if (scheme != 1 || strategy != 2) throw Error(PSCU_EINVAL, "3D layout: hho-hp vp-cond only");
+  l = pscu_layout{};
+  l.scheme = scheme;
+  l.strategy = strategy;
+  l.k = k;
+  l.n_faces = n_faces;
+  l.n_elements = n_elements;
+  l.face_vel = l.face_press = (k + 1) * (k + 2) / 2;
+  l.dim = 3;
+}
+
+void layout_at(const pscu_layout& lf, int k, pscu_layout& out) {
+  if (lf.dim == 3) make_layout3(lf.scheme, lf.strategy, k, lf.n_faces, lf.n_elements, out);
+  else make_layout(lf.scheme, lf.strategy, k, lf.n_faces, lf.n_elements, out);
 }
 
 void make_layout(int scheme, int strategy, int k, int n_faces, int n_elements, pscu_layout& l) {
@@ -336,6 +354,7 @@ void make_layout(int scheme, int strategy, int k, int n_faces, int n_elements, p
   l.k = k;
   l.n_faces = n_faces;
   l.n_elements = n_elements;
+  l.dim = 2;
   const int nf = k + 1, np = (k + 1) * (k + 2) / 2;
   const int ke = scheme == 1 ? k + 1 : k;
   const int ne = (ke + 1) * (ke + 2) / 2;
@@ -378,20 +397,22 @@ void coarse_to_fine(const pscu_layout& f, const pscu_layout& c, int64_t* map) {
   if (c.face_vel > f.face_vel || c.face_press > f.face_press || c.elem_vel > f.elem_vel ||
       c.elem_press > f.elem_press)
     throw Error(PSCU_EINVAL, "transfer: coarse layout is not nested in the fine one");
-  const int64_t cfb = 2 * c.face_vel + c.face_press, ffb = 2 * f.face_vel + f.face_press;
-  const int64_t ceb = 2 * c.elem_vel + c.elem_press, feb = 2 * f.elem_vel + f.elem_press;
+  if (ncomp(c) != ncomp(f)) throw Error(PSCU_EINVAL, "transfer: layouts of different dimension");
+  const int nc = ncomp(c);
+  const int64_t cfb = nc * c.face_vel + c.face_press, ffb = nc * f.face_vel + f.face_press;
+  const int64_t ceb = nc * c.elem_vel + c.elem_press, feb = nc * f.elem_vel + f.elem_press;
   for (int64_t fc = 0; fc < c.n_faces; ++fc) {
     const int64_t cb = fc * cfb, fb = fc * ffb;
-    for (int comp = 0; comp < 2; ++comp)
+    for (int comp = 0; comp < nc; ++comp)
       for (int m = 0; m < c.face_vel; ++m) map[cb + comp * c.face_vel + m] = fb + comp * f.face_vel + m;
-    for (int m = 0; m < c.face_press; ++m) map[cb + 2 * c.face_vel + m] = fb + 2 * f.face_vel + m;
+    for (int m = 0; m < c.face_press; ++m) map[cb + nc * c.face_vel + m] = fb + nc * f.face_vel + m;
   }
   const int64_t co = int64_t(c.n_faces) * cfb, fo = int64_t(f.n_faces) * ffb;
   for (int64_t e = 0; e < c.n_elements; ++e) {
     const int64_t cb = co + e * ceb, fb = fo + e * feb;
-    for (int comp = 0; comp < 2; ++comp)
+    for (int comp = 0; comp < nc; ++comp)
       for (int m = 0; m < c.elem_vel; ++m) map[cb + comp * c.elem_vel + m] = fb + comp * f.elem_vel + m;
-    for (int m = 0; m < c.elem_press; ++m) map[cb + 2 * c.elem_vel + m] = fb + 2 * f.elem_vel + m;
+    for (int m = 0; m < c.elem_press; ++m) map[cb + nc * c.elem_vel + m] = fb + nc * f.elem_vel + m;
   }
 }
 
@@ -501,7 +522,7 @@ void Hierarchy::build(Context& c, const Csr* fine, const pscu_layout& lf, const 
     Level& L = *levels[l];
     Level& P = *levels[l - 1];
     L.k = degrees[l];
-    make_layout(lf.scheme, lf.strategy, degrees[l], lf.n_faces, lf.n_elements, L.layout);
+    layout_at(lf, degrees[l], L.layout);
     std::vector<int64_t> c2f(layout_dim(L.layout));
     coarse_to_fine(P.layout, L.layout, c2f.data());
     P.nc = int64_t(c2f.size());
@@ -510,7 +531,26 @@ void Hierarchy::build(Context& c, const Csr* fine, const pscu_layout& lf, const 
     for (int64_t i = 0; i < P.nc; ++i) f2c[c2f[i]] = int32_t(i);
     P.f2c.upload(f2c, c.stream);
     const auto t0 = std::chrono::steady_clock::now();
-    inherit(c, *P.a, c2f, L.own);
+    if (P.a->bs) {
+      // face-block operators: the coarse blocks are sub-blocks of the fine
+      // ones (face f's coarse dofs map into face f's fine block)
+      const int fbc = ncomp(L.layout) * L.layout.face_vel + L.layout.face_press;
+      if (L.layout.elem_vel || L.layout.elem_press || P.layout.elem_vel || P.layout.elem_press)
+        throw Error(PSCU_EINVAL, "hierarchy: block storage needs face-only layouts");
+      std::vector<int32_t> in_block(fbc);
+      for (int j = 0; j < fbc; ++j) in_block[j] = int32_t(c2f[j]);
+      const bool needs_csr = (l + 1 == nlev) || cfg.smoother != PSCU_SMOOTHER_BJACOBI;
+      if (needs_csr) {
+        Csr tmp;
+        inherit_bsr(c, *P.a, in_block, tmp);
+        bsr_to_csr(c, tmp, L.own);
+        PSCU_CUDA(cudaStreamSynchronize(c.stream));
+      } else {
+        inherit_bsr(c, *P.a, in_block, L.own);
+      }
+    } else {
+      inherit(c, *P.a, c2f, L.own);
+    }
     L.a = &L.own;
     if (getenv("PSCU_DEBUG"))
       fprintf(stderr, "[setup] inherit level %d: %.3f s\n", l,
@@ -522,6 +562,13 @@ void Hierarchy::build(Context& c, const Csr* fine, const pscu_layout& lf, const 
   std::vector<int> ilu_levels;
   for (int l = 0; l < nlev; ++l) {
     Level& L = *levels[l];
+    const bool wants_csr = (l + 1 == nlev) || cfg.smoother != PSCU_SMOOTHER_BJACOBI;
+    if (L.a->bs && wants_csr) {
+      // ILU(0) / dense LU work on CSR storage: a private CSR copy
+      bsr_to_csr(c, *L.a, L.own);
+      PSCU_CUDA(cudaStreamSynchronize(c.stream));
+      L.a = &L.own;
+    }
     if (l + 1 == nlev && cfg.coarse == PSCU_COARSE_LU) {
       L.dense_lu.factor(c, *L.a);
     } else if (l + 1 < nlev && cfg.smoother == PSCU_SMOOTHER_BJACOBI) {

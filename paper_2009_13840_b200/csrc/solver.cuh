@@ -113,6 +113,9 @@ struct Hierarchy {
 
 int64_t layout_dim(const pscu_layout& l);
 void make_layout(int scheme, int strategy, int k, int n_faces, int n_elements, pscu_layout& l);
+void make_layout3(int scheme, int strategy, int k, int n_faces, int n_elements, pscu_layout& l);
+/// The layout of lf's scheme at degree k (2D or 3D).
+void layout_at(const pscu_layout& lf, int k, pscu_layout& out);
 void coarse_to_fine(const pscu_layout& f, const pscu_layout& c, int64_t* map);
 void inherit(Context& c, const Csr& fine, const std::vector<int64_t>& c2f, Csr& out);
 

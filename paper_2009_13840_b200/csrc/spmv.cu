@@ -76,6 +76,7 @@ __global__ void residual_restrict_warp(int64_t nc, const int64_t* __restrict__ m
 } // namespace
 
 void spmv(Context& c, const Csr& a, const double* x, double* y) {
+  if (a.bs) return spmv_bsr(c, a, x, y);
   if (a.n == 0) return;
   const unsigned grid = unsigned((a.n + kRows - 1) / kRows);
   Context::Scope prof(&c, PROF_SPMV, 8.0 * double(a.nnz) + 16.0 * double(a.n));
@@ -85,6 +86,7 @@ void spmv(Context& c, const Csr& a, const double* x, double* y) {
 
 void residual_restrict(Context& c, const Csr& a, const double* d, const double* w,
                        const int64_t* map, int64_t nc, double* rc) {
+  if (a.bs) return residual_restrict_bsr(c, a, d, w, map, nc, rc);
   if (nc == 0) return;
   const int threads = 256;
   const unsigned grid = unsigned((nc * 32 + threads - 1) / threads);

@@ -293,3 +293,63 @@ class HpLocal3:
         _check3(load3().psh3_local_blocks(mesh.h, self.k, DATA3[data], seed, eta, e0, e1, nthreads,
                                           N.ptr(mats), N.ptr(rhs)))
         return mats, rhs
+
+
+def assemble_stokes3(mesh: Mesh3, k: int, data: str = "random", seed: int = 0, eta: float = 0.0,
+                     batch: int = 4096, nthreads: int = 0, ctx=None, recovery: bool = False):
+    """assemble_hho (assemble.hpp:136-172) for the 3D HHO-hp vp-cond scheme
+    into face-block device storage, streamed over element batches: the host
+    builds a batch of local blocks, the device condenses it and scatters the
+    Schur blocks and reduced loads (pscu_assembly_add). Returns (A, rhs,
+    layout, info) with A a device CsrMatrix in block storage; with recovery
+    the per-element elim_coupling / elim_rhs are returned in info."""
+    from . import solver as S
+
+    ctx = ctx or S.default_context()
+    L = HpLocal3(k)
+    brp, bcols = mesh.block_pattern()
+    h = C.c_void_p()
+    N.check(ctx.lib.pscu_assembly_begin(ctx.h, mesh.n_faces, L.face_block, brp.ctypes.data,
+                                        bcols.ctypes.data, C.byref(h)))
+    A = S.CsrMatrix(None, None, None, ctx=ctx, _handle=h.value)
+    A._owned = True
+    ef = mesh.element_faces()
+    keep_pos = np.ascontiguousarray(L.keep_pos, np.int32)
+    n = L.n_local
+    nb = min(batch, mesh.n_elements)
+    bufs = [(np.empty(nb * n * n), np.empty(nb * n)) for _ in range(2)]
+    coup = erhs = None
+    if recovery:
+        coup = np.empty((mesh.n_elements, L.n_elim, L.n_keep))
+        erhs = np.empty((mesh.n_elements, L.n_elim))
+    import time
+    t_host = t_dev = 0.0
+    for i, e0 in enumerate(range(0, mesh.n_elements, nb)):
+        e1 = min(mesh.n_elements, e0 + nb)
+        mats, rhs = bufs[i % 2]
+        t0 = time.perf_counter()
+        L.local_blocks(mesh, e0, e1, data=data, seed=seed, eta=eta, nthreads=nthreads,
+                       out=(mats, rhs))
+        t1 = time.perf_counter()
+        efb = np.ascontiguousarray(ef[e0:e1], np.int32)
+        cp = ep = None
+        if recovery:
+            cp = np.empty((e1 - e0) * L.n_elim * L.n_keep)
+            ep = np.empty((e1 - e0) * L.n_elim)
+        N.check(ctx.lib.pscu_assembly_add(ctx.h, A.h, e0, e1 - e0, n, mats.ctypes.data,
+                                          rhs.ctypes.data, L.n_elim, L.elim.ctypes.data,
+                                          efb.ctypes.data, 6, keep_pos.ctypes.data,
+                                          None if cp is None else cp.ctypes.data,
+                                          None if ep is None else ep.ctypes.data, N.PSCU_HOST))
+        if recovery:
+            # column-major ne x nk blocks -> (ne, nk)
+            coup[e0:e1] = np.transpose(cp.reshape(e1 - e0, L.n_keep, L.n_elim), (0, 2, 1))
+            erhs[e0:e1] = ep.reshape(e1 - e0, L.n_elim)
+        t_host += t1 - t0
+        t_dev += time.perf_counter() - t1
+    b = np.zeros(A.n)
+    N.check(ctx.lib.pscu_assembly_rhs(ctx.h, A.h, b.ctypes.data, N.PSCU_HOST))
+    lay = S.make_layout3(k, mesh.n_faces, mesh.n_elements)
+    info = dict(t_local_s=t_host, t_condense_s=t_dev, brow_ptr=brp, bcols=bcols, local=L,
+                elim_coupling=coup, elim_rhs=erhs)
+    return A, b, lay, info

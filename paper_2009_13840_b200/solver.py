@@ -230,6 +230,46 @@ def make_layout(scheme: str | int, strategy: str | int, k: int, n_faces: int,
     return lay
 
 
+def make_layout3(k: int, n_faces: int, n_elements: int, scheme: str | int = "hho-hp",
+                 strategy: str | int = "vp-cond") -> N.Layout:
+    """The 3D generalisation of make_layout (BASELINE.json configs 3/5; the
+    reference is 2D only): hho-hp vp-cond face blocks [vx | vy | vz | p]."""
+    s = SCHEMES[scheme] if isinstance(scheme, str) else scheme
+    t = STRATEGIES[strategy] if isinstance(strategy, str) else strategy
+    lay = N.Layout()
+    N.check(N.load().pscu_layout_make3(s, t, k, n_faces, n_elements, C.byref(lay)))
+    return lay
+
+
+def bsr_matrix(brow_ptr, bcols, vals, bs: int, ctx: Context | None = None) -> "CsrMatrix":
+    """A CsrMatrix held in dense face-block storage (pscu_bsr_create): block
+    row f covers rows [f bs, (f+1) bs), vals are the blocks column-major."""
+    ctx = ctx or default_context()
+    rp = np.ascontiguousarray(brow_ptr, np.int64)
+    cl = np.ascontiguousarray(bcols, np.int32)
+    vl = _f64(vals)
+    h = C.c_void_p()
+    N.check(ctx.lib.pscu_bsr_create(ctx.h, len(rp) - 1, bs, rp.ctypes.data, cl.ctypes.data,
+                                    vl.ctypes.data, N.PSCU_HOST, C.byref(h)))
+    m = CsrMatrix(None, None, None, ctx=ctx, _handle=h.value)
+    m._owned = True
+    return m
+
+
+def csr_to_bsr_values(row_ptr, cols, vals, brow_ptr, bcols, bs: int) -> np.ndarray:
+    """Column-major block values of a CSR matrix whose pattern is the dense
+    expansion of (brow_ptr, bcols) (e.g. an oracle-assembled operator)."""
+    rp = np.asarray(row_ptr, np.int64)
+    nb = len(brow_ptr) - 1
+    out = np.empty(int(brow_ptr[-1]) * bs * bs)
+    v = np.asarray(vals, np.float64)
+    for f in range(nb):
+        q0, q1 = int(brow_ptr[f]), int(brow_ptr[f + 1])
+        rows = v[rp[f * bs]:rp[(f + 1) * bs]].reshape(bs, q1 - q0, bs)  # (r, block, c)
+        out[q0 * bs * bs:q1 * bs * bs] = np.transpose(rows, (1, 2, 0)).ravel()
+    return out
+
+
 def layout_dim(lay: N.Layout) -> int:
     return int(N.load().pscu_layout_dim(C.byref(lay)))
 
@@ -363,6 +403,31 @@ def solve_system(row_ptr, cols, vals, rhs, layout: N.Layout, cfg: LevelConfig,
                                       b.ctypes.data, C.byref(layout), deg.ctypes.data, len(deg),
                                       C.byref(ncfg), cfg.outer_rtol, cfg.outer_maxit, cfg.restart,
                                       x.ctypes.data, hist.ctypes.data, C.byref(rep)))
+    r = SolverReport(rep.outer_its, rep.coarse_its, rep.vcycles, rep.rel_residual,
+                     bool(rep.converged), rep.t_setup, rep.t_solve)
+    return x, hist[: rep.outer_its].copy(), r
+
+
+def solve_system_bsr(brow_ptr, bcols, vals, bs: int, rhs, layout: N.Layout, cfg: LevelConfig,
+                     ctx: Context | None = None):
+    """solve_system through the one-call C ABI entry for a face-block
+    operator (pscu_solve_system_bsr): host buffers in, x out, everything
+    inside the timed t_solve. Returns (x, hist, SolverReport)."""
+    ctx = ctx or default_context()
+    rp = np.ascontiguousarray(brow_ptr, np.int64)
+    cl = np.ascontiguousarray(bcols, np.int32)
+    vl = _f64(vals)
+    b = _f64(rhs)
+    deg = np.ascontiguousarray(cfg.degrees, np.int32)
+    x = np.zeros(len(b))
+    hist = np.zeros(cfg.outer_maxit + 1)
+    rep = N.Report()
+    ncfg = cfg.native()
+    N.check(ctx.lib.pscu_solve_system_bsr(ctx.h, len(rp) - 1, bs, rp.ctypes.data, cl.ctypes.data,
+                                          vl.ctypes.data, b.ctypes.data, C.byref(layout),
+                                          deg.ctypes.data, len(deg), C.byref(ncfg),
+                                          cfg.outer_rtol, cfg.outer_maxit, cfg.restart,
+                                          x.ctypes.data, hist.ctypes.data, C.byref(rep)))
     r = SolverReport(rep.outer_its, rep.coarse_its, rep.vcycles, rep.rel_residual,
                      bool(rep.converged), rep.t_setup, rep.t_solve)
     return x, hist[: rep.outer_its].copy(), r

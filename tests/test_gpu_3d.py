@@ -1,0 +1,140 @@
+"""GPU parity of the 3D HHO-hp path (BASELINE.json configs 3 and 5) against
+the oracle restatement on identical host-built local blocks
+(host/pstokes_host3d.cpp): streamed device condensation + face-block
+assembly, the face-block SpMV, p-level inheritance, block-Jacobi smoothing,
+V-cycles and full FGMRES solves. The 3D path has no reference (the
+reference is 2D only); the oracle is oracle/pstokes_oracle.c's
+restatement of the reference's algorithms in 3D. Bar: bitwise (IEEE ==)."""
+import numpy as np
+import pytest
+
+import oracle_ref as O
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not O.port_available(),
+                                                  reason="oracle restatement not built")]
+
+
+def same(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+@pytest.fixture(scope="module")
+def M():
+    from paper_2009_13840_b200 import build, host, solver
+    build.build_host()
+    return host, solver
+
+
+def _oracle_system(host, n, jitter, data, k=2, seed=2):
+    m = host.Mesh3(n, jitter=jitter, seed=1)
+    L = host.HpLocal3(k)
+    mats, rhs = L.local_blocks(m, 0, m.n_elements, data=data, seed=seed)
+    brp, bcols = m.block_pattern()
+    rp, cols = O.bsr_to_csr_pattern(brp, bcols, L.face_block)
+    lay = O.po_layout(1, 2, k, m.n_faces, m.n_elements, dim=3)
+    a, b = O.port_condense_assemble(mats, rhs, L.n_local, L.elim, L.kept_global(m.element_faces()),
+                                    lay, rp, cols)
+    return m, L, mats, rhs, brp, bcols, a, b, lay
+
+
+@pytest.mark.parametrize("n,jitter,batch", [(2, 0.0, 3), (3, 0.15, 7), (4, 0.15, 4096)])
+def test_streamed_assembly_bitwise(M, n, jitter, batch):
+    host, S = M
+    m, L, mats, rhs, brp, bcols, a, b, lay = _oracle_system(host, n, jitter, "random")
+    A, bd, lay_d, info = host.assemble_stokes3(m, 2, data="random", seed=2, batch=batch)
+    rp, cl, vl = A.download()
+    assert np.array_equal(rp, a.row_ptr) and np.array_equal(cl, a.cols)
+    assert same(vl, a.vals)
+    assert same(bd, b)
+    assert S.layout_dim(lay_d) == a.n
+
+
+def test_recovery_data_bitwise(M):
+    host, S = M
+    m = host.Mesh3(2, jitter=0.1, seed=1)
+    L = host.HpLocal3(2)
+    mats, rhs = L.local_blocks(m, 0, m.n_elements, data="random", seed=5)
+    A, b, lay, info = host.assemble_stokes3(m, 2, data="random", seed=5, batch=3, recovery=True)
+    lib = O.port_lib()
+    n, ne, nk = L.n_local, L.n_elim, L.n_keep
+    for e in range(m.n_elements):
+        sch, rr = np.zeros(nk * nk), np.zeros(nk)
+        cp, er = np.zeros(ne * nk), np.zeros(ne)
+        el = np.ascontiguousarray(L.elim, np.int32)
+        assert lib.po_condense(n, mats[e * n * n:(e + 1) * n * n].copy(), rhs[e * n:(e + 1) * n].copy(),
+                               ne, el, sch, rr, cp, er) == 0
+        assert same(info["elim_coupling"][e], cp.reshape(nk, ne).T)
+        assert same(info["elim_rhs"][e], er)
+
+
+def test_bsr_spmv_bitwise(M):
+    host, S = M
+    m, L, mats, rhs, brp, bcols, a, b, lay = _oracle_system(host, 4, 0.15, "random")
+    bv = S.csr_to_bsr_values(a.row_ptr, a.cols, a.vals, brp, bcols, L.face_block)
+    A = S.bsr_matrix(brp, bcols, bv, L.face_block)
+    lib = O.port_lib()
+    pa = O.po_csr(a)
+    import ctypes as C
+    for seed in range(3):
+        x = np.random.default_rng(seed).standard_normal(a.n)
+        y = np.zeros(a.n)
+        lib.po_csr_multiply(C.byref(pa), x, y)
+        assert same(A.multiply(x), y)
+
+
+@pytest.mark.parametrize("n,jitter,data", [(3, 0.15, "random"), (4, 0.15, "manufactured")])
+def test_hierarchy_vcycle_and_solve_bitwise(M, n, jitter, data):
+    """Levels 2 -> 1 -> 0, block-Jacobi-preconditioned GMRES(2) smoothing on
+    the face-block levels, ILU-GMRES on the coarsest (CSR) level, FGMRES(30)
+    to 1e-8: inherited operators, a V-cycle, ITs and the whole residual
+    history and solution bit for bit against the oracle."""
+    host, S = M
+    m, L, mats, rhs, brp, bcols, a, b, lay = _oracle_system(host, n, jitter, data)
+    A, bd, lay_d, info = host.assemble_stokes3(m, 2, data=data, seed=2)
+    ref = O.PortHierarchy(a, lay, [2, 1, 0], smoother_iters=2, smoother=1)
+    cfg = S.LevelConfig(degrees=[2, 1, 0], coarse="gmres-ilu", smoother="bjacobi",
+                        outer_rtol=1e-8, restart=30)
+    h = S.LevelHierarchy(A, lay_d, cfg)
+    for l in range(3):
+        rp, cl, vl = h.level_matrix(l).download()
+        r = ref.level_csr(l)
+        assert np.array_equal(rp, r.row_ptr) and np.array_equal(cl, r.cols) and same(vl, r.vals), l
+    d = np.random.default_rng(4).standard_normal(a.n)
+    assert same(h.vcycle(0, d), ref.vcycle(0, d))
+    r = ref.solve(b, rtol=1e-8, maxit=200, restart=30)
+    x, hist, rep = h.solve(bd)
+    assert rep.converged and r["converged"]
+    assert rep.outer_its == r["its"] and rep.coarse_its == r["coarse_its"]
+    assert same(hist, r["hist"]) and same(x, r["x"])
+    # one-call drop-in entry on host buffers
+    bv = S.csr_to_bsr_values(a.row_ptr, a.cols, a.vals, brp, bcols, L.face_block)
+    x2, hist2, rep2 = S.solve_system_bsr(brp, bcols, bv, L.face_block, b, lay_d, cfg)
+    assert rep2.outer_its == r["its"] and same(x2, r["x"]) and same(hist2, r["hist"])
+
+
+def test_bjacobi_face_blocks_bitwise(M):
+    host, S = M
+    m, L, mats, rhs, brp, bcols, a, b, lay = _oracle_system(host, 3, 0.15, "random")
+    A, bd, lay_d, info = host.assemble_stokes3(m, 2, data="random", seed=2)
+    bj = S.BlockJacobi(A, lay_d)
+    ref = O.PortBlockJacobi(a, lay)
+    for seed in range(2):
+        x = np.random.default_rng(seed).standard_normal(a.n)
+        assert same(bj.apply(x), ref.apply(x))
+
+
+def test_inherit_bsr_matches_csr(M):
+    """pscu_inherit on block storage equals inherit_matrix on the CSR
+    expansion (plevels.hpp:93-113), for both coarse degrees."""
+    host, S = M
+    m, L, mats, rhs, brp, bcols, a, b, lay = _oracle_system(host, 3, 0.1, "random")
+    bv = S.csr_to_bsr_values(a.row_ptr, a.cols, a.vals, brp, bcols, L.face_block)
+    A = S.bsr_matrix(brp, bcols, bv, L.face_block)
+    Ac = S.CsrMatrix(a.row_ptr, a.cols, a.vals)
+    lf = S.make_layout3(2, m.n_faces, m.n_elements)
+    for kc in (1, 0):
+        lc = S.make_layout3(kc, m.n_faces, m.n_elements)
+        r1 = S.inherit_matrix(A, lf, lc).download()
+        r2 = S.inherit_matrix(Ac, lf, lc).download()
+        assert all(np.array_equal(u, v) for u, v in zip(r1, r2))
