@@ -362,13 +362,23 @@ struct ElemBasis {
   V3 c;
   double h = 1.0;
   Mat C;
-  void monos(V3 p, double* m) const {
+  /// powers px[a] = x^a (a <= deg) of the scaled coordinates
+  void powers(V3 p, double* px, double* py, double* pz) const {
     const double x = (p.x - c.x) / h, y = (p.y - c.y) / h, z = (p.z - c.z) / h;
+    px[0] = py[0] = pz[0] = 1.0;
+    for (int a = 1; a <= deg; ++a) {
+      px[a] = px[a - 1] * x;
+      py[a] = py[a - 1] * y;
+      pz[a] = pz[a - 1] * z;
+    }
+  }
+  void monos(V3 p, double* m) const {
+    double px[8], py[8], pz[8];
+    powers(p, px, py, pz);
     int idx = 0;
     for (int d = 0; d <= deg; ++d)
       for (int az = 0; az <= d; ++az)
-        for (int ay = 0; ay <= d - az; ++ay)
-          m[idx++] = std::pow(x, d - ay - az) * std::pow(y, ay) * std::pow(z, az);
+        for (int ay = 0; ay <= d - az; ++ay) m[idx++] = px[d - ay - az] * py[ay] * pz[az];
   }
   void init(const ElemRule& r, V3 center, double diam, int degree) {
     deg = degree;
@@ -395,17 +405,17 @@ struct ElemBasis {
   }
   /// gradients out[3 i + d]
   void grad(V3 p, double* out) const {
-    const double x = (p.x - c.x) / h, y = (p.y - c.y) / h, z = (p.z - c.z) / h;
+    double X[8], Y[8], Z[8];
+    powers(p, X, Y, Z);
     double gx[kMaxMono], gy[kMaxMono], gz[kMaxMono];
     int idx = 0;
     for (int d = 0; d <= deg; ++d)
       for (int az = 0; az <= d; ++az)
         for (int ay = 0; ay <= d - az; ++ay) {
           const int ax = d - ay - az;
-          const double px = std::pow(x, ax), py = std::pow(y, ay), pz = std::pow(z, az);
-          gx[idx] = ax == 0 ? 0.0 : ax * std::pow(x, ax - 1) * py * pz / h;
-          gy[idx] = ay == 0 ? 0.0 : ay * px * std::pow(y, ay - 1) * pz / h;
-          gz[idx] = az == 0 ? 0.0 : az * px * py * std::pow(z, az - 1) / h;
+          gx[idx] = ax == 0 ? 0.0 : ax * X[ax - 1] * Y[ay] * Z[az] / h;
+          gy[idx] = ay == 0 ? 0.0 : ay * X[ax] * Y[ay - 1] * Z[az] / h;
+          gz[idx] = az == 0 ? 0.0 : az * X[ax] * Y[ay] * Z[az - 1] / h;
           ++idx;
         }
     for (int i = 0; i < dim; ++i) {
@@ -430,9 +440,15 @@ struct FaceBasis {
   void monos(V3 p, double* m) const {
     const V3 d = p - c;
     const double x = dot(d, t1) / h, y = dot(d, t2) / h;
+    double px[8], py[8];
+    px[0] = py[0] = 1.0;
+    for (int a = 1; a <= deg; ++a) {
+      px[a] = px[a - 1] * x;
+      py[a] = py[a - 1] * y;
+    }
     int idx = 0;
     for (int dd = 0; dd <= deg; ++dd)
-      for (int ay = 0; ay <= dd; ++ay) m[idx++] = std::pow(x, dd - ay) * std::pow(y, ay);
+      for (int ay = 0; ay <= dd; ++ay) m[idx++] = px[dd - ay] * py[ay];
   }
   void init(const Mesh& m, int f, const FaceRule& r, int degree) {
     deg = degree;
