@@ -112,6 +112,9 @@ int pscu_bsr_create(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow_ptr,
                     const int32_t* bcols, const double* vals, int mem, pscu_mat** out);
 /* 0 for CSR storage, else the block size. */
 int pscu_mat_block_size(const pscu_mat* m);
+/* The block pattern and values of a block-stored operator (host, nullable). */
+int pscu_bsr_download(pscu_ctx* ctx, const pscu_mat* m, int64_t* brow_ptr, int32_t* bcols,
+                      double* vals);
 /* CsrMatrix::multiply (csr.hpp:68-74): y = A x, per-row sequential sums. */
 int pscu_spmv(pscu_ctx* ctx, const pscu_mat* a, const double* x, double* y, int mem);
 

@@ -30,7 +30,7 @@ EXPORTS = [
     "pscu_condense_batch", "pscu_condense_assemble", "pscu_recover_batch", "pscu_bj_create",
     "pscu_bj_destroy", "pscu_bj_apply", "pscu_layout_make3", "pscu_bsr_create",
     "pscu_mat_block_size", "pscu_assembly_begin", "pscu_assembly_add", "pscu_assembly_rhs",
-    "pscu_solve_system_bsr",
+    "pscu_solve_system_bsr", "pscu_bsr_download",
 ]
 
 
@@ -124,6 +124,7 @@ def load(path: str = LIB):
     lib.pscu_layout_make3.argtypes = [i32, i32, i32, i32, i32, C.POINTER(Layout)]
     lib.pscu_bsr_create.argtypes = [vp, i64, i32, vp, vp, vp, i32, C.POINTER(vp)]
     lib.pscu_mat_block_size.argtypes = [vp]
+    lib.pscu_bsr_download.argtypes = [vp, vp, vp, vp, vp]
     lib.pscu_assembly_begin.argtypes = [vp, i64, i32, vp, vp, C.POINTER(vp)]
     lib.pscu_assembly_add.argtypes = [vp, vp, i32, i32, i32, vp, vp, i32, vp, vp, i32, vp, vp,
                                       vp, i32]

@@ -576,6 +576,20 @@ int pscu_bsr_create(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow_ptr,
 
 int pscu_mat_block_size(const pscu_mat* m) { return m->m.bs; }
 
+int pscu_bsr_download(pscu_ctx* ctx, const pscu_mat* m, int64_t* brow_ptr, int32_t* bcols,
+                      double* vals) {
+  return guard([&] {
+    const Csr& a = m->m;
+    if (!a.bs) throw Error(PSCU_EINVAL, "bsr_download: not a block-stored operator");
+    if (brow_ptr) std::memcpy(brow_ptr, a.h_brow_ptr.data(), sizeof(int64_t) * a.h_brow_ptr.size());
+    if (bcols) std::memcpy(bcols, a.h_bcols.data(), sizeof(int32_t) * a.h_bcols.size());
+    if (vals && a.nnz)
+      PSCU_CUDA(cudaMemcpyAsync(vals, a.vals.p, sizeof(double) * size_t(a.nnz),
+                                cudaMemcpyDeviceToHost, ctx->c.stream));
+    PSCU_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
 int pscu_assembly_begin(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow_ptr,
                         const int32_t* bcols, pscu_mat** out) {
   return guard([&] {

@@ -118,6 +118,25 @@ class CsrMatrix:
                                            vl.ctypes.data))
         return rp, cl, vl
 
+    @property
+    def block_size(self) -> int:
+        """0 for CSR storage, else the dense face-block size."""
+        return int(self.lib.pscu_mat_block_size(self.h))
+
+    def download_blocks(self):
+        """(brow_ptr, bcols, vals) of a block-stored operator, vals column-major per block."""
+        bs = self.block_size
+        if not bs:
+            raise ValueError("not a block-stored operator")
+        nb = self.n // bs
+        rp = np.zeros(nb + 1, np.int64)
+        N.check(self.lib.pscu_bsr_download(self.ctx.h, self.h, rp.ctypes.data, None, None))
+        cl = np.zeros(int(rp[-1]), np.int32)
+        vl = np.zeros(self.nnz)
+        N.check(self.lib.pscu_bsr_download(self.ctx.h, self.h, None, cl.ctypes.data,
+                                           vl.ctypes.data))
+        return rp, cl, vl
+
     def multiply(self, x) -> np.ndarray:
         """CsrMatrix::multiply (csr.hpp:68-79)."""
         x = _f64(x)

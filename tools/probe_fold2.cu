@@ -9,6 +9,7 @@
 //      subtractions (software pipelining)
 //  v3: plain dependent dsub chain from registers (lower bound)
 #include <cstdio>
+#include <cstring>
 constexpr int kRows = 16, kLen = 32, kN = kRows * kLen;
 
 __global__ void fold(const double2* g, long long* cyc, double* out, int variant) {
@@ -102,7 +103,9 @@ int main() {
     const int r = i / kLen, k = i % kLen;
     // the last entry of every row (but the first) reads the previous row
     const long long s = (k == kLen - 1 && r > 0) ? r - 1 : -1;
-    h[i] = make_double2(1e-3 * (i + 1), __longlong_as_double(s));
+    double sd;
+    memcpy(&sd, &s, 8);
+    h[i] = make_double2(1e-3 * (i + 1), sd);
   }
   cudaMemcpy(g, h, sizeof(h), cudaMemcpyHostToDevice);
   const char* nm[4] = {"v0 lane-0 smem fold", "v1 warp-uniform broadcast", "v2 pipelined broadcast",
