@@ -158,6 +158,8 @@ struct WalkPlan {
   mutable DevBuf<double> ybuf;
   mutable DevBuf<unsigned long long> barrier;  // persistent task-level kernel
   int persist_grid = 0;                        // its grid (0: per-level launches)
+  int flow_grid = 0;                           // dataflow sweep grid (0: off)
+  int64_t ny = 0;                              // rows of the sweep (sentinel fill)
 };
 
 struct Ilu {

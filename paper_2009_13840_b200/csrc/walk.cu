@@ -768,7 +768,31 @@ __global__ void wide_kernel(WalkArgs a, int ch, const double* rhs, double* y, do
 /// just computed). Same rounded operations as ilu0.hpp:53-65.
 constexpr int kLevelWarps = 4;
 
-template <bool kFwd, bool kPdl>
+/// Dataflow sweeps (level_flow_kernel): y starts filled with a signalling-NaN
+/// sentinel (arithmetic never produces it), every row's result is published
+/// by its 8-byte store and a reader of an out-of-task source spins until the
+/// value is no longer the sentinel — no grid barrier between task levels.
+constexpr unsigned long long kFlowSentinel = 0xFFF7DEADBEEF5A5Aull;
+
+__device__ __forceinline__ double flow_wait(const double* p) {
+  unsigned long long v;
+  do {
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  } while (v == kFlowSentinel);
+  return __longlong_as_double((long long)v);
+}
+
+__device__ __forceinline__ void flow_store(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+__global__ void fill_sentinel(int64_t n, double* y) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    y[i] = __longlong_as_double((long long)kFlowSentinel);
+}
+
+template <bool kFwd, bool kPdl, bool kFlow = false>
 __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const double* rhs, double* y,
                                             double* yb) {
   constexpr int kPer = kLevelMaxNz / 32;  // entries per lane
@@ -826,7 +850,9 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int e = lane + 32 * u;
-      yv[u] = (e < ne && sv[u] < 0 && sv[u] != kPadSrc) ? __ldcg(y + (-sv[u] - 1)) : 0.0;
+      const bool out = e < ne && sv[u] < 0 && sv[u] != kPadSrc;
+      if (kFlow) yv[u] = out ? flow_wait(y + (-sv[u] - 1)) : 0.0;
+      else yv[u] = out ? __ldcg(y + (-sv[u] - 1)) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
@@ -872,7 +898,8 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         }
         if (!kFwd) acc = __ddiv_rn(acc, dvb[w][r]);
         cv[w][r] = acc;
-        y[m.y] = acc;
+        if (kFlow) flow_store(y + m.y, acc);
+        else y[m.y] = acc;
         if (kFwd) yb[m.z] = acc;
       }
 #ifdef PSCU_TRACE
@@ -921,6 +948,17 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
     level_chunk<kFwd, false>(a, ch, rhs, y, yb);
     if (ch + 1 < c1) level_barrier(cnt, (unsigned long long)(ch - c0 + 1) * gridDim.x);
   }
+}
+
+/// All task levels of a level-plan sweep in one cooperative launch without
+/// barriers: every warp takes its tasks in level order and waits on the
+/// values of its out-of-task sources only (kFlowSentinel). Every task waits
+/// on tasks of strictly lower levels and all warps are co-resident, so the
+/// lowest unfinished level always progresses.
+template <bool kFwd>
+__global__ void __launch_bounds__(32 * kLevelWarps)
+    level_flow_kernel(WalkArgs a, int c0, int c1, const double* rhs, double* y, double* yb) {
+  for (int ch = c0; ch < c1; ++ch) level_chunk<kFwd, false, true>(a, ch, rhs, y, yb);
 }
 
 /// Values of the static out-of-ring sources of one walker launch.
@@ -1666,6 +1704,15 @@ static bool level_persist() {
   return v;
 }
 
+/// Dataflow (barrier-free) level-plan sweeps: PSCU_LEVEL_FLOW (default on).
+static bool level_flow() {
+  static const bool v = [] {
+    const char* e = getenv("PSCU_LEVEL_FLOW");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
+}
+
 void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   cudaStream_t st = c.stream;
   w.fwd = fwd;
@@ -1704,6 +1751,21 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
     const int want = (std::min(most, cap) + kLevelWarps - 1) / kLevelWarps;
     w.persist_grid = std::max(1, std::min(want, per_sm * sms));
     w.barrier.alloc(1);
+  }
+  w.flow_grid = 0;
+  w.ny = int64_t(h.pos.size());
+  if (h.levels && all_fit && level_flow()) {
+    int per_sm = 0, sms = 0, dev = 0;
+    PSCU_CUDA(cudaGetDevice(&dev));
+    PSCU_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    void* fn = fwd ? (void*)level_flow_kernel<true> : (void*)level_flow_kernel<false>;
+    PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kLevelWarps, 0));
+    int most = 0;
+    for (size_t s = 0; s < h.sl_nt.size(); ++s) most = std::max(most, h.sl_nt[s]);
+    const char* ge = getenv("PSCU_LEVEL_FLOW_WARPS");
+    const int cap = ge ? std::max(32, atoi(ge)) : 2048;
+    const int want = (std::min(most, cap) + kLevelWarps - 1) / kLevelWarps;
+    w.flow_grid = std::max(1, std::min(want, per_sm * sms));
   }
   w.flow = h.flow;
   w.S = h.S;
@@ -2065,6 +2127,17 @@ static void level_trace_report(Context& c, const WalkPlan& w) {
 static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y, double* yb) {
   WalkArgs a = args_of(w);
   a.trace = trace_buffer();
+  if (w.levels && w.flow_grid > 0 && !a.trace) {
+    fill_sentinel<<<grid1(w.ny), 256, 0, c.stream>>>(w.ny, y);
+    PSCU_LAUNCHED(&c);
+    int c0 = 0, c1 = w.nsub;
+    void* args[] = {&a, &c0, &c1, (void*)&rhs, (void*)&y, (void*)&yb};
+    void* fn = w.fwd ? (void*)level_flow_kernel<true> : (void*)level_flow_kernel<false>;
+    PSCU_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(w.flow_grid)), dim3(32 * kLevelWarps),
+                                          args, 0, c.stream));
+    PSCU_LAUNCHED(&c);
+    return;
+  }
   if (w.levels && w.persist_grid > 0 && !a.trace) {
     // every task level of the sweep in one cooperative launch
     PSCU_CUDA(cudaMemsetAsync(w.barrier.p, 0, sizeof(unsigned long long), c.stream));
@@ -2133,6 +2206,7 @@ void run_walk(Context& c, const WalkPlan& wf, const WalkPlan& wb, const double* 
     return e ? atoi(e) != 0 : true;
   }();
   if (graphs && (wf.levels || wb.levels) && wf.persist_grid == 0 && wb.persist_grid == 0 &&
+      wf.flow_grid == 0 && wb.flow_grid == 0 &&
       wf.segments.size() + wb.segments.size() > 16) {
     // hundreds of task-level launches: replay them as one captured graph on
     // fixed buffers (the launch rate no longer bounds the sweep)

@@ -476,10 +476,11 @@ def test_ilu0_factor_variants_bitwise(S, monkeypatch, thread_rows, ci):
 
 
 @pytest.mark.parametrize("pad", ["0", "1"])
-@pytest.mark.parametrize("persist", ["0", "1"])
-def test_ilu0_persistent_levels_bitwise(S, monkeypatch, pad, persist):
+@pytest.mark.parametrize("persist,flow", [("0", "0"), ("1", "0"), ("0", "1")])
+def test_ilu0_persistent_levels_bitwise(S, monkeypatch, pad, persist, flow):
     """Task-level plans swept by one cooperative launch per sweep (grid
-    barrier between task levels, PSCU_LEVEL_PERSIST) or per-level launches,
+    barrier between task levels, PSCU_LEVEL_PERSIST; or barrier-free
+    dataflow waits on the sources, PSCU_LEVEL_FLOW) or per-level launches,
     with and without the 8-entry row padding (PSCU_LEVEL_PAD, cached per
     process: a fresh process per variant); byte-level comparison."""
     import subprocess, sys, os
@@ -498,7 +499,7 @@ for c in [dict(mesh="unit-tri", n=12, jitter=0.2, seed=0, side="top", scheme="hh
 print("persistent ok")
 '''
     env = dict(os.environ, PSCU_LEVEL_PERSIST=persist, PSCU_WALK_MODE="levels",
-               PSCU_LEVEL_PERSIST_MIN_ROWS="0", PSCU_LEVEL_PAD=pad)
+               PSCU_LEVEL_PERSIST_MIN_ROWS="0", PSCU_LEVEL_PAD=pad, PSCU_LEVEL_FLOW=flow)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                        text=True, timeout=600)
