@@ -737,12 +737,25 @@ void build_local(const Mesh& mesh, int e, int k, double eta, const Data& data, d
         R[size_t(q) * ns + s] = a1 - a2;
       }
     }
-    for (int j = 0; j < ns; ++j)
-      for (int i = 0; i < ns; ++i) {
-        double acc = 0.0;
-        for (int q = 0; q < m; ++q) acc += R[size_t(q) * ns + i] * w[q] * R[size_t(q) * ns + j];
-        A(i, j) += acc / hf[lf];
+    {
+      // stabilisation R^T W R / h_F with q-contiguous operands (RT: ns x m)
+      std::vector<double> RT(size_t(ns) * m), WRT(size_t(ns) * m);
+      for (int q = 0; q < m; ++q)
+        for (int i = 0; i < ns; ++i) {
+          RT[size_t(i) * m + q] = R[size_t(q) * ns + i];
+          WRT[size_t(i) * m + q] = w[q] * R[size_t(q) * ns + i];
+        }
+      const double ih = 1.0 / hf[lf];
+      for (int j = 0; j < ns; ++j) {
+        const double* wj = &WRT[size_t(j) * m];
+        for (int i = 0; i < ns; ++i) {
+          const double* ri = &RT[size_t(i) * m];
+          double acc = 0.0;
+          for (int q = 0; q < m; ++q) acc += ri[q] * wj[q];
+          A(i, j) += acc * ih;
+        }
       }
+    }
     if (mesh.tag[fid[lf]] == 1) {
       const double* dnw = DNW[lf].data();
       for (int j = 0; j < ns; ++j)
