@@ -44,6 +44,14 @@ void psh_mesh_counts(const psh_mesh* m, int64_t* out);
 /* faces: 5 ints per face (a, b, left, right, tag 0 interior/1 Dirichlet/2 Neumann) */
 void psh_mesh_faces(const psh_mesh* m, int32_t* faces);
 void psh_mesh_vertices(const psh_mesh* m, double* xy);
+/* Wire formats, byte-compatible with the reference's writers: pmesh2 v1
+ * mesh files (write_mesh / read_mesh, mesh.hpp:535-645; nf = 0 lets the
+ * reader derive the faces) and the MatrixMarket coordinate export of a CSR
+ * operator (write_matrix_market, csr.hpp:98-111; 1-based, precision 17). */
+int psh_mesh_write(const psh_mesh* m, const char* path);
+int psh_mesh_read(const char* path, psh_mesh** out);
+int psh_write_matrix_market(int64_t n, const int64_t* row_ptr, const int32_t* cols,
+                            const double* vals, const char* path);
 
 /* Local blocks + layout + pattern (assemble_hho front end). scheme 0 hho-dp,
  * 1 hho-hp; strategy 0 uncond, 1 v-cond, 2 vp-cond; eta <= 0 selects the

@@ -138,6 +138,7 @@ void* ref_system_create(int mesh_kind, const char* family, int n, unsigned long 
 
 void ref_system_destroy(void* h) { delete static_cast<System*>(h); }
 
+
 long long ref_system_dim(void* h) { return static_cast<System*>(h)->sys.a.n; }
 long long ref_system_nnz(void* h) { return static_cast<System*>(h)->sys.a.nnz(); }
 double ref_system_t_assembly(void* h) { return static_cast<System*>(h)->sys.t_assembly; }

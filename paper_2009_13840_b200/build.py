@@ -104,6 +104,7 @@ def build_oracle(force: bool = False) -> None:
     targets = ["restatement"]
     if os.path.isdir("/root/reference/proj/include"):
         targets.append(os.path.join(oracle, "_ref", "libpstokes_ref.so"))
+        targets.append(os.path.join(oracle, "_ref", "wire_ref"))
         if os.path.exists(LIB):
             targets.append("dropin")  # links the solver library
     cmd = ["make", "-C", oracle, *targets]

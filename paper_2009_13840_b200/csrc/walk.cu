@@ -955,145 +955,10 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
 /// values of its out-of-task sources only (kFlowSentinel). Every task waits
 /// on tasks of strictly lower levels and all warps are co-resident, so the
 /// lowest unfinished level always progresses.
-///
-/// Each warp walks its task sequence (chunk by chunk, tasks gw, gw + W, ...)
-/// with the next task's static operands — task record, rows, entries,
-/// right-hand sides, diagonals — loaded while the current task waits on its
-/// sources and folds, so only the source values and the fold stay on the
-/// critical path of a dependency step. Same rounded operations as
-/// level_chunk (ilu0.hpp:53-65).
-struct FlowTask {
-  int ch = -1, task = 0, r0 = 0, nrows = 0, ne = 0, k0 = 0;
-  int sv[kLevelMaxNz / 32];
-  double v[kLevelMaxNz / 32];
-  int4 meta;     // lane < nrows: {len, row, backward position, 0}
-  double rb, dv; // lane < nrows: right-hand side, diagonal (backward)
-};
-
-template <bool kFwd>
-__device__ __forceinline__ bool flow_next(const WalkArgs& a, int nsub, int gw, int W, int& ch,
-                                          int& task) {
-  // next task of this warp: task + W in the same chunk, else gw in the next
-  // chunk that has that many tasks
-  task += W;
-  while (ch < nsub) {
-    const int nt = a.sl_hdr[kHdr * ch + 8];
-    if (task < nt) return true;
-    ++ch;
-    task = gw;
-  }
-  return false;
-}
-
-template <bool kFwd>
-__device__ __forceinline__ void flow_load(const WalkArgs& a, const double* rhs, int ch, int task,
-                                          int lane, FlowTask& t) {
-  constexpr int kPer = kLevelMaxNz / 32;
-  const int* hd = a.sl_hdr + kHdr * ch;
-  const int nq = hd[2];
-  const int32_t* tt = a.tt + hd[9];
-  const int32_t* tq = a.tq + hd[9];
-  t.ch = ch;
-  t.task = task;
-  t.k0 = a.sl_k[ch];
-  const int nr = a.sl_nr[ch];
-  t.r0 = tt[task];
-  t.nrows = tt[task + 1] - t.r0;
-  const int e0 = tq[task];
-  t.ne = tq[task + 1] - e0;
-  const int64_t qa = a.sl_q[ch] + e0;
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const int e = lane + 32 * u;
-    t.sv[u] = e < t.ne ? __ldg(a.src + qa + e) : 0;
-    t.v[u] = e < t.ne ? __ldg(a.val + qa + e) : 0.0;
-  }
-  if (lane < t.nrows) {
-    const int k = t.k0 + t.r0 + lane;
-    const int len = int((t.r0 + lane + 1 < nr ? a.off[k + 1] : nq) - a.off[k]);
-    t.meta = make_int4(len, a.rows[k], kFwd ? a.opos[k] : 0, 0);
-    t.dv = kFwd ? 1.0 : a.dv[k];
-    t.rb = __ldcg(rhs + k);
-  }
-}
-
 template <bool kFwd>
 __global__ void __launch_bounds__(32 * kLevelWarps)
     level_flow_kernel(WalkArgs a, int c0, int c1, const double* rhs, double* y, double* yb) {
-  constexpr int kPer = kLevelMaxNz / 32;
-  __shared__ double2 rec[kLevelWarps][kLevelMaxNz];
-  __shared__ double rbs[kLevelWarps][kLevelMaxRows], dvs[kLevelWarps][kLevelMaxRows],
-      cv[kLevelWarps][kLevelMaxRows];
-  __shared__ int4 mbs[kLevelWarps][kLevelMaxRows];
-  const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
-  const int gw = int(blockIdx.x) * kLevelWarps + w, W = int(gridDim.x) * kLevelWarps;
-  int ch = c0, task = gw - W;
-  if (!flow_next<kFwd>(a, c1, gw, W, ch, task)) return;
-  FlowTask cur, nxt;
-  flow_load<kFwd>(a, rhs, ch, task, lane, cur);
-  bool more = true;
-  while (more) {
-    int nch = ch, ntask = task;
-    more = flow_next<kFwd>(a, c1, gw, W, nch, ntask);
-    if (more) flow_load<kFwd>(a, rhs, nch, ntask, lane, nxt);  // in flight during this task
-    // sources outside the task: wait for their values, form the products
-    double yv[kPer];
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int e = lane + 32 * u;
-      const bool out = e < cur.ne && cur.sv[u] < 0 && cur.sv[u] != kPadSrc;
-      yv[u] = out ? flow_wait(y + (-cur.sv[u] - 1)) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int e = lane + 32 * u;
-      if (e < cur.ne)
-        rec[w][e] = make_double2(cur.sv[u] == kPadSrc ? 0.0
-                                                       : (cur.sv[u] < 0 ? dmul(cur.v[u], yv[u]) : cur.v[u]),
-                                 __longlong_as_double((long long)cur.sv[u]));
-    }
-    if (lane < cur.nrows) {
-      mbs[w][lane] = cur.meta;
-      rbs[w][lane] = cur.rb;
-      dvs[w][lane] = cur.dv;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      int e = 0;
-      for (int r = 0; r < cur.nrows; ++r) {
-        const int4 m = mbs[w][r];
-        double acc = rbs[w][r];
-        const int e1 = e + m.x;
-        for (; e + 8 <= e1; e += 8) {
-          int s8[8];
-          double p8[8], c8[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const double2 r2 = rec[w][e + k];
-            s8[k] = int(__double_as_longlong(r2.y));
-            p8[k] = r2.x;
-          }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) c8[k] = s8[k] < 0 ? 0.0 : cv[w][s8[k]];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc = dsub(acc, s8[k] < 0 ? p8[k] : dmul(p8[k], c8[k]));
-        }
-        for (; e < e1; ++e) {
-          const double2 r2 = rec[w][e];
-          const int sidx = int(__double_as_longlong(r2.y));
-          acc = dsub(acc, sidx < 0 ? r2.x : dmul(r2.x, cv[w][sidx]));
-        }
-        if (!kFwd) acc = __ddiv_rn(acc, dvs[w][r]);
-        cv[w][r] = acc;
-        flow_store(y + m.y, acc);
-        if (kFwd) yb[m.z] = acc;
-      }
-    }
-    __syncwarp();
-    ch = nch;
-    task = ntask;
-    cur = nxt;
-  }
+  for (int ch = c0; ch < c1; ++ch) level_chunk<kFwd, false, true>(a, ch, rhs, y, yb);
 }
 
 /// Values of the static out-of-ring sources of one walker launch.
@@ -1771,6 +1636,33 @@ int pick_cluster(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
   return (2 * nr <= 3 * int64_t(kStageRows) * cnt && nq <= int64_t(kMaxNz) * cnt) ? 4 : kMaxCluster;
 }
 
+/// Chain cap of a task-level plan: a dataflow / level step costs a fixed
+/// latency (~2.5 us: source loads, the value hand-over) plus the serial fold
+/// of its longest task (~26 cycles per entry), i.e. about 180 entries' worth
+/// per level. Short chains mean more levels, long ones longer folds; both
+/// caps are planned and the cheaper one kept (256^2 k=3: 16; 3D coarse
+/// face blocks: 4). PSCU_LEVEL_CHAIN_ROWS fixes the cap.
+Tasks level_tasks(const Csr& a, const std::vector<int64_t>& diag, bool fwd, Tasks* t16 = nullptr) {
+  if (getenv("PSCU_LEVEL_CHAIN_ROWS")) {
+    Tasks T = build_tasks(a, diag, fwd, level_chain_rows(), level_chain_nz(), level_pad());
+    if (t16) *t16 = T;
+    return T;
+  }
+  Tasks T4;
+  std::thread th([&] { T4 = build_tasks(a, diag, fwd, 4, level_chain_nz(), level_pad()); });
+  Tasks T16 = build_tasks(a, diag, fwd, 16, level_chain_nz(), level_pad());
+  th.join();
+  auto cost = [](const Tasks& T) {
+    std::vector<int64_t> mx(T.nlev, 0);
+    for (size_t t = 0; t < T.lvl.size(); ++t) mx[T.lvl[t]] = std::max<int64_t>(mx[T.lvl[t]], T.nz[t]);
+    int64_t c = 0;
+    for (int l = 0; l < T.nlev; ++l) c += 180 + mx[l];
+    return c;
+  };
+  if (t16) *t16 = T16;
+  return cost(T4) < cost(T16) ? T4 : T16;
+}
+
 HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
   HostPlan h;
   if (a.nnz >= (int64_t(1) << 31))
@@ -1786,8 +1678,9 @@ HostPlan plan(const Csr& a, const std::vector<int64_t>& diag, bool fwd) {
     // too much data per level for the rings: task-level launches. Narrow
     // ones (the coarse level, ~2 k rows per task level at 256^2): the push
     // walker on four CTAs (1.05 ms per 256^2 coarse apply; 1.01 ms on 8).
-    const Tasks T = build_tasks(a, diag, fwd, level_chain_rows(), level_chain_nz(), level_pad());
-    if (a.n >= int64_t(3000) * std::max(1, T.nlev)) {
+    Tasks T16;
+    const Tasks T = level_tasks(a, diag, fwd, &T16);
+    if (a.n >= int64_t(3000) * std::max(1, T16.nlev)) {
       plan_sweep(a, diag, fwd, 1, false, 0, level_chain_rows(), h, true, &T);
       return h;
     }

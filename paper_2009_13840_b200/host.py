@@ -45,6 +45,9 @@ def load():
             getattr(lib, f).argtypes = [vp]
         lib.psh_build_seconds.restype = C.c_double
         lib.psh_build_seconds.argtypes = [vp]
+        lib.psh_mesh_write.argtypes = [vp, C.c_char_p]
+        lib.psh_mesh_read.argtypes = [C.c_char_p, C.POINTER(vp)]
+        lib.psh_write_matrix_market.argtypes = [C.c_int64, vp, vp, vp, C.c_char_p]
         _lib = lib
     return _lib
 
@@ -83,6 +86,17 @@ class Mesh:
             self.lib.psh_mesh_destroy(self.h)
             self.h = None
 
+    @classmethod
+    def read(cls, path: str) -> "Mesh":
+        """read_mesh (mesh.hpp:562-645): pmesh2 v1 file, faces derived when nf = 0."""
+        h = C.c_void_p()
+        _check(load().psh_mesh_read(os.fsencode(path), C.byref(h)))
+        return cls(h)
+
+    def write(self, path: str) -> None:
+        """write_mesh (mesh.hpp:540-560), byte-compatible with the reference."""
+        _check(self.lib.psh_mesh_write(self.h, os.fsencode(path)))
+
     def faces(self) -> np.ndarray:
         f = np.zeros(5 * self.n_faces, np.int32)
         self.lib.psh_mesh_faces(self.h, f.ctypes.data)
@@ -92,6 +106,16 @@ class Mesh:
         v = np.zeros(2 * self.n_vertices)
         self.lib.psh_mesh_vertices(self.h, v.ctypes.data)
         return v.reshape(-1, 2)
+
+
+def write_matrix_market(row_ptr, cols, vals, path: str) -> None:
+    """write_matrix_market (csr.hpp:98-111): 1-based coordinate triplets at
+    precision 17, byte-compatible with the reference's export."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    cl = np.ascontiguousarray(cols, np.int32)
+    vl = np.ascontiguousarray(vals, np.float64)
+    _check(load().psh_write_matrix_market(len(rp) - 1, rp.ctypes.data, cl.ctypes.data,
+                                          vl.ctypes.data, os.fsencode(path)))
 
 
 def _view(ptr, dtype, count):

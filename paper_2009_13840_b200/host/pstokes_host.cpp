@@ -18,6 +18,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -97,6 +99,38 @@ struct Mesh {
     }
     for (auto& f : faces)
       if (f.right < 0) f.tag = 1;
+    measures();
+  }
+
+  /// Element-face links of an explicit face list (mesh.hpp:121-142; the
+  /// reader's finalize_with_faces), then the measures.
+  void finalize_with_faces() {
+    std::unordered_map<uint64_t, int> byedge;
+    byedge.reserve(faces.size() * 2);
+    for (int f = 0; f < nfaces(); ++f) {
+      const int a = faces[f].a, b = faces[f].b;
+      byedge.emplace((uint64_t(uint32_t(std::min(a, b))) << 32) | uint32_t(std::max(a, b)), f);
+    }
+    efac.assign(loop.size(), -1);
+    esgn.assign(loop.size(), 0);
+    for (int e = 0; e < nelem(); ++e) {
+      const int n = nv_of(e);
+      for (int i = 0; i < n; ++i) {
+        const int a = loop[eoff[e] + i], b = loop[eoff[e] + (i + 1) % n];
+        auto it = byedge.find((uint64_t(uint32_t(std::min(a, b))) << 32) | uint32_t(std::max(a, b)));
+        if (it == byedge.end()) throw std::runtime_error("mesh: element edge without a face record");
+        const FaceRec& f = faces[it->second];
+        const int sign = f.left == e ? 1 : -1;
+        if (sign < 0 && f.right != e)
+          throw std::runtime_error("mesh: face incidence does not match element loop");
+        efac[eoff[e] + i] = it->second;
+        esgn[eoff[e] + i] = sign;
+      }
+    }
+    measures();
+  }
+
+  void measures() {
     // measures (mesh.hpp:144-173)
     const int ne = nelem();
     area.assign(ne, 0.0);
@@ -900,6 +934,124 @@ void psh_mesh_faces(const psh_mesh* m, int32_t* faces) {
     faces[5 * f + 3] = r.right;
     faces[5 * f + 4] = r.tag;
   }
+}
+
+// ---------------------------------------------------------------------------
+// wire formats: MatrixMarket coordinate export (csr.hpp:98-111) and the
+// pmesh2 v1 mesh file (mesh.hpp:535-645), byte-compatible with the
+// reference's writers (same iostream formatting, precision 17)
+// ---------------------------------------------------------------------------
+
+int psh_write_matrix_market(int64_t n, const int64_t* row_ptr, const int32_t* cols,
+                            const double* vals, const char* path) {
+  return guard([&] {
+    std::ofstream os(path);
+    if (!os) throw std::runtime_error(std::string("write_matrix_market: cannot open '") + path + "'");
+    os << "%%MatrixMarket matrix coordinate real general\n";
+    os << n << ' ' << n << ' ' << row_ptr[n] << '\n';
+    os.precision(17);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+        os << i + 1 << ' ' << cols[p] + 1 << ' ' << vals[p] << '\n';
+    if (!os) throw std::runtime_error("write_matrix_market: write failed");
+  });
+}
+
+int psh_mesh_write(const psh_mesh* pm, const char* path) {
+  return guard([&] {
+    const Mesh& m = pm->m;
+    std::ofstream os(path);
+    if (!os) throw std::runtime_error(std::string("write_mesh: cannot open '") + path + "'");
+    os.precision(17);
+    os << "pmesh2 v1 " << m.v.size() << ' ' << m.nelem() << ' ' << m.nfaces() << '\n';
+    for (const P2& p : m.v) os << "v " << p.x << ' ' << p.y << '\n';
+    for (int e = 0; e < m.nelem(); ++e) {
+      os << 'e';
+      for (int i = m.eoff[e]; i < m.eoff[e + 1]; ++i) os << ' ' << m.loop[i];
+      os << '\n';
+    }
+    for (const FaceRec& f : m.faces)
+      os << "f " << f.a << ' ' << f.b << ' ' << f.left << ' ' << f.right << ' '
+         << (f.tag == 0 ? 'i' : (f.tag == 1 ? 'd' : 'n')) << '\n';
+  });
+}
+
+int psh_mesh_read(const char* path, psh_mesh** out) {
+  return guard([&] {
+    std::ifstream is(path);
+    if (!is) throw std::runtime_error(std::string("read_mesh: cannot open '") + path + "'");
+    auto fail = [](int line, const std::string& what) {
+      throw std::runtime_error("read_mesh: line " + std::to_string(line) + ": " + what);
+    };
+    std::string line;
+    int lineno = 0;
+    if (!std::getline(is, line)) fail(1, "empty file");
+    ++lineno;
+    std::istringstream hs(line);
+    std::string magic, version;
+    int nv = 0, ne = 0, nf = 0;
+    if (!(hs >> magic >> version >> nv >> ne >> nf) || magic != "pmesh2" || version != "v1")
+      fail(lineno, "malformed header, expected 'pmesh2 v1 <nv> <ne> <nf>'");
+    if (ne == 0) fail(lineno, "no elements");
+    auto next_record = [&](char want) -> std::istringstream {
+      while (std::getline(is, line)) {
+        ++lineno;
+        if (line.empty() || line[0] == '#') continue;
+        std::istringstream ls(line);
+        std::string kind;
+        ls >> kind;
+        if (kind.size() != 1 || kind[0] != want)
+          fail(lineno, std::string("expected a '") + want + "' record");
+        return ls;
+      }
+      fail(lineno + 1, std::string("unexpected end of file, wanted a '") + want + "' record");
+      return std::istringstream();
+    };
+    auto pm = std::make_unique<psh_mesh>();
+    Mesh& m = pm->m;
+    for (int i = 0; i < nv; ++i) {
+      auto ls = next_record('v');
+      double x, y;
+      if (!(ls >> x >> y)) fail(lineno, "malformed vertex");
+      m.v.push_back({x, y});
+    }
+    for (int i = 0; i < ne; ++i) {
+      auto ls = next_record('e');
+      int v, cnt = 0;
+      while (ls >> v) {
+        if (v < 0 || v >= nv) fail(lineno, "vertex index " + std::to_string(v) + " out of range");
+        m.loop.push_back(v);
+        ++cnt;
+      }
+      if (cnt < 3) fail(lineno, "element with fewer than 3 vertices");
+      m.eoff.push_back(int(m.loop.size()));
+    }
+    if (nf == 0) {
+      m.finalize();
+      *out = pm.release();
+      return;
+    }
+    for (int i = 0; i < nf; ++i) {
+      auto ls = next_record('f');
+      FaceRec f{};
+      std::string tag;
+      if (!(ls >> f.a >> f.b >> f.left >> f.right >> tag)) fail(lineno, "malformed face");
+      if (f.a < 0 || f.a >= nv || f.b < 0 || f.b >= nv) fail(lineno, "face vertex out of range");
+      if (f.left < 0 || f.left >= ne)
+        fail(lineno, "face references element " + std::to_string(f.left) + " of " + std::to_string(ne));
+      if (f.right >= ne)
+        fail(lineno, "face references element " + std::to_string(f.right) + " of " + std::to_string(ne));
+      if (tag == "i") f.tag = 0;
+      else if (tag == "d") f.tag = 1;
+      else if (tag == "n") f.tag = 2;
+      else fail(lineno, "unknown face tag '" + tag + "'");
+      if (f.right < 0 && f.tag == 0) fail(lineno, "boundary face tagged interior");
+      if (f.right >= 0 && f.tag != 0) fail(lineno, "interior face carries a boundary tag");
+      m.faces.push_back(f);
+    }
+    m.finalize_with_faces();
+    *out = pm.release();
+  });
 }
 
 void psh_mesh_vertices(const psh_mesh* m, double* xy) {

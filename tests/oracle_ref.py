@@ -598,3 +598,33 @@ class PortHierarchy:
                           C.byref(rel), C.byref(conv))
         return dict(x=x, hist=hist[: its.value].copy(), its=its.value, coarse_its=cits.value,
                     vcycles=vcs.value, rel=rel.value, converged=bool(conv.value))
+
+
+WIRE = os.path.join(ROOT, "oracle", "_ref", "wire_ref")
+_KIND = {"family": 0, "unit-quad": 1, "unit-tri": 2}
+
+
+def _wire(*args):
+    import subprocess
+    r = subprocess.run([WIRE, *[str(a) for a in args]], capture_output=True, text=True)
+    if r.returncode:
+        raise RuntimeError(r.stderr.strip())
+    return r.stdout
+
+
+def ref_write_mesh(path, kind="family", family="trapz", n=2, jitter=0.0, side="right"):
+    """The reference's write_mesh of the mesh RefSystem would build."""
+    _wire("mesh", _KIND[kind], family, n, jitter, SIDES[side], path)
+
+
+def ref_write_matrix_market(path, kind="family", family="trapz", n=2, jitter=0.0, side="right",
+                            scheme="hho-dp", strategy="v-cond", k=1):
+    """The reference's write_matrix_market of the operator assembled with the
+    exp manufactured data (the pattern and values of RefSystem(data='exp'))."""
+    _wire("mtx", _KIND[kind], family, n, jitter, SIDES[side], SCHEMES[scheme],
+          STRATEGIES[strategy], k, path)
+
+
+def ref_mesh_roundtrip(src: str, dst: str):
+    """The reference's read_mesh then write_mesh; returns (nv, ne, nf)."""
+    return tuple(int(v) for v in _wire("roundtrip", src, dst).split())
