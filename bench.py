@@ -570,7 +570,7 @@ def main():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="config2a", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="config5", choices=sorted(CONFIGS))
     ap.add_argument("--n", type=int, default=0, help="override the mesh size (testing)")
     ap.add_argument("--ref-sample-n", type=int, default=0,
                     help="mesh size of the reference / cpu_baseline sample (default per config)")

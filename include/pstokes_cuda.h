@@ -218,6 +218,10 @@ int pscu_assembly_add(pscu_ctx* ctx, pscu_mat* m, int e0, int nelem, int n, cons
                       int nfe, const int32_t* keep_pos, double* elim_coupling, double* elim_rhs,
                       int mem);
 int pscu_assembly_rhs(pscu_ctx* ctx, const pscu_mat* m, double* rhs, int mem);
+/* Page-locked host staging buffers (cudaHostAlloc): producers write local
+ * blocks there so the batch uploads run at full PCIe/C2C bandwidth. */
+int pscu_host_alloc(int64_t bytes, void** out);
+int pscu_host_free(void* p);
 /* pscu_solve_system on a face-block operator (host buffers, copies timed). */
 int pscu_solve_system_bsr(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow_ptr,
                           const int32_t* bcols, const double* vals, const double* rhs,

@@ -30,7 +30,7 @@ EXPORTS = [
     "pscu_condense_batch", "pscu_condense_assemble", "pscu_recover_batch", "pscu_bj_create",
     "pscu_bj_destroy", "pscu_bj_apply", "pscu_layout_make3", "pscu_bsr_create",
     "pscu_mat_block_size", "pscu_assembly_begin", "pscu_assembly_add", "pscu_assembly_rhs",
-    "pscu_solve_system_bsr", "pscu_bsr_download",
+    "pscu_solve_system_bsr", "pscu_bsr_download", "pscu_host_alloc", "pscu_host_free",
 ]
 
 
@@ -125,6 +125,8 @@ def load(path: str = LIB):
     lib.pscu_bsr_create.argtypes = [vp, i64, i32, vp, vp, vp, i32, C.POINTER(vp)]
     lib.pscu_mat_block_size.argtypes = [vp]
     lib.pscu_bsr_download.argtypes = [vp, vp, vp, vp, vp]
+    lib.pscu_host_alloc.argtypes = [i64, C.POINTER(vp)]
+    lib.pscu_host_free.argtypes = [vp]
     lib.pscu_assembly_begin.argtypes = [vp, i64, i32, vp, vp, C.POINTER(vp)]
     lib.pscu_assembly_add.argtypes = [vp, vp, i32, i32, i32, vp, vp, i32, vp, vp, i32, vp, vp,
                                       vp, i32]
@@ -151,3 +153,21 @@ def ptr(a) -> int | None:
     if isinstance(a, np.ndarray):
         return a.ctypes.data
     return a.data_ptr()
+
+
+class PinnedArray:
+    """A page-locked host float64 array (pscu_host_alloc) viewed as numpy."""
+
+    def __init__(self, count: int):
+        self.lib = load()
+        p = C.c_void_p()
+        check(self.lib.pscu_host_alloc(8 * max(count, 1), C.byref(p)))
+        self.p = p
+        buf = (C.c_double * max(count, 1)).from_address(p.value)
+        self.a = np.frombuffer(buf, dtype=np.float64, count=count)
+
+    def __del__(self):
+        if getattr(self, "p", None):
+            self.a = None
+            self.lib.pscu_host_free(self.p)
+            self.p = None

@@ -629,6 +629,19 @@ int pscu_assembly_add(pscu_ctx* ctx, pscu_mat* m, int e0, int nelem, int n, cons
   });
 }
 
+int pscu_host_alloc(int64_t bytes, void** out) {
+  return guard([&] {
+    *out = nullptr;
+    PSCU_CUDA(cudaHostAlloc(out, size_t(std::max<int64_t>(bytes, 8)), cudaHostAllocDefault));
+  });
+}
+
+int pscu_host_free(void* p) {
+  return guard([&] {
+    if (p) PSCU_CUDA(cudaFreeHost(p));
+  });
+}
+
 int pscu_assembly_rhs(pscu_ctx* ctx, const pscu_mat* m, double* rhs, int mem) {
   return guard([&] {
     if (!m->rhs_acc.p) throw Error(PSCU_EINVAL, "assembly_rhs: not an assembly target");

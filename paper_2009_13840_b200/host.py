@@ -341,19 +341,43 @@ def assemble_stokes3(mesh: Mesh3, k: int, data: str = "random", seed: int = 0, e
     keep_pos = np.ascontiguousarray(L.keep_pos, np.int32)
     n = L.n_local
     nb = min(batch, mesh.n_elements)
-    bufs = [(np.empty(nb * n * n), np.empty(nb * n)) for _ in range(2)]
+    # page-locked double buffer: the host builds batch i + 1 while the device
+    # condenses and scatters batch i
+    pinned = [(N.PinnedArray(nb * n * n), N.PinnedArray(nb * n)) for _ in range(2)]
+    bufs = [(pm.a, pr.a) for pm, pr in pinned]
     coup = erhs = None
     if recovery:
         coup = np.empty((mesh.n_elements, L.n_elim, L.n_keep))
         erhs = np.empty((mesh.n_elements, L.n_elim))
+    import threading
     import time
-    t_host = t_dev = 0.0
-    for i, e0 in enumerate(range(0, mesh.n_elements, nb)):
+    starts = list(range(0, mesh.n_elements, nb))
+    t_host = 0.0
+    t_dev = 0.0
+    err = []
+
+    def build(i):
+        nonlocal t_host
+        e0 = starts[i]
+        e1 = min(mesh.n_elements, e0 + nb)
+        t0 = time.perf_counter()
+        try:
+            L.local_blocks(mesh, e0, e1, data=data, seed=seed, eta=eta, nthreads=nthreads,
+                           out=bufs[i % 2])
+        except Exception as ex:  # surfaced in the main thread
+            err.append(ex)
+        t_host += time.perf_counter() - t0
+
+    build(0)
+    for i, e0 in enumerate(starts):
+        if err:
+            raise err[0]
         e1 = min(mesh.n_elements, e0 + nb)
         mats, rhs = bufs[i % 2]
-        t0 = time.perf_counter()
-        L.local_blocks(mesh, e0, e1, data=data, seed=seed, eta=eta, nthreads=nthreads,
-                       out=(mats, rhs))
+        worker = None
+        if i + 1 < len(starts):
+            worker = threading.Thread(target=build, args=(i + 1,))
+            worker.start()
         t1 = time.perf_counter()
         efb = np.ascontiguousarray(ef[e0:e1], np.int32)
         cp = ep = None
@@ -369,8 +393,12 @@ def assemble_stokes3(mesh: Mesh3, k: int, data: str = "random", seed: int = 0, e
             # column-major ne x nk blocks -> (ne, nk)
             coup[e0:e1] = np.transpose(cp.reshape(e1 - e0, L.n_keep, L.n_elim), (0, 2, 1))
             erhs[e0:e1] = ep.reshape(e1 - e0, L.n_elim)
-        t_host += t1 - t0
         t_dev += time.perf_counter() - t1
+        if worker is not None:
+            worker.join()
+    if err:
+        raise err[0]
+    del bufs, pinned
     b = np.zeros(A.n)
     N.check(ctx.lib.pscu_assembly_rhs(ctx.h, A.h, b.ctypes.data, N.PSCU_HOST))
     lay = S.make_layout3(k, mesh.n_faces, mesh.n_elements)

@@ -229,9 +229,13 @@ def test_golden_iterations_lu_coarse(S):
         h = S.LevelHierarchy(m, _layout(S, s), S.LevelConfig(degrees=[3, 2, 1], coarse="lu"))
         x, hist, rep = h.solve(s.rhs())
         assert rep.converged and rep.outer_its == its == r["its"]
-        # 1e-9 relative, with a floor at 1e-13 of ||b|| where the estimates
-        # reach roundoff (the two coarse LUs round differently)
-        assert np.all(np.abs(hist - r["hist"]) <= 1e-9 * np.abs(r["hist"]) + 1e-13)
+        # 1e-9 relative wherever the estimate is above 1e-10 of ||b||; the
+        # last entries sit at roundoff (rtol 1e-13) where the dense device LU
+        # and the reference's sparse LU round differently: 1e-3 relative there
+        ref_h = np.asarray(r["hist"])
+        rel = np.abs(hist - ref_h) / np.abs(ref_h)
+        big = ref_h >= 1e-10
+        assert np.all(rel[big] <= 1e-9) and np.all(rel[~big] <= 1e-3), rel
         assert rel_close(x, r["x"], 1e-9)
 
 
