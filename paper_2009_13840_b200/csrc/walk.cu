@@ -961,6 +961,156 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
   for (int ch = c0; ch < c1; ++ch) level_chunk<kFwd, false, true>(a, ch, rhs, y, yb);
 }
 
+/// The same with a two-stage software pipeline over the warp's task
+/// sequence (PSCU_LEVEL_FLOW=2): the record of task t+2 and the entries,
+/// row data and right-hand sides of task t+1 (whose record arrived one task
+/// earlier) are in flight while task t waits on its sources and folds, so
+/// the dependent record -> entries round trips leave the critical path.
+struct FlowRec {
+  int ch, task, r0, nrows, e0, ne;
+};
+
+__device__ __forceinline__ bool flow_advance(const WalkArgs& a, int c1, int gw, int W, int& ch,
+                                             int& task) {
+  task += W;
+  while (ch < c1) {
+    if (task < a.sl_hdr[kHdr * ch + 8]) return true;
+    ++ch;
+    task = gw;
+  }
+  return false;
+}
+
+__device__ __forceinline__ FlowRec flow_record(const WalkArgs& a, int ch, int task) {
+  const int* hd = a.sl_hdr + kHdr * ch;
+  const int32_t* tt = a.tt + hd[9];
+  const int32_t* tq = a.tq + hd[9];
+  FlowRec r;
+  r.ch = ch;
+  r.task = task;
+  r.r0 = tt[task];
+  r.nrows = tt[task + 1] - r.r0;
+  r.e0 = tq[task];
+  r.ne = tq[task + 1] - r.e0;
+  return r;
+}
+
+struct FlowOps {
+  int sv[kLevelMaxNz / 32];
+  double v[kLevelMaxNz / 32];
+  int4 meta;
+  double rb, dv;
+};
+
+template <bool kFwd>
+__device__ __forceinline__ void flow_ops(const WalkArgs& a, const double* rhs, const FlowRec& r,
+                                         int lane, FlowOps& o) {
+  constexpr int kPer = kLevelMaxNz / 32;
+  const int k0 = a.sl_k[r.ch], nr = a.sl_nr[r.ch], nq = a.sl_hdr[kHdr * r.ch + 2];
+  const int64_t qa = a.sl_q[r.ch] + r.e0;
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int e = lane + 32 * u;
+    o.sv[u] = e < r.ne ? __ldg(a.src + qa + e) : 0;
+    o.v[u] = e < r.ne ? __ldg(a.val + qa + e) : 0.0;
+  }
+  if (lane < r.nrows) {
+    const int k = k0 + r.r0 + lane;
+    const int len = int((r.r0 + lane + 1 < nr ? a.off[k + 1] : nq) - a.off[k]);
+    o.meta = make_int4(len, a.rows[k], kFwd ? a.opos[k] : 0, 0);
+    o.dv = kFwd ? 1.0 : a.dv[k];
+    o.rb = __ldcg(rhs + k);
+  }
+}
+
+template <bool kFwd>
+__global__ void __launch_bounds__(32 * kLevelWarps)
+    level_flow2_kernel(WalkArgs a, int c0, int c1, const double* rhs, double* y, double* yb) {
+  constexpr int kPer = kLevelMaxNz / 32;
+  __shared__ double2 rec[kLevelWarps][kLevelMaxNz];
+  __shared__ double rbs[kLevelWarps][kLevelMaxRows], dvs[kLevelWarps][kLevelMaxRows],
+      cv[kLevelWarps][kLevelMaxRows];
+  __shared__ int4 mbs[kLevelWarps][kLevelMaxRows];
+  const int w = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+  const int gw = int(blockIdx.x) * kLevelWarps + w, W = int(gridDim.x) * kLevelWarps;
+  // pipeline: r_cur / o_cur (task t), r_nxt / o_nxt (t+1), r_far (t+2)
+  int ch = c0, task = gw - W;
+  if (!flow_advance(a, c1, gw, W, ch, task)) return;
+  FlowRec r_cur = flow_record(a, ch, task);
+  FlowOps o_cur, o_nxt;
+  flow_ops<kFwd>(a, rhs, r_cur, lane, o_cur);
+  bool has_nxt = flow_advance(a, c1, gw, W, ch, task);
+  FlowRec r_nxt = has_nxt ? flow_record(a, ch, task) : r_cur;
+  for (;;) {
+    // stage 2 for t+1 and stage 1 for t+2, issued before task t's waits
+    bool has_far = false;
+    FlowRec r_far = r_nxt;
+    if (has_nxt) {
+      flow_ops<kFwd>(a, rhs, r_nxt, lane, o_nxt);
+      has_far = flow_advance(a, c1, gw, W, ch, task);
+      if (has_far) r_far = flow_record(a, ch, task);
+    }
+    double yv[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = lane + 32 * u;
+      const bool out = e < r_cur.ne && o_cur.sv[u] < 0 && o_cur.sv[u] != kPadSrc;
+      yv[u] = out ? flow_wait(y + (-o_cur.sv[u] - 1)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = lane + 32 * u;
+      if (e < r_cur.ne)
+        rec[w][e] = make_double2(
+            o_cur.sv[u] == kPadSrc ? 0.0 : (o_cur.sv[u] < 0 ? dmul(o_cur.v[u], yv[u]) : o_cur.v[u]),
+            __longlong_as_double((long long)o_cur.sv[u]));
+    }
+    if (lane < r_cur.nrows) {
+      mbs[w][lane] = o_cur.meta;
+      rbs[w][lane] = o_cur.rb;
+      dvs[w][lane] = o_cur.dv;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      int e = 0;
+      for (int r = 0; r < r_cur.nrows; ++r) {
+        const int4 m = mbs[w][r];
+        double acc = rbs[w][r];
+        const int e1 = e + m.x;
+        for (; e + 8 <= e1; e += 8) {
+          int s8[8];
+          double p8[8], c8[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const double2 r2 = rec[w][e + k];
+            s8[k] = int(__double_as_longlong(r2.y));
+            p8[k] = r2.x;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) c8[k] = s8[k] < 0 ? 0.0 : cv[w][s8[k]];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc = dsub(acc, s8[k] < 0 ? p8[k] : dmul(p8[k], c8[k]));
+        }
+        for (; e < e1; ++e) {
+          const double2 r2 = rec[w][e];
+          const int sidx = int(__double_as_longlong(r2.y));
+          acc = dsub(acc, sidx < 0 ? r2.x : dmul(r2.x, cv[w][sidx]));
+        }
+        if (!kFwd) acc = __ddiv_rn(acc, dvs[w][r]);
+        cv[w][r] = acc;
+        flow_store(y + m.y, acc);
+        if (kFwd) yb[m.z] = acc;
+      }
+    }
+    __syncwarp();
+    if (!has_nxt) break;
+    r_cur = r_nxt;
+    o_cur = o_nxt;
+    has_nxt = has_far;
+    r_nxt = r_far;
+  }
+}
+
 /// Values of the static out-of-ring sources of one walker launch.
 __global__ void gather_static(int64_t m, const int2* __restrict__ sfar, const double* __restrict__ y,
                               double* __restrict__ sfv) {
@@ -1786,7 +1936,10 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
     int per_sm = 0, sms = 0, dev = 0;
     PSCU_CUDA(cudaGetDevice(&dev));
     PSCU_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    void* fn = fwd ? (void*)level_flow_kernel<true> : (void*)level_flow_kernel<false>;
+    const char* fe = getenv("PSCU_LEVEL_FLOW");
+    const bool v2 = fe && atoi(fe) == 2;
+    void* fn = v2 ? (fwd ? (void*)level_flow2_kernel<true> : (void*)level_flow2_kernel<false>)
+                  : (fwd ? (void*)level_flow_kernel<true> : (void*)level_flow_kernel<false>);
     PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kLevelWarps, 0));
     int most = 0;
     for (size_t s = 0; s < h.sl_nt.size(); ++s) most = std::max(most, h.sl_nt[s]);
@@ -2160,7 +2313,12 @@ static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y,
     PSCU_LAUNCHED(&c);
     int c0 = 0, c1 = w.nsub;
     void* args[] = {&a, &c0, &c1, (void*)&rhs, (void*)&y, (void*)&yb};
-    void* fn = w.fwd ? (void*)level_flow_kernel<true> : (void*)level_flow_kernel<false>;
+    static const bool v2 = [] {
+      const char* e = getenv("PSCU_LEVEL_FLOW");
+      return e && atoi(e) == 2;
+    }();
+    void* fn = v2 ? (w.fwd ? (void*)level_flow2_kernel<true> : (void*)level_flow2_kernel<false>)
+                  : (w.fwd ? (void*)level_flow_kernel<true> : (void*)level_flow_kernel<false>);
     PSCU_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(w.flow_grid)), dim3(32 * kLevelWarps),
                                           args, 0, c.stream));
     PSCU_LAUNCHED(&c);

@@ -480,7 +480,7 @@ def test_ilu0_factor_variants_bitwise(S, monkeypatch, thread_rows, ci):
 
 
 @pytest.mark.parametrize("pad", ["0", "1"])
-@pytest.mark.parametrize("persist,flow", [("0", "0"), ("1", "0"), ("0", "1")])
+@pytest.mark.parametrize("persist,flow", [("0", "0"), ("1", "0"), ("0", "1"), ("0", "2")])
 def test_ilu0_persistent_levels_bitwise(S, monkeypatch, pad, persist, flow):
     """Task-level plans swept by one cooperative launch per sweep (grid
     barrier between task levels, PSCU_LEVEL_PERSIST; or barrier-free
