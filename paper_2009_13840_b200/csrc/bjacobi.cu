@@ -33,37 +33,42 @@ __global__ void bj_factor_kernel(int64_t nb, int bs, int64_t s0, int64_t b0,
                                  const double* __restrict__ vals, double* __restrict__ inv,
                                  double* __restrict__ work, int* __restrict__ perm_ws,
                                  unsigned long long* __restrict__ bad) {
+  // scratch is element-major, block-minor (entry (i, j) of block b at
+  // (i bs + j) nb + b): the threads of a warp (consecutive blocks) touch
+  // consecutive addresses at every step of their identical loops
   for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < nb;
        b += int64_t(gridDim.x) * blockDim.x) {
     const int64_t s = s0 + b * bs;
-    double* d = work + b * bs * bs;  // row-major
-    double* y = work + nb * bs * bs + b * bs;
-    int* perm = perm_ws + b * bs;
+#define D(i, j) work[(int64_t(i) * bs + (j)) * nb + b]
+#define Y(i) work[nb * bs * bs + int64_t(i) * nb + b]
+#define PERM(i) perm_ws[int64_t(i) * nb + b]
     double* out = inv + b * bs * bs;  // column-major
     if (kBsr) {
       int64_t q = rp[b];
       while (q < rp[b + 1] && cols[q] != b) ++q;
       const double* blk = vals + q * bs * bs;
       for (int i = 0; i < bs; ++i)
-        for (int c = 0; c < bs; ++c) d[i * bs + c] = q < rp[b + 1] ? blk[c * bs + i] : 0.0;
+        for (int c = 0; c < bs; ++c) D(i, c) = q < rp[b + 1] ? blk[c * bs + i] : 0.0;
     } else {
-      for (int i = 0; i < bs * bs; ++i) d[i] = 0.0;
+      for (int i = 0; i < bs; ++i)
+        for (int c = 0; c < bs; ++c) D(i, c) = 0.0;
       for (int i = 0; i < bs; ++i)
         for (int64_t q = rp[s + i]; q < rp[s + i + 1]; ++q) {
           const int64_t c = cols[q];
-          if (c >= s && c < s + bs) d[i * bs + (c - s)] = vals[q];
+          if (c >= s && c < s + bs) D(i, c - s) = vals[q];
         }
     }
     double amax = 0.0;
-    for (int i = 0; i < bs * bs; ++i) amax = fmax(amax, fabs(d[i]));
-    for (int i = 0; i < bs; ++i) perm[i] = i;
+    for (int i = 0; i < bs; ++i)
+      for (int j = 0; j < bs; ++j) amax = fmax(amax, fabs(D(i, j)));
+    for (int i = 0; i < bs; ++i) PERM(i) = i;
     bool ok = true;
     for (int k = 0; k < bs && ok; ++k) {
       int p = k;
-      double m = fabs(d[k * bs + k]);
+      double m = fabs(D(k, k));
       for (int i = k + 1; i < bs; ++i)
-        if (fabs(d[i * bs + k]) > m) {
-          m = fabs(d[i * bs + k]);
+        if (fabs(D(i, k)) > m) {
+          m = fabs(D(i, k));
           p = i;
         }
       if (!(m > dmul(1e-14, amax))) {
@@ -72,18 +77,18 @@ __global__ void bj_factor_kernel(int64_t nb, int bs, int64_t s0, int64_t b0,
       }
       if (p != k) {
         for (int j = 0; j < bs; ++j) {
-          const double t = d[k * bs + j];
-          d[k * bs + j] = d[p * bs + j];
-          d[p * bs + j] = t;
+          const double t = D(k, j);
+          D(k, j) = D(p, j);
+          D(p, j) = t;
         }
-        const int t = perm[k];
-        perm[k] = perm[p];
-        perm[p] = t;
+        const int t = PERM(k);
+        PERM(k) = PERM(p);
+        PERM(p) = t;
       }
       for (int i = k + 1; i < bs; ++i) {
-        const double f = __ddiv_rn(d[i * bs + k], d[k * bs + k]);
-        d[i * bs + k] = f;
-        for (int j = k + 1; j < bs; ++j) d[i * bs + j] = dsub(d[i * bs + j], dmul(f, d[k * bs + j]));
+        const double f = __ddiv_rn(D(i, k), D(k, k));
+        D(i, k) = f;
+        for (int j = k + 1; j < bs; ++j) D(i, j) = dsub(D(i, j), dmul(f, D(k, j)));
       }
     }
     if (!ok) {
@@ -92,17 +97,20 @@ __global__ void bj_factor_kernel(int64_t nb, int bs, int64_t s0, int64_t b0,
     }
     for (int c = 0; c < bs; ++c) {
       for (int i = 0; i < bs; ++i) {
-        double v = perm[i] == c ? 1.0 : 0.0;
-        for (int j = 0; j < i; ++j) v = dsub(v, dmul(d[i * bs + j], y[j]));
-        y[i] = v;
+        double v = PERM(i) == c ? 1.0 : 0.0;
+        for (int j = 0; j < i; ++j) v = dsub(v, dmul(D(i, j), Y(j)));
+        Y(i) = v;
       }
       for (int i = bs - 1; i >= 0; --i) {
-        double v = y[i];
-        for (int j = i + 1; j < bs; ++j) v = dsub(v, dmul(d[i * bs + j], y[j]));
-        y[i] = __ddiv_rn(v, d[i * bs + i]);
+        double v = Y(i);
+        for (int j = i + 1; j < bs; ++j) v = dsub(v, dmul(D(i, j), Y(j)));
+        Y(i) = __ddiv_rn(v, D(i, i));
       }
-      for (int i = 0; i < bs; ++i) out[c * bs + i] = y[i];
+      for (int i = 0; i < bs; ++i) out[c * bs + i] = Y(i);
     }
+#undef D
+#undef Y
+#undef PERM
   }
 }
 
