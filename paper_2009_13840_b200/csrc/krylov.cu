@@ -223,14 +223,21 @@ __device__ long long* g_mgs_trace = nullptr;  // per-pass clock64 stamps of CTA 
 
 constexpr int kEpt = 16;  // elements per lane (repro_lanes guarantees <= 16 up to n = 2^22)
 
+// Slot pairs are written and read as single 128-bit accesses (.b128 types:
+// one STG.E.128 / LDG.E.128, never split into two 64-bit accesses), so a
+// reader sees either the old or the new pair, never a torn mix; the
+// {value, value ^ tag} check then only distinguishes stale from current.
 __device__ __forceinline__ void st_pair(ulonglong2* p, unsigned long long a, unsigned long long b) {
-  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+  asm volatile(
+      "{\n .reg .b128 t;\n mov.b128 t, {%1, %2};\n st.relaxed.gpu.global.b128 [%0], t;\n}"
+      ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 
 __device__ __forceinline__ ulonglong2 ld_pair(const ulonglong2* p) {
   ulonglong2 v;
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p)
-               : "memory");
+  asm volatile(
+      "{\n .reg .b128 t;\n ld.relaxed.gpu.global.b128 t, [%2];\n mov.b128 {%0, %1}, t;\n}"
+      : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
   return v;
 }
 
@@ -344,9 +351,10 @@ __global__ void __launch_bounds__(kStepThreads, kL == 1 ? 2 : 1)
         if (blockIdx.x == 0) hcol[i] = v;
       }
     } else if (kPairs) {
-      // relaxed 16-byte {value, value ^ tag} pairs: a pair is accepted only
-      // when its two words agree on this pass's tag (a torn read never
-      // passes), so neither side needs a fence: the value is the only datum
+      // relaxed 128-bit {value, value ^ tag} pairs (single-access .b128
+      // stores/loads, never torn): a pair is accepted only when its two words
+      // agree on this pass's tag, so neither side needs a fence: the value is
+      // the only datum
       ulonglong2* pairs = reinterpret_cast<ulonglong2*>(slot_tag);
       if (blockIdx.x == 0) {
         double v = 0.0;

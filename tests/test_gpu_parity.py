@@ -368,6 +368,22 @@ def test_ilu0_plan_variants_bitwise(S, monkeypatch, mode, rows, ci):
         assert same(ilu.apply(x), ri.apply(x))
 
 
+@pytest.mark.parametrize("ci", range(len(PLAN_CASES)))
+def test_ilu0_single_cta_dataflow_walker_bitwise(S, monkeypatch, ci):
+    """The single-CTA dataflow walker (walk.cu flow_kernel: chunks span task
+    levels, rows wait on their own sources; PSCU_WALK_FLOW with a one-CTA
+    cluster) reproduces Ilu0::apply bitwise."""
+    monkeypatch.setenv("PSCU_WALK_CLUSTER", "1")
+    monkeypatch.setenv("PSCU_WALK_FLOW", "1")
+    s = O.RefSystem(**PLAN_CASES[ci])
+    a = s.csr()
+    ri = O.RefIlu(O.RefCsr(a))
+    ilu = S.Ilu0(S.CsrMatrix(a.row_ptr, a.cols, a.vals))
+    for seed in range(2):
+        x = np.random.default_rng(seed).standard_normal(a.n)
+        assert ilu.apply(x).tobytes() == ri.apply(x).tobytes()
+
+
 # Block-Jacobi over entity blocks (BASELINE.json's smoother; a labelled
 # alternative to the reference's ILU(0), oracle: po_bj_* / po_hier_create_ex
 # in oracle/pstokes_oracle.c). Apply, V-cycle and full solves bitwise.
