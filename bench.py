@@ -133,15 +133,15 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def traffic_record(cls: str):
-    """dram bytes per launch of the dominant kernel class from the committed
-    `ncu --set full` capture summary (profiles/ncu_summary.json), if any."""
+def traffic_record(cls: str, config: str):
+    """dram bytes per launch of the dominant kernel class on this config from
+    the committed `ncu --set full` capture summary (profiles/ncu_summary.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
         d = json.load(open(p))
-        return d.get("traffic_bytes_per_launch", {}).get(cls)
+        return d.get("traffic_bytes_per_launch", {}).get(config, {}).get(cls)
     except Exception:
         return None
 
@@ -424,7 +424,7 @@ def run_ours3(args, cfg):
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches // max(args.steps, 1)),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_record(dom),
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_record(dom, args.config),
                      "peak_source": peak_src, "launch_groups": cnt, "avg_ms": ms / max(cnt, 1),
                      "share_of_step": (ms / 1e3) / (sum(times))},
         "kernel_classes": {k: {"launch_groups": v[0], "ms": v[1],
@@ -511,7 +511,7 @@ def run_ours(args, cfg):
     dom = max(prof, key=lambda k: prof[k][1])
     cnt, ms, byt = prof[dom]
     achieved = (byt / (ms / 1e3)) / 1e9 if ms > 0 else 0.0
-    traffic = traffic_record(dom)
+    traffic = traffic_record(dom, args.config)
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
         try:

@@ -82,6 +82,7 @@ struct WalkArgs {
   const int2* sfar;       // ... {entry offset in chunk, source row}
   const double* sfv;      // ... their source values, gathered before the launch
   long long* trace;       // PSCU_WALK_TRACE: per-sub-level clock64 stamps of CTA 0
+  int spin_ns;            // dataflow sweeps: back-off between polls of a source (0: none)
 };
 
 constexpr int kTraceSub = 4096;
@@ -774,11 +775,13 @@ constexpr int kLevelWarps = 4;
 /// value is no longer the sentinel — no grid barrier between task levels.
 constexpr unsigned long long kFlowSentinel = 0xFFF7DEADBEEF5A5Aull;
 
-__device__ __forceinline__ double flow_wait(const double* p) {
+__device__ __forceinline__ double flow_wait(const double* p, int spin_ns = 0) {
   unsigned long long v;
-  do {
+  for (;;) {
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  } while (v == kFlowSentinel);
+    if (v != kFlowSentinel) break;
+    if (spin_ns) __nanosleep(spin_ns);
+  }
   return __longlong_as_double((long long)v);
 }
 
@@ -851,7 +854,7 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
     for (int u = 0; u < kPer; ++u) {
       const int e = lane + 32 * u;
       const bool out = e < ne && sv[u] < 0 && sv[u] != kPadSrc;
-      if (kFlow) yv[u] = out ? flow_wait(y + (-sv[u] - 1)) : 0.0;
+      if (kFlow) yv[u] = out ? flow_wait(y + (-sv[u] - 1), a.spin_ns) : 0.0;
       else yv[u] = out ? __ldcg(y + (-sv[u] - 1)) : 0.0;
     }
 #pragma unroll
@@ -1055,7 +1058,7 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
     for (int u = 0; u < kPer; ++u) {
       const int e = lane + 32 * u;
       const bool out = e < r_cur.ne && o_cur.sv[u] < 0 && o_cur.sv[u] != kPadSrc;
-      yv[u] = out ? flow_wait(y + (-o_cur.sv[u] - 1)) : 0.0;
+      yv[u] = out ? flow_wait(y + (-o_cur.sv[u] - 1), a.spin_ns) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
@@ -1139,11 +1142,21 @@ __global__ void gather_vals(int64_t m, const I* __restrict__ from,
   }
 }
 
+/// Back-off (ns) between polls of a not-yet-published source in the
+/// dataflow sweeps (PSCU_FLOW_SPIN_NS; default 0 = tight polling).
+static int flow_spin_ns() {
+  static const int v = [] {
+    const char* e = getenv("PSCU_FLOW_SPIN_NS");
+    return e ? std::max(0, atoi(e)) : 0;
+  }();
+  return v;
+}
+
 WalkArgs args_of(const WalkPlan& w) {
   return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_hdr.p, w.tt.p, w.tq.p, w.rows.p, w.off.p, w.dp.p, w.meta.p,
           w.opos.p, w.val.p,  w.src.p,  w.dv.p,     w.sl_f.p,
           reinterpret_cast<const int2*>(w.far.p), w.sl_s.p,
-          reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr};
+          reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr, flow_spin_ns()};
 }
 
 size_t walk_smem() { return sizeof(double) * kRing + kStages * sizeof(Stage); }
