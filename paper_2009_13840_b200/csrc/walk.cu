@@ -83,6 +83,7 @@ struct WalkArgs {
   const double* sfv;      // ... their source values, gathered before the launch
   long long* trace;       // PSCU_WALK_TRACE: per-sub-level clock64 stamps of CTA 0
   int spin_ns;            // dataflow sweeps: back-off between polls of a source (0: none)
+  long long* ftrace;      // trace build, PSCU_FLOW_TRACE: 4 globaltimer stamps per task
 };
 
 constexpr int kTraceSub = 4096;
@@ -828,6 +829,10 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
     unsigned long long gt0 = 0;
     if (tr2) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
 #endif
+#ifdef PSCU_TRACE
+    unsigned long long fts[4] = {0, 0, 0, 0};
+    if (kFlow && a.ftrace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[0]));
+#endif
     const int r0 = tt[task], r1 = tt[task + 1];
     const int e0 = tq[task], ne = tq[task + 1] - e0;
     const int64_t qa = q0 + e0;
@@ -850,6 +855,16 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
       waited = true;
     }
     if (lane < r1 - r0) rb[w][lane] = __ldcg(rhs + k0 + r0 + lane);
+#ifdef PSCU_TRACE
+    if (kFlow && a.ftrace) {
+      // the static loads have landed once their values are consumed
+      int chk = 0;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) chk += sv[u] + int(v[u] != 0.0);
+      chk = __reduce_add_sync(0xffffffffu, chk);
+      if (lane == 0 && chk != 0x7fffffff) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[1]));
+    }
+#endif
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int e = lane + 32 * u;
@@ -867,6 +882,7 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
     }
     __syncwarp();
 #ifdef PSCU_TRACE
+    if (kFlow && a.ftrace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[2]));
     if (tr) {
       a.trace[size_t(ch) * 16 + 1] = clock64();
       a.trace[size_t(ch) * 16 + 3] = ne;
@@ -906,6 +922,11 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         if (kFwd) yb[m.z] = acc;
       }
 #ifdef PSCU_TRACE
+      if (kFlow && a.ftrace) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[3]));
+        long long* ft = a.ftrace + (size_t(hd[9]) + task) * 4;
+        for (int q = 0; q < 4; ++q) ft[q] = (long long)fts[q];
+      }
       if (tr) a.trace[size_t(ch) * 16 + 2] = clock64();
       if (tr2) {
         unsigned long long gt1;
@@ -1156,7 +1177,7 @@ WalkArgs args_of(const WalkPlan& w) {
   return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_hdr.p, w.tt.p, w.tq.p, w.rows.p, w.off.p, w.dp.p, w.meta.p,
           w.opos.p, w.val.p,  w.src.p,  w.dv.p,     w.sl_f.p,
           reinterpret_cast<const int2*>(w.far.p), w.sl_s.p,
-          reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr, flow_spin_ns()};
+          reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr, flow_spin_ns(), nullptr};
 }
 
 size_t walk_smem() { return sizeof(double) * kRing + kStages * sizeof(Stage); }
@@ -2322,6 +2343,22 @@ static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y,
   WalkArgs a = args_of(w);
   a.trace = trace_buffer();
   if (w.levels && w.flow_grid > 0 && !a.trace) {
+#ifdef PSCU_TRACE
+    // PSCU_FLOW_TRACE=<prefix>: globaltimer stamps {start, operands loaded,
+    // sources arrived, folded} of every task of the PSCU_FLOW_TRACE_APPLY-th
+    // sweep of the largest plan traced so far, dumped to <prefix>_{fwd,bwd}.bin
+    // with the chunk table (task-table start, task count per chunk)
+    static int sweep_no = 0;
+    static const char* ft_path = getenv("PSCU_FLOW_TRACE");
+    static const int ft_at = getenv("PSCU_FLOW_TRACE_APPLY") ? atoi(getenv("PSCU_FLOW_TRACE_APPLY")) : 50;
+    DevBuf<long long> ftb;
+    const bool ft_now = ft_path && w.ny > 100000 && sweep_no++ / 2 == ft_at;
+    if (ft_now) {
+      ftb.alloc(size_t(w.tt.n) * 4 + 4);
+      PSCU_CUDA(cudaMemsetAsync(ftb.p, 0, sizeof(long long) * (size_t(w.tt.n) * 4 + 4), c.stream));
+      a.ftrace = ftb.p;
+    }
+#endif
     fill_sentinel<<<grid1(w.ny), 256, 0, c.stream>>>(w.ny, y);
     PSCU_LAUNCHED(&c);
     int c0 = 0, c1 = w.nsub;
@@ -2335,6 +2372,24 @@ static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y,
     PSCU_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(w.flow_grid)), dim3(32 * kLevelWarps),
                                           args, 0, c.stream));
     PSCU_LAUNCHED(&c);
+#ifdef PSCU_TRACE
+    if (ft_now) {
+      std::vector<long long> st(size_t(w.tt.n) * 4);
+      std::vector<int32_t> hdr(size_t(w.nsub) * kHdr);
+      PSCU_CUDA(cudaMemcpyAsync(st.data(), ftb.p, sizeof(long long) * st.size(), cudaMemcpyDeviceToHost, c.stream));
+      PSCU_CUDA(cudaMemcpyAsync(hdr.data(), w.sl_hdr.p, sizeof(int32_t) * hdr.size(), cudaMemcpyDeviceToHost, c.stream));
+      PSCU_CUDA(cudaStreamSynchronize(c.stream));
+      const std::string path = std::string(ft_path) + (w.fwd ? "_fwd.bin" : "_bwd.bin");
+      if (FILE* f = fopen(path.c_str(), "wb")) {
+        const int64_t nsub = w.nsub, ntt = int64_t(w.tt.n);
+        fwrite(&nsub, 8, 1, f);
+        fwrite(&ntt, 8, 1, f);
+        fwrite(hdr.data(), sizeof(int32_t), hdr.size(), f);
+        fwrite(st.data(), sizeof(long long), st.size(), f);
+        fclose(f);
+      }
+    }
+#endif
     return;
   }
   if (w.levels && w.persist_grid > 0 && !a.trace) {
