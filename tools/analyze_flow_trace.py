@@ -1,0 +1,46 @@
+#!/usr/bin/env python
+"""Summary of a dataflow-sweep trace (trace build, PSCU_FLOW_TRACE=<prefix>):
+per task globaltimer stamps {start, operands loaded, sources arrived,
+folded}. Prints the sweep span, the per-level advance of the latest finish,
+and where a task's time goes (operand loads, waiting for sources, fold).
+Usage: python tools/analyze_flow_trace.py gpurun_out/ft_fwd.bin"""
+import sys
+
+import numpy as np
+
+
+def load(path):
+    raw = open(path, "rb").read()
+    nsub, ntt = np.frombuffer(raw[:16], np.int64)
+    hdr = np.frombuffer(raw[16:16 + 4 * 16 * nsub], np.int32).reshape(nsub, 16)
+    st = np.frombuffer(raw[16 + 4 * 16 * nsub:], np.int64).reshape(ntt, 4)
+    return hdr, st
+
+
+def main(path):
+    hdr, st = load(path)
+    rows = []
+    for ch in range(len(hdr)):
+        nt, t0 = int(hdr[ch, 8]), int(hdr[ch, 9])
+        s = st[t0:t0 + nt]
+        s = s[s[:, 3] > 0]
+        if len(s):
+            rows.append((ch, len(s), s[:, 0].min(), s[:, 3].max(), np.mean(s[:, 1] - s[:, 0]),
+                         np.mean(s[:, 2] - s[:, 1]), np.mean(s[:, 3] - s[:, 2]),
+                         np.max(s[:, 3] - s[:, 2])))
+    r = np.array(rows, dtype=float)
+    t_begin, t_end = r[:, 2].min(), r[:, 3].max()
+    adv = np.diff(r[:, 3])
+    print(f"{path}: {len(r)} task levels, span {(t_end - t_begin) / 1e3:.1f} us, "
+          f"{(t_end - t_begin) / len(r):.0f} ns per level")
+    print(f"  latest-finish advance per level: median {np.median(adv):.0f} ns, "
+          f"p90 {np.percentile(adv, 90):.0f} ns")
+    print(f"  per task (mean over levels): operand loads {r[:, 4].mean():.0f} ns, "
+          f"wait for sources {r[:, 5].mean():.0f} ns, fold {r[:, 6].mean():.0f} ns "
+          f"(slowest fold per level {r[:, 7].mean():.0f} ns)")
+    print(f"  tasks per level: median {np.median(r[:, 1]):.0f}")
+
+
+if __name__ == "__main__":
+    for p in sys.argv[1:]:
+        main(p)
