@@ -361,10 +361,23 @@ Mat orthonormalize(Mat& vals, const std::vector<double>& w, const char* what) {
   const int n = vals.c, nq = vals.r;
   Mat C(n, n);
   for (int i = 0; i < n; ++i) C(i, i) = 1.0;
+  // dot(col i, w .* col j) with the Eigen subset's fixed-shape reduction
+  // (include/eigen_subset/Eigen/Dense repro_dot: T = pow2 >= ceil(nq/16)
+  // strided lane partials in index order, then an adjacent-pair tree), the
+  // arithmetic the reference's mgs_coefficients (basis.hpp:29-52) runs with
   auto ip = [&](int i, int j) {
-    double s = 0.0;
-    for (int q = 0; q < nq; ++q) s += vals(q, i) * (w[q] * vals(q, j));
-    return s;
+    int T = 1;
+    while (T < (nq + 15) / 16 && T < (1 << 18)) T <<= 1;
+    if (T == 1) {
+      double s = 0.0;
+      for (int q = 0; q < nq; ++q) s = s + vals(q, i) * (w[q] * vals(q, j));
+      return s;
+    }
+    std::vector<double> part(T, 0.0);
+    for (int q = 0; q < nq; ++q) part[q % T] = part[q % T] + vals(q, i) * (w[q] * vals(q, j));
+    for (int width = T; width > 1; width >>= 1)
+      for (int k = 0; k < width / 2; ++k) part[k] = part[2 * k] + part[2 * k + 1];
+    return part[0];
   };
   for (int i = 0; i < n; ++i) {
     for (int pass = 0; pass < 2; ++pass)
@@ -590,8 +603,10 @@ void build_local(const Mesh& mesh, int e, int k, bool hybrid, double eta, const 
     const double w = rb.rule.w[q];
     rb.grad(rb.rule.p[q], g.data());
     rb.eval(rb.rule.p[q], nrec, phi.data());
+    // m_stiff += w * g * g^T (hho_local.hpp:136): (w g_id) g_jd summed over d from 0
     for (int j = 0; j < nrec; ++j)
-      for (int i = 0; i < nrec; ++i) K(i, j) += w * (g[2 * i] * g[2 * j] + g[2 * i + 1] * g[2 * j + 1]);
+      for (int i = 0; i < nrec; ++i)
+        K(i, j) += (w * g[2 * i]) * g[2 * j] + (w * g[2 * i + 1]) * g[2 * j + 1];
     for (int i = 0; i < nrec; ++i) mom[i] += w * phi[i];
   }
   Mat B(nrec + 1, ns);
@@ -627,17 +642,18 @@ void build_local(const Mesh& mesh, int e, int k, bool hybrid, double eta, const 
     for (int i = 0; i < nrec; ++i) P(i, j) = B(i, j);
 
   // viscous block A = P^T K P + stabilisation + Nitsche
-  Mat KP(nrec, ns), A(ns, ns);
-  for (int j = 0; j < ns; ++j)
-    for (int i = 0; i < nrec; ++i) {
+  // a = P^T K P evaluated left to right like the reference (hho_local.hpp:78)
+  Mat PK(ns, nrec), A(ns, ns);
+  for (int j = 0; j < nrec; ++j)
+    for (int i = 0; i < ns; ++i) {
       double s = 0.0;
-      for (int l = 0; l < nrec; ++l) s += K(i, l) * P(l, j);
-      KP(i, j) = s;
+      for (int l = 0; l < nrec; ++l) s = s + P(l, i) * K(l, j);
+      PK(i, j) = s;
     }
   for (int j = 0; j < ns; ++j)
     for (int i = 0; i < ns; ++i) {
       double s = 0.0;
-      for (int l = 0; l < nrec; ++l) s += P(l, i) * KP(l, j);
+      for (int l = 0; l < nrec; ++l) s = s + PK(i, l) * P(l, j);
       A(i, j) = s;
     }
   std::vector<double> R, DN;
@@ -684,11 +700,14 @@ void build_local(const Mesh& mesh, int e, int k, bool hybrid, double eta, const 
         }
         R[size_t(q) * ns + s] = a1 - a2;
       }
+    // a += (1/hF) r^T diag(w) r (hho_local.hpp:86): ((1/hF) r_qi) w_q r_qj over q from 0
+    const double ih = 1.0 / hf;
     for (int j = 0; j < ns; ++j)
       for (int i = 0; i < ns; ++i) {
         double acc = 0.0;
-        for (int q = 0; q < nq; ++q) acc += R[size_t(q) * ns + i] * fr.w[q] * R[size_t(q) * ns + j];
-        A(i, j) += acc / hf;
+        for (int q = 0; q < nq; ++q)
+          acc = acc + ((ih * R[size_t(q) * ns + i]) * fr.w[q]) * R[size_t(q) * ns + j];
+        A(i, j) += acc;
       }
     if (mesh.faces[fid[lf]].tag == 1) {
       for (int j = 0; j < ns; ++j)
@@ -697,15 +716,17 @@ void build_local(const Mesh& mesh, int e, int k, bool hybrid, double eta, const 
           double cij = 0.0, cji = 0.0, pen = 0.0;
           const bool jf = j >= fo(lf) && j < fo(lf) + nf;
           const bool iff = i >= fo(lf) && i < fo(lf) + nf;
+          const double eh = eta / hf;
           for (int q = 0; q < nq; ++q) {
             const double vj = jf ? psi[size_t(q) * nf + (j - fo(lf))] : 0.0;
             const double vi = iff ? psi[size_t(q) * nf + (i - fo(lf))] : 0.0;
-            cij += DN[size_t(q) * ns + i] * fr.w[q] * vj;
-            cji += DN[size_t(q) * ns + j] * fr.w[q] * vi;
-            pen += vi * fr.w[q] * vj;
+            cij = cij + (DN[size_t(q) * ns + i] * fr.w[q]) * vj;
+            cji = cji + (DN[size_t(q) * ns + j] * fr.w[q]) * vi;
+            // a += (eta/hF) vf^T diag(w) vf (hho_local.hpp:92)
+            pen = pen + ((eh * vi) * fr.w[q]) * vj;
           }
           A(i, j) -= cij + cji;
-          A(i, j) += (eta / hf) * pen;
+          A(i, j) += pen;
         }
     }
   }

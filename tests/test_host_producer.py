@@ -1,7 +1,9 @@
 """The product's host input producer (include/pstokes_host.h) against the
 reference front end: mesh / face numbering, eliminated dofs, retained
-global ids and the CSR pattern must match exactly; local blocks and loads
-to 1e-11 relative (independent arithmetic order)."""
+global ids and the CSR pattern must match exactly, and so must the local
+blocks and loads, bit for bit: the producer evaluates every expression of
+basis.hpp / hho_local.hpp in the order the reference's Eigen subset does
+(left-to-right products, sums from 0, the fixed-shape reproducible dot)."""
 import numpy as np
 import pytest
 
@@ -77,9 +79,34 @@ def test_local_blocks(H, c):
     for e in range(loc.nelem):
         m_ref, r_ref, el_ref = ref.local_blocks(e, data=c[5])
         assert np.array_equal(loc.elim(), el_ref)
-        m = mats[e].T
-        scale = np.max(np.abs(m_ref))
-        assert np.max(np.abs(m - m_ref)) <= 1e-11 * scale
-        assert np.max(np.abs(rhs[e] - r_ref)) <= 1e-11 * max(np.max(np.abs(r_ref)), 1e-300) + 1e-14
+        m = np.ascontiguousarray(mats[e].T)
+        assert m.tobytes() == np.ascontiguousarray(m_ref).tobytes()
+        assert np.ascontiguousarray(rhs[e]).tobytes() == np.ascontiguousarray(r_ref).tobytes()
         if loc.n_elim:
             assert np.array_equal(kept[e], ref.condensation(e)["kept_global"])
+
+
+def test_benchmark_operator_digest_matches_reference_fixture(H):
+    """Config 2a recipe at 64^2 through the product's host producer and the
+    oracle's element-order condensation: the assembled operator and load
+    hash to the reference solve's fixture (tests/golden/c2_vcond_64.json)."""
+    import hashlib
+    import json
+    import os
+
+    fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c2_vcond_64.json")))
+    mesh = H.Mesh.unit_square(64, tri=True, jitter=0.2, seed=0, neumann="top")
+    loc = H.LocalSystem(mesh, "hho-dp", "v-cond", 3, data="sincos")
+    lay = O.po_layout(0, 1, 3, loc.n_faces, loc.nelem)
+    a, b = O.port_condense_assemble(loc.mats(), loc.rhs(), loc.n_local, loc.elim(),
+                                    loc.kept_global().reshape(loc.nelem, loc.n_keep), lay,
+                                    loc.row_ptr(), loc.cols())
+
+    def digest(*arrays):
+        h = hashlib.sha256()
+        for x in arrays:
+            h.update(np.ascontiguousarray(x).tobytes())
+        return h.hexdigest()
+
+    assert digest(a.row_ptr, a.cols, a.vals) == fx["operator_sha256"]
+    assert digest(b) == fx["rhs_sha256"]
