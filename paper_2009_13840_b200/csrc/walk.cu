@@ -786,6 +786,12 @@ __device__ __forceinline__ double flow_wait(const double* p, int spin_ns = 0) {
   return __longlong_as_double((long long)v);
 }
 
+__device__ __forceinline__ unsigned long long flow_peek(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void flow_store(double* p, double v) {
   asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
@@ -865,12 +871,30 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
       if (lane == 0 && chk != 0x7fffffff) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[1]));
     }
 #endif
+    if (kFlow) {
+      // all source values requested at once (one round trip), then only the
+      // ones still holding the sentinel are polled again
+      unsigned long long raw[kPer];
 #pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int e = lane + 32 * u;
-      const bool out = e < ne && sv[u] < 0 && sv[u] != kPadSrc;
-      if (kFlow) yv[u] = out ? flow_wait(y + (-sv[u] - 1), a.spin_ns) : 0.0;
-      else yv[u] = out ? __ldcg(y + (-sv[u] - 1)) : 0.0;
+      for (int u = 0; u < kPer; ++u) {
+        const int e = lane + 32 * u;
+        const bool out = e < ne && sv[u] < 0 && sv[u] != kPadSrc;
+        raw[u] = out ? flow_peek(y + (-sv[u] - 1)) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int e = lane + 32 * u;
+        const bool out = e < ne && sv[u] < 0 && sv[u] != kPadSrc;
+        if (out && raw[u] == kFlowSentinel) raw[u] = __double_as_longlong(flow_wait(y + (-sv[u] - 1), a.spin_ns));
+        yv[u] = out ? __longlong_as_double((long long)raw[u]) : 0.0;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int e = lane + 32 * u;
+        const bool out = e < ne && sv[u] < 0 && sv[u] != kPadSrc;
+        yv[u] = out ? __ldcg(y + (-sv[u] - 1)) : 0.0;
+      }
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
@@ -1075,11 +1099,20 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
       if (has_far) r_far = flow_record(a, ch, task);
     }
     double yv[kPer];
+    unsigned long long raw[kPer];
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int e = lane + 32 * u;
       const bool out = e < r_cur.ne && o_cur.sv[u] < 0 && o_cur.sv[u] != kPadSrc;
-      yv[u] = out ? flow_wait(y + (-o_cur.sv[u] - 1), a.spin_ns) : 0.0;
+      raw[u] = out ? flow_peek(y + (-o_cur.sv[u] - 1)) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = lane + 32 * u;
+      const bool out = e < r_cur.ne && o_cur.sv[u] < 0 && o_cur.sv[u] != kPadSrc;
+      if (out && raw[u] == kFlowSentinel)
+        raw[u] = __double_as_longlong(flow_wait(y + (-o_cur.sv[u] - 1), a.spin_ns));
+      yv[u] = out ? __longlong_as_double((long long)raw[u]) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
