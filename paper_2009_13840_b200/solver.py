@@ -123,8 +123,9 @@ class CsrMatrix:
         """0 for CSR storage, else the dense face-block size."""
         return int(self.lib.pscu_mat_block_size(self.h))
 
-    def download_blocks(self):
-        """(brow_ptr, bcols, vals) of a block-stored operator, vals column-major per block."""
+    def download_blocks(self, vals_out=None):
+        """(brow_ptr, bcols, vals) of a block-stored operator, vals column-major
+        per block (into vals_out when given, e.g. a pinned buffer)."""
         bs = self.block_size
         if not bs:
             raise ValueError("not a block-stored operator")
@@ -132,7 +133,7 @@ class CsrMatrix:
         rp = np.zeros(nb + 1, np.int64)
         N.check(self.lib.pscu_bsr_download(self.ctx.h, self.h, rp.ctypes.data, None, None))
         cl = np.zeros(int(rp[-1]), np.int32)
-        vl = np.zeros(self.nnz)
+        vl = np.zeros(self.nnz) if vals_out is None else vals_out
         N.check(self.lib.pscu_bsr_download(self.ctx.h, self.h, None, cl.ctypes.data,
                                            vl.ctypes.data))
         return rp, cl, vl
