@@ -824,10 +824,7 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
   // this grid (griddepcontrol.wait) before touching right-hand sides and y
   if (kPdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   bool waited = !kPdl;
-  const int W = int(gridDim.x) * kLevelWarps;
-  int first = int(blockIdx.x) * kLevelWarps + w;
-  if (kFlow) first = int((int64_t(first) - hd[10] % W + W) % W);
-  for (int task = first; task < nt; task += W) {
+  for (int task = int(blockIdx.x) * kLevelWarps + w; task < nt; task += gridDim.x * kLevelWarps) {
     // one round trip for the task record, one for its rows and entries
     // (both static), one for the sources outside the task
 #ifdef PSCU_TRACE
@@ -884,11 +881,22 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         const bool out = e < ne && sv[u] < 0 && sv[u] != kPadSrc;
         raw[u] = out ? flow_peek(y + (-sv[u] - 1)) : 0ull;
       }
+      // re-poll every still-unpublished source in the same round (one round
+      // trip per round, not one per source)
+      for (;;) {
+        bool pending = false;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) pending = pending || raw[u] == kFlowSentinel;
+        if (!pending) break;
+        if (a.spin_ns) __nanosleep(a.spin_ns);
+#pragma unroll
+        for (int u = 0; u < kPer; ++u)
+          if (raw[u] == kFlowSentinel) raw[u] = flow_peek(y + (-sv[u] - 1));
+      }
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
         const int e = lane + 32 * u;
         const bool out = e < ne && sv[u] < 0 && sv[u] != kPadSrc;
-        if (out && raw[u] == kFlowSentinel) raw[u] = __double_as_longlong(flow_wait(y + (-sv[u] - 1), a.spin_ns));
         yv[u] = out ? __longlong_as_double((long long)raw[u]) : 0.0;
       }
     } else {
@@ -1109,12 +1117,19 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
       const bool out = e < r_cur.ne && o_cur.sv[u] < 0 && o_cur.sv[u] != kPadSrc;
       raw[u] = out ? flow_peek(y + (-o_cur.sv[u] - 1)) : 0ull;
     }
+    for (;;) {
+      bool pending = false;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) pending = pending || raw[u] == kFlowSentinel;
+      if (!pending) break;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u)
+        if (raw[u] == kFlowSentinel) raw[u] = flow_peek(y + (-o_cur.sv[u] - 1));
+    }
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
       const int e = lane + 32 * u;
       const bool out = e < r_cur.ne && o_cur.sv[u] < 0 && o_cur.sv[u] != kPadSrc;
-      if (out && raw[u] == kFlowSentinel)
-        raw[u] = __double_as_longlong(flow_wait(y + (-o_cur.sv[u] - 1), a.spin_ns));
       yv[u] = out ? __longlong_as_double((long long)raw[u]) : 0.0;
     }
 #pragma unroll
@@ -2046,7 +2061,6 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   w.sl_q.upload(h.sl_q, st);
   {
     std::vector<int32_t> hdr(size_t(w.nsub) * kHdr, 0);
-    int64_t run_tasks = 0;
     for (int s = 0; s < w.nsub; ++s) {
       hdr[size_t(s) * kHdr] = h.sl_k[s];
       hdr[size_t(s) * kHdr + 1] = h.sl_nr[s];
@@ -2057,11 +2071,6 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
       hdr[size_t(s) * kHdr + 6] = h.sl_d[s];
       hdr[size_t(s) * kHdr + 8] = h.sl_nt[s];
       hdr[size_t(s) * kHdr + 9] = h.sl_t[s];
-      // running task count before this chunk (mod 2^30): the dataflow sweeps
-      // rotate the task-to-warp assignment by it, so consecutive task levels
-      // land on different warps and no warp serialises two near levels
-      hdr[size_t(s) * kHdr + 10] = int32_t(run_tasks & ((int64_t(1) << 30) - 1));
-      run_tasks += h.sl_nt[s];
       if (h.S && !h.sl_wide[s]) {
         // bytes the peers of this chunk push during its sub-level
         int first = s;
