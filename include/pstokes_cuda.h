@@ -218,6 +218,21 @@ int pscu_assembly_add(pscu_ctx* ctx, pscu_mat* m, int e0, int nelem, int n, cons
                       int nfe, const int32_t* keep_pos, double* elim_coupling, double* elim_rhs,
                       int mem);
 int pscu_assembly_rhs(pscu_ctx* ctx, const pscu_mat* m, double* rhs, int mem);
+/* Shards of a face-block operator (z-slab partition, paper_2009_13840_b200/
+ * zslab.py): nb owned block rows over ncb block columns
+ * (ghost faces of the neighbour slabs included, numbered in global order);
+ * the diagonal block of block row b is block column b + diag_off. The local
+ * assembly takes per element the block row of each face (-1: held by
+ * another shard, skipped) and its block column. */
+int pscu_bsr_create_local(pscu_ctx* ctx, int64_t nb, int64_t ncb, int bs, int64_t diag_off,
+                          const int64_t* brow_ptr, const int32_t* bcols, const double* vals,
+                          int mem, pscu_mat** out);
+int pscu_assembly_begin_local(pscu_ctx* ctx, int64_t nb, int64_t ncb, int bs, int64_t diag_off,
+                              const int64_t* brow_ptr, const int32_t* bcols, pscu_mat** out);
+int pscu_assembly_add_local(pscu_ctx* ctx, pscu_mat* m, int e0, int nelem, int n,
+                            const double* mats, const double* rhs, int n_elim, const int* elim,
+                            const int32_t* erows, const int32_t* ecols, int nfe,
+                            const int32_t* keep_pos, int mem);
 /* Page-locked host staging buffers (cudaHostAlloc): producers write local
  * blocks there so the batch uploads run at full PCIe/C2C bandwidth. */
 int pscu_host_alloc(int64_t bytes, void** out);

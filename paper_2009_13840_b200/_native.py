@@ -31,6 +31,7 @@ EXPORTS = [
     "pscu_bj_destroy", "pscu_bj_apply", "pscu_layout_make3", "pscu_bsr_create",
     "pscu_mat_block_size", "pscu_assembly_begin", "pscu_assembly_add", "pscu_assembly_rhs",
     "pscu_solve_system_bsr", "pscu_bsr_download", "pscu_host_alloc", "pscu_host_free",
+    "pscu_bsr_create_local", "pscu_assembly_begin_local", "pscu_assembly_add_local",
 ]
 
 
@@ -126,6 +127,10 @@ def load(path: str = LIB):
     lib.pscu_mat_block_size.argtypes = [vp]
     lib.pscu_bsr_download.argtypes = [vp, vp, vp, vp, vp]
     lib.pscu_host_alloc.argtypes = [i64, C.POINTER(vp)]
+    lib.pscu_bsr_create_local.argtypes = [vp, i64, i64, i32, i64, vp, vp, vp, i32, C.POINTER(vp)]
+    lib.pscu_assembly_begin_local.argtypes = [vp, i64, i64, i32, i64, vp, vp, C.POINTER(vp)]
+    lib.pscu_assembly_add_local.argtypes = [vp, vp, i32, i32, i32, vp, vp, i32, vp, vp, vp, i32,
+                                            vp, i32]
     lib.pscu_host_free.argtypes = [vp]
     lib.pscu_assembly_begin.argtypes = [vp, i64, i32, vp, vp, C.POINTER(vp)]
     lib.pscu_assembly_add.argtypes = [vp, vp, i32, i32, i32, vp, vp, i32, vp, vp, i32, vp, vp,

@@ -28,7 +28,7 @@ namespace {
 /// size; the diagonal block of block row b is copied directly (rp / cols
 /// are then the block row pointer / block columns).
 template <bool kBsr>
-__global__ void bj_factor_kernel(int64_t nb, int bs, int64_t s0, int64_t b0,
+__global__ void bj_factor_kernel(int64_t nb, int bs, int64_t s0, int64_t b0, int64_t diag_off,
                                  const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
                                  const double* __restrict__ vals, double* __restrict__ inv,
                                  double* __restrict__ work, int* __restrict__ perm_ws,
@@ -45,7 +45,7 @@ __global__ void bj_factor_kernel(int64_t nb, int bs, int64_t s0, int64_t b0,
     double* out = inv + b * bs * bs;  // column-major
     if (kBsr) {
       int64_t q = rp[b];
-      while (q < rp[b + 1] && cols[q] != b) ++q;
+      while (q < rp[b + 1] && cols[q] != b + diag_off) ++q;
       const double* blk = vals + q * bs * bs;
       for (int i = 0; i < bs; ++i)
         for (int c = 0; c < bs; ++c) D(i, c) = q < rp[b + 1] ? blk[c * bs + i] : 0.0;
@@ -191,11 +191,11 @@ void bj_factor(Context& c, const Csr& a, const pscu_layout& l, BlockJacobi& bj) 
     DevBuf<int> perm(size_t(nb) * bs);
     if (a.bs)
       bj_factor_kernel<true><<<grid_rows(nb), 256, 0, c.stream>>>(
-          nb, bs, s0[t], t ? nf : 0, a.brow_ptr.p, a.bcols.p, a.vals.p, bj.inv.p + off[t], work.p,
+          nb, bs, s0[t], t ? nf : 0, a.diag_off, a.brow_ptr.p, a.bcols.p, a.vals.p, bj.inv.p + off[t], work.p,
           perm.p, bad.p);
     else
       bj_factor_kernel<false><<<grid_rows(nb), 256, 0, c.stream>>>(
-          nb, bs, s0[t], t ? nf : 0, a.row_ptr.p, a.cols.p, a.vals.p, bj.inv.p + off[t], work.p,
+          nb, bs, s0[t], t ? nf : 0, int64_t(0), a.row_ptr.p, a.cols.p, a.vals.p, bj.inv.p + off[t], work.p,
           perm.p, bad.p);
     PSCU_LAUNCHED(&c);
     PSCU_CUDA(cudaStreamSynchronize(c.stream));  // scratch freed at scope end

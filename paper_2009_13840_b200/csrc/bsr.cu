@@ -131,10 +131,16 @@ __global__ void bsr_to_csr_kernel(int64_t total, int bs, const int64_t* __restri
   }
 }
 
-void set_pattern(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp, const int32_t* bcols) {
+void set_pattern(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp, const int32_t* bcols,
+                 int64_t ncb = -1, int64_t diag_off = 0) {
   if (bs < 1 || bs > 64) throw Error(PSCU_EINVAL, "block matrix: block size must be in [1, 64]");
+  if (ncb < 0) ncb = nb;
+  if (ncb < nb || diag_off < 0 || diag_off + nb > ncb)
+    throw Error(PSCU_EINVAL, "block matrix: inconsistent column count / diagonal offset");
   m.bs = bs;
   m.nb = nb;
+  m.ncb = ncb;
+  m.diag_off = diag_off;
   m.n = nb * bs;
   m.h_brow_ptr.assign(brp, brp + nb + 1);
   m.nblk = m.h_brow_ptr[nb];
@@ -145,7 +151,7 @@ void set_pattern(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp, con
     if (m.h_brow_ptr[f + 1] < m.h_brow_ptr[f]) throw Error(PSCU_EINVAL, "block matrix: bad row pointer");
     for (int64_t q = m.h_brow_ptr[f]; q < m.h_brow_ptr[f + 1]; ++q) {
       of[q] = int32_t(f);
-      if (m.h_bcols[q] < 0 || m.h_bcols[q] >= nb ||
+      if (m.h_bcols[q] < 0 || m.h_bcols[q] >= ncb ||
           (q > m.h_brow_ptr[f] && m.h_bcols[q] <= m.h_bcols[q - 1]))
         throw Error(PSCU_EINVAL, "block matrix: block columns must be ascending and in range");
     }
@@ -161,22 +167,23 @@ void set_pattern(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp, con
 
 } // namespace
 
-void alloc_bsr(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp, const int32_t* bcols) {
-  set_pattern(c, m, nb, bs, brp, bcols);
+void alloc_bsr(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp, const int32_t* bcols,
+               int64_t ncb, int64_t diag_off) {
+  set_pattern(c, m, nb, bs, brp, bcols, ncb, diag_off);
   m.vals.alloc(size_t(std::max<int64_t>(1, m.nnz)));
   PSCU_CUDA(cudaMemsetAsync(m.vals.p, 0, sizeof(double) * size_t(m.nnz), c.stream));
 }
 
 void upload_bsr(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp, const int32_t* bcols,
-                const double* vals, int mem) {
+                const double* vals, int mem, int64_t ncb, int64_t diag_off) {
   if (mem == PSCU_HOST) {
-    set_pattern(c, m, nb, bs, brp, bcols);
+    set_pattern(c, m, nb, bs, brp, bcols, ncb, diag_off);
   } else {
     std::vector<int64_t> hrp(nb + 1);
     PSCU_CUDA(cudaMemcpy(hrp.data(), brp, sizeof(int64_t) * (nb + 1), cudaMemcpyDeviceToHost));
     std::vector<int32_t> hc(hrp[nb]);
     PSCU_CUDA(cudaMemcpy(hc.data(), bcols, sizeof(int32_t) * hc.size(), cudaMemcpyDeviceToHost));
-    set_pattern(c, m, nb, bs, hrp.data(), hc.data());
+    set_pattern(c, m, nb, bs, hrp.data(), hc.data(), ncb, diag_off);
   }
   m.vals.alloc(size_t(std::max<int64_t>(1, m.nnz)));
   if (m.nnz)
@@ -217,7 +224,8 @@ void bsr_to_csr(Context& c, const Csr& b, Csr& out) {
 void inherit_bsr(Context& c, const Csr& fine, const std::vector<int32_t>& m, Csr& out) {
   const int bc = int(m.size());
   out = Csr{};
-  set_pattern(c, out, fine.nb, bc, fine.h_brow_ptr.data(), fine.h_bcols.data());
+  set_pattern(c, out, fine.nb, bc, fine.h_brow_ptr.data(), fine.h_bcols.data(), fine.ncb,
+              fine.diag_off);
   out.vals.alloc(size_t(std::max<int64_t>(1, out.nnz)));
   DevBuf<int32_t> dm;
   dm.upload(m, c.stream);

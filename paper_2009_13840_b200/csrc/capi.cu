@@ -17,8 +17,8 @@ void assemble_values(Context& c, int nelem, int nk, const int64_t* kept, const d
                      const double* rrhs, const pscu_layout& l, Csr& a, double* rhs);
 void condense_scatter_bsr(Context& c, Csr& a, int e0, int nelem, int n, const double* mats,
                           const double* rhs, int ne, const int* elim_host, const int32_t* efaces,
-                          int nfe, const int32_t* keep_pos_host, double* rhs_acc,
-                          double* coupling, double* erhs);
+                          const int32_t* erows, int nfe, const int32_t* keep_pos_host,
+                          double* rhs_acc, double* coupling, double* erhs);
 
 Context::~Context() {
   for (auto e : ev_pool) cudaEventDestroy(e);
@@ -621,8 +621,8 @@ int pscu_assembly_add(pscu_ctx* ctx, pscu_mat* m, int e0, int nelem, int n, cons
     }
     double* dc = elim_coupling ? out_vec(int64_t(nelem) * n_elim * nk, elim_coupling, mem, bc) : nullptr;
     double* de = elim_rhs ? out_vec(int64_t(nelem) * n_elim, elim_rhs, mem, be) : nullptr;
-    condense_scatter_bsr(c, m->m, e0, nelem, n, dm, dr, n_elim, elim, df, nfe, keep_pos,
-                         m->rhs_acc.p, dc, de);
+    condense_scatter_bsr(c, m->m, e0, nelem, n, dm, dr, n_elim, elim, df, nullptr, nfe,
+                         keep_pos, m->rhs_acc.p, dc, de);
     if (elim_coupling) finish_out(c, elim_coupling, dc, int64_t(nelem) * n_elim * nk, mem);
     if (elim_rhs) finish_out(c, elim_rhs, de, int64_t(nelem) * n_elim, mem);
     PSCU_CUDA(cudaStreamSynchronize(c.stream));
@@ -639,6 +639,53 @@ int pscu_host_alloc(int64_t bytes, void** out) {
 int pscu_host_free(void* p) {
   return guard([&] {
     if (p) PSCU_CUDA(cudaFreeHost(p));
+  });
+}
+
+int pscu_bsr_create_local(pscu_ctx* ctx, int64_t nb, int64_t ncb, int bs, int64_t diag_off,
+                          const int64_t* brow_ptr, const int32_t* bcols, const double* vals,
+                          int mem, pscu_mat** out) {
+  return guard([&] {
+    auto m = std::make_unique<pscu_mat>();
+    upload_bsr(ctx->c, m->m, nb, bs, brow_ptr, bcols, vals, mem, ncb, diag_off);
+    PSCU_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    *out = m.release();
+  });
+}
+
+int pscu_assembly_begin_local(pscu_ctx* ctx, int64_t nb, int64_t ncb, int bs, int64_t diag_off,
+                              const int64_t* brow_ptr, const int32_t* bcols, pscu_mat** out) {
+  return guard([&] {
+    auto m = std::make_unique<pscu_mat>();
+    alloc_bsr(ctx->c, m->m, nb, bs, brow_ptr, bcols, ncb, diag_off);
+    m->rhs_acc.alloc(size_t(std::max<int64_t>(1, m->m.n)));
+    PSCU_CUDA(cudaMemsetAsync(m->rhs_acc.p, 0, sizeof(double) * size_t(m->m.n), ctx->c.stream));
+    PSCU_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    *out = m.release();
+  });
+}
+
+int pscu_assembly_add_local(pscu_ctx* ctx, pscu_mat* m, int e0, int nelem, int n,
+                            const double* mats, const double* rhs, int n_elim, const int* elim,
+                            const int32_t* erows, const int32_t* ecols, int nfe,
+                            const int32_t* keep_pos, int mem) {
+  return guard([&] {
+    Context& c = ctx->c;
+    if (!m->rhs_acc.p) throw Error(PSCU_EINVAL, "assembly_add: not an assembly target");
+    DevBuf<double> bm, br;
+    DevBuf<int32_t> bfr, bfc;
+    const double* dm = in_vec(c, mats, int64_t(nelem) * n * n, mem, bm);
+    const double* dr = in_vec(c, rhs, int64_t(nelem) * n, mem, br);
+    const int32_t *dfr = erows, *dfc = ecols;
+    if (mem == PSCU_HOST) {
+      bfr.upload(erows, size_t(nelem) * nfe, c.stream);
+      bfc.upload(ecols, size_t(nelem) * nfe, c.stream);
+      dfr = bfr.p;
+      dfc = bfc.p;
+    }
+    condense_scatter_bsr(c, m->m, e0, nelem, n, dm, dr, n_elim, elim, dfc, dfr, nfe, keep_pos,
+                         m->rhs_acc.p, nullptr, nullptr);
+    PSCU_CUDA(cudaStreamSynchronize(c.stream));
   });
 }
 

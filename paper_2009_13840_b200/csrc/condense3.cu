@@ -46,7 +46,8 @@ struct ScatterArgs {
   double* vals;  // BSR values (column-major blocks)
   double* rhs;   // assembled reduced load
   int bs;
-  const int32_t* efaces;  // nelem x nfe global face ids
+  const int32_t* efaces;  // nelem x nfe block-column ids of the element's faces
+  const int32_t* erows;   // nelem x nfe block-row ids (-1: a row this operator does not hold)
   int nfe;
   const int2* keep_pos;   // nk x (local face, offset in the face block)
 };
@@ -80,8 +81,12 @@ __global__ void __launch_bounds__(kThreads)
     for (int t = threadIdx.x; t < ne; t += blockDim.x) perm[t] = t;
     // block position of every (local face, local face) pair of this element
     for (int t = threadIdx.x; t < sa.nfe * sa.nfe; t += blockDim.x) {
-      const int F = sa.efaces[size_t(le) * sa.nfe + t / sa.nfe];
+      const int F = sa.erows[size_t(le) * sa.nfe + t / sa.nfe];
       const int G = sa.efaces[size_t(le) * sa.nfe + t % sa.nfe];
+      if (F < 0) {
+        qpair[t] = -3;  // row held by another shard: skipped
+        continue;
+      }
       int64_t q = sa.brp[F];
       const int64_t q1 = sa.brp[F + 1];
       while (q < q1 && sa.bcols[q] != G) ++q;
@@ -232,13 +237,15 @@ __global__ void __launch_bounds__(kThreads)
             const double v = dsub(src[keep[i]], sv[di][dj]);
             const int2 pi = sa.keep_pos[i];
             if (j == nk) {
-              atomicAdd(sa.rhs + int64_t(sa.efaces[size_t(le) * sa.nfe + pi.x]) * sa.bs + pi.y, v);
+              const int F = sa.erows[size_t(le) * sa.nfe + pi.x];
+              if (F >= 0) atomicAdd(sa.rhs + int64_t(F) * sa.bs + pi.y, v);
               continue;
             }
             const int2 pj = sa.keep_pos[j];
             const bool diag = pi.x == pj.x && pi.y == pj.y;
             if (v == 0.0 && !diag) continue;
             const int64_t q = qpair[pi.x * sa.nfe + pj.x];
+            if (q == -3) continue;
             if (q < 0) {
               atomicExch(bad, -2);
               continue;
@@ -255,8 +262,8 @@ __global__ void __launch_bounds__(kThreads)
 
 void condense_scatter_bsr(Context& c, Csr& a, int e0, int nelem, int n, const double* mats,
                           const double* rhs, int ne, const int* elim_host, const int32_t* efaces,
-                          int nfe, const int32_t* keep_pos_host, double* rhs_acc,
-                          double* coupling, double* erhs) {
+                          const int32_t* erows, int nfe, const int32_t* keep_pos_host,
+                          double* rhs_acc, double* coupling, double* erhs) {
   if (!a.bs) throw Error(PSCU_EINVAL, "condense_scatter: the operator must use block storage");
   if (n > 256 || ne > 128 || ne < 1 || nfe > kMaxFacesPerElem)
     throw Error(PSCU_EINVAL, "condense_scatter: local block too large for the kernel");
@@ -289,7 +296,8 @@ void condense_scatter_bsr(Context& c, Csr& a, int e0, int nelem, int n, const do
                                    int(smem)));
     attr = smem;
   }
-  ScatterArgs sa{a.brow_ptr.p, a.bcols.p, a.vals.p, rhs_acc, a.bs, efaces, nfe, d_kp.p};
+  ScatterArgs sa{a.brow_ptr.p, a.bcols.p, a.vals.p, rhs_acc, a.bs, efaces,
+                 erows ? erows : efaces, nfe, d_kp.p};
   int per_sm = 1;
   PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, condense_bsr_kernel, kThreads, smem));
   const int grid = std::max(1, std::min(nelem, 148 * std::max(1, per_sm)));

@@ -114,6 +114,10 @@ struct Csr {
   // nnz = nblk bs^2 structural entries.
   int bs = 0;
   int64_t nb = 0, nblk = 0;
+  // sharded operators (zslab.py): block columns may exceed the block rows
+  // (ghost faces of the neighbour slabs); the diagonal block of block row b
+  // is block column b + diag_off
+  int64_t ncb = 0, diag_off = 0;
   DevBuf<int64_t> brow_ptr;
   DevBuf<int32_t> bcols, brow_of;  // block columns, block row of every block
   std::vector<int64_t> h_brow_ptr;
@@ -240,10 +244,11 @@ void upload_csr(Context& c, Csr& m, int64_t n, const int64_t* rp, const int32_t*
 
 // bsr.cu
 void upload_bsr(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brow_ptr,
-                const int32_t* bcols, const double* vals, int mem);
+                const int32_t* bcols, const double* vals, int mem, int64_t ncb = -1,
+                int64_t diag_off = 0);
 /// Zero-valued block matrix over a block pattern (host arrays).
 void alloc_bsr(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brow_ptr,
-               const int32_t* bcols);
+               const int32_t* bcols, int64_t ncb = -1, int64_t diag_off = 0);
 /// The same operator in CSR storage (pattern on the host too: ILU plans).
 void bsr_to_csr(Context& c, const Csr& b, Csr& out);
 /// inherit_matrix (plevels.hpp:93-113) between face-block operators: every
