@@ -432,3 +432,188 @@ def _bsr_vals_to_csr(vals, brow_ptr, bs):
         out.append(np.transpose(blk, (2, 0, 1)).ravel())  # [r, q, c]
     return np.concatenate(out)
 
+
+
+# ---------------------------------------------------------------------------
+# GPU backend: the sm_100a kernels through the C ABI on device tensors
+# ---------------------------------------------------------------------------
+
+class GpuOps:
+    """Sharded level operators on the GPU: rank-local face-block operators
+    (pscu_bsr_create_local / pscu_assembly_*_local: owned block rows, ghost
+    block columns), inherited per level with pscu_inherit, block-Jacobi by
+    pscu_bj_*, SpMV by the bitwise face-block kernel; the replicated coarse
+    ILU-GMRES by pscu_gmres on the gathered coarse operator. Vectors are
+    float64 CUDA tensors; ghost exchange and gathers go through
+    torch.distributed (NCCL)."""
+
+    def __init__(self, view: RankView, fine, k: int, partition: SlabPartition, ctx, group=None):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _native as N
+        from . import solver as S
+
+        self.C, self.N, self.S, self.torch = C, N, S, torch
+        self.v, self.ctx, self.group = view, ctx, group
+        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        lib = ctx.lib
+        self.mats, self.bjs, self.bs, self.in_block = [fine], [], [], []
+        lay = S.make_layout3(k, view.nown, 0)
+        layouts = [lay]
+        for kc in range(k - 1, -1, -1):
+            lc = S.make_layout3(kc, view.nown, 0)
+            self.mats.append(S.inherit_matrix(self.mats[-1], layouts[-1], lc))
+            c2f = S.coarse_to_fine_map(layouts[-1], lc)
+            fbc = 3 * lc.face_vel + lc.face_press
+            self.in_block.append(torch.as_tensor(c2f[:fbc], device=self.dev))
+            layouts.append(lc)
+        for l, L in enumerate(layouts):
+            self.bs.append(3 * L.face_vel + L.face_press)
+            if l + 1 < len(layouts):
+                self.bjs.append(S.BlockJacobi(self.mats[l], L))
+        # replicated coarse operator: gather the owned coarse block rows
+        bsc = self.bs[-1]
+        _, _, own_vals = self.mats[-1].download_blocks()
+        full = _allgather(self.dist, group, own_vals, view.nranks) if self.dist is None else \
+            self._gather_dev(torch.as_tensor(own_vals, device=self.dev)).cpu().numpy()
+        self.coarse = S.bsr_matrix(partition.brp, partition.bcols, full, bsc, ctx=ctx)
+        self.coarse_ilu = S.Ilu0(self.coarse)
+        self.lib = lib
+
+    # vector helpers
+    def zeros_like(self, a):
+        return self.torch.zeros_like(a)
+
+    @staticmethod
+    def dot(a, b) -> float:
+        return float((a * b).sum().item())
+
+    def _sync(self):
+        self.torch.cuda.current_stream().synchronize()
+
+    def _gather_dev(self, own):
+        torch = self.torch
+        if self.dist is None or self.v.nranks == 1:
+            return own
+        n = torch.tensor([own.numel()], device=self.dev)
+        sizes = [torch.zeros_like(n) for _ in range(self.v.nranks)]
+        self.dist.all_gather(sizes, n, group=self.group)
+        mx = int(max(int(s.item()) for s in sizes))
+        buf = torch.zeros(mx, dtype=own.dtype, device=self.dev)
+        buf[:own.numel()] = own
+        parts = [torch.zeros_like(buf) for _ in range(self.v.nranks)]
+        self.dist.all_gather(parts, buf, group=self.group)
+        return torch.cat([p[:int(s.item())] for p, s in zip(parts, sizes)])
+
+    def _exchange(self, l, x_own):
+        torch, v, bs = self.torch, self.v, self.bs[l]
+        below = torch.zeros(v.recv_down * bs, dtype=x_own.dtype, device=self.dev)
+        above = torch.zeros(v.recv_up * bs, dtype=x_own.dtype, device=self.dev)
+        if self.dist is not None and v.nranks > 1:
+            xo = x_own.view(-1, bs)
+            ops = []
+            if v.rank > 0:
+                ops.append(self.dist.P2POp(self.dist.isend, xo[torch.as_tensor(
+                    v.send_down, device=self.dev)].reshape(-1).contiguous(), v.rank - 1,
+                    group=self.group))
+                ops.append(self.dist.P2POp(self.dist.irecv, below, v.rank - 1, group=self.group))
+            if v.rank + 1 < v.nranks:
+                ops.append(self.dist.P2POp(self.dist.isend, xo[torch.as_tensor(
+                    v.send_up, device=self.dev)].reshape(-1).contiguous(), v.rank + 1,
+                    group=self.group))
+                ops.append(self.dist.P2POp(self.dist.irecv, above, v.rank + 1, group=self.group))
+            for r in self.dist.batch_isend_irecv(ops):
+                r.wait()
+        return torch.cat([below, x_own, above])
+
+    def spmv(self, l, x_own):
+        ext = self._exchange(l, x_own.contiguous())
+        y = self.torch.empty(self.mats[l].n, dtype=ext.dtype, device=self.dev)
+        self._sync()
+        self.N.check(self.lib.pscu_spmv(self.ctx.h, self.mats[l].h, self.N.ptr(ext),
+                                        self.N.ptr(y), self.N.PSCU_DEVICE))
+        return y
+
+    def bj(self, l, x_own):
+        x = x_own.contiguous()
+        y = self.torch.empty_like(x)
+        self._sync()
+        self.N.check(self.lib.pscu_bj_apply(self.ctx.h, self.bjs[l].h, self.N.ptr(x), self.N.ptr(y),
+                                            self.N.PSCU_DEVICE))
+        return y
+
+    def resid_restrict(self, l, d, w):
+        r = d - self.spmv(l, w)
+        return r.view(-1, self.bs[l])[:, self.in_block[l]].reshape(-1)
+
+    def prolong_add(self, l, w, c):
+        out = w.view(-1, self.bs[l]).clone()
+        out[:, self.in_block[l]] = out[:, self.in_block[l]] + c.view(out.shape[0], -1)
+        return out.reshape(-1)
+
+    def coarse_solve(self, d_own, rtol, maxit):
+        C, N = self.C, self.N
+        full = self._gather_dev(d_own.contiguous())
+        x = self.torch.zeros_like(full)
+        its, rel, conv = C.c_int(), C.c_double(), C.c_int()
+        self._sync()
+        N.check(self.lib.pscu_gmres(self.ctx.h, self.coarse.h, self.coarse_ilu.h, N.ptr(full), None,
+                                    maxit, rtol, 0, N.ptr(x), C.byref(its), C.byref(rel),
+                                    C.byref(conv), N.PSCU_DEVICE))
+        bs = self.bs[-1]
+        return x[self.v.f0 * bs:self.v.f1 * bs].clone(), its.value
+
+
+def assemble_local(mesh, view: RankView, k: int, data: str = "random", seed: int = 0,
+                   batch: int = 4096, ctx=None):
+    """The rank's shard of assemble_hho (3D HHO-hp vp-cond): local blocks of
+    the elements touching an owned face, condensed on the device and scattered
+    into the owned block rows (ghost block columns kept); returns the shard
+    operator and its owned reduced load."""
+    import ctypes as C
+
+    from . import _native as N
+    from . import host
+    from . import solver as S
+
+    ctx = ctx or S.default_context()
+    L = host.HpLocal3(k)
+    h = C.c_void_p()
+    N.check(ctx.lib.pscu_assembly_begin_local(ctx.h, view.nown, view.ncols, L.face_block,
+                                              view.nbelow, view.brow_ptr.ctypes.data,
+                                              view.bcols.ctypes.data, C.byref(h)))
+    A = S.CsrMatrix(None, None, None, ctx=ctx, _handle=h.value)
+    A._owned = True
+    ef = mesh.element_faces()
+    keep_pos = np.ascontiguousarray(L.keep_pos, np.int32)
+    n = L.n_local
+    els = view.elements
+    for b0 in range(0, len(els), batch):
+        sel = els[b0:b0 + batch]
+        mats = np.empty(len(sel) * n * n)
+        rhs = np.empty(len(sel) * n)
+        # build the selected elements, one producer call per run of ids
+        off = 0
+        runs = np.split(sel, np.nonzero(np.diff(sel) != 1)[0] + 1)
+        for run in runs:
+            e0, e1 = int(run[0]), int(run[-1]) + 1
+            m_ = mats[off * n * n:(off + e1 - e0) * n * n]
+            r_ = rhs[off * n:(off + e1 - e0) * n]
+            L.local_blocks(mesh, e0, e1, data=data, seed=seed, out=(m_, r_))
+            off += e1 - e0
+        cols = np.searchsorted(view.faces, ef[sel]).astype(np.int32)
+        rows = np.where((ef[sel] >= view.f0) & (ef[sel] < view.f1), ef[sel] - view.f0, -1)
+        rows = np.ascontiguousarray(rows, np.int32)
+        cols = np.ascontiguousarray(cols, np.int32)
+        N.check(ctx.lib.pscu_assembly_add_local(ctx.h, A.h, int(sel[0]), len(sel), n,
+                                                mats.ctypes.data, rhs.ctypes.data, L.n_elim,
+                                                L.elim.ctypes.data, rows.ctypes.data,
+                                                cols.ctypes.data, 6, keep_pos.ctypes.data,
+                                                N.PSCU_HOST))
+    b = np.zeros(A.n)
+    N.check(ctx.lib.pscu_assembly_rhs(ctx.h, A.h, b.ctypes.data, N.PSCU_HOST))
+    return A, b
