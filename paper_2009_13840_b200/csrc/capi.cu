@@ -275,7 +275,9 @@ int pscu_spmv(pscu_ctx* ctx, const pscu_mat* a, const double* x, double* y, int 
   return guard([&] {
     Context& c = ctx->c;
     DevBuf<double> bx, by;
-    const double* dx = in_vec(c, x, a->m.n, mem, bx);
+    // a shard's input spans its ghost block columns too
+    const int64_t nx = a->m.bs ? a->m.ncb * a->m.bs : a->m.n;
+    const double* dx = in_vec(c, x, nx, mem, bx);
     double* dy = out_vec(a->m.n, y, mem, by);
     spmv(c, a->m, dx, dy);
     finish_out(c, y, dy, a->m.n, mem);
