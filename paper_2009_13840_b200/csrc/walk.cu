@@ -924,7 +924,67 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
       a.trace[size_t(ch) * 16 + 4] = r1 - r0;
     }
 #endif
-    if (lane == 0) {
+    // forward sweeps: when every row's in-task sources trail its
+    // out-of-task ones (the face-block tasks of 3D coarse levels), lane r
+    // folds row r's out-of-task prefix and the in-task terms follow row by
+    // row through shuffles; each row still takes its operations in column
+    // order, so the result is bitwise that of the sequential fold
+    bool par = false;
+    if (kFwd) {
+      const unsigned full = 0xffffffffu;
+      const int nrows = r1 - r0;
+      const int len = lane < nrows ? mb[w][lane].x : 0;
+      int off = len;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(full, off, d);
+        if (lane >= d) off += t;
+      }
+      off -= len;
+      bool ok = true;
+      int first_in = len;
+      for (int e = 0; e < len; ++e) {
+        const int sidx = int(__double_as_longlong(rec[w][off + e].y));
+        if (sidx >= 0) {
+          if (first_in == len) first_in = e;
+        } else if (first_in < len && sidx != kPadSrc) {
+          ok = false;
+        }
+      }
+      par = nrows > 1 && __all_sync(full, ok);
+      if (par) {
+        double acc = 0.0;
+        if (lane < nrows) {
+          acc = rb[w][lane];
+          for (int e = 0; e < first_in; ++e) acc = dsub(acc, rec[w][off + e].x);
+        }
+        int cur = first_in;
+        for (int sr = 0; sr < nrows; ++sr) {
+          const double xs = __shfl_sync(full, acc, sr);
+          if (lane > sr && lane < nrows && cur < len) {
+            const double2 r2 = rec[w][off + cur];
+            if (int(__double_as_longlong(r2.y)) == sr) {
+              acc = dsub(acc, dmul(r2.x, xs));
+              ++cur;
+            }
+          }
+        }
+        if (lane < nrows) {
+          const int4 m = mb[w][lane];
+          if (kFlow) flow_store(y + m.y, acc);
+          else y[m.y] = acc;
+          yb[m.z] = acc;
+        }
+#ifdef PSCU_TRACE
+        if (kFlow && a.ftrace && lane == 0) {
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[3]));
+          long long* ft = a.ftrace + (size_t(hd[9]) + task) * 4;
+          for (int q = 0; q < 4; ++q) ft[q] = (long long)fts[q];
+        }
+#endif
+      }
+    }
+    if (!par && lane == 0) {
       int e = 0;
       for (int r = 0; r < r1 - r0; ++r) {
         const int4 m = mb[w][r];
