@@ -941,23 +941,39 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         if (lane >= d) off += t;
       }
       off -= len;
+      // one pass per lane: fold the out-of-task prefix while checking that
+      // only in-task (or pad) entries follow it
       bool ok = true;
       int first_in = len;
-      for (int e = 0; e < len; ++e) {
-        const int sidx = int(__double_as_longlong(rec[w][off + e].y));
-        if (sidx >= 0) {
-          if (first_in == len) first_in = e;
-        } else if (first_in < len && sidx != kPadSrc) {
+      double acc = lane < nrows ? rb[w][lane] : 0.0;
+      int e = 0;
+      for (; e + 4 <= len; e += 4) {
+        double2 q4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q4[k] = rec[w][off + e + k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int sidx = int(__double_as_longlong(q4[k].y));
+          if (first_in == len) {
+            if (sidx >= 0) first_in = e + k;
+            else acc = dsub(acc, q4[k].x);
+          } else if (sidx < 0 && sidx != kPadSrc) {
+            ok = false;
+          }
+        }
+      }
+      for (; e < len; ++e) {
+        const double2 q1 = rec[w][off + e];
+        const int sidx = int(__double_as_longlong(q1.y));
+        if (first_in == len) {
+          if (sidx >= 0) first_in = e;
+          else acc = dsub(acc, q1.x);
+        } else if (sidx < 0 && sidx != kPadSrc) {
           ok = false;
         }
       }
       par = nrows > 1 && __all_sync(full, ok);
       if (par) {
-        double acc = 0.0;
-        if (lane < nrows) {
-          acc = rb[w][lane];
-          for (int e = 0; e < first_in; ++e) acc = dsub(acc, rec[w][off + e].x);
-        }
         int cur = first_in;
         for (int sr = 0; sr < nrows; ++sr) {
           const double xs = __shfl_sync(full, acc, sr);
