@@ -493,7 +493,7 @@ int pscu_solve(pscu_ctx* ctx, pscu_hier* h, const double* rhs, double rtol, int 
     DevBuf<double> brhs, bx;
     const double* drhs = in_vec(c, rhs, n, mem, brhs);
     double* dx = out_vec(n, x, mem, bx);
-    SpmvOpC op(h->h.levels[0]->a);
+    SpmvOpC op(h->h.levels[0]->op);
     VcycleOp pc(&h->h, n);
     h->h.coarse_its = 0;
     std::vector<double> hv;

@@ -518,6 +518,7 @@ void Hierarchy::build(Context& c, const Csr* fine, const pscu_layout& lf, const 
   levels[0]->k = degrees[0];
   levels[0]->layout = lf;
   levels[0]->a = fine;
+  levels[0]->op = fine;
   for (int l = 1; l < nlev; ++l) {
     Level& L = *levels[l];
     Level& P = *levels[l - 1];
@@ -531,7 +532,7 @@ void Hierarchy::build(Context& c, const Csr* fine, const pscu_layout& lf, const 
     for (int64_t i = 0; i < P.nc; ++i) f2c[c2f[i]] = int32_t(i);
     P.f2c.upload(f2c, c.stream);
     const auto t0 = std::chrono::steady_clock::now();
-    if (P.a->bs) {
+    if (P.op->bs) {
       // face-block operators: the coarse blocks are sub-blocks of the fine
       // ones (face f's coarse dofs map into face f's fine block)
       const int fbc = ncomp(L.layout) * L.layout.face_vel + L.layout.face_press;
@@ -541,17 +542,18 @@ void Hierarchy::build(Context& c, const Csr* fine, const pscu_layout& lf, const 
       for (int j = 0; j < fbc; ++j) in_block[j] = int32_t(c2f[j]);
       const bool needs_csr = (l + 1 == nlev) || cfg.smoother != PSCU_SMOOTHER_BJACOBI;
       if (needs_csr) {
-        Csr tmp;
-        inherit_bsr(c, *P.a, in_block, tmp);
-        bsr_to_csr(c, tmp, L.own);
+        inherit_bsr(c, *P.op, in_block, L.own_bsr);
+        bsr_to_csr(c, L.own_bsr, L.own);
+        L.op = &L.own_bsr;
         PSCU_CUDA(cudaStreamSynchronize(c.stream));
       } else {
-        inherit_bsr(c, *P.a, in_block, L.own);
+        inherit_bsr(c, *P.op, in_block, L.own);
       }
     } else {
       inherit(c, *P.a, c2f, L.own);
     }
     L.a = &L.own;
+    if (!L.op) L.op = &L.own;
     if (getenv("PSCU_DEBUG"))
       fprintf(stderr, "[setup] inherit level %d: %.3f s\n", l,
               std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
@@ -564,8 +566,15 @@ void Hierarchy::build(Context& c, const Csr* fine, const pscu_layout& lf, const 
     Level& L = *levels[l];
     const bool wants_csr = (l + 1 == nlev) || cfg.smoother != PSCU_SMOOTHER_BJACOBI;
     if (L.a->bs && wants_csr) {
-      // ILU(0) / dense LU work on CSR storage: a private CSR copy
-      bsr_to_csr(c, *L.a, L.own);
+      // ILU(0) / dense LU work on CSR storage: a private CSR copy (the block
+      // storage stays the operator of the level's SpMVs)
+      if (L.a == &L.own) {
+        L.own_bsr = std::move(L.own);
+        L.op = &L.own_bsr;
+        bsr_to_csr(c, L.own_bsr, L.own);
+      } else {
+        bsr_to_csr(c, *L.a, L.own);
+      }
       PSCU_CUDA(cudaStreamSynchronize(c.stream));
       L.a = &L.own;
     }
@@ -631,7 +640,7 @@ void Hierarchy::coarse_solve(Context& c, const double* d, double* out) {
     B.dense_lu.solve(c, d, out);
     return;
   }
-  SpmvOp op(B.a);
+  SpmvOp op(B.op);
   IluOp pc(&B.ilu);
   const KrylovResultDev r = gmres_dev(c, op, &pc, d, nullptr, cfg.coarse_maxit, cfg.coarse_rtol,
                                       false, out, B.ws, nullptr);
@@ -644,7 +653,7 @@ void Hierarchy::vcycle(Context& c, int l, const double* d, double* out) {
     return;
   }
   Level& L = *levels[l];
-  SpmvOp op(L.a);
+  SpmvOp op(L.op);
   IluOp ilu_pc(&L.ilu);
   BjOp bj_pc(&L.bj);
   Op& pc = L.use_bj ? static_cast<Op&>(bj_pc) : static_cast<Op&>(ilu_pc);
@@ -652,7 +661,7 @@ void Hierarchy::vcycle(Context& c, int l, const double* d, double* out) {
   // pre-smoothing from zero: gmres(op, pc, d, 0, s, 0, Left) (plevels.hpp:175-176)
   gmres_dev(c, op, &pc, d, nullptr, s, 0.0, true, L.w.p, L.ws, nullptr);
   // d_coarse = restrict(d - A w)
-  residual_restrict(c, *L.a, d, L.w.p, L.down_map.p, L.nc, L.dc.p);
+  residual_restrict(c, *L.op, d, L.w.p, L.down_map.p, L.nc, L.dc.p);
   vcycle(c, l + 1, L.dc.p, L.cc.p);
   // w += prolong(c)
   prolong_add_launch(c, L.a->n, L.f2c.p, L.cc.p, L.w.p);

@@ -88,6 +88,10 @@ struct Level {
   pscu_layout layout{};
   const Csr* a = nullptr;  // level 0 borrows the fine matrix
   Csr own;
+  // operator applications (SpMV, residual) use the block storage when the
+  // level also holds a CSR copy for ILU(0) / dense LU: fewer bytes, same sums
+  const Csr* op = nullptr;
+  Csr own_bsr;
   Ilu ilu;
   BlockJacobi bj;
   bool use_bj = false;  // smoother preconditioner: block-Jacobi instead of ILU(0)
