@@ -84,6 +84,7 @@ struct WalkArgs {
   long long* trace;       // PSCU_WALK_TRACE: per-sub-level clock64 stamps of CTA 0
   int spin_ns;            // dataflow sweeps: back-off between polls of a source (0: none)
   long long* ftrace;      // trace build, PSCU_FLOW_TRACE: 4 globaltimer stamps per task
+  int rotate;             // dataflow sweeps: rotate the task-to-warp assignment per level
 };
 
 constexpr int kTraceSub = 4096;
@@ -824,7 +825,12 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
   // this grid (griddepcontrol.wait) before touching right-hand sides and y
   if (kPdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   bool waited = !kPdl;
-  for (int task = int(blockIdx.x) * kLevelWarps + w; task < nt; task += gridDim.x * kLevelWarps) {
+  // dataflow sweeps may rotate the task-to-warp assignment by the running
+  // task count (hd[10]), so consecutive levels start on different warps
+  const int Wg = int(gridDim.x) * kLevelWarps;
+  int first = int(blockIdx.x) * kLevelWarps + w;
+  if (kFlow && a.rotate) first = int((int64_t(first) - hd[10] % Wg + Wg) % Wg);
+  for (int task = first; task < nt; task += Wg) {
     // one round trip for the task record, one for its rows and entries
     // (both static), one for the sources outside the task
 #ifdef PSCU_TRACE
@@ -1091,7 +1097,7 @@ __global__ void __launch_bounds__(32 * kLevelWarps)
 /// on tasks of strictly lower levels and all warps are co-resident, so the
 /// lowest unfinished level always progresses.
 template <bool kFwd>
-__global__ void __launch_bounds__(32 * kLevelWarps)
+__global__ void __launch_bounds__(32 * kLevelWarps, 4)
     level_flow_kernel(WalkArgs a, int c0, int c1, const double* rhs, double* y, double* yb) {
   for (int ch = c0; ch < c1; ++ch) level_chunk<kFwd, false, true>(a, ch, rhs, y, yb);
 }
@@ -1300,11 +1306,21 @@ static int flow_spin_ns() {
   return v;
 }
 
+/// PSCU_FLOW_ROTATE=1: rotate the dataflow sweeps' task-to-warp assignment.
+static int flow_rotate() {
+  static const int v = [] {
+    const char* e = getenv("PSCU_FLOW_ROTATE");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 WalkArgs args_of(const WalkPlan& w) {
   return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_hdr.p, w.tt.p, w.tq.p, w.rows.p, w.off.p, w.dp.p, w.meta.p,
           w.opos.p, w.val.p,  w.src.p,  w.dv.p,     w.sl_f.p,
           reinterpret_cast<const int2*>(w.far.p), w.sl_s.p,
-          reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr, flow_spin_ns(), nullptr};
+          reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr, flow_spin_ns(), nullptr,
+          flow_rotate()};
 }
 
 size_t walk_smem() { return sizeof(double) * kRing + kStages * sizeof(Stage); }
@@ -2105,7 +2121,7 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
     int most = 0;
     for (size_t s = 0; s < h.sl_nt.size(); ++s) most = std::max(most, h.sl_nt[s]);
     const char* ge = getenv("PSCU_LEVEL_FLOW_WARPS");
-    const int cap = ge ? std::max(32, atoi(ge)) : 2048;
+    const int cap = ge ? std::max(32, atoi(ge)) : 4096;
     const int want = (std::min(most, cap) + kLevelWarps - 1) / kLevelWarps;
     w.flow_grid = std::max(1, std::min(want, per_sm * sms));
   }
@@ -2137,6 +2153,7 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
   w.sl_q.upload(h.sl_q, st);
   {
     std::vector<int32_t> hdr(size_t(w.nsub) * kHdr, 0);
+    int64_t run_tasks = 0;
     for (int s = 0; s < w.nsub; ++s) {
       hdr[size_t(s) * kHdr] = h.sl_k[s];
       hdr[size_t(s) * kHdr + 1] = h.sl_nr[s];
@@ -2147,6 +2164,8 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
       hdr[size_t(s) * kHdr + 6] = h.sl_d[s];
       hdr[size_t(s) * kHdr + 8] = h.sl_nt[s];
       hdr[size_t(s) * kHdr + 9] = h.sl_t[s];
+      hdr[size_t(s) * kHdr + 10] = int32_t(run_tasks & ((int64_t(1) << 30) - 1));
+      run_tasks += h.sl_nt[s];
       if (h.S && !h.sl_wide[s]) {
         // bytes the peers of this chunk push during its sub-level
         int first = s;
