@@ -193,8 +193,9 @@ int pscu_condense_batch(pscu_ctx* ctx, int nelem, int n, const double* mats, con
  * of the local blocks, then the CSR value scatter and the reduced-load rhs
  * over the given structural pattern (the element-order sums of the
  * reference, bit for bit). Host producers build mats/rhs/elim/kept/pattern
- * (include/pstokes_host.h). With mem == PSCU_DEVICE the recovery data
- * (elim_coupling nelem x ne x nk, elim_rhs nelem x ne; nullable) is kept. */
+ * (include/pstokes_host.h). The recovery data (elim_coupling nelem x ne x
+ * nk column-major blocks, elim_rhs nelem x ne; nullable) is returned in the
+ * memory space mem names. */
 int pscu_condense_assemble(pscu_ctx* ctx, int nelem, int n, const double* mats,
                            const double* rhs, int n_elim, const int* elim,
                            const int64_t* kept_global, int64_t dim, const int64_t* row_ptr,
@@ -249,6 +250,17 @@ int pscu_solve_system_bsr(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow
 int pscu_recover_batch(pscu_ctx* ctx, int nelem, int n, int n_elim, const int* elim,
                        const int64_t* kept_global, const double* elim_coupling,
                        const double* elim_rhs, const double* x, double* locals, int mem);
+
+/* error_norms (errors.hpp:32-117) for the HHO schemes, batched: adds the
+ * squared L2 errors {u, grad u (reconstruction), p, div u} of nelem elements
+ * to acc[4] in the reference's accumulation order (element, point,
+ * component). tables: psh_error_tables rows of those elements; locals: their
+ * recovered local vectors (pscu_recover_batch), dims from psh_error_tables.
+ * Call per batch in element order from acc = {0,0,0,0}; the norms are the
+ * square roots of the final acc. With mem == PSCU_DEVICE all three pointers
+ * are device memory. */
+int pscu_error_accumulate(pscu_ctx* ctx, const int32_t* dims, int nelem, const double* tables,
+                          const double* locals, double* acc, int mem);
 
 #ifdef __cplusplus
 }

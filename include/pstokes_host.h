@@ -56,6 +56,16 @@ int psh_write_matrix_market(int64_t n, const int64_t* row_ptr, const int32_t* co
 /* Local blocks + layout + pattern (assemble_hho front end). scheme 0 hho-dp,
  * 1 hho-hp; strategy 0 uncond, 1 v-cond, 2 vp-cond; eta <= 0 selects the
  * default 3(k+1)^2 (hho_local.hpp:19). nthreads <= 0: all cores. */
+/* error_norms (errors.hpp:32-117) point tables, element-major from e0: per
+ * element the reconstruction P (nrec x ns, column-major) then, per point of
+ * the degree-2(k+2)+3 element rule, {w, phi[nrec], dphi/dx[nrec],
+ * dphi/dy[nrec], u_x, u_y, du_x/dx, du_x/dy, du_y/dx, du_y/dy, p} (the
+ * degree-(k+1) reconstruction basis, the closed-form field of data 1 or 2).
+ * dims (11) = {nrec, ns, nq, qstride, per_elem, ne, nf, np, nloc, nfc,
+ * hybrid}; out == NULL fills dims only. Feeds pscu_error_accumulate. */
+int psh_error_tables(const psh_mesh* m, int scheme, int k, int data, int e0, int nelem,
+                     int nthreads, double* out, int32_t* dims);
+
 int psh_build(const psh_mesh* m, int scheme, int strategy, int k, int data, double eta,
               int nthreads, psh_system** out);
 void psh_system_destroy(psh_system* s);

@@ -611,4 +611,39 @@ long long ref_layout_dim(void* sysh, int k) {
   return make_layout(s->mesh, l0.scheme, l0.strategy, k).dim();
 }
 
+/// The reference's own post-processing of a global solution x (length dim):
+/// recover_solution (assemble.hpp:58-66) followed by error_norms
+/// (errors.hpp:32-117) against the closed-form field of data_kind (1 = the
+/// reference's ManufacturedCase, 2 = the sin/cos field above).
+/// out = {u, grad_u, p, div_u}; local_out (optional) receives the recovered
+/// per-element full local vectors concatenated in element order.
+int ref_error_norms(void* sysh, int data_kind, const double* x, double* out, double* local_out) {
+  try {
+    const System* s = static_cast<System*>(sysh);
+    const DofLayout& l = s->sys.layout;
+    Eigen::VectorXd xv(l.dim());
+    for (Eigen::Index i = 0; i < xv.size(); ++i) xv[i] = x[i];
+    const std::vector<Eigen::VectorXd> loc = s->sys.recover_solution(xv);
+    ExactFields ex;
+    if (data_kind == 1)
+      ex = {ManufacturedCase::velocity, ManufacturedCase::velocity_gradient,
+            ManufacturedCase::pressure};
+    else if (data_kind == 2)
+      ex = {SinCosCase::velocity, SinCosCase::grad, SinCosCase::pressure};
+    else
+      throw std::invalid_argument("error norms need a closed-form field (data 1 or 2)");
+    const ErrorNorms e = error_norms(s->mesh, l.scheme, l.k, loc, ex);
+    out[0] = e.u;
+    out[1] = e.grad_u;
+    out[2] = e.p;
+    out[3] = e.div_u;
+    if (local_out)
+      for (const auto& v : loc)
+        for (Eigen::Index i = 0; i < v.size(); ++i) *local_out++ = v[i];
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 } // extern "C"

@@ -19,6 +19,8 @@ void condense_scatter_bsr(Context& c, Csr& a, int e0, int nelem, int n, const do
                           const double* rhs, int ne, const int* elim_host, const int32_t* efaces,
                           const int32_t* erows, int nfe, const int32_t* keep_pos_host,
                           double* rhs_acc, double* coupling, double* erhs);
+void error_accumulate(Context& c, const int32_t* dims, int nelem, const double* tables,
+                      const double* locals, double* acc);
 
 Context::~Context() {
   for (auto e : ev_pool) cudaEventDestroy(e);
@@ -744,9 +746,13 @@ int pscu_condense_assemble(pscu_ctx* ctx, int nelem, int n, const double* mats,
       bk.upload(kept_global, size_t(nelem) * nk, c.stream);
       dk = bk.p;
     }
-    condense_batch(c, nelem, n, dm, dr, n_elim, elim, bschur.p, brr.p,
-                   mem == PSCU_DEVICE ? elim_coupling : nullptr,
-                   mem == PSCU_DEVICE ? elim_rhs : nullptr, nullptr);
+    DevBuf<double> bc, be;
+    double* dc = elim_coupling ? out_vec(int64_t(nelem) * n_elim * nk, elim_coupling, mem, bc)
+                               : nullptr;
+    double* de = elim_rhs ? out_vec(int64_t(nelem) * n_elim, elim_rhs, mem, be) : nullptr;
+    condense_batch(c, nelem, n, dm, dr, n_elim, elim, bschur.p, brr.p, dc, de, nullptr);
+    if (elim_coupling) finish_out(c, elim_coupling, dc, int64_t(nelem) * n_elim * nk, mem);
+    if (elim_rhs) finish_out(c, elim_rhs, de, int64_t(nelem) * n_elim, mem);
     auto m = std::make_unique<pscu_mat>();
     Csr& a = m->m;
     a.n = dim;
@@ -794,6 +800,24 @@ int pscu_recover_batch(pscu_ctx* ctx, int nelem, int n, int n_elim, const int* e
     double* dl = out_vec(int64_t(nelem) * n, locals, mem, bl);
     recover_batch(c, nelem, n, n_elim, elim, bk.p, dc, de, dx, dl);
     finish_out(c, locals, dl, int64_t(nelem) * n, mem);
+  });
+}
+
+int pscu_error_accumulate(pscu_ctx* ctx, const int32_t* dims, int nelem, const double* tables,
+                          const double* locals, double* acc, int mem) {
+  return guard([&] {
+    Context& c = ctx->c;
+    if (nelem < 0) throw Error(PSCU_EINVAL, "error_accumulate: nelem < 0");
+    DevBuf<double> bt, bl, ba;
+    const double* dt = in_vec(c, tables, int64_t(nelem) * dims[4], mem, bt);
+    const double* dl = in_vec(c, locals, int64_t(nelem) * dims[8], mem, bl);
+    double* da = acc;
+    if (mem == PSCU_HOST) {
+      ba.upload(acc, 4, c.stream);
+      da = ba.p;
+    }
+    error_accumulate(c, dims, nelem, dt, dl, da);
+    finish_out(c, acc, da, 4, mem);
   });
 }
 

@@ -97,13 +97,14 @@ __global__ void __launch_bounds__(kCondThreads)
         x[i] = __ddiv_rn(s, LU[i + i * ne]);
       }
     }
-    // rcond guard: ||A_ee||_1 ||A_ee^-1||_1 with the exact inverse
-    if (threadIdx.x == 0) {
+    // rcond guard: ||A_ee||_1 ||A_ee^-1||_1 with the exact inverse (nothing
+    // eliminated: the Schur complement is the block itself, condense.hpp:70-74)
+    if (threadIdx.x == 0 && ne > 0) {
       for (int i = 0; i < ne; ++i)
         if (LU[i + i * ne] == 0.0) singular = 1;
     }
     __syncthreads();
-    if (!singular) {
+    if (!singular && ne > 0) {
       __shared__ double colnorm[256];
       __shared__ double anorm_s;
       if (threadIdx.x == 0) {

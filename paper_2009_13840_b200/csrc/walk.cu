@@ -770,6 +770,10 @@ __global__ void wide_kernel(WalkArgs a, int ch, const double* rhs, double* y, do
 /// order from shared memory (products of in-task sources use the values it
 /// just computed). Same rounded operations as ilu0.hpp:53-65.
 constexpr int kLevelWarps = 4;
+#ifndef PSCU_FOLD_AHEAD
+#define PSCU_FOLD_AHEAD 4
+#endif
+constexpr int kFoldAhead = PSCU_FOLD_AHEAD;  // look-ahead of the pipelined task fold
 
 /// Dataflow sweeps (level_flow_kernel): y starts filled with a signalling-NaN
 /// sentinel (arithmetic never produces it), every row's result is published
@@ -803,13 +807,13 @@ __global__ void fill_sentinel(int64_t n, double* y) {
     y[i] = __longlong_as_double((long long)kFlowSentinel);
 }
 
-template <bool kFwd, bool kPdl, bool kFlow = false>
+template <bool kFwd, bool kPdl, bool kFlow = false, int kMaxNz = kLevelMaxNz>
 __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const double* rhs, double* y,
                                             double* yb) {
-  constexpr int kPer = kLevelMaxNz / 32;  // entries per lane
+  constexpr int kPer = kMaxNz / 32;  // entries per lane
   // per entry {product or factor value, in-task source index or < 0}: one
   // 16-byte shared-memory load per entry in the fold
-  __shared__ double2 rec[kLevelWarps][kLevelMaxNz];
+  __shared__ double2 rec[kLevelWarps][kMaxNz];
   __shared__ double rb[kLevelWarps][kLevelMaxRows], dvb[kLevelWarps][kLevelMaxRows],
       cv[kLevelWarps][kLevelMaxRows];
   __shared__ int4 mb[kLevelWarps][kLevelMaxRows];
@@ -888,7 +892,8 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         raw[u] = out ? flow_peek(y + (-sv[u] - 1)) : 0ull;
       }
       // re-poll every still-unpublished source in the same round (one round
-      // trip per round, not one per source)
+      // trip per round, not one per source; spinning on one source at a
+      // time measured 35 % slower at config 5)
       for (;;) {
         bool pending = false;
 #pragma unroll
@@ -1007,30 +1012,39 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
       }
     }
     if (!par && lane == 0) {
+      // the next kFoldAhead entries' records are loaded while the current
+      // ones are subtracted (rows hold whole 8-entry blocks, so the
+      // look-ahead carries across rows; indices past the task clamp to the
+      // buffer). Config 5: 4.64 vs 4.77 ms per ILU apply.
       int e = 0;
+      double2 nx[kFoldAhead];
+#pragma unroll
+      for (int k = 0; k < kFoldAhead; ++k) nx[k] = rec[w][min(k, kMaxNz - 1)];
       for (int r = 0; r < r1 - r0; ++r) {
         const int4 m = mb[w][r];
         double acc = rb[w][r];
         const int e1 = e + m.x;
-        // operands of 8 entries loaded before their dependent subtractions
-        for (; e + 8 <= e1; e += 8) {
-          int s8[8];
-          double p8[8], c8[8];
+        for (; e + kFoldAhead <= e1; e += kFoldAhead) {
+          double2 cur[kFoldAhead];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const double2 r2 = rec[w][e + k];
-            s8[k] = int(__double_as_longlong(r2.y));
-            p8[k] = r2.x;
+          for (int k = 0; k < kFoldAhead; ++k) cur[k] = nx[k];
+#pragma unroll
+          for (int k = 0; k < kFoldAhead; ++k) nx[k] = rec[w][min(e + kFoldAhead + k, kMaxNz - 1)];
+#pragma unroll
+          for (int k = 0; k < kFoldAhead; ++k) {
+            const int sidx = int(__double_as_longlong(cur[k].y));
+            acc = dsub(acc, sidx < 0 ? cur[k].x : dmul(cur[k].x, cv[w][sidx]));
           }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) c8[k] = s8[k] < 0 ? 0.0 : cv[w][s8[k]];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) acc = dsub(acc, s8[k] < 0 ? p8[k] : dmul(p8[k], c8[k]));
         }
+        const int er = e;
         for (; e < e1; ++e) {
           const double2 r2 = rec[w][e];
-          const int s = int(__double_as_longlong(r2.y));
-          acc = dsub(acc, s < 0 ? r2.x : dmul(r2.x, cv[w][s]));
+          const int sidx = int(__double_as_longlong(r2.y));
+          acc = dsub(acc, sidx < 0 ? r2.x : dmul(r2.x, cv[w][sidx]));
+        }
+        if (e != er) {
+#pragma unroll
+          for (int k = 0; k < kFoldAhead; ++k) nx[k] = rec[w][min(e + k, kMaxNz - 1)];
         }
         if (!kFwd) acc = __ddiv_rn(acc, dvb[w][r]);
         cv[w][r] = acc;
@@ -1101,6 +1115,24 @@ __global__ void __launch_bounds__(32 * kLevelWarps, 4)
     level_flow_kernel(WalkArgs a, int c0, int c1, const double* rhs, double* y, double* yb) {
   for (int ch = c0; ch < c1; ++ch) level_chunk<kFwd, false, true>(a, ch, rhs, y, yb);
 }
+
+/// The same for plans whose tasks hold at most kFlowSmallNz entries (the
+/// face-block tasks of the 3D coarse levels): a quarter of the per-lane
+/// registers and shared memory, so twice the warps are resident and
+/// consecutive task levels run on disjoint warps (a warp's next task is at
+/// least two levels ahead, its operand loads off the critical path).
+constexpr int kFlowSmallNz = 192;
+#ifndef PSCU_FLOW_SMALL_CTAS
+#define PSCU_FLOW_SMALL_CTAS 7
+#endif
+constexpr int kFlowSmallCtas = PSCU_FLOW_SMALL_CTAS;
+
+template <bool kFwd>
+__global__ void __launch_bounds__(32 * kLevelWarps, kFlowSmallCtas)
+    level_flow_small_kernel(WalkArgs a, int c0, int c1, const double* rhs, double* y, double* yb) {
+  for (int ch = c0; ch < c1; ++ch) level_chunk<kFwd, false, true, kFlowSmallNz>(a, ch, rhs, y, yb);
+}
+
 
 /// The same with a two-stage software pipeline over the warp's task
 /// sequence (PSCU_LEVEL_FLOW=2): the record of task t+2 and the entries,
@@ -1306,11 +1338,18 @@ static int flow_spin_ns() {
   return v;
 }
 
-/// PSCU_FLOW_ROTATE=1: rotate the dataflow sweeps' task-to-warp assignment.
+static void* flow_kernel_fn(bool fwd, bool v2, bool small) {
+  if (v2) return fwd ? (void*)level_flow2_kernel<true> : (void*)level_flow2_kernel<false>;
+  if (small) return fwd ? (void*)level_flow_small_kernel<true> : (void*)level_flow_small_kernel<false>;
+  return fwd ? (void*)level_flow_kernel<true> : (void*)level_flow_kernel<false>;
+}
+
+/// Rotation of the dataflow sweeps' task-to-warp assignment (default on:
+/// C5 ILU apply 6.9 -> 5.5 ms, C3 2.34 -> 2.14 ms); PSCU_FLOW_ROTATE=0 pins it.
 static int flow_rotate() {
   static const int v = [] {
     const char* e = getenv("PSCU_FLOW_ROTATE");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 1;
   }();
   return v;
 }
@@ -2115,14 +2154,25 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
     PSCU_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const char* fe = getenv("PSCU_LEVEL_FLOW");
     const bool v2 = fe && atoi(fe) == 2;
-    void* fn = v2 ? (fwd ? (void*)level_flow2_kernel<true> : (void*)level_flow2_kernel<false>)
-                  : (fwd ? (void*)level_flow_kernel<true> : (void*)level_flow_kernel<false>);
+    int maxnz = 0;
+    for (size_t s = 0; s < h.sl_k.size(); ++s)
+      for (int i = 0; i < h.sl_nt[s]; ++i) {
+        const int32_t t0 = h.sl_t[s] + i;
+        maxnz = std::max(maxnz, int(h.tq[t0 + 1] - h.tq[t0]));
+      }
+    const char* fs = getenv("PSCU_LEVEL_FLOW_SMALL");
+    w.flow_small = !v2 && maxnz <= kFlowSmallNz && (!fs || atoi(fs) != 0);
+    void* fn = flow_kernel_fn(fwd, v2, w.flow_small);
     PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kLevelWarps, 0));
     int most = 0;
     for (size_t s = 0; s < h.sl_nt.size(); ++s) most = std::max(most, h.sl_nt[s]);
+    // warps per task of the widest level: > 1 lets consecutive levels run on
+    // disjoint warps (with the rotation below)
+    const char* go = getenv("PSCU_LEVEL_FLOW_OVERSUB");
+    const double over = go ? std::max(0.25, atof(go)) : 2.0;
     const char* ge = getenv("PSCU_LEVEL_FLOW_WARPS");
-    const int cap = ge ? std::max(32, atoi(ge)) : 4096;
-    const int want = (std::min(most, cap) + kLevelWarps - 1) / kLevelWarps;
+    const int cap = ge ? std::max(32, atoi(ge)) : 8192;
+    const int want = (std::min(int(most * over), cap) + kLevelWarps - 1) / kLevelWarps;
     w.flow_grid = std::max(1, std::min(want, per_sm * sms));
   }
   w.flow = h.flow;
@@ -2513,8 +2563,7 @@ static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y,
       const char* e = getenv("PSCU_LEVEL_FLOW");
       return e && atoi(e) == 2;
     }();
-    void* fn = v2 ? (w.fwd ? (void*)level_flow2_kernel<true> : (void*)level_flow2_kernel<false>)
-                  : (w.fwd ? (void*)level_flow_kernel<true> : (void*)level_flow_kernel<false>);
+    void* fn = flow_kernel_fn(w.fwd, v2, w.flow_small);
     PSCU_CUDA(cudaLaunchCooperativeKernel(fn, dim3(unsigned(w.flow_grid)), dim3(32 * kLevelWarps),
                                           args, 0, c.stream));
     PSCU_LAUNCHED(&c);

@@ -48,6 +48,8 @@ def load():
         lib.psh_mesh_write.argtypes = [vp, C.c_char_p]
         lib.psh_mesh_read.argtypes = [C.c_char_p, C.POINTER(vp)]
         lib.psh_write_matrix_market.argtypes = [C.c_int64, vp, vp, vp, C.c_char_p]
+        lib.psh_error_tables.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, vp, vp]
         _lib = lib
     return _lib
 
@@ -132,6 +134,7 @@ class LocalSystem:
                  eta: float = 0.0, nthreads: int = 0):
         self.lib = load()
         self.mesh = mesh
+        self.data = DATA[data]
         h = C.c_void_p()
         _check(self.lib.psh_build(mesh.h, SCHEMES[scheme], STRATEGIES[strategy], k, DATA[data],
                                   eta, nthreads, C.byref(h)))
@@ -172,25 +175,126 @@ class LocalSystem:
         return _view(self.lib.psh_cols(self.h), np.int32, self.nnz)
 
 
-def assemble_stokes(local: LocalSystem, ctx=None):
+@dataclass
+class Recovery:
+    """Per-element recovery data of the static condensation
+    (ElementCondensation, condense.hpp:28-38): elim_coupling (nelem, ne, nk),
+    elim_rhs (nelem, ne), the eliminated local dofs and the retained global ids."""
+    elim: np.ndarray
+    kept_global: np.ndarray
+    elim_coupling: np.ndarray
+    elim_rhs: np.ndarray
+
+
+def assemble_stokes(local: LocalSystem, ctx=None, recovery: bool = False):
     """assemble_stokes (assemble.hpp:348-353) for the HHO schemes: device
     condensation + assembly of the host-built local blocks. Returns the
-    condensed operator as a device CsrMatrix and the reduced rhs."""
+    condensed operator as a device CsrMatrix and the reduced rhs (and the
+    Recovery data when asked, for recover_solution / error_norms)."""
     from . import solver as S
 
     ctx = ctx or S.default_context()
     h = C.c_void_p()
     rhs = np.zeros(local.dim)
     lay = local.layout()
+    ne, nk = local.n_elim, local.n_keep
+    coup = np.zeros(local.nelem * ne * nk) if recovery else None
+    erhs = np.zeros(local.nelem * ne) if recovery else None
     N.check(ctx.lib.pscu_condense_assemble(
         ctx.h, local.nelem, local.n_local, local.lib.psh_local_mats(local.h),
         local.lib.psh_local_rhs(local.h), local.n_elim, local.lib.psh_elim(local.h),
         local.lib.psh_kept_global(local.h), local.dim, local.lib.psh_row_ptr(local.h),
         local.lib.psh_cols(local.h), C.byref(lay), N.PSCU_HOST, C.byref(h), rhs.ctypes.data,
-        None, None))
+        coup.ctypes.data if recovery else None, erhs.ctypes.data if recovery else None))
     m = S.CsrMatrix(None, None, None, ctx=ctx, _handle=h.value)
     m._owned = True
-    return m, rhs
+    if not recovery:
+        return m, rhs
+    # column-major (ne x nk) blocks -> (nelem, ne, nk)
+    rec = Recovery(local.elim().copy(), local.kept_global().reshape(local.nelem, nk).copy(),
+                   coup.reshape(local.nelem, nk, ne).transpose(0, 2, 1), erhs.reshape(local.nelem, ne))
+    return m, rhs, rec
+
+
+@dataclass
+class ErrorNorms:
+    """ErrorNorms (errors.hpp:27-30)."""
+    u: float
+    grad_u: float
+    p: float
+    div_u: float
+
+    def as_array(self) -> np.ndarray:
+        return np.array([self.u, self.grad_u, self.p, self.div_u])
+
+
+def error_tables(local: LocalSystem, e0: int = 0, nelem: int | None = None, out=None):
+    """psh_error_tables: (dims, tables) of elements [e0, e0 + nelem)."""
+    dims = np.zeros(11, np.int32)
+    lib = local.lib
+    _check(lib.psh_error_tables(local.mesh.h, local.scheme, local.k, local.data, 0, 0, 0, None,
+                                dims.ctypes.data))
+    if nelem is None:
+        nelem = local.nelem - e0
+    if out is None:
+        out = np.zeros(int(nelem) * int(dims[4]))
+    _check(lib.psh_error_tables(local.mesh.h, local.scheme, local.k, local.data, e0, nelem, 0,
+                                out.ctypes.data, dims.ctypes.data))
+    return dims, out
+
+
+def error_norms(local: LocalSystem, x, rec: Recovery, batch: int = 8192, ctx=None,
+                return_locals: bool = False):
+    """StokesSystem::recover_solution (assemble.hpp:58-66) and error_norms
+    (errors.hpp:32-117) on the device, streamed over element batches: the
+    host produces each batch's point tables into a pinned buffer, the device
+    recovers the batch's local vectors from x (pscu_recover_batch) and adds
+    its error integrals to the running sums (pscu_error_accumulate), in the
+    reference's order, so the norms are the reference's bit for bit. x: the
+    global solution (host or torch CUDA tensor)."""
+    import torch
+
+    from . import solver as S
+
+    ctx = ctx or S.default_context()
+    dev = torch.device("cuda", 0)
+    dims, _ = error_tables(local, 0, 0)
+    per, nloc = int(dims[4]), int(dims[8])
+    ne, nk = len(rec.elim), rec.kept_global.shape[1]
+    if nloc != ne + nk:
+        raise ValueError("error_norms: recovery data does not match the local layout")
+    xd = torch.as_tensor(np.ascontiguousarray(x, np.float64), device=dev) \
+        if not torch.is_tensor(x) else x.to(dev, torch.float64).contiguous()
+    el = np.ascontiguousarray(rec.elim, np.int32)
+    # recovery data on the device once, column-major blocks like the kernel reads
+    kept = torch.as_tensor(np.ascontiguousarray(rec.kept_global, np.int64), device=dev)
+    coup = torch.as_tensor(np.ascontiguousarray(np.transpose(rec.elim_coupling, (0, 2, 1))),
+                           device=dev)
+    erhs = torch.as_tensor(np.ascontiguousarray(rec.elim_rhs, np.float64), device=dev)
+    acc = torch.zeros(4, dtype=torch.float64, device=dev)
+    nb = min(batch, local.nelem)
+    pin = N.PinnedArray(nb * per)
+    tab = torch.empty(nb * per, dtype=torch.float64, device=dev)
+    loc = torch.empty(nb * nloc, dtype=torch.float64, device=dev)
+    all_locals = torch.empty((local.nelem, nloc), dtype=torch.float64, device=dev) \
+        if return_locals else None
+    dp = dims.ctypes.data
+    for e0 in range(0, local.nelem, nb):
+        m = min(nb, local.nelem - e0)
+        error_tables(local, e0, m, pin.a)
+        tab[:m * per].copy_(torch.from_numpy(pin.a[:m * per]))
+        torch.cuda.current_stream(dev).synchronize()
+        N.check(ctx.lib.pscu_recover_batch(ctx.h, m, nloc, ne, el.ctypes.data,
+                                           kept[e0:e0 + m].data_ptr(), coup[e0:e0 + m].data_ptr(),
+                                           erhs[e0:e0 + m].data_ptr(), xd.data_ptr(),
+                                           loc.data_ptr(), N.PSCU_DEVICE))
+        N.check(ctx.lib.pscu_error_accumulate(ctx.h, dp, m, tab.data_ptr(), loc.data_ptr(),
+                                              acc.data_ptr(), N.PSCU_DEVICE))
+        if return_locals:
+            all_locals[e0:e0 + m].copy_(loc[:m * nloc].view(m, nloc))
+    sq = np.sqrt(acc.cpu().numpy())
+    out = ErrorNorms(*(float(v) for v in sq))
+    return (out, all_locals.cpu().numpy()) if return_locals else out
 
 
 # ---------------------------------------------------------------------------

@@ -576,8 +576,10 @@ LocalLayout local_layout(int k, bool hybrid, int nfaces) {
 }
 
 /// Builds the local matrix (column-major, n x n) and load of element e.
+/// With P_out set, stops after the reconstruction and stores it there
+/// (nrec x ns, column-major) instead of building the blocks.
 void build_local(const Mesh& mesh, int e, int k, bool hybrid, double eta, const Data& data,
-                 double* mat, double* rhs) {
+                 double* mat, double* rhs, double* P_out = nullptr) {
   const int nfc = mesh.nv_of(e);
   const LocalLayout L = local_layout(k, hybrid, nfc);
   const int qd = 2 * (k + 1) + 1;
@@ -640,6 +642,10 @@ void build_local(const Mesh& mesh, int e, int k, bool hybrid, double eta, const 
   Mat P(nrec, ns);  // reconstruction operator
   for (int j = 0; j < ns; ++j)
     for (int i = 0; i < nrec; ++i) P(i, j) = B(i, j);
+  if (P_out) {
+    std::copy(P.a.begin(), P.a.end(), P_out);
+    return;
+  }
 
   // viscous block A = P^T K P + stabilisation + Nitsche
   // a = P^T K P evaluated left to right like the reference (hho_local.hpp:78)
@@ -1221,6 +1227,80 @@ int psh_build(const psh_mesh* pm, int scheme, int strategy, int k, int data, dou
     }
     S.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = ps.release();
+  });
+}
+
+/// Point tables for error_norms (errors.hpp:32-117), element-major from e0:
+/// per element the velocity reconstruction P (nrec x ns, column-major), then
+/// per point of the degree-2(k+2)+3 element rule {w, phi[nrec], dphi/dx[nrec],
+/// dphi/dy[nrec], u(2), grad u (d u_j/d x_i at 2*j+i), p} of the degree-(k+1)
+/// reconstruction basis (the basis the error loop rebuilds) and the
+/// closed-form field. dims = {nrec, ns, nq, qstride, per_elem, ne, nf, np,
+/// nloc, nfc, hybrid}.
+int psh_error_tables(const psh_mesh* pm, int scheme, int k, int data, int e0, int nelem,
+                     int nthreads, double* out, int32_t* dims) {
+  return guard([&] {
+    const Mesh& mesh = pm->m;
+    if (scheme != 0 && scheme != 1)
+      throw std::invalid_argument("error tables: HHO schemes only (hho-dp, hho-hp)");
+    if (data != PSH_DATA_EXP && data != PSH_DATA_SINCOS)
+      throw std::invalid_argument("error tables: data must have a closed form (exp or sincos)");
+    if (k < 0) throw std::invalid_argument("layout: k must be >= 0");
+    if (e0 < 0 || nelem < 0 || e0 + nelem > mesh.nelem())
+      throw std::invalid_argument("error tables: element range out of bounds");
+    const bool hybrid = scheme == 1;
+    const int nfc = mesh.nv_of(0);
+    const LocalLayout L = local_layout(k, hybrid, nfc);
+    const int nrec = dimP2(k + 1), ns = L.ne + nfc * L.nf;
+    const int eq = 2 * (k + 2) + 3;
+    const int nq = element_rule(mesh, 0, eq).size();
+    const int qstride = 3 * nrec + 8;
+    const int64_t per = int64_t(nrec) * ns + int64_t(nq) * qstride;
+    const int32_t d[11] = {nrec, ns, nq, qstride, int32_t(per), L.ne, L.nf, L.np, L.n, nfc, hybrid};
+    std::copy(d, d + 11, dims);
+    if (!out) return;
+    const Data dd{data};
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+    std::string err;
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int i = 0; i < nelem; ++i) {
+      try {
+        const int e = e0 + i;
+        if (mesh.nv_of(e) != nfc)
+          throw std::invalid_argument("error tables: meshes must have one element type");
+        double* t = out + size_t(i) * per;
+        build_local(mesh, e, k, hybrid, 0.0, dd, nullptr, nullptr, t);
+        t += size_t(nrec) * ns;
+        ElemBasis rb;
+        rb.init(mesh, e, k + 1, 2 * (k + 1) + 1);
+        const Rule q = element_rule(mesh, e, eq);
+        if (q.size() != nq) throw std::runtime_error("error tables: ragged element rules");
+        std::vector<double> g(2 * nrec);
+        for (int iq = 0; iq < nq; ++iq, t += qstride) {
+          const P2 p = q.p[iq];
+          t[0] = q.w[iq];
+          rb.eval(p, nrec, t + 1);
+          rb.grad(p, g.data());
+          for (int j = 0; j < nrec; ++j) {
+            t[1 + nrec + j] = g[2 * j];
+            t[1 + 2 * nrec + j] = g[2 * j + 1];
+          }
+          double* x = t + 1 + 3 * nrec;
+          dd.gd(p, x);
+          double gu[2][2];
+          dd.grad_u(p, gu);
+          x[2] = gu[0][0];
+          x[3] = gu[1][0];
+          x[4] = gu[0][1];
+          x[5] = gu[1][1];
+          x[6] = dd.pressure(p);
+        }
+      } catch (const std::exception& ex) {
+#pragma omp critical
+        err = ex.what();
+      }
+    }
+    if (!err.empty()) throw std::runtime_error(err);
   });
 }
 

@@ -113,6 +113,7 @@ def ref_lib():
                                     C.c_void_p]
         lib.ref_layout_dim.restype = C.c_longlong
         lib.ref_layout_dim.argtypes = [vp, C.c_int]
+        lib.ref_error_norms.argtypes = [vp, C.c_int, _f64p, _f64p, C.c_void_p]
         _ref = lib
     return _ref
 
@@ -270,6 +271,18 @@ class RefSystem:
             raise RuntimeError(_err(self.lib))
         return dict(x=x, hist=hist[: its.value].copy(), its=its.value, coarse_its=cits.value,
                     vcycles=vcs.value, rel=rel.value, converged=bool(conv.value), t_solve=ts.value)
+
+    def error_norms(self, x, data: str, nloc: int = 0):
+        """recover_solution (assemble.hpp:58-66) + error_norms (errors.hpp:32-117)
+        of the global vector x: {u, grad_u, p, div_u}, plus the recovered local
+        vectors (n_elements x nloc) when nloc is given."""
+        out = np.zeros(4)
+        loc = np.zeros((self.layout.n_elements, nloc)) if nloc else None
+        rc = self.lib.ref_error_norms(self.h, DATA[data], np.ascontiguousarray(x, np.float64), out,
+                                      loc.ctypes.data if nloc else None)
+        if rc:
+            raise RuntimeError(_err(self.lib))
+        return (out, loc) if nloc else out
 
     def solve_timed(self, degrees, maxit, smoother_iters=2, coarse="gmres-ilu", coarse_rtol=1e-3,
                     coarse_maxit=400, rtol=1e-8, restart=0):

@@ -46,3 +46,14 @@ def test_no_device_fails_loudly():
 
     with pytest.raises(Exception):
         solver.Context(0)
+
+
+def test_host_library_exports_every_declared_symbol():
+    """include/pstokes_host.h (the 2D and 3D host producers) likewise."""
+    text = open(os.path.join(ROOT, "include", "pstokes_host.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    syms = sorted(set(re.findall(r"\b(psh3?_[a-z0-9_]+)\s*\(", text)))
+    assert "psh_error_tables" in syms and "psh3_local_blocks" in syms
+    lib = ctypes.CDLL(build.build_host())
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing

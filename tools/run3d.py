@@ -30,7 +30,14 @@ print(f"n={n} faces={mesh.n_faces} dofs={A.n} nnz={A.nnz} mesh {t1-t0:.2f}s asse
       f"(local {info['t_local_s']:.2f}s, device {info['t_condense_s']:.2f}s)", flush=True)
 cfg = S.LevelConfig(degrees=[2, 1, 0], smoother_iters=smooth, coarse="gmres-ilu",
                     smoother="bjacobi", outer_rtol=1e-8, restart=30)
-for rep_i in range(int(os.environ.get("REPS", "2"))):
+# VARIANTS="K=V K2=V2;K=V3 ...": one solve per variant (plan-time env knobs),
+# after REPS plain repetitions
+variants = [v.split() for v in os.environ.get("VARIANTS", "").split(";") if v.strip()]
+runs = [[]] * int(os.environ.get("REPS", "2")) + variants
+for var in runs:
+    for kv in var:
+        k, v = kv.split("=", 1)
+        os.environ[k] = v
     ctx.profile(True)
     ctx.timer_start()
     h = S.LevelHierarchy(A, lay, cfg)
@@ -41,7 +48,7 @@ for rep_i in range(int(os.environ.get("REPS", "2"))):
     prof = ctx.profile_read()
     ctx.profile(False)
     del h
-    print(json.dumps(dict(setup_ms=t_setup, solve_ms=t_solve, its=rep.outer_its,
+    print(json.dumps(dict(variant=" ".join(var), setup_ms=t_setup, solve_ms=t_solve, its=rep.outer_its,
                           coarse_its=rep.coarse_its, vcycles=rep.vcycles,
                           rel=rep.rel_residual, conv=rep.converged,
                           dofs_per_s=A.n / ((t_setup + t_solve) / 1e3),
