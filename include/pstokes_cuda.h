@@ -262,6 +262,19 @@ int pscu_recover_batch(pscu_ctx* ctx, int nelem, int n, int n_elim, const int* e
 int pscu_error_accumulate(pscu_ctx* ctx, const int32_t* dims, int nelem, const double* tables,
                           const double* locals, double* acc, int mem);
 
+/* The 3D HHO-hp local element blocks on the device (the host producer's
+ * build_local, psh3_local_blocks, bit for bit; hho_local.hpp:26-318 in 3D):
+ * nelem elements given by their hex vertex ids, element faces and signs
+ * (psh3_device_inputs, batch-relative), the mesh vertices (nv x 3) and face
+ * table (nfaces x {4 vertex ids, tag}), the Gauss-Legendre rule gl (nq1
+ * points, then nq1 weights) and, for data 3, the random modal coefficients.
+ * mats (nelem x n x n, column-major) and rhs (nelem x n) as the host
+ * producer writes them. data: 0 or 3 (data 4 needs the host's libm). */
+int pscu_local_blocks3(pscu_ctx* ctx, int k, int data, double eta, int nq1, const double* gl,
+                       int64_t nv, const double* xyz, int64_t nfaces, const int32_t* ftab,
+                       int nelem, const int32_t* hex, const int32_t* ef, const int32_t* es,
+                       const double* coef, double* mats, double* rhs, int mem);
+
 #ifdef __cplusplus
 }
 #endif

@@ -112,6 +112,15 @@ int psh3_local_blocks(const psh_mesh3* m, int k, int data, uint64_t seed, double
                       int e1, int nthreads, double* mats, double* rhs);
 /* Face-block pattern of the condensed operator (block row f: faces of the
  * elements holding f, ascending). Returns the block count; arrays nullable. */
+/* Inputs of the device local-block producer (pscu_local_blocks3) for
+ * elements [e0, e1): hex vertex ids (8 per element), element faces and
+ * orientation signs (6 each), the face table {4 vertex ids, tag} of all
+ * faces, the Gauss-Legendre rule (points, then weights) and, for data 3, the
+ * per-element random modal coefficients (3 x dim P_k). Null outputs are
+ * skipped. Returns the rule size (> 0) or minus the error code. */
+int psh3_device_inputs(const psh_mesh3* m, int k, int data, uint64_t seed, int e0, int e1,
+                       int32_t* hex, int32_t* ef, int32_t* es, int32_t* ftab, double* gl,
+                       double* coef);
 int64_t psh3_block_pattern(const psh_mesh3* m, int64_t* brow_ptr, int32_t* bcols);
 /* Face L2 projections of the manufactured solution (n_faces x 4 nf). */
 int psh3_face_projection(const psh_mesh3* m, int k, double* out);

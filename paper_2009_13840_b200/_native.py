@@ -32,7 +32,7 @@ EXPORTS = [
     "pscu_mat_block_size", "pscu_assembly_begin", "pscu_assembly_add", "pscu_assembly_rhs",
     "pscu_solve_system_bsr", "pscu_bsr_download", "pscu_host_alloc", "pscu_host_free",
     "pscu_bsr_create_local", "pscu_assembly_begin_local", "pscu_assembly_add_local",
-    "pscu_error_accumulate",
+    "pscu_error_accumulate", "pscu_local_blocks3",
 ]
 
 
@@ -124,6 +124,8 @@ def load(path: str = LIB):
                                            C.POINTER(Layout), i32, C.POINTER(vp), vp, vp, vp]
     lib.pscu_recover_batch.argtypes = [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, i32]
     lib.pscu_error_accumulate.argtypes = [vp, vp, i32, vp, vp, vp, i32]
+    lib.pscu_local_blocks3.argtypes = [vp, i32, i32, f64, i32, vp, i64, vp, i64, vp, i32, vp, vp, vp,
+                                       vp, vp, vp, i32]
     lib.pscu_layout_make3.argtypes = [i32, i32, i32, i32, i32, C.POINTER(Layout)]
     lib.pscu_bsr_create.argtypes = [vp, i64, i32, vp, vp, vp, i32, C.POINTER(vp)]
     lib.pscu_mat_block_size.argtypes = [vp]

@@ -21,6 +21,10 @@ void condense_scatter_bsr(Context& c, Csr& a, int e0, int nelem, int n, const do
                           double* rhs_acc, double* coupling, double* erhs);
 void error_accumulate(Context& c, const int32_t* dims, int nelem, const double* tables,
                       const double* locals, double* acc);
+void local_blocks3(Context& c, int k, int data, double eta, int nq1, const double* glx,
+                   const double* glw, const double* xyz, const int32_t* hex, const int32_t* ef,
+                   const int32_t* es, const int32_t* ftab, const double* coef, int e0, int nelem,
+                   double* mats, double* rhs);
 
 Context::~Context() {
   for (auto e : ev_pool) cudaEventDestroy(e);
@@ -818,6 +822,41 @@ int pscu_error_accumulate(pscu_ctx* ctx, const int32_t* dims, int nelem, const d
     }
     error_accumulate(c, dims, nelem, dt, dl, da);
     finish_out(c, acc, da, 4, mem);
+  });
+}
+
+int pscu_local_blocks3(pscu_ctx* ctx, int k, int data, double eta, int nq1, const double* gl,
+                       int64_t nv, const double* xyz, int64_t nfaces, const int32_t* ftab,
+                       int nelem, const int32_t* hex, const int32_t* ef, const int32_t* es,
+                       const double* coef, double* mats, double* rhs, int mem) {
+  return guard([&] {
+    Context& c = ctx->c;
+    if (nq1 < 1 || nq1 > 8) throw Error(PSCU_EINVAL, "local_blocks3: rule size out of range");
+    if (k < 0 || k > 4) throw Error(PSCU_EINVAL, "hho3: k must be in [0, 4]");
+    const auto d3 = [](int d) { return (d + 1) * (d + 2) * (d + 3) / 6; };
+    const auto d2 = [](int d) { return (d + 1) * (d + 2) / 2; };
+    const int64_t n = 3 * (d3(k + 1) + 6 * d2(k)) + d3(k) + 6 * d2(k);
+    const int64_t ncoef = data == 3 ? int64_t(nelem) * 3 * d3(k) : 0;
+    if (mem != PSCU_HOST) {
+      local_blocks3(c, k, data, eta, nq1, gl, gl + nq1, xyz, hex, ef, es, ftab, coef, 0, nelem,
+                    mats, rhs);
+      return;
+    }
+    DevBuf<double> bg, bx, bc, bm, br;
+    DevBuf<int32_t> bh, be, bs, bf;
+    bg.upload(gl, size_t(2 * nq1), c.stream);
+    bx.upload(xyz, size_t(3 * nv), c.stream);
+    bf.upload(ftab, size_t(5 * nfaces), c.stream);
+    bh.upload(hex, size_t(8) * nelem, c.stream);
+    be.upload(ef, size_t(6) * nelem, c.stream);
+    bs.upload(es, size_t(6) * nelem, c.stream);
+    if (ncoef) bc.upload(coef, size_t(ncoef), c.stream);
+    double* dm = out_vec(int64_t(nelem) * n * n, mats, mem, bm);
+    double* dr = out_vec(int64_t(nelem) * n, rhs, mem, br);
+    local_blocks3(c, k, data, eta, nq1, bg.p, bg.p + nq1, bx.p, bh.p, be.p, bs.p, bf.p,
+                  ncoef ? bc.p : nullptr, 0, nelem, dm, dr);
+    finish_out(c, mats, dm, int64_t(nelem) * n * n, mem);
+    finish_out(c, rhs, dr, int64_t(nelem) * n, mem);
   });
 }
 

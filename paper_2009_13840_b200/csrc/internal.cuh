@@ -229,6 +229,7 @@ struct Context {
   DevBuf<double> scal;             // device scalars (Hessenberg column etc.)
   double* h_pinned = nullptr;      // pinned host mirror of scal
   DevBuf<int> err_flag;
+  DevBuf<double> l3_scratch;        // device local-block producer work arrays
   DevBuf<unsigned long long> slot_tag;  // tagged reduction slots (arnoldi_step_kernel)
   unsigned long long pass_tag = 0;      // monotonic pass id across launches
   size_t scal_cap = 0;

@@ -569,6 +569,150 @@ __global__ void __launch_bounds__(kStepThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// The Arnoldi step for coarse levels too large for register-resident w
+// (config 5: n = 3.2 M, 2^18 reproducible-dot lanes, 13 elements per lane):
+// one 1024-thread CTA per SM holds its 2048 lanes' slice of w in shared
+// memory (epl x 16 KB), so a pass streams only v_{i-1} (the w update; read
+// one pass earlier, an L2 hit) and v_i (prefetched into L2 by a bulk
+// prefetch one pass ahead, overlapping the grid reduction). Same lanes,
+// same per-lane order, same adjacent-pair tree as arnoldi_step_kernel.
+// ---------------------------------------------------------------------------
+
+constexpr int kSmemThreads = 1024;
+constexpr int kSmemLanes = 2 * kSmemThreads;  // lanes per CTA (two per thread)
+constexpr int kSmemBatch = 4;                 // element slices loaded per batch
+
+/// block_tree for up to 1024 lanes (32 warp partials).
+__device__ double block_tree_1k(double v, int nlanes) {
+  __shared__ double wsum[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wl = nlanes < 32 ? nlanes : 32;
+  for (int off = 1; off < wl; off <<= 1) {
+    const double o = __shfl_down_sync(0xffffffffu, v, off);
+    if ((lane & (2 * off - 1)) == 0) v = dadd(v, o);
+  }
+  if (nlanes <= 32) return v;
+  if (lane == 0) wsum[wid] = v;
+  __syncthreads();
+  const int nw = nlanes >> 5;
+  if (wid == 0) {
+    v = lane < nw ? wsum[lane] : 0.0;
+    for (int off = 1; off < nw; off <<= 1) {
+      const double o = __shfl_down_sync(0xffffffffu, v, off);
+      if ((lane & (2 * off - 1)) == 0) v = dadd(v, o);
+    }
+  }
+  return v;
+}
+
+__device__ __forceinline__ double2 ldcg2(const double* p) {
+  return __ldcg(reinterpret_cast<const double2*>(p));
+}
+
+/// L2 prefetch of this CTA's slices of one basis vector (bulk, one thread).
+__device__ __forceinline__ void prefetch_l2(const double* v, int64_t n, int64_t T, int epl,
+                                            int64_t lane_base) {
+  for (int k = 0; k < epl; ++k) {
+    const int64_t s0 = lane_base + int64_t(k) * T;
+    if (s0 >= n) break;
+    const int64_t cnt = n - s0 < kSmemLanes ? n - s0 : kSmemLanes;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(v + s0),
+                 "r"(unsigned(cnt) * 8u)
+                 : "memory");
+  }
+}
+
+__global__ void __launch_bounds__(kSmemThreads, 1)
+    arnoldi_smem_kernel(int64_t n, int64_t T, int epl, int j, const double* __restrict__ wg,
+                        const double* V, int64_t ldv, double* __restrict__ hcol,
+                        unsigned long long* slot_tag, unsigned long long tag_base, double* vout) {
+  extern __shared__ __align__(16) double2 wsm[];  // epl x kSmemThreads: lanes (2t, 2t+1)
+  __shared__ double hsh;
+  const int G = gridDim.x;
+  const int tid = threadIdx.x;
+  const int64_t lane_base = int64_t(blockIdx.x) * kSmemLanes;
+  const int64_t lane0 = lane_base + 2 * tid;  // even; n even, so e < n covers the pair
+  if (tid == 0) prefetch_l2(V, n, T, epl, lane_base);
+  for (int k = 0; k < epl; ++k) {
+    const int64_t e = lane0 + int64_t(k) * T;
+    wsm[k * kSmemThreads + tid] = e < n ? ldcg2(wg + e) : make_double2(0.0, 0.0);
+  }
+  ulonglong2* pairs = reinterpret_cast<ulonglong2*>(slot_tag);
+  double hprev = 0.0;
+  for (int i = 0; i <= j + 1; ++i) {
+    // v_{i+1} towards L2 while this pass computes and reduces
+    if (tid == 0 && i + 1 <= j) prefetch_l2(V + int64_t(i + 1) * ldv, n, T, epl, lane_base);
+    const double* vi = V + int64_t(i) * ldv;
+    const double* vp = V + int64_t(i - 1) * ldv;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int k0 = 0; k0 < epl; k0 += kSmemBatch) {
+      double2 a[kSmemBatch], b[kSmemBatch];
+#pragma unroll
+      for (int c = 0; c < kSmemBatch; ++c) {
+        const int k = k0 + c;
+        const int64_t e = lane0 + int64_t(k) * T;
+        const bool ok = k < epl && e < n;
+        a[c] = ok && i > 0 ? ldcg2(vp + e) : make_double2(0.0, 0.0);
+        b[c] = ok && i <= j ? ldcg2(vi + e) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int c = 0; c < kSmemBatch; ++c) {
+        const int k = k0 + c;
+        const int64_t e = lane0 + int64_t(k) * T;
+        if (k < epl && e < n) {
+          double2 wv = wsm[k * kSmemThreads + tid];
+          if (i > 0) {
+            wv.x = dsub(wv.x, dmul(hprev, a[c].x));
+            wv.y = dsub(wv.y, dmul(hprev, a[c].y));
+            wsm[k * kSmemThreads + tid] = wv;
+          }
+          const double2 o = i <= j ? b[c] : wv;
+          acc0 = dadd(acc0, dmul(wv.x, o.x));
+          acc1 = dadd(acc1, dmul(wv.y, o.y));
+        }
+      }
+    }
+    const double cta = block_tree_1k(dadd(acc0, acc1), kSmemThreads);
+    const int par = i & 1;
+    const unsigned long long want = tag_base + unsigned(i) + 1ull;
+    if (tid == 0) {
+      const unsigned long long bits = __double_as_longlong(cta);
+      st_pair(pairs + par * G + blockIdx.x, bits, bits ^ want);
+    }
+    // every CTA gathers all G pairs and rebuilds the same tree (a slot of
+    // parity par is rewritten two passes later, after every CTA read it)
+    double v = 0.0;
+    if (tid < G) {
+      ulonglong2 p;
+      do {
+        p = ld_pair(pairs + par * G + tid);
+      } while ((p.x ^ p.y) != want);
+      v = __longlong_as_double(p.x);
+    }
+    __syncthreads();  // warp 0 finished reading block_tree_1k's scratch of this pass
+    v = block_tree_1k(v, G);
+    if (tid == 0) {
+      if (i == j + 1) v = __dsqrt_rn(v);
+      hsh = v;
+      if (blockIdx.x == 0) hcol[i] = v;
+    }
+    __syncthreads();
+    hprev = hsh;
+  }
+  // v_{j+1} = w / h, or 0 on a happy breakdown (gmres.hpp:66-67)
+  for (int k = 0; k < epl; ++k) {
+    const int64_t e = lane0 + int64_t(k) * T;
+    if (e < n) {
+      const double2 wv = wsm[k * kSmemThreads + tid];
+      double2 o;
+      o.x = hprev > 0.0 ? __ddiv_rn(wv.x, hprev) : 0.0;
+      o.y = hprev > 0.0 ? __ddiv_rn(wv.y, hprev) : 0.0;
+      *reinterpret_cast<double2*>(vout + e) = o;
+    }
+  }
+}
+
 } // namespace
 
 /// Cooperative single-launch Arnoldi step; returns false when the problem
@@ -646,10 +790,13 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     const char* e = getenv("PSCU_MGS_LANES");
     return e ? atoi(e) : 2;
   }();
+  // PSCU_MGS_FORCE_SMEM=1 (tests): skip the register-resident kernels
+  const char* fs = getenv("PSCU_MGS_FORCE_SMEM");
+  const bool force_smem = fs && atoi(fs) != 0;
   // two lanes per thread when that keeps >= 64 CTAs (fewer participants per
   // grid-wide reduction) and the elements fit the kL = 2 register budget
   for (int L = (max_lanes >= 2 && T / (2 * kStepThreads) >= 64 && epl <= StepShape<2>::kE) ? 2 : 1;
-       L >= 1; L >>= 1) {
+       L >= 1 && !force_smem; L >>= 1) {
     const int64_t G = T / (int64_t(kStepThreads) * L);
     if (G < 1 || G > 1024) continue;
     const size_t smem = 0;
@@ -703,6 +850,44 @@ bool arnoldi_step_fused(Context& c, int64_t n, int j, double* w, double* V, int6
     }
 #endif
     return true;
+  }
+  // w in shared memory (coarse levels beyond the register budget)
+  static const bool smem_ok = [] {
+    const char* e = getenv("PSCU_MGS_SMEM");
+    return e ? atoi(e) != 0 : true;
+  }();
+  if (smem_ok && (n % 2) == 0 && (ldv % 2) == 0 && T % kSmemLanes == 0 &&
+      (reinterpret_cast<uintptr_t>(w) % 16) == 0 && (reinterpret_cast<uintptr_t>(V) % 16) == 0) {
+    const int64_t G = T / kSmemLanes;
+    const size_t smem = sizeof(double2) * size_t(epl) * kSmemThreads;
+    if (G >= 1 && G <= sm_count && smem <= 220 * 1024) {
+      static size_t attr_smem = 0;
+      if (smem > attr_smem) {
+        PSCU_CUDA(cudaFuncSetAttribute(arnoldi_smem_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        attr_smem = smem;
+      }
+      int per_sm = 0;
+      PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, arnoldi_smem_kernel,
+                                                              kSmemThreads, smem));
+      if (int64_t(per_sm) * sm_count >= G) {
+        ensure_slot_tags(c, G);
+        int ei = epl, jj = j;
+        int64_t nn = n, TT = T, ld = ldv;
+        const double* pw = w;
+        const double* pV = V;
+        double* ph = hcol;
+        unsigned long long* pt = c.slot_tag.p;
+        unsigned long long base = c.pass_tag;
+        double* vo = V + int64_t(j + 1) * ldv;
+        c.pass_tag += unsigned(j + 2);
+        void* args[] = {&nn, &TT, &ei, &jj, &pw, &pV, &ld, &ph, &pt, &base, &vo};
+        PSCU_CUDA(cudaLaunchCooperativeKernel((void*)arnoldi_smem_kernel, dim3(unsigned(G)),
+                                              dim3(kSmemThreads), args, smem, c.stream));
+        PSCU_LAUNCHED(&c);
+        return true;
+      }
+    }
   }
   return false;
 }

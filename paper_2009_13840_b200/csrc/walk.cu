@@ -83,7 +83,8 @@ struct WalkArgs {
   const double* sfv;      // ... their source values, gathered before the launch
   long long* trace;       // PSCU_WALK_TRACE: per-sub-level clock64 stamps of CTA 0
   int spin_ns;            // dataflow sweeps: back-off between polls of a source (0: none)
-  long long* ftrace;      // trace build, PSCU_FLOW_TRACE: 4 globaltimer stamps per task
+  long long* ftrace;      // trace build, PSCU_FLOW_TRACE: per task 4 globaltimer stamps,
+                          // fold cycles, lane-parallel fold flag
   int rotate;             // dataflow sweeps: rotate the task-to-warp assignment per level
 };
 
@@ -807,6 +808,28 @@ __global__ void fill_sentinel(int64_t n, double* y) {
     y[i] = __longlong_as_double((long long)kFlowSentinel);
 }
 
+/// acc - r[0].x - r[1].x - ... - r[cnt-1].x in that order (the
+/// out-of-task part of a row: products only), operands loaded four ahead.
+__device__ __forceinline__ double chain_sub(double acc, const double2* r, int cnt) {
+  double nx[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) nx[k] = k < cnt ? r[k].x : 0.0;
+  int e = 0;
+  for (; e + 4 <= cnt; e += 4) {
+    double cur[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cur[k] = nx[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) nx[k] = e + 4 + k < cnt ? r[e + 4 + k].x : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc = dsub(acc, cur[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (e + k < cnt) acc = dsub(acc, nx[k]);
+  return acc;
+}
+
 template <bool kFwd, bool kPdl, bool kFlow = false, int kMaxNz = kLevelMaxNz>
 __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const double* rhs, double* y,
                                             double* yb) {
@@ -817,6 +840,7 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
   __shared__ double rb[kLevelWarps][kLevelMaxRows], dvb[kLevelWarps][kLevelMaxRows],
       cv[kLevelWarps][kLevelMaxRows];
   __shared__ int4 mb[kLevelWarps][kLevelMaxRows];
+  __shared__ int2 rinfo[kLevelWarps][kLevelMaxRows];  // per row {entry offset, leading in-task}
   const int k0 = a.sl_k[ch], nr = a.sl_nr[ch];
   const int64_t q0 = a.sl_q[ch];
   const int* hd = a.sl_hdr + kHdr * ch;
@@ -847,6 +871,7 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
 #endif
 #ifdef PSCU_TRACE
     unsigned long long fts[4] = {0, 0, 0, 0};
+    long long fc0 = 0;
     if (kFlow && a.ftrace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[0]));
 #endif
     const int r0 = tt[task], r1 = tt[task + 1];
@@ -860,12 +885,51 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
       sv[u] = e < ne ? __ldg(a.src + qa + e) : 0;
       v[u] = e < ne ? __ldg(a.val + qa + e) : 0.0;
     }
-    if (lane < r1 - r0) {
+    const unsigned full = 0xffffffffu;
+    const int nrows = r1 - r0;
+    int rlen = 0;
+    if (lane < nrows) {
       const int k = k0 + r0 + lane;
-      const int len = int((r0 + lane + 1 < nr ? a.off[k + 1] : nq) - a.off[k]);
-      mb[w][lane] = make_int4(len, a.rows[k], kFwd ? a.opos[k] : 0, 0);
+      rlen = int((r0 + lane + 1 < nr ? a.off[k + 1] : nq) - a.off[k]);
+      mb[w][lane] = make_int4(rlen, a.rows[k], kFwd ? a.opos[k] : 0, 0);
       if (!kFwd) dvb[w][lane] = a.dv[k];
     }
+    // static row structure, found while the sources are still in flight:
+    // lane r < nrows locates row r's in-task entries (sources inside the
+    // task) among its out-of-task ones. Forward face-block rows have them
+    // trailing (lane-parallel fold), backward rows leading (lane 0 folds the
+    // leading in-task terms, then the rest as a pure product chain).
+    int roff = rlen;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(full, roff, d);
+      if (lane >= d) roff += t;
+    }
+    roff -= rlen;
+    int fin = rlen, lin = -1, fout = rlen, lout = -1;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = lane + 32 * u;
+      const unsigned bi = __ballot_sync(full, e < ne && sv[u] >= 0);
+      const unsigned bo = __ballot_sync(full, e < ne && sv[u] < 0 && sv[u] != kPadSrc);
+      const int lo = max(roff, 32 * u), hi = min(roff + rlen, 32 * u + 32);
+      if (lane < nrows && lo < hi) {
+        const int b0 = lo - 32 * u, b1 = hi - 32 * u;
+        const unsigned m = (b1 == 32 ? full : ((1u << b1) - 1u)) & ~((1u << b0) - 1u);
+        const unsigned mi = bi & m, mo = bo & m;
+        if (mi) {
+          fin = min(fin, 32 * u + __ffs(int(mi)) - 1 - roff);
+          lin = max(lin, 32 * u + 31 - __clz(int(mi)) - roff);
+        }
+        if (mo) {
+          fout = min(fout, 32 * u + __ffs(int(mo)) - 1 - roff);
+          lout = max(lout, 32 * u + 31 - __clz(int(mo)) - roff);
+        }
+      }
+    }
+    const bool trail_ok = __all_sync(full, lane >= nrows || lout < fin);
+    const bool lead_ok = __all_sync(full, lane >= nrows || lin < fout);
+    if (lane < nrows) rinfo[w][lane] = make_int2(roff, lin + 1);
     if (!waited) {
       asm volatile("griddepcontrol.wait;" ::: "memory");
       waited = true;
@@ -928,7 +992,10 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
     }
     __syncwarp();
 #ifdef PSCU_TRACE
-    if (kFlow && a.ftrace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[2]));
+    if (kFlow && a.ftrace && lane == 0) {
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[2]));
+      fc0 = clock64();
+    }
     if (tr) {
       a.trace[size_t(ch) * 16 + 1] = clock64();
       a.trace[size_t(ch) * 16 + 3] = ne;
@@ -941,81 +1008,71 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
     // row through shuffles; each row still takes its operations in column
     // order, so the result is bitwise that of the sequential fold
     bool par = false;
-    if (kFwd) {
-      const unsigned full = 0xffffffffu;
-      const int nrows = r1 - r0;
-      const int len = lane < nrows ? mb[w][lane].x : 0;
-      int off = len;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int t = __shfl_up_sync(full, off, d);
-        if (lane >= d) off += t;
+    if (kFwd && trail_ok && nrows > 1) {
+      par = true;
+      double acc = 0.0;
+      int cur = 0;
+      if (lane < nrows) {
+        acc = chain_sub(rb[w][lane], &rec[w][roff], fin);
+        cur = fin;
       }
-      off -= len;
-      // one pass per lane: fold the out-of-task prefix while checking that
-      // only in-task (or pad) entries follow it
-      bool ok = true;
-      int first_in = len;
-      double acc = lane < nrows ? rb[w][lane] : 0.0;
-      int e = 0;
-      for (; e + 4 <= len; e += 4) {
-        double2 q4[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) q4[k] = rec[w][off + e + k];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int sidx = int(__double_as_longlong(q4[k].y));
-          if (first_in == len) {
-            if (sidx >= 0) first_in = e + k;
-            else acc = dsub(acc, q4[k].x);
-          } else if (sidx < 0 && sidx != kPadSrc) {
-            ok = false;
+      for (int sr = 0; sr < nrows; ++sr) {
+        const double xs = __shfl_sync(full, acc, sr);
+        if (lane > sr && lane < nrows && cur < rlen) {
+          const double2 r2 = rec[w][roff + cur];
+          if (int(__double_as_longlong(r2.y)) == sr) {
+            acc = dsub(acc, dmul(r2.x, xs));
+            ++cur;
           }
         }
       }
-      for (; e < len; ++e) {
-        const double2 q1 = rec[w][off + e];
-        const int sidx = int(__double_as_longlong(q1.y));
-        if (first_in == len) {
-          if (sidx >= 0) first_in = e;
-          else acc = dsub(acc, q1.x);
-        } else if (sidx < 0 && sidx != kPadSrc) {
-          ok = false;
-        }
+      if (lane < nrows) {
+        const int4 m = mb[w][lane];
+        if (kFlow) flow_store(y + m.y, acc);
+        else y[m.y] = acc;
+        yb[m.z] = acc;
       }
-      par = nrows > 1 && __all_sync(full, ok);
-      if (par) {
-        int cur = first_in;
-        for (int sr = 0; sr < nrows; ++sr) {
-          const double xs = __shfl_sync(full, acc, sr);
-          if (lane > sr && lane < nrows && cur < len) {
-            const double2 r2 = rec[w][off + cur];
-            if (int(__double_as_longlong(r2.y)) == sr) {
-              acc = dsub(acc, dmul(r2.x, xs));
-              ++cur;
-            }
-          }
-        }
-        if (lane < nrows) {
-          const int4 m = mb[w][lane];
-          if (kFlow) flow_store(y + m.y, acc);
-          else y[m.y] = acc;
-          yb[m.z] = acc;
-        }
 #ifdef PSCU_TRACE
-        if (kFlow && a.ftrace && lane == 0) {
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[3]));
-          long long* ft = a.ftrace + (size_t(hd[9]) + task) * 4;
-          for (int q = 0; q < 4; ++q) ft[q] = (long long)fts[q];
-        }
-#endif
+      if (kFlow && a.ftrace && lane == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[3]));
+        long long* ft = a.ftrace + (size_t(hd[9]) + task) * 6;
+        for (int q = 0; q < 4; ++q) ft[q] = (long long)fts[q];
+        ft[4] = clock64() - fc0;
+        ft[5] = 1;
       }
+#endif
     }
-    if (!par && lane == 0) {
-      // the next kFoldAhead entries' records are loaded while the current
-      // ones are subtracted (rows hold whole 8-entry blocks, so the
-      // look-ahead carries across rows; indices past the task clamp to the
-      // buffer). Config 5: 4.64 vs 4.77 ms per ILU apply.
+    if (!par && lane == 0 && lead_ok) {
+      // every row: its leading in-task terms, then a pure product chain
+      for (int r = 0; r < nrows; ++r) {
+        const int4 m = mb[w][r];
+        const int2 ri = rinfo[w][r];
+        double acc = rb[w][r];
+        for (int t = 0; t < ri.y; ++t) {
+          const double2 r2 = rec[w][ri.x + t];
+          acc = dsub(acc, dmul(r2.x, cv[w][int(__double_as_longlong(r2.y))]));
+        }
+        acc = chain_sub(acc, &rec[w][ri.x + ri.y], m.x - ri.y);
+        if (!kFwd) acc = __ddiv_rn(acc, dvb[w][r]);
+        cv[w][r] = acc;
+        if (kFlow) flow_store(y + m.y, acc);
+        else y[m.y] = acc;
+        if (kFwd) yb[m.z] = acc;
+      }
+#ifdef PSCU_TRACE
+      if (kFlow && a.ftrace) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[3]));
+        long long* ft = a.ftrace + (size_t(hd[9]) + task) * 6;
+        for (int q = 0; q < 4; ++q) ft[q] = (long long)fts[q];
+        ft[4] = clock64() - fc0;
+        ft[5] = 2;
+      }
+#endif
+    } else if (!par && lane == 0) {
+      // general order: the next kFoldAhead entries' records are loaded while
+      // the current ones are subtracted (rows hold whole 8-entry blocks, so
+      // the look-ahead carries across rows; indices past the task clamp to
+      // the buffer)
       int e = 0;
       double2 nx[kFoldAhead];
 #pragma unroll
@@ -1055,8 +1112,10 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
 #ifdef PSCU_TRACE
       if (kFlow && a.ftrace) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[3]));
-        long long* ft = a.ftrace + (size_t(hd[9]) + task) * 4;
+        long long* ft = a.ftrace + (size_t(hd[9]) + task) * 6;
         for (int q = 0; q < 4; ++q) ft[q] = (long long)fts[q];
+        ft[4] = clock64() - fc0;
+        ft[5] = 0;
       }
       if (tr) a.trace[size_t(ch) * 16 + 2] = clock64();
       if (tr2) {
@@ -2550,8 +2609,8 @@ static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y,
     DevBuf<long long> ftb;
     const bool ft_now = ft_path && w.ny > 100000 && sweep_no++ / 2 == ft_at;
     if (ft_now) {
-      ftb.alloc(size_t(w.tt.n) * 4 + 4);
-      PSCU_CUDA(cudaMemsetAsync(ftb.p, 0, sizeof(long long) * (size_t(w.tt.n) * 4 + 4), c.stream));
+      ftb.alloc(size_t(w.tt.n) * 6 + 6);
+      PSCU_CUDA(cudaMemsetAsync(ftb.p, 0, sizeof(long long) * (size_t(w.tt.n) * 6 + 6), c.stream));
       a.ftrace = ftb.p;
     }
 #endif
@@ -2569,7 +2628,7 @@ static void run_one(Context& c, const WalkPlan& w, const double* rhs, double* y,
     PSCU_LAUNCHED(&c);
 #ifdef PSCU_TRACE
     if (ft_now) {
-      std::vector<long long> st(size_t(w.tt.n) * 4);
+      std::vector<long long> st(size_t(w.tt.n) * 6);
       std::vector<int32_t> hdr(size_t(w.nsub) * kHdr);
       PSCU_CUDA(cudaMemcpyAsync(st.data(), ftb.p, sizeof(long long) * st.size(), cudaMemcpyDeviceToHost, c.stream));
       PSCU_CUDA(cudaMemcpyAsync(hdr.data(), w.sl_hdr.p, sizeof(int32_t) * hdr.size(), cudaMemcpyDeviceToHost, c.stream));

@@ -323,6 +323,8 @@ def load3():
         lib.psh3_block_pattern.argtypes = [vp, vp, vp]
         lib.psh3_face_projection.argtypes = [vp, C.c_int, vp]
         lib.psh3_geometry.argtypes = [vp, vp]
+        lib.psh3_device_inputs.argtypes = [vp, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, vp,
+                                           vp, vp, vp, vp, vp]
         lib._psh3 = True
     return lib
 
@@ -380,6 +382,30 @@ class Mesh3:
         lib.psh3_block_pattern(self.h, rp.ctypes.data, cols.ctypes.data)
         return rp, cols
 
+    def device_inputs(self, k: int, data: str = "random", seed: int = 0, e0: int = 0,
+                      e1: int | None = None, mesh_tables: bool = True) -> dict:
+        """psh3_device_inputs: what the device local-block producer reads for
+        elements [e0, e1) (hex, ef, es, coef; batch-relative) and, with
+        mesh_tables, the whole-mesh vertices, face table and quadrature rule."""
+        e1 = self.n_elements if e1 is None else e1
+        m = e1 - e0
+        npk = (k + 1) * (k + 2) * (k + 3) // 6
+        d = dict(hex=np.zeros(8 * m, np.int32), ef=np.zeros(6 * m, np.int32),
+                 es=np.zeros(6 * m, np.int32),
+                 coef=np.zeros(3 * npk * m) if DATA3[data] == 3 else None)
+        gl = np.zeros(16) if mesh_tables else None
+        ftab = np.zeros(5 * self.n_faces, np.int32) if mesh_tables else None
+        npts = self.lib.psh3_device_inputs(self.h, k, DATA3[data], seed, e0, e1,
+                                           d["hex"].ctypes.data, d["ef"].ctypes.data,
+                                           d["es"].ctypes.data, N.ptr(ftab), N.ptr(gl),
+                                           N.ptr(d["coef"]))
+        if npts < 0:
+            _check3(-npts)
+        if mesh_tables:
+            d.update(nq1=npts, gl=np.ascontiguousarray(gl[:2 * npts]), ftab=ftab,
+                     xyz=self.vertices().ravel())
+        return d
+
     def face_projection(self, k: int) -> np.ndarray:
         nf = (k + 1) * (k + 2) // 2
         out = np.zeros(self.n_faces * 4 * nf)
@@ -423,17 +449,121 @@ class HpLocal3:
         return mats, rhs
 
 
-def assemble_stokes3(mesh: Mesh3, k: int, data: str = "random", seed: int = 0, eta: float = 0.0,
-                     batch: int = 4096, nthreads: int = 0, ctx=None, recovery: bool = False):
-    """assemble_hho (assemble.hpp:136-172) for the 3D HHO-hp vp-cond scheme
-    into face-block device storage, streamed over element batches: the host
-    builds a batch of local blocks, the device condenses it and scatters the
-    Schur blocks and reduced loads (pscu_assembly_add). Returns (A, rhs,
-    layout, info) with A a device CsrMatrix in block storage; with recovery
-    the per-element elim_coupling / elim_rhs are returned in info."""
+def _assemble_stokes3_device(mesh, k, data, seed, eta, batch, ctx, recovery):
+    """assemble_stokes3 with the local blocks built on the device: per batch
+    the host packs the element connectivity (and data-3 coefficients), the
+    device builds the blocks into a device buffer and condenses / scatters
+    them in place (pscu_local_blocks3 + pscu_assembly_add, device memory)."""
+    import time
+
+    import torch
+
+    from . import solver as S
+
+    dev = torch.device("cuda", 0)
+    L = HpLocal3(k)
+    brp, bcols = mesh.block_pattern()
+    h = C.c_void_p()
+    N.check(ctx.lib.pscu_assembly_begin(ctx.h, mesh.n_faces, L.face_block, brp.ctypes.data,
+                                        bcols.ctypes.data, C.byref(h)))
+    A = S.CsrMatrix(None, None, None, ctx=ctx, _handle=h.value)
+    A._owned = True
+    keep_pos = np.ascontiguousarray(L.keep_pos, np.int32)
+    n = L.n_local
+    nb = min(batch, mesh.n_elements)
+    tab = mesh.device_inputs(k, data, seed, 0, 0)
+    xyz = torch.as_tensor(tab["xyz"], device=dev)
+    ftab = torch.as_tensor(tab["ftab"], device=dev)
+    gl = torch.as_tensor(tab["gl"], device=dev)
+    mats = torch.empty(nb * n * n, dtype=torch.float64, device=dev)
+    rhs = torch.empty(nb * n, dtype=torch.float64, device=dev)
+    eta_v = eta if eta > 0.0 else 3.0 * (k + 1) * (k + 1)
+    coup = erhs = None
+    if recovery:
+        coup = np.empty((mesh.n_elements, L.n_elim, L.n_keep))
+        erhs = np.empty((mesh.n_elements, L.n_elim))
+        cpd = torch.empty(nb * L.n_elim * L.n_keep, dtype=torch.float64, device=dev)
+        epd = torch.empty(nb * L.n_elim, dtype=torch.float64, device=dev)
+    t_local = t_dev = 0.0
+    for e0 in range(0, mesh.n_elements, nb):
+        e1 = min(mesh.n_elements, e0 + nb)
+        m = e1 - e0
+        d = mesh.device_inputs(k, data, seed, e0, e1, mesh_tables=False)
+        hx = torch.as_tensor(d["hex"], device=dev)
+        ef = torch.as_tensor(d["ef"], device=dev)
+        es = torch.as_tensor(d["es"], device=dev)
+        cf = torch.as_tensor(d["coef"], device=dev) if d["coef"] is not None else None
+        torch.cuda.current_stream(dev).synchronize()
+        t0 = time.perf_counter()
+        N.check(ctx.lib.pscu_local_blocks3(ctx.h, k, DATA3[data], eta_v, tab["nq1"], gl.data_ptr(),
+                                           mesh.n_vertices, xyz.data_ptr(), mesh.n_faces,
+                                           ftab.data_ptr(), m, hx.data_ptr(), ef.data_ptr(),
+                                           es.data_ptr(), N.ptr(cf), mats.data_ptr(),
+                                           rhs.data_ptr(), N.PSCU_DEVICE))
+        t1 = time.perf_counter()
+        N.check(ctx.lib.pscu_assembly_add(ctx.h, A.h, e0, m, n, mats.data_ptr(), rhs.data_ptr(),
+                                          L.n_elim, L.elim.ctypes.data, ef.data_ptr(), 6,
+                                          keep_pos.ctypes.data,
+                                          cpd.data_ptr() if recovery else None,
+                                          epd.data_ptr() if recovery else None, N.PSCU_DEVICE))
+        if recovery:
+            cp = cpd[:m * L.n_elim * L.n_keep].cpu().numpy()
+            coup[e0:e1] = np.transpose(cp.reshape(m, L.n_keep, L.n_elim), (0, 2, 1))
+            erhs[e0:e1] = epd[:m * L.n_elim].cpu().numpy().reshape(m, L.n_elim)
+        t_local += t1 - t0
+        t_dev += time.perf_counter() - t1
+    del mats, rhs
+    b = np.zeros(A.n)
+    N.check(ctx.lib.pscu_assembly_rhs(ctx.h, A.h, b.ctypes.data, N.PSCU_HOST))
+    lay = S.make_layout3(k, mesh.n_faces, mesh.n_elements)
+    info = dict(t_local_s=t_local, t_condense_s=t_dev, brow_ptr=brp, bcols=bcols, local=L,
+                elim_coupling=coup, elim_rhs=erhs, producer="device")
+    return A, b, lay, info
+
+
+def local_blocks3_device(mesh: Mesh3, k: int, e0: int, e1: int, data: str = "random",
+                         seed: int = 0, eta: float = 0.0, ctx=None):
+    """The 3D local blocks of elements [e0, e1) built on the device
+    (pscu_local_blocks3), host buffers in and out: the same arrays as
+    HpLocal3.local_blocks, bit for bit."""
     from . import solver as S
 
     ctx = ctx or S.default_context()
+    L = HpLocal3(k)
+    d = mesh.device_inputs(k, data, seed, e0, e1)
+    m, n = e1 - e0, L.n_local
+    mats, rhs = np.zeros(m * n * n), np.zeros(m * n)
+    eta_v = eta if eta > 0.0 else 3.0 * (k + 1) * (k + 1)
+    N.check(ctx.lib.pscu_local_blocks3(ctx.h, k, DATA3[data], eta_v, d["nq1"], d["gl"].ctypes.data,
+                                       mesh.n_vertices, d["xyz"].ctypes.data, mesh.n_faces,
+                                       d["ftab"].ctypes.data, m, d["hex"].ctypes.data,
+                                       d["ef"].ctypes.data, d["es"].ctypes.data, N.ptr(d["coef"]),
+                                       mats.ctypes.data, rhs.ctypes.data, N.PSCU_HOST))
+    return mats, rhs
+
+
+def assemble_stokes3(mesh: Mesh3, k: int, data: str = "random", seed: int = 0, eta: float = 0.0,
+                     batch: int = 4096, nthreads: int = 0, ctx=None, recovery: bool = False,
+                     producer: str = "auto"):
+    """assemble_hho (assemble.hpp:136-172) for the 3D HHO-hp vp-cond scheme
+    into face-block device storage, streamed over element batches: a batch of
+    local blocks is built — on the device (pscu_local_blocks3, producer
+    "device"; the default for data "zero"/"random") or by the host producer
+    ("host", overlapped with the device work; needed for "manufactured") —
+    and the device condenses it and scatters the Schur blocks and reduced
+    loads (pscu_assembly_add). Both producers give the same blocks bit for
+    bit. Returns (A, rhs, layout, info) with A a device CsrMatrix in block
+    storage; with recovery the per-element elim_coupling / elim_rhs are
+    returned in info."""
+    from . import solver as S
+
+    ctx = ctx or S.default_context()
+    if producer == "auto":
+        producer = "device" if DATA3[data] in (0, 3) else "host"
+    if producer == "device":
+        return _assemble_stokes3_device(mesh, k, data, seed, eta, batch, ctx, recovery)
+    if producer != "host":
+        raise ValueError(f"unknown producer {producer!r}")
     L = HpLocal3(k)
     brp, bcols = mesh.block_pattern()
     h = C.c_void_p()

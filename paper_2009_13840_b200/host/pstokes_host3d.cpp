@@ -1006,6 +1006,58 @@ int psh3_local_blocks(const psh_mesh3* pm, int k, int data, uint64_t seed, doubl
   });
 }
 
+/// Inputs of the device local-block producer (pscu_local_blocks3) for
+/// elements [e0, e1): hexahedron vertex ids (8 per element), element faces
+/// and orientation signs (6 each), the face table {4 vertex ids, tag}
+/// (all faces), the Gauss-Legendre rule of the degree-2(k+1)+1 tensor rules
+/// (points then weights, rule_points entries each) and, for data 3, the
+/// per-element random modal coefficients (3 x dim P_k(3D), SplitMix64 /
+/// Box-Muller on the host's libm, as build_local draws them). Null outputs
+/// are skipped; returns the rule size.
+int psh3_device_inputs(const psh_mesh3* pm, int k, int data, uint64_t seed, int e0, int e1,
+                       int32_t* hex, int32_t* ef, int32_t* es, int32_t* ftab, double* gl,
+                       double* coef) {
+  int npts = 0;
+  const int rc = guard([&] {
+    const Mesh& m = pm->m;
+    if (k < 0 || k > 4) throw std::invalid_argument("hho3: k must be in [0, 4]");
+    if (e0 < 0 || e1 > m.nelem() || e0 > e1) throw std::invalid_argument("hho3: element range");
+    const int qd = 2 * (k + 1) + 1;
+    npts = rule_points(qd);
+    for (int e = e0; e < e1; ++e) {
+      const size_t i = size_t(e - e0);
+      if (hex)
+        for (int a = 0; a < 8; ++a) hex[8 * i + a] = m.hex[e][a];
+      for (int lf = 0; lf < 6; ++lf) {
+        if (ef) ef[6 * i + lf] = m.ef[e][lf];
+        if (es) es[6 * i + lf] = m.es[e][lf];
+      }
+    }
+    if (ftab)
+      for (int f = 0; f < m.nfaces(); ++f) {
+        for (int a = 0; a < 4; ++a) ftab[5 * f + a] = m.fv[f][a];
+        ftab[5 * f + 4] = m.tag[f];
+      }
+    if (gl) {
+      std::vector<double> x, w;
+      gauss_legendre(npts, x, w);
+      for (int i = 0; i < npts; ++i) {
+        gl[i] = x[i];
+        gl[npts + i] = w[i];
+      }
+    }
+    if (coef && data == 3) {
+      const int np = dimP3(k);
+      for (int e = e0; e < e1; ++e) {
+        SplitMix64 rng{seed + uint64_t(e) * uint64_t(6 * np) * 0x9e3779b97f4a7c15ULL};
+        double* c = coef + size_t(e - e0) * 3 * np;
+        for (int t = 0; t < 3 * np; ++t) c[t] = rng.normal();
+      }
+    }
+  });
+  return rc ? -rc : npts;
+}
+
 /// Face-block pattern of the condensed hho-hp vp-cond operator: block row f
 /// couples every face of the (<= 2) elements holding f, columns ascending.
 /// Returns the block count; brow_ptr (n_faces + 1) / bcols may be null.

@@ -541,3 +541,42 @@ def test_ilu0_oversize_tasks_bitwise(S, monkeypatch, mode):
     for seed in range(2):
         x = np.random.default_rng(seed).standard_normal(a.n)
         assert ilu.apply(x).tobytes() == ri.apply(x).tobytes()
+
+
+def _banded(n, seed):
+    """Diagonally dominant banded CSR (columns i-3, i-1, i, i+1, i+5):
+    a cheap stand-in with the coarse level's size for Krylov parity."""
+    rng = np.random.default_rng(seed)
+    offs = np.array([-3, -1, 0, 1, 5])
+    rows = np.repeat(np.arange(n), len(offs))
+    cols = (rows.reshape(n, -1) + offs).ravel()
+    keep = (cols >= 0) & (cols < n)
+    rows, cols = rows[keep], cols[keep]
+    vals = rng.uniform(-1.0, 1.0, len(cols))
+    vals[rows == cols] = 3.0 + rng.uniform(0.0, 1.0, n)
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    return O.Csr(np.cumsum(rp), cols.astype(np.int32), vals)
+
+
+@pytest.mark.parametrize("n,force", [(400_000, "1"), (3_194_880, "0")],
+                         ids=["forced-400k", "config5-coarse-size"])
+def test_gmres_smem_arnoldi_bitwise(S, monkeypatch, n, force):
+    """The shared-memory Arnoldi step (arnoldi_smem_kernel: w resident in
+    shared memory, 2048 lanes per CTA, basis vectors streamed through L2):
+    forced at 400 k unknowns, and at the config-5 coarse size (3,194,880:
+    2^18 lanes, 13 elements per lane, 128 CTAs) where it is the production
+    path. Unpreconditioned GMRES (the banded matrix's ILU(0) would be one
+    sequential chain), bitwise against the reference."""
+    monkeypatch.setenv("PSCU_MGS_FORCE_SMEM", force)
+    a = _banded(n, 3)
+    ra = O.RefCsr(a)
+    m = S.CsrMatrix(a.row_ptr, a.cols, a.vals)
+    rng = np.random.default_rng(9)
+    b = rng.standard_normal(n)
+    x0 = rng.standard_normal(n)
+    maxit = 40 if n < 1_000_000 else 24
+    r = O.ref_gmres(ra, None, b, x0, maxit, 0.0)
+    g = S.gmres(m, None, b, x0, maxit, 0.0)
+    assert g.iterations == r["its"] and g.rel_residual == r["rel"]
+    assert same(g.x, r["x"])

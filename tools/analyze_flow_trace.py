@@ -13,7 +13,9 @@ def load(path):
     raw = open(path, "rb").read()
     nsub, ntt = np.frombuffer(raw[:16], np.int64)
     hdr = np.frombuffer(raw[16:16 + 4 * 16 * nsub], np.int32).reshape(nsub, 16)
-    st = np.frombuffer(raw[16 + 4 * 16 * nsub:], np.int64).reshape(ntt, 4)
+    body = raw[16 + 4 * 16 * nsub:]
+    stride = len(body) // (8 * ntt)  # 4 (stamps) or 6 (+ fold cycles, lane-parallel flag)
+    st = np.frombuffer(body[:8 * ntt * stride], np.int64).reshape(ntt, stride)
     return hdr, st
 
 
@@ -39,6 +41,14 @@ def main(path):
           f"wait for sources {r[:, 5].mean():.0f} ns, fold {r[:, 6].mean():.0f} ns "
           f"(slowest fold per level {r[:, 7].mean():.0f} ns)")
     print(f"  tasks per level: median {np.median(r[:, 1]):.0f}")
+    if st.shape[1] >= 6:
+        done = st[st[:, 3] > 0]
+        par = done[:, 5] == 1
+        for name, sel in (("lane-parallel", par), ("lane-0", ~par)):
+            if sel.any():
+                cyc = done[sel, 4]
+                print(f"  {name} folds: {int(sel.sum())} tasks, {np.median(cyc):.0f} cycles median, "
+                      f"p90 {np.percentile(cyc, 90):.0f}")
 
 
 if __name__ == "__main__":
