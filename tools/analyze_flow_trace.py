@@ -41,10 +41,29 @@ def main(path):
           f"wait for sources {r[:, 5].mean():.0f} ns, fold {r[:, 6].mean():.0f} ns "
           f"(slowest fold per level {r[:, 7].mean():.0f} ns)")
     print(f"  tasks per level: median {np.median(r[:, 1]):.0f}")
+    # the critical path level by level: the task that finishes a level last,
+    # measured from the previous level's last finish
+    lastf = []
+    for ch in range(len(hdr)):
+        nt, t0 = int(hdr[ch, 8]), int(hdr[ch, 9])
+        s = st[t0:t0 + nt]
+        s = s[s[:, 3] > 0]
+        if len(s):
+            lastf.append(s[np.argmax(s[:, 3])])
+    lastf = np.array(lastf)
+    if len(lastf) > 2:
+        prev = lastf[:-1, 3]
+        cur = lastf[1:]
+        print(f"  level-closing task vs previous level's close: start {np.median(cur[:, 0] - prev):.0f} ns, "
+              f"loads done {np.median(cur[:, 1] - prev):.0f} ns, sources in {np.median(cur[:, 2] - prev):.0f} ns, "
+              f"folded {np.median(cur[:, 3] - prev):.0f} ns (medians)")
+        if st.shape[1] >= 6:
+            print(f"  level-closing task fold: {np.median(cur[:, 4]):.0f} cycles median")
     if st.shape[1] >= 6:
         done = st[st[:, 3] > 0]
-        par = done[:, 5] == 1
-        for name, sel in (("lane-parallel", par), ("lane-0", ~par)):
+        kinds = done[:, 5]
+        for name, sel in (("lane-parallel", kinds == 1), ("lane-0 leading in-task + chain", kinds == 2),
+                          ("lane-0 general order", kinds == 0)):
             if sel.any():
                 cyc = done[sel, 4]
                 print(f"  {name} folds: {int(sel.sum())} tasks, {np.median(cyc):.0f} cycles median, "
