@@ -782,16 +782,6 @@ constexpr int kFoldAhead = PSCU_FOLD_AHEAD;  // look-ahead of the pipelined task
 /// value is no longer the sentinel — no grid barrier between task levels.
 constexpr unsigned long long kFlowSentinel = 0xFFF7DEADBEEF5A5Aull;
 
-__device__ __forceinline__ double flow_wait(const double* p, int spin_ns = 0) {
-  unsigned long long v;
-  for (;;) {
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    if (v != kFlowSentinel) break;
-    if (spin_ns) __nanosleep(spin_ns);
-  }
-  return __longlong_as_double((long long)v);
-}
-
 __device__ __forceinline__ unsigned long long flow_peek(const double* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");

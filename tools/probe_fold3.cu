@@ -130,6 +130,104 @@ __global__ void fold(const double2* g, const double* dv, long long* cyc, double*
   }
 }
 
+__global__ void fold_many(const double2* g, const double* dv, long long* cyc, double* out, int variant) {
+  // every warp of the grid folds its own copy (issue / FP64 pipe sharing of a loaded SM)
+  __shared__ double2 rec[8][kN + 16];
+  __shared__ double cv[8][kRows];
+  __shared__ double dvb[8][kRows];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = lane; i < kN; i += 32) rec[w][i] = g[i];
+  if (lane < 16) rec[w][kN + lane] = make_double2(0.0, __longlong_as_double(-1ll));
+  if (lane < kRows) dvb[w][lane] = dv[lane];
+  __syncwarp();
+  double acc = 0.0;
+  long long t0 = clock64();
+  if (lane == 0 || variant == 5) {
+    int e = 0;
+    for (int r = 0; r < kRows; ++r) {
+      acc = 1.0 + r;
+      const int e1 = e + kLen;
+      if (variant == 6) {
+        for (;;) {
+          const double2 r2 = rec[w][e];
+          const int s = src_of(r2);
+          if (e >= e1 || s < 0) break;
+          acc = __dsub_rn(acc, __dmul_rn(r2.x, cv[w][s]));
+          ++e;
+        }
+        // the tail in register batches of 16 (all loads issued, then the chain)
+        for (; e < e1; e += 16) {
+          double b[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) b[k] = e + k < e1 ? rec[w][e + k].x : 0.0;
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (e + k < e1) acc = __dsub_rn(acc, b[k]);
+        }
+        e = e1;
+      } else if (variant == 5) {
+        // warp-cooperative: leading in-task terms warp-uniformly, then the
+        // tail's products one per lane, folded through shuffles
+        for (;;) {
+          const double2 r2 = rec[w][e];
+          const int s = src_of(r2);
+          if (e >= e1 || s < 0) break;
+          acc = __dsub_rn(acc, __dmul_rn(r2.x, cv[w][s]));
+          ++e;
+        }
+        for (int base = e; base < e1; base += 32) {
+          const double p = base + lane < e1 ? rec[w][base + lane].x : 0.0;
+          const int cnt = e1 - base < 32 ? e1 - base : 32;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const double x = __shfl_sync(0xffffffffu, p, k);
+            if (k < cnt) acc = __dsub_rn(acc, x);
+          }
+        }
+        e = e1;
+      } else if (variant == 2) {
+        for (;;) {
+          const double2 r2 = rec[w][e];
+          const int s = src_of(r2);
+          if (e >= e1 || s < 0) break;
+          acc = __dsub_rn(acc, __dmul_rn(r2.x, cv[w][s]));
+          ++e;
+        }
+        double nx[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nx[k] = rec[w][e + k].x;
+        for (; e + 4 <= e1; e += 4) {
+          double cur[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) cur[k] = nx[k];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) nx[k] = rec[w][e + 4 + k].x;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc = __dsub_rn(acc, cur[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (e + k < e1) acc = __dsub_rn(acc, nx[k]);
+        e = e1;
+      } else {
+        for (; e < e1; ++e) {
+          const double2 r2 = rec[w][e];
+          const int s = src_of(r2);
+          acc = __dsub_rn(acc, s < 0 ? r2.x : __dmul_rn(r2.x, cv[w][s]));
+        }
+      }
+      acc = __ddiv_rn(acc, dvb[w][r]);
+      if (lane == 0) cv[w][r] = acc;
+      __syncwarp(variant == 5 ? 0xffffffffu : 1u);
+    }
+  }
+  long long t1 = clock64();
+  if (lane == 0 && blockIdx.x == 0 && w == 0) {
+    out[variant] = acc;
+    cyc[variant] = t1 - t0;
+  }
+}
+
 int main() {
   double2* g;
   double *o, *dv;
@@ -159,6 +257,16 @@ int main() {
     cudaMemcpy(hc, c, sizeof(hc), cudaMemcpyDeviceToHost);
     cudaMemcpy(res, o, sizeof(res), cudaMemcpyDeviceToHost);
     printf("%-28s %.1f cycles/entry (result %.17g)\n", nm[v], double(hc[v]) / kN, res[v]);
+  }
+  for (int v : {2, 6}) {
+    for (int ctas : {1, 148, 148 * 7}) {
+      fold_many<<<ctas, 128>>>(g, dv, c, o, v);
+      fold_many<<<ctas, 128>>>(g, dv, c, o, v);
+      long long hc[8];
+      cudaMemcpy(hc, c, sizeof(hc), cudaMemcpyDeviceToHost);
+      printf("fold_many variant %d, %4d CTAs x 4 warps: %.1f cycles/entry (whole task %lld cycles)\n", v,
+             ctas, double(hc[v]) / kN, hc[v]);
+    }
   }
   return 0;
 }
