@@ -61,6 +61,15 @@ CONFIGS3 = {
                     name="3D unit cube 64^3 hexahedra (jitter 0.1h, seed 4), HHO-hp vp-cond, k=2, "
                          "levels 2-1-0, V(2,2) block-Jacobi, random modal f (seed 5)",
                     ref_sample_n=8),
+    # config 4: the reference's DG (BR2, assemble.hpp:177-346) in 3D; levels
+    # 3-2-1 because DG needs a coarsest degree >= 1 (plevels.hpp:137-139,
+    # SURVEY.md §0 finding 7)
+    "config4": dict(dim=3, scheme="dg", n=32, jitter=0.0, seed=0, fseed=3, k=3,
+                    degrees=[3, 2, 1], smooth=2,
+                    name="3D unit cube 32^3 uniform hexahedra, DG (BR2) k=3 equal order "
+                         "(80x80 element blocks, DG block storage), levels 3-2-1, V(2,2) "
+                         "block-Jacobi, random modal f (seed 3)",
+                    ref_sample_n=4),
 }
 CONFIGS.update(CONFIGS3)
 METRIC = "condensed DoFs/s solved to rtol 1e-8 (FGMRES+p-MG V-cycle)"
@@ -242,6 +251,12 @@ def _port3_worker(args):
     from paper_2009_13840_b200 import host
 
     m = host.Mesh3(n, jitter=cfg["jitter"], seed=cfg["seed"])
+    if cfg.get("scheme") == "dg":
+        D = host.DgLocal3(cfg["k"])
+        lay = O.po_layout(2, 0, cfg["k"], m.n_faces, m.n_elements, dim=3)
+        a, b = O.port_dg_assemble(lay, m.faces(), *D.local_terms(m, data="random",
+                                                                 seed=cfg["fseed"], nthreads=1))
+        return _port3_solves(O, a, b, lay, cfg, rounds)
     L = host.HpLocal3(cfg["k"])
     mats, rhs = L.local_blocks(m, 0, m.n_elements, data="random", seed=cfg["fseed"], nthreads=1)
     brp, bcols = m.block_pattern()
@@ -250,6 +265,10 @@ def _port3_worker(args):
     a, b = O.port_condense_assemble(mats, rhs, L.n_local, L.elim, L.kept_global(m.element_faces()),
                                     lay, rp, cols)
     del mats
+    return _port3_solves(O, a, b, lay, cfg, rounds)
+
+
+def _port3_solves(O, a, b, lay, cfg, rounds):
     out = []
     for _ in range(rounds):
         t0 = time.perf_counter()
@@ -334,8 +353,14 @@ def run_ours3(args, cfg):
     ctx = S.Context(local)
     t0 = time.time()
     mesh = host.Mesh3(n, jitter=cfg["jitter"], seed=cfg["seed"])
-    A, b, lay, info = host.assemble_stokes3(mesh, cfg["k"], data="random", seed=cfg["fseed"],
+    dg = cfg.get("scheme") == "dg"
+    if dg:
+        A, b, lay, info = host.assemble_dg3(mesh, cfg["k"], data="random", seed=cfg["fseed"],
                                             ctx=ctx)
+        info.update(t_local_s=info["t_assembly_s"], t_condense_s=0.0)
+    else:
+        A, b, lay, info = host.assemble_stokes3(mesh, cfg["k"], data="random", seed=cfg["fseed"],
+                                                ctx=ctx)
     t_asm = time.time() - t0
     lcfg = S.LevelConfig(degrees=cfg["degrees"], smoother_iters=cfg["smooth"], coarse="gmres-ilu",
                          smoother="bjacobi", outer_rtol=RTOL, restart=RESTART)
@@ -380,7 +405,10 @@ def run_ours3(args, cfg):
     e2e_times = []
     for _ in range(max(1, args.e2e_steps)):
         ctx.timer_start()
-        x, hist, r2 = S.solve_system_bsr(brp, bcols, bvals, bs, bh, lay, lcfg, ctx=ctx)
+        if dg:
+            x, hist, r2 = S.solve_system_dgb(brp, bcols, bvals, A.dg_modes, bh, lay, lcfg, ctx=ctx)
+        else:
+            x, hist, r2 = S.solve_system_bsr(brp, bcols, bvals, bs, bh, lay, lcfg, ctx=ctx)
         e2e_times.append(ctx.timer_stop() / 1e3)
     t_e2e = max_over_ranks(statistics.mean(e2e_times))
     h2d = brp.nbytes + bcols.nbytes + bvals.nbytes + bh.nbytes
@@ -412,13 +440,15 @@ def run_ours3(args, cfg):
             "dofs": dofs, "nnz": A.nnz, "fgmres_its": rep.outer_its,
             "coarse_its_per_vcycle": rep.coarse_its / max(rep.vcycles, 1),
             "converged": rep.converged, "rel_residual": rep.rel_residual,
-            "smoother": f"block-Jacobi (24x24 face blocks) GMRES V({cfg['smooth']},{cfg['smooth']})",
+            "smoother": (f"block-Jacobi ({A.block_size}x{A.block_size} "
+                         f"{'element' if dg else 'face'} blocks) GMRES "
+                         f"V({cfg['smooth']},{cfg['smooth']})"),
             "coarse": "ILU-GMRES rtol 1e-3 maxit 400", "restart": RESTART,
             "step": "hierarchy setup + FGMRES (reference t_solve)",
             "l2": "inputs larger than L2 (fine operator %.2f GB)" % (8 * A.nnz / 1e9),
             "assembly_s_untimed": round(t_asm, 3),
             "local_blocks_host_s": round(info["t_local_s"], 3),
-            "condense_device_s": round(t_cond, 3),
+            "condense_device_s": round(t_cond, 3) if not dg else None,
             "dofs_per_s_incl_condense": dofs * ws / (t_step + t_cond),
             "parallelism": f"replicas x{ws}",
             "hierarchy_setup_s_in_step": round(setup_s[-1], 3),

@@ -139,7 +139,8 @@ int pscu_bj_apply(pscu_ctx* ctx, const pscu_bj* p, const double* x, double* y, i
 int pscu_layout_make(int scheme, int strategy, int k, int n_faces, int n_elements,
                      pscu_layout* out);
 /* 3D generalisation of make_layout (no reference: mesh.hpp is 2D): hho-hp
- * vp-cond only, face blocks [vx | vy | vz | p], no element unknowns. */
+ * vp-cond (face blocks [vx | vy | vz | p], no element unknowns) or dg uncond
+ * (element blocks [vx | vy | vz | p] of dim P^k(3D) modes, no face unknowns). */
 int pscu_layout_make3(int scheme, int strategy, int k, int n_faces, int n_elements,
                       pscu_layout* out);
 int64_t pscu_layout_dim(const pscu_layout* l);
@@ -240,6 +241,31 @@ int pscu_host_alloc(int64_t bytes, void** out);
 int pscu_host_free(void* p);
 /* pscu_solve_system on a face-block operator (host buffers, copies timed). */
 int pscu_solve_system_bsr(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow_ptr,
+                          const int32_t* bcols, const double* vals, const double* rhs,
+                          const pscu_layout* lf, const int* degrees, int nlev,
+                          const pscu_level_cfg* cfg, double rtol, int maxit, int restart,
+                          double* x, double* hist, pscu_report* rep);
+
+/* DG block storage (3D DG, BASELINE.json config 4: the reference's BR2
+ * assemble_dg, assemble.hpp:177-346, with three velocity components). The
+ * operator couples element blocks [ux | uy | uz | p] of nm modes each but
+ * not velocity components with each other (DofLayout::couples_components,
+ * dof_layout.hpp:79-84), so each block stores its 10 nm^2 structural
+ * entries as column-major panels: velocity component c's rows (nm x 2nm,
+ * columns [u_c | p]) at c 2nm^2, pressure rows (nm x 4nm, [ux|uy|uz|p]) at
+ * 6nm^2. Block row e covers rows [e 4nm, (e+1) 4nm); bcols ascending; vals
+ * NULL = zero. Every pscu_mat operation accepts it, bit-identical to the
+ * CSR expansion (pscu_mat_download). nm: 4, 10, 20 or 35 (k = 1..4). */
+int pscu_dgb_create(pscu_ctx* ctx, int64_t nb, int nm, const int64_t* brow_ptr,
+                    const int32_t* bcols, const double* vals, int mem, pscu_mat** out);
+/* 0 unless DG block storage, else the modes per component. */
+int pscu_mat_dg_modes(const pscu_mat* m);
+/* Writes count values at offset of any storage's value array (streamed
+ * producers fill an operator block range by block range). */
+int pscu_mat_set_values(pscu_ctx* ctx, pscu_mat* m, int64_t offset, int64_t count,
+                        const double* vals, int mem);
+/* pscu_solve_system on a DG block-stored operator (host buffers, timed). */
+int pscu_solve_system_dgb(pscu_ctx* ctx, int64_t nb, int nm, const int64_t* brow_ptr,
                           const int32_t* bcols, const double* vals, const double* rhs,
                           const pscu_layout* lf, const int* degrees, int nlev,
                           const pscu_level_cfg* cfg, double rtol, int maxit, int restart,

@@ -122,6 +122,29 @@ int psh3_device_inputs(const psh_mesh3* m, int k, int data, uint64_t seed, int e
                        int32_t* hex, int32_t* ef, int32_t* es, int32_t* ftab, double* gl,
                        double* coef);
 int64_t psh3_block_pattern(const psh_mesh3* m, int64_t* brow_ptr, int32_t* bcols);
+/* ---- DG (BR2) in 3D: BASELINE.json config 4 (the reference's DG scheme,
+ * assemble.hpp:177-346, with three velocity components; recipe in
+ * host/pstokes_host3d.cpp). Element blocks [ux | uy | uz | p], ne = dim
+ * P^k(3D) modes each; the operator's storage is the DG block storage of
+ * pscu_dgb_create (10 ne^2 structural entries per element pair). ---- */
+int psh3_dg_info(int k, int32_t* info);  /* info[0..1] = ne, 4 ne */
+/* Block row e: e and its neighbours across interior faces, ascending.
+ * Returns the block count; arrays nullable. */
+int64_t psh3_dg_block_pattern(const psh_mesh3* m, int64_t* brow_ptr, int32_t* bcols);
+/* Local terms for the oracle's reference-order scatter (small meshes):
+ * volume blocks (nelem x (4ne)^2) and loads, face blocks over [left | right]
+ * (nfaces x (8ne)^2, leading dimension 8ne) and face loads (nfaces x 8ne);
+ * data: PSH3_DATA_*; eta <= 0: the BR2 default 7. Outputs nullable. */
+int psh3_dg_local(const psh_mesh3* m, int k, int data, uint64_t seed, double eta, int nthreads,
+                  double* vol, double* vrhs, double* fmat, double* frhs);
+/* Block rows [e0, e1) of the assembled operator in DG block storage
+ * (blocks brow_ptr[e0] .. brow_ptr[e1]-1) and their loads, summed in the
+ * reference's scatter order (volume, then faces by id). */
+int psh3_dg_rows(const psh_mesh3* m, int k, int data, uint64_t seed, double eta, int e0, int e1,
+                 const int64_t* brow_ptr, const int32_t* bcols, int nthreads, double* vals,
+                 double* rhs);
+/* ||u_h - u||, ||p_h - p|| of a DG solution against the data-4 field. */
+int psh3_dg_l2_errors(const psh_mesh3* m, int k, const double* x, double* out);
 /* Face L2 projections of the manufactured solution (n_faces x 4 nf). */
 int psh3_face_projection(const psh_mesh3* m, int k, double* out);
 /* nelem volumes, then nelem closure norms |sum_F int_F n dA|. */

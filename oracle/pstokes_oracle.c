@@ -71,15 +71,27 @@ static int64_t elem_block(const po_layout* l) { return ncomp(l) * l->elem_vel + 
  * (k+1)(k+2)/2 modes */
 int po_make_layout3(int scheme, int strategy, int k, int n_faces, int n_elements, po_layout* l) {
   if (k < 0) return set_err("layout: k must be >= 0");
-  if (scheme != 1 || strategy != 2) return set_err("3D layout: hho-hp vp-cond only");
+  if (scheme == 2) {
+    /* DG (config 4): element blocks [ux | uy | uz | p] of dim P^k(3D) modes
+     * each (dof_layout.hpp:118-123 with three components) */
+    if (k < 1) return set_err("dg: k must be >= 1");
+    if (strategy != 0) return set_err("dg: no static condensation exists, use uncond");
+  } else if (scheme != 1 || strategy != 2) {
+    return set_err("3D layout: hho-hp vp-cond or dg uncond only");
+  }
   memset(l, 0, sizeof *l);
   l->scheme = scheme;
   l->strategy = strategy;
   l->k = k;
   l->n_faces = n_faces;
   l->n_elements = n_elements;
-  l->face_vel = dim_p2(k);
-  l->face_press = dim_p2(k);
+  if (scheme == 2) {
+    l->elem_vel = (k + 1) * (k + 2) * (k + 3) / 6;
+    l->elem_press = l->elem_vel;
+  } else {
+    l->face_vel = dim_p2(k);
+    l->face_press = dim_p2(k);
+  }
   l->dim = 3;
   return 0;
 }
@@ -1034,7 +1046,7 @@ static int coupled(const po_layout* l, int ka, int kb) {
   const int nc = ncomp(l);
   const int av = ka != nc, bv = kb != nc;
   if (av && bv && ka != kb) return l->strategy == 2;
-  if (!av && !bv) return l->strategy != 0;
+  if (!av && !bv) return l->strategy != 0 || l->scheme == 2; /* couples_pressures() */
   return 1;
 }
 
@@ -1084,5 +1096,115 @@ int po_condense_assemble(int nelem, int n, const double* mats, const double* rhs
   free(coup);
   free(er);
   free(kinds);
+  return rc;
+}
+
+/* ---------------------------------------------------------------------------
+ * DG assembly (assemble.hpp:177-346) from shared local terms: the structural
+ * pattern (add_pattern_block per element, add_pattern_cross per interior
+ * face, then from_pattern's sort: assemble.hpp:203-211, csr.hpp:30-44) and
+ * the value scatter in the reference's order — every element's volume block
+ * (element order), then every face's block in face order, exact zeros skipped
+ * except on the diagonal (scatter_block, assemble.hpp:121-131); loads: the
+ * element's volume load, then the face loads in face order.
+ * ------------------------------------------------------------------------- */
+static int64_t dg_pattern_pass(const po_layout* l, int nfaces, const int32_t* left,
+                               const int32_t* right, int64_t* row_ptr, int32_t* cols) {
+  const int eb = (int)elem_block(l);
+  const int64_t n = po_layout_dim(l);
+  const int ne = l->n_elements;
+  /* neighbours per element (at most one face per neighbour) */
+  int32_t* nb = (int32_t*)malloc(sizeof(int32_t) * (size_t)ne * 8 + 1);
+  int* cnt = (int*)calloc((size_t)ne + 1, sizeof(int));
+  for (int e = 0; e < ne; ++e) nb[(size_t)e * 8 + cnt[e]++] = e;
+  for (int f = 0; f < nfaces; ++f)
+    if (right[f] >= 0) {
+      nb[(size_t)left[f] * 8 + cnt[left[f]]++] = right[f];
+      nb[(size_t)right[f] * 8 + cnt[right[f]]++] = left[f];
+    }
+  int64_t total = 0;
+  int* kinds = (int*)malloc(sizeof(int) * (size_t)eb);
+  for (int i = 0; i < eb; ++i) kinds[i] = dof_kind(l, (int64_t)i);
+  for (int e = 0; e < ne; ++e) {
+    /* ascending neighbour order */
+    int32_t* b = nb + (size_t)e * 8;
+    for (int i = 1; i < cnt[e]; ++i)
+      for (int j = i; j > 0 && b[j - 1] > b[j]; --j) {
+        const int32_t t = b[j];
+        b[j] = b[j - 1];
+        b[j - 1] = t;
+      }
+    for (int r = 0; r < eb; ++r) {
+      const int64_t row = (int64_t)e * eb + r;
+      if (row_ptr) row_ptr[row] = total;
+      for (int q = 0; q < cnt[e]; ++q)
+        for (int c = 0; c < eb; ++c) {
+          if (r != c || b[q] != e)
+            if (!coupled(l, kinds[r], kinds[c])) continue;
+          if (cols) cols[total] = (int32_t)((int64_t)b[q] * eb + c);
+          ++total;
+        }
+    }
+  }
+  if (row_ptr) row_ptr[n] = total;
+  free(nb);
+  free(cnt);
+  free(kinds);
+  return total;
+}
+
+int64_t po_dg_pattern(const po_layout* l, int nfaces, const int32_t* left, const int32_t* right,
+                      int64_t* row_ptr, int32_t* cols) {
+  if (l->scheme != 2 || l->n_faces != 0 && l->face_vel) return set_err("dg pattern: dg layout expected"), -1;
+  return dg_pattern_pass(l, nfaces, left, right, row_ptr, cols);
+}
+
+static int csr_add(const po_csr* pat, double* vals, int64_t i, int64_t j, double v) {
+  int64_t lo = pat->row_ptr[i], hi = pat->row_ptr[i + 1];
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (pat->cols[mid] < j) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo == pat->row_ptr[i + 1] || pat->cols[lo] != j)
+    return set_err("CsrMatrix::add: entry outside the sparsity pattern");
+  vals[lo] += v;
+  return 0;
+}
+
+static int scatter(const po_layout* l, const po_csr* pat, double* vals, const int64_t* g, int n,
+                   const double* m, int ld) {
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      if (g[i] != g[j] && !coupled(l, dof_kind(l, g[i]), dof_kind(l, g[j]))) continue;
+      const double v = m[(size_t)i + (size_t)j * ld];
+      if (!(v != 0.0 || g[i] == g[j])) continue;
+      if (csr_add(pat, vals, g[i], g[j], v)) return -1;
+    }
+  return 0;
+}
+
+int po_dg_assemble(const po_layout* l, int nfaces, const int32_t* left, const int32_t* right,
+                   const double* vol, const double* vrhs, const double* fmat, const double* frhs,
+                   const po_csr* pat, double* vals, double* rhs) {
+  const int eb = (int)elem_block(l), n2 = 2 * eb;
+  int64_t* g = (int64_t*)malloc(sizeof(int64_t) * (size_t)n2);
+  memset(vals, 0, sizeof(double) * (size_t)pat->row_ptr[pat->n]);
+  memset(rhs, 0, sizeof(double) * (size_t)pat->n);
+  int rc = 0;
+  for (int e = 0; e < l->n_elements && !rc; ++e) {
+    for (int i = 0; i < eb; ++i) g[i] = (int64_t)e * eb + i;
+    rc = scatter(l, pat, vals, g, eb, vol + (size_t)e * eb * eb, eb);
+    for (int i = 0; i < eb; ++i) rhs[g[i]] += vrhs[(size_t)e * eb + i];
+  }
+  for (int f = 0; f < nfaces && !rc; ++f) {
+    const int ns = right[f] >= 0 ? 2 : 1;
+    for (int s = 0; s < ns; ++s)
+      for (int i = 0; i < eb; ++i) g[s * eb + i] = (int64_t)(s ? right[f] : left[f]) * eb + i;
+    rc = scatter(l, pat, vals, g, ns * eb, fmat + (size_t)f * n2 * n2, n2);
+    for (int s = 0; s < ns; ++s)
+      for (int i = 0; i < eb; ++i) rhs[g[s * eb + i]] += frhs[(size_t)f * n2 + s * eb + i];
+  }
+  free(g);
   return rc;
 }

@@ -105,6 +105,17 @@ int po_condense_assemble(int nelem, int n, const double* mats, const double* rhs
 int po_condense(int n, const double* mat, const double* rhs, int n_elim, const int* elim,
                 double* schur, double* reduced_rhs, double* elim_coupling, double* elim_rhs);
 
+/* DG in 3D (config 4; assemble.hpp:177-346 restated with three velocity
+ * components): the structural CSR pattern (two-pass: null outputs count)
+ * and the reference-order value scatter of shared local terms (volume
+ * blocks nelem x (4ne)^2, face blocks nfaces x (8ne)^2 over [left | right],
+ * column-major; loads alike). Returns the nnz / 0, or -1 with po_last_error. */
+int64_t po_dg_pattern(const po_layout* l, int nfaces, const int32_t* left, const int32_t* right,
+                      int64_t* row_ptr, int32_t* cols);
+int po_dg_assemble(const po_layout* l, int nfaces, const int32_t* left, const int32_t* right,
+                   const double* vol, const double* vrhs, const double* fmat, const double* frhs,
+                   const po_csr* pattern, double* vals, double* rhs);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,7 +30,8 @@ EXPORTS = [
     "pscu_condense_batch", "pscu_condense_assemble", "pscu_recover_batch", "pscu_bj_create",
     "pscu_bj_destroy", "pscu_bj_apply", "pscu_layout_make3", "pscu_bsr_create",
     "pscu_mat_block_size", "pscu_assembly_begin", "pscu_assembly_add", "pscu_assembly_rhs",
-    "pscu_solve_system_bsr", "pscu_bsr_download", "pscu_host_alloc", "pscu_host_free",
+    "pscu_solve_system_bsr", "pscu_bsr_download", "pscu_dgb_create", "pscu_mat_dg_modes",
+    "pscu_mat_set_values", "pscu_solve_system_dgb", "pscu_host_alloc", "pscu_host_free",
     "pscu_bsr_create_local", "pscu_assembly_begin_local", "pscu_assembly_add_local",
     "pscu_error_accumulate", "pscu_local_blocks3",
 ]
@@ -129,6 +130,9 @@ def load(path: str = LIB):
     lib.pscu_layout_make3.argtypes = [i32, i32, i32, i32, i32, C.POINTER(Layout)]
     lib.pscu_bsr_create.argtypes = [vp, i64, i32, vp, vp, vp, i32, C.POINTER(vp)]
     lib.pscu_mat_block_size.argtypes = [vp]
+    lib.pscu_dgb_create.argtypes = [vp, i64, i32, vp, vp, vp, i32, C.POINTER(vp)]
+    lib.pscu_mat_dg_modes.argtypes = [vp]
+    lib.pscu_mat_set_values.argtypes = [vp, vp, i64, i64, vp, i32]
     lib.pscu_bsr_download.argtypes = [vp, vp, vp, vp, vp]
     lib.pscu_host_alloc.argtypes = [i64, C.POINTER(vp)]
     lib.pscu_bsr_create_local.argtypes = [vp, i64, i64, i32, i64, vp, vp, vp, i32, C.POINTER(vp)]
@@ -143,6 +147,7 @@ def load(path: str = LIB):
     lib.pscu_solve_system_bsr.argtypes = [vp, i64, i32, vp, vp, vp, vp, C.POINTER(Layout), vp,
                                           i32, C.POINTER(LevelCfg), f64, i32, i32, vp, vp,
                                           C.POINTER(Report)]
+    lib.pscu_solve_system_dgb.argtypes = lib.pscu_solve_system_bsr.argtypes
     _lib = lib
     return lib
 

@@ -27,8 +27,10 @@ namespace {
 /// kBsr: the operator is in dense-block storage (bsr.cu) with this block
 /// size; the diagonal block of block row b is copied directly (rp / cols
 /// are then the block row pointer / block columns).
+/// kDgm > 0 (runtime dgm): DG block storage (dgb.cu panels), structural
+/// zeros of the dense block filled in.
 template <bool kBsr>
-__global__ void bj_factor_kernel(int64_t nb, int bs, int64_t s0, int64_t b0, int64_t diag_off,
+__global__ void bj_factor_kernel(int64_t nb, int bs, int dgm, int64_t s0, int64_t b0, int64_t diag_off,
                                  const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
                                  const double* __restrict__ vals, double* __restrict__ inv,
                                  double* __restrict__ work, int* __restrict__ perm_ws,
@@ -46,9 +48,24 @@ __global__ void bj_factor_kernel(int64_t nb, int bs, int64_t s0, int64_t b0, int
     if (kBsr) {
       int64_t q = rp[b];
       while (q < rp[b + 1] && cols[q] != b + diag_off) ++q;
-      const double* blk = vals + q * bs * bs;
-      for (int i = 0; i < bs; ++i)
-        for (int c = 0; c < bs; ++c) D(i, c) = q < rp[b + 1] ? blk[c * bs + i] : 0.0;
+      if (dgm) {
+        const int nm = dgm;
+        const double* blk = vals + q * 10 * nm * nm;
+        for (int i = 0; i < bs; ++i)
+          for (int c = 0; c < bs; ++c) {
+            const int ri = i / nm, ci = c / nm;
+            double v = 0.0;
+            if (q < rp[b + 1] && (ri == 3 || ci == 3 || ri == ci)) {
+              if (ri < 3) v = blk[ri * 2 * nm * nm + (ci == 3 ? nm + c % nm : c % nm) * nm + i % nm];
+              else v = blk[6 * nm * nm + c * nm + i % nm];
+            }
+            D(i, c) = v;
+          }
+      } else {
+        const double* blk = vals + q * bs * bs;
+        for (int i = 0; i < bs; ++i)
+          for (int c = 0; c < bs; ++c) D(i, c) = q < rp[b + 1] ? blk[c * bs + i] : 0.0;
+      }
     } else {
       for (int i = 0; i < bs; ++i)
         for (int c = 0; c < bs; ++c) D(i, c) = 0.0;
@@ -155,6 +172,9 @@ void apply_batch(Context& c, int64_t rows, int bs, int64_t s0, const double* inv
     case 10: bj_apply_kernel<10><<<g, 256, 0, c.stream>>>(rows, bs, s0, inv, x, y); break;
     case 12: bj_apply_kernel<12><<<g, 256, 0, c.stream>>>(rows, bs, s0, inv, x, y); break;
     case 24: bj_apply_kernel<24><<<g, 256, 0, c.stream>>>(rows, bs, s0, inv, x, y); break;
+    case 16: bj_apply_kernel<16><<<g, 256, 0, c.stream>>>(rows, bs, s0, inv, x, y); break;
+    case 40: bj_apply_kernel<40><<<g, 256, 0, c.stream>>>(rows, bs, s0, inv, x, y); break;
+    case 80: bj_apply_kernel<80><<<g, 256, 0, c.stream>>>(rows, bs, s0, inv, x, y); break;
     default:
       if (bs > 64) throw Error(PSCU_EINVAL, "block-Jacobi: blocks larger than 64 unsupported");
       bj_apply_kernel<0><<<g, 256, 0, c.stream>>>(rows, bs, s0, inv, x, y);
@@ -168,8 +188,12 @@ void bj_factor(Context& c, const Csr& a, const pscu_layout& l, BlockJacobi& bj) 
   bj.layout = l;
   bj.fb = ncomp(l) * l.face_vel + l.face_press;
   bj.eb = ncomp(l) * l.elem_vel + l.elem_press;
-  if (a.bs && (bj.eb != 0 || bj.fb != a.bs))
+  if (a.dgm) {
+    if (bj.fb != 0 || bj.eb != a.bs)
+      throw Error(PSCU_EINVAL, "block-Jacobi: DG block storage must match the layout's element blocks");
+  } else if (a.bs && (bj.eb != 0 || bj.fb != a.bs)) {
     throw Error(PSCU_EINVAL, "block-Jacobi: block storage must match the layout's face blocks");
+  }
   bj.eoff = int64_t(l.n_faces) * bj.fb;
   bj.n = a.n;
   if (layout_dim(l) != a.n) throw Error(PSCU_EINVAL, "block-Jacobi: layout/matrix size mismatch");
@@ -191,11 +215,11 @@ void bj_factor(Context& c, const Csr& a, const pscu_layout& l, BlockJacobi& bj) 
     DevBuf<int> perm(size_t(nb) * bs);
     if (a.bs)
       bj_factor_kernel<true><<<grid_rows(nb), 256, 0, c.stream>>>(
-          nb, bs, s0[t], t ? nf : 0, a.diag_off, a.brow_ptr.p, a.bcols.p, a.vals.p, bj.inv.p + off[t], work.p,
+          nb, bs, a.dgm, s0[t], t ? nf : 0, a.diag_off, a.brow_ptr.p, a.bcols.p, a.vals.p, bj.inv.p + off[t], work.p,
           perm.p, bad.p);
     else
       bj_factor_kernel<false><<<grid_rows(nb), 256, 0, c.stream>>>(
-          nb, bs, s0[t], t ? nf : 0, int64_t(0), a.row_ptr.p, a.cols.p, a.vals.p, bj.inv.p + off[t], work.p,
+          nb, bs, 0, s0[t], t ? nf : 0, int64_t(0), a.row_ptr.p, a.cols.p, a.vals.p, bj.inv.p + off[t], work.p,
           perm.p, bad.p);
     PSCU_LAUNCHED(&c);
     PSCU_CUDA(cudaStreamSynchronize(c.stream));  // scratch freed at scope end

@@ -131,9 +131,11 @@ __global__ void bsr_to_csr_kernel(int64_t total, int bs, const int64_t* __restri
   }
 }
 
-void set_pattern(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp, const int32_t* bcols,
-                 int64_t ncb = -1, int64_t diag_off = 0) {
-  if (bs < 1 || bs > 64) throw Error(PSCU_EINVAL, "block matrix: block size must be in [1, 64]");
+} // namespace
+
+void bsr_set_pattern(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp,
+                     const int32_t* bcols, int64_t ncb, int64_t diag_off) {
+  if (bs < 1 || bs > 160) throw Error(PSCU_EINVAL, "block matrix: block size must be in [1, 160]");
   if (ncb < 0) ncb = nb;
   if (ncb < nb || diag_off < 0 || diag_off + nb > ncb)
     throw Error(PSCU_EINVAL, "block matrix: inconsistent column count / diagonal offset");
@@ -163,8 +165,15 @@ void set_pattern(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp, con
   m.cols.alloc(0);
   m.h_row_ptr.clear();
   m.h_cols.clear();
+  m.dgm = 0;
 }
 
+namespace {
+void set_pattern(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp, const int32_t* bcols,
+                 int64_t ncb = -1, int64_t diag_off = 0) {
+  if (bs > 64) throw Error(PSCU_EINVAL, "block matrix: block size must be in [1, 64]");
+  bsr_set_pattern(c, m, nb, bs, brp, bcols, ncb, diag_off);
+}
 } // namespace
 
 void alloc_bsr(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp, const int32_t* bcols,
@@ -193,6 +202,7 @@ void upload_bsr(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp, cons
 }
 
 void bsr_to_csr(Context& c, const Csr& b, Csr& out) {
+  if (b.dgm) return dgb_to_csr(c, b, out);
   const int bs = b.bs;
   out = Csr{};
   out.n = b.n;
@@ -238,6 +248,7 @@ void inherit_bsr(Context& c, const Csr& fine, const std::vector<int32_t>& m, Csr
 }
 
 void spmv_bsr(Context& c, const Csr& a, const double* x, double* y) {
+  if (a.dgm) return spmv_dgb(c, a, x, y);
   if (a.n == 0) return;
   Context::Scope prof(&c, PROF_SPMV, 8.0 * double(a.nnz) + 16.0 * double(a.n));
   const unsigned g = grid_for(a.n, 256);
@@ -252,6 +263,7 @@ void spmv_bsr(Context& c, const Csr& a, const double* x, double* y) {
 
 void residual_restrict_bsr(Context& c, const Csr& a, const double* d, const double* w,
                            const int64_t* map, int64_t nc, double* rc) {
+  if (a.dgm) return residual_restrict_dgb(c, a, d, w, nc, rc);
   if (nc == 0) return;
   const unsigned g = grid_for(nc, 256);
   switch (a.bs) {

@@ -379,7 +379,10 @@ int pscu_inherit(pscu_ctx* ctx, const pscu_mat* fine, const pscu_layout* lf,
     std::vector<int64_t> c2f(layout_dim(*lc));
     coarse_to_fine(*lf, *lc, c2f.data());
     auto m = std::make_unique<pscu_mat>();
-    if (fine->m.bs) {
+    if (fine->m.dgm) {
+      if (lc->scheme != 2 || lc->dim != 3) throw Error(PSCU_EINVAL, "inherit: DG block storage needs 3D dg layouts");
+      inherit_dgb(ctx->c, fine->m, lc->elem_vel, m->m);
+    } else if (fine->m.bs) {
       const int fbc = ncomp(*lc) * lc->face_vel + lc->face_press;
       if (lc->elem_vel || lc->elem_press)
         throw Error(PSCU_EINVAL, "inherit: block storage needs face-only layouts");
@@ -568,6 +571,58 @@ int pscu_solve_system_bsr(pscu_ctx* ctx, int64_t nb, int bs, const int64_t* brow
     r.t_setup = std::chrono::duration<double>(t1 - t0).count();
     r.t_solve = std::chrono::duration<double>(t2 - t0).count();
     if (rep) *rep = r;
+  });
+}
+
+int pscu_solve_system_dgb(pscu_ctx* ctx, int64_t nb, int nm, const int64_t* brow_ptr,
+                          const int32_t* bcols, const double* vals, const double* rhs,
+                          const pscu_layout* lf, const int* degrees, int nlev,
+                          const pscu_level_cfg* cfg, double rtol, int maxit, int restart,
+                          double* x, double* hist, pscu_report* rep) {
+  return guard([&] {
+    Context& c = ctx->c;
+    const auto t0 = std::chrono::steady_clock::now();
+    pscu_mat fine;
+    upload_dgb(c, fine.m, nb, nm, brow_ptr, bcols, vals, PSCU_HOST);
+    if (layout_dim(*lf) != fine.m.n) throw Error(PSCU_EINVAL, "solve: layout/matrix mismatch");
+    pscu_hier h;
+    h.fine = &fine;
+    h.h.build(c, &fine.m, *lf, degrees, nlev, *cfg);
+    PSCU_CUDA(cudaStreamSynchronize(c.stream));
+    const auto t1 = std::chrono::steady_clock::now();
+    pscu_report r{};
+    const int rc = pscu_solve(ctx, &h, rhs, rtol, maxit, restart, x, hist, &r, PSCU_HOST);
+    if (rc) throw Error(rc, g_err);
+    const auto t2 = std::chrono::steady_clock::now();
+    r.t_setup = std::chrono::duration<double>(t1 - t0).count();
+    r.t_solve = std::chrono::duration<double>(t2 - t0).count();
+    if (rep) *rep = r;
+  });
+}
+
+int pscu_dgb_create(pscu_ctx* ctx, int64_t nb, int nm, const int64_t* brow_ptr,
+                    const int32_t* bcols, const double* vals, int mem, pscu_mat** out) {
+  return guard([&] {
+    if (nb < 0) throw Error(PSCU_EINVAL, "pscu_dgb_create: negative dimension");
+    auto m = std::make_unique<pscu_mat>();
+    upload_dgb(ctx->c, m->m, nb, nm, brow_ptr, bcols, vals, mem);
+    PSCU_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    *out = m.release();
+  });
+}
+
+int pscu_mat_dg_modes(const pscu_mat* m) { return m->m.dgm; }
+
+int pscu_mat_set_values(pscu_ctx* ctx, pscu_mat* m, int64_t offset, int64_t count,
+                        const double* vals, int mem) {
+  return guard([&] {
+    if (offset < 0 || count < 0 || offset + count > m->m.nnz)
+      throw Error(PSCU_EINVAL, "set_values: range outside the value array");
+    if (count)
+      PSCU_CUDA(cudaMemcpyAsync(m->m.vals.p + offset, vals, sizeof(double) * size_t(count),
+                                mem == PSCU_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                                ctx->c.stream));
+    if (mem == PSCU_HOST) PSCU_CUDA(cudaStreamSynchronize(ctx->c.stream));
   });
 }
 

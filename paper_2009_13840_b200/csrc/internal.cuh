@@ -118,6 +118,11 @@ struct Csr {
   // (ghost faces of the neighbour slabs); the diagonal block of block row b
   // is block column b + diag_off
   int64_t ncb = 0, diag_off = 0;
+  // DG block storage (dgb.cu): dgm > 0 modes per component, bs = 4 dgm,
+  // every block holds its 10 dgm^2 structural entries as panels (velocity
+  // component c: dgm x 2dgm [u_c | p] columns; pressure: dgm x 4dgm), nnz =
+  // nblk 10 dgm^2
+  int dgm = 0;
   DevBuf<int64_t> brow_ptr;
   DevBuf<int32_t> bcols, brow_of;  // block columns, block row of every block
   std::vector<int64_t> h_brow_ptr;
@@ -259,6 +264,19 @@ void inherit_bsr(Context& c, const Csr& fine, const std::vector<int32_t>& in_blo
 void spmv_bsr(Context& c, const Csr& a, const double* x, double* y);
 void residual_restrict_bsr(Context& c, const Csr& a, const double* d, const double* w,
                            const int64_t* map, int64_t nc, double* rc);
+
+void bsr_set_pattern(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brow_ptr,
+                     const int32_t* bcols, int64_t ncb, int64_t diag_off);
+
+// dgb.cu — DG block storage (3D DG, BASELINE.json config 4)
+void upload_dgb(Context& c, Csr& m, int64_t nb, int nm, const int64_t* brow_ptr,
+                const int32_t* bcols, const double* vals, int mem);
+void spmv_dgb(Context& c, const Csr& a, const double* x, double* y);
+/// rc = restriction of (d - A w) to the leading nc/(4 nb) modes per component
+void residual_restrict_dgb(Context& c, const Csr& a, const double* d, const double* w,
+                           int64_t nc, double* rc);
+void inherit_dgb(Context& c, const Csr& fine, int nmc, Csr& out);
+void dgb_to_csr(Context& c, const Csr& b, Csr& out);
 
 // sptrsv.cu
 void ilu0_factor(Context& c, Ilu& ilu);

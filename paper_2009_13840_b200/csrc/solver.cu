@@ -330,14 +330,22 @@ int64_t layout_dim(const pscu_layout& l) {
 
 void make_layout3(int scheme, int strategy, int k, int n_faces, int n_elements, pscu_layout& l) {
   if (k < 0) throw Error(PSCU_EINVAL, "layout: k must be >= 0");
-  if (scheme != 1 || strategy != 2) throw Error(PSCU_EINVAL, "3D layout: hho-hp vp-cond only");
+  if (scheme == 2) {
+    // DG (config 4): element blocks [ux | uy | uz | p], dim P^k(3D) modes
+    // each (dof_layout.hpp:118-123 with three components)
+    if (k < 1) throw Error(PSCU_EINVAL, "dg: k must be >= 1");
+    if (strategy != 0) throw Error(PSCU_EINVAL, "dg: no static condensation exists, use uncond");
+  } else if (scheme != 1 || strategy != 2) {
+    throw Error(PSCU_EINVAL, "3D layout: hho-hp vp-cond or dg uncond only");
+  }
   l = pscu_layout{};
   l.scheme = scheme;
   l.strategy = strategy;
   l.k = k;
   l.n_faces = n_faces;
   l.n_elements = n_elements;
-  l.face_vel = l.face_press = (k + 1) * (k + 2) / 2;
+  if (scheme == 2) l.elem_vel = l.elem_press = (k + 1) * (k + 2) * (k + 3) / 6;
+  else l.face_vel = l.face_press = (k + 1) * (k + 2) / 2;
   l.dim = 3;
 }
 
@@ -532,7 +540,21 @@ void Hierarchy::build(Context& c, const Csr* fine, const pscu_layout& lf, const 
     for (int64_t i = 0; i < P.nc; ++i) f2c[c2f[i]] = int32_t(i);
     P.f2c.upload(f2c, c.stream);
     const auto t0 = std::chrono::steady_clock::now();
-    if (P.op->bs) {
+    if (P.op->dgm) {
+      // DG block storage: the coarse panels are the leading modes of the
+      // fine ones (element e's coarse dofs map into element e's fine block)
+      if (L.layout.scheme != 2 || L.layout.dim != 3 || L.layout.elem_vel != L.layout.elem_press)
+        throw Error(PSCU_EINVAL, "hierarchy: DG block storage needs 3D dg layouts");
+      const bool needs_csr = (l + 1 == nlev) || cfg.smoother != PSCU_SMOOTHER_BJACOBI;
+      if (needs_csr) {
+        inherit_dgb(c, *P.op, L.layout.elem_vel, L.own_bsr);
+        dgb_to_csr(c, L.own_bsr, L.own);
+        L.op = &L.own_bsr;
+        PSCU_CUDA(cudaStreamSynchronize(c.stream));
+      } else {
+        inherit_dgb(c, *P.op, L.layout.elem_vel, L.own);
+      }
+    } else if (P.op->bs) {
       // face-block operators: the coarse blocks are sub-blocks of the fine
       // ones (face f's coarse dofs map into face f's fine block)
       const int fbc = ncomp(L.layout) * L.layout.face_vel + L.layout.face_press;

@@ -325,6 +325,14 @@ def load3():
         lib.psh3_geometry.argtypes = [vp, vp]
         lib.psh3_device_inputs.argtypes = [vp, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, vp,
                                            vp, vp, vp, vp, vp]
+        lib.psh3_dg_info.argtypes = [C.c_int, vp]
+        lib.psh3_dg_block_pattern.restype = C.c_int64
+        lib.psh3_dg_block_pattern.argtypes = [vp, vp, vp]
+        lib.psh3_dg_local.argtypes = [vp, C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_int, vp,
+                                      vp, vp, vp]
+        lib.psh3_dg_rows.argtypes = [vp, C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_int,
+                                     C.c_int, vp, vp, C.c_int, vp, vp]
+        lib.psh3_dg_l2_errors.argtypes = [vp, C.c_int, vp, vp]
         lib._psh3 = True
     return lib
 
@@ -411,6 +419,63 @@ class Mesh3:
         out = np.zeros(self.n_faces * 4 * nf)
         _check3(self.lib.psh3_face_projection(self.h, k, out.ctypes.data))
         return out
+
+
+class DgLocal3:
+    """3D DG (BR2) at degree k (BASELINE.json config 4; the reference's DG,
+    assemble.hpp:177-346, with three velocity components): element blocks
+    [ux | uy | uz | p] of ne = dim P^k(3D) modes each."""
+
+    def __init__(self, k: int):
+        info = np.zeros(2, np.int32)
+        _check3(load3().psh3_dg_info(k, info.ctypes.data))
+        self.k = k
+        self.ne, self.elem_block = int(info[0]), int(info[1])
+
+    @staticmethod
+    def block_pattern(mesh: "Mesh3"):
+        lib = load3()
+        nb = lib.psh3_dg_block_pattern(mesh.h, None, None)
+        rp = np.zeros(mesh.n_elements + 1, np.int64)
+        cols = np.zeros(nb, np.int32)
+        lib.psh3_dg_block_pattern(mesh.h, rp.ctypes.data, cols.ctypes.data)
+        return rp, cols
+
+    def local_terms(self, mesh: "Mesh3", data: str = "random", seed: int = 0, eta: float = 0.0,
+                    nthreads: int = 0):
+        """(vol, vrhs, fmat, frhs) for the oracle's reference-order scatter."""
+        nl = self.elem_block
+        vol = np.zeros(mesh.n_elements * nl * nl)
+        vr = np.zeros(mesh.n_elements * nl)
+        fm = np.zeros(mesh.n_faces * 4 * nl * nl)
+        fr = np.zeros(mesh.n_faces * 2 * nl)
+        _check3(load3().psh3_dg_local(mesh.h, self.k, DATA3[data], seed, eta, nthreads,
+                                      vol.ctypes.data, vr.ctypes.data, fm.ctypes.data,
+                                      fr.ctypes.data))
+        return vol, vr, fm, fr
+
+    def rows(self, mesh: "Mesh3", brow_ptr, bcols, e0: int, e1: int, data: str = "random",
+             seed: int = 0, eta: float = 0.0, nthreads: int = 0, out=None):
+        """Block rows [e0, e1) in DG block storage (10 ne^2 per block) and
+        their loads (psh3_dg_rows)."""
+        rp = np.ascontiguousarray(brow_ptr, np.int64)
+        cl = np.ascontiguousarray(bcols, np.int32)
+        nblk = int(rp[e1] - rp[e0])
+        if out is None:
+            vals = np.zeros(nblk * 10 * self.ne * self.ne)
+            rhs = np.zeros((e1 - e0) * self.elem_block)
+        else:
+            vals, rhs = out
+        _check3(load3().psh3_dg_rows(mesh.h, self.k, DATA3[data], seed, eta, e0, e1,
+                                     rp.ctypes.data, cl.ctypes.data, nthreads, N.ptr(vals),
+                                     N.ptr(rhs)))
+        return vals, rhs
+
+    def l2_errors(self, mesh: "Mesh3", x) -> tuple:
+        x = np.ascontiguousarray(x, np.float64)
+        out = np.zeros(2)
+        _check3(load3().psh3_dg_l2_errors(mesh.h, self.k, x.ctypes.data, out.ctypes.data))
+        return float(out[0]), float(out[1])
 
 
 class HpLocal3:
@@ -639,3 +704,77 @@ def assemble_stokes3(mesh: Mesh3, k: int, data: str = "random", seed: int = 0, e
     info = dict(t_local_s=t_host, t_condense_s=t_dev, brow_ptr=brp, bcols=bcols, local=L,
                 elim_coupling=coup, elim_rhs=erhs)
     return A, b, lay, info
+
+
+def assemble_dg3(mesh: Mesh3, k: int, data: str = "random", seed: int = 0, eta: float = 0.0,
+                 batch: int = 2048, nthreads: int = 0, ctx=None):
+    """assemble_dg (assemble.hpp:177-346) for the 3D DG scheme (BASELINE.json
+    config 4) into DG block device storage: the host producer (C++/OpenMP)
+    writes batches of block rows — every entry summed in the reference's
+    scatter order — into a page-locked buffer, and each batch is copied into
+    the device operator while the next is built. Returns (A, rhs, layout,
+    info) with A a device CsrMatrix in DG block storage."""
+    import threading
+    import time
+
+    from . import solver as S
+
+    ctx = ctx or S.default_context()
+    D = DgLocal3(k)
+    brp, bcols = D.block_pattern(mesh)
+    A = S.dgb_matrix(brp, bcols, None, D.ne, ctx=ctx)
+    bsz = 10 * D.ne * D.ne
+    ne = mesh.n_elements
+    nb = min(batch, ne)
+    max_blocks = int(max(brp[min(e0 + nb, ne)] - brp[e0] for e0 in range(0, ne, nb)))
+    lib = ctx.lib
+    bufs = []
+    for _ in range(2):
+        p = C.c_void_p()
+        N.check(lib.pscu_host_alloc(8 * max_blocks * bsz, C.byref(p)))
+        bufs.append(p)
+    rhs = np.zeros(ne * D.elem_block)
+    t0 = time.perf_counter()
+    t_host = 0.0
+    try:
+        views = [np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_double)), (max_blocks * bsz,))
+                 for p in bufs]
+        ranges = [(e0, min(ne, e0 + nb)) for e0 in range(0, ne, nb)]
+
+        def build(i):
+            e0, e1 = ranges[i]
+            D.rows(mesh, brp, bcols, e0, e1, data=data, seed=seed, eta=eta, nthreads=nthreads,
+                   out=(views[i % 2], rhs[e0 * D.elem_block:e1 * D.elem_block]))
+
+        th = None
+        err = []
+
+        def run(i):
+            try:
+                build(i)
+            except Exception as ex:  # surfaced after join
+                err.append(ex)
+
+        th0 = time.perf_counter()
+        build(0)
+        t_host += time.perf_counter() - th0
+        for i, (e0, e1) in enumerate(ranges):
+            if i + 1 < len(ranges):
+                N.check(lib.pscu_synchronize(ctx.h))  # buffer (i + 1) % 2 is free again
+                th = threading.Thread(target=run, args=(i + 1,))
+                th.start()
+            q0, q1 = int(brp[e0]), int(brp[e1])
+            N.check(lib.pscu_mat_set_values(ctx.h, A.h, q0 * bsz, (q1 - q0) * bsz,
+                                            bufs[i % 2].value, N.PSCU_HOST))
+            if th is not None:
+                th.join()
+                th = None
+                if err:
+                    raise err[0]
+    finally:
+        for p in bufs:
+            lib.pscu_host_free(p)
+    lay = S.make_layout3(k, mesh.n_faces, mesh.n_elements, scheme="dg", strategy="uncond")
+    info = dict(t_assembly_s=time.perf_counter() - t0, brow_ptr=brp, bcols=bcols, local=D,
+                producer="host")
+    return A, rhs, lay, info

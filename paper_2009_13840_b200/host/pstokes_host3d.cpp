@@ -862,6 +862,303 @@ void build_local(const Mesh& mesh, int e, int k, double eta, const Data& data, d
   }
 }
 
+// ---------------------------------------------------------------------------
+// DG (BR2) local terms in 3D — BASELINE.json config 4 (equal-order DG, 80 x 80
+// element blocks at k = 3). The reference's DG is BR2 in 2D
+// (assemble.hpp:177-346, dg_local.hpp); this is the same scheme with three
+// velocity components (SURVEY.md §0 finding 7: the reference DG, not SIP).
+//  * element basis: orthonormal P^k (ElemBasis), quadrature degree 2(k+1)+1;
+//    local order [u_x | u_y | u_z | p], ne = dim P^k(3D) modes each.
+//  * volume: grad-grad per component, +int div(u) q rows, -int p div v
+//    columns (assemble.hpp:219-231); loads int f_c v.
+//  * faces (assemble.hpp:238-345): BR2 penalty eta = (max faces of the
+//    adjacent elements) + 1 = 7 on hexahedra (dg_penalty_bound); Dirichlet:
+//    4 eta <L,L> - cons - cons^T, momentum pressure flux with the trace;
+//    interior: the jump/average tables; pressure-jump stabilisation scaled by
+//    h_F = face diameter. Normals are taken per quadrature point from the
+//    vector area element (exact on the bilinear face), so n_c x (table)
+//    becomes the table with weights na_c: identical on planar faces.
+//  * face loads (Dirichlet consistency + penalty, Neumann traction) are
+//    formed as local vectors and added once per face.
+//  * assembly order (the reference's scatter_block sequence): every entry is
+//    0.0 + volume term, then + each face term in face-id order.
+// ---------------------------------------------------------------------------
+
+inline int dg_ne(int k) { return dimP3(k); }
+
+struct DgElem {
+  ElemRule er;
+  ElemBasis b;
+  Geo geo;
+};
+
+void dg_elem_init(const Mesh& mesh, int e, int k, DgElem& d) {
+  const int qd = 2 * (k + 1) + 1;
+  d.er = element_rule(mesh, e, qd);
+  d.geo = element_geo(mesh, e, d.er);
+  d.b.init(d.er, d.geo.cen, d.geo.diam, k);
+}
+
+/// Volume block (nloc x nloc column-major, nloc = 4 ne) and load of element e.
+void dg_volume(const Mesh& mesh, int e, int k, const Data& data, const DgElem& d, double* mat,
+               double* rhs) {
+  const int ne = dg_ne(k), nloc = 4 * ne;
+  const int nq = d.er.size();
+  std::vector<double> st(size_t(ne) * ne, 0.0), dv[3];
+  for (int c = 0; c < 3; ++c) dv[c].assign(size_t(ne) * ne, 0.0);
+  double v[kMaxMono], g[3 * kMaxMono];
+  double coef[3][kMaxMono] = {};
+  if (data.kind == 3) {
+    SplitMix64 rng{data.seed + uint64_t(e) * uint64_t(6 * ne) * 0x9e3779b97f4a7c15ULL};
+    for (int c = 0; c < 3; ++c)
+      for (int m = 0; m < ne; ++m) coef[c][m] = rng.normal();
+  }
+  std::fill(rhs, rhs + nloc, 0.0);
+  for (int q = 0; q < nq; ++q) {
+    const double w = d.er.w[q];
+    d.b.eval(d.er.p[q], v);
+    d.b.grad(d.er.p[q], g);
+    // m_stiff += w g g^T ; m_div_c += w v g_c^T (dg_local.hpp:67-71)
+    for (int j = 0; j < ne; ++j)
+      for (int i = 0; i < ne; ++i) {
+        double s = 0.0;
+        for (int a = 0; a < 3; ++a) s += (w * g[3 * i + a]) * g[3 * j + a];
+        st[size_t(i) + size_t(j) * ne] += s;
+        for (int c = 0; c < 3; ++c) dv[c][size_t(i) + size_t(j) * ne] += (w * v[i]) * g[3 * j + c];
+      }
+    double fv[3] = {0.0, 0.0, 0.0};
+    if (data.kind == 3) {
+      for (int c = 0; c < 3; ++c)
+        for (int m = 0; m < ne; ++m) fv[c] += coef[c][m] * v[m];
+    } else if (data.kind == 4) {
+      data.f_manufactured(d.er.p[q], fv);
+    }
+    if (data.kind != 0)
+      for (int c = 0; c < 3; ++c)
+        for (int i = 0; i < ne; ++i) rhs[c * ne + i] += (w * fv[c]) * v[i];
+  }
+  std::fill(mat, mat + size_t(nloc) * nloc, 0.0);
+  auto M = [&](int i, int j) -> double& { return mat[size_t(i) + size_t(j) * nloc]; };
+  for (int c = 0; c < 3; ++c)
+    for (int j = 0; j < ne; ++j)
+      for (int i = 0; i < ne; ++i) {
+        M(c * ne + i, c * ne + j) += st[size_t(i) + size_t(j) * ne];
+        M(3 * ne + i, c * ne + j) += dv[c][size_t(i) + size_t(j) * ne];
+        M(c * ne + i, 3 * ne + j) -= dv[c][size_t(j) + size_t(i) * ne];
+      }
+}
+
+/// Scalar face tables of face f over the stacked element dofs [left | right]
+/// (side count ns = 1 on boundary faces): visc, vmom_c, mass_c, pjump, all
+/// (ns ne) x (ns ne) column-major, plus the per-side loads (3 x ns ne).
+struct DgFace {
+  int ns = 0, tag = 0, m = 0;
+  std::vector<double> visc, vmom[3], mass[3], pjump, load;
+};
+
+double dg_penalty_bound3(const Mesh&, int) { return 6.0; }  // hexahedra: 6 faces per element
+
+void dg_face(const Mesh& mesh, int f, int k, const Data& data, double eta_override,
+             const DgElem& dl, const DgElem* dr, DgFace& out) {
+  const int ne = dg_ne(k), qd = 2 * (k + 1) + 1;
+  const FaceRule fr = face_rule(mesh, f, qd);
+  const int nq = fr.size();
+  const double hF = face_diameter(mesh, f);
+  const double bound = dg_penalty_bound3(mesh, f);
+  const double eta = eta_override > 0.0 ? eta_override : bound + 1.0;
+  out.tag = mesh.tag[f];
+  out.ns = (mesh.right[f] >= 0) ? 2 : 1;
+  const int ns = out.ns, m = ns * ne;
+  out.m = m;
+  // per point: values, normal derivatives, unit normal, weights
+  std::vector<double> psi(size_t(nq) * m), dn(size_t(nq) * m), nu(size_t(nq) * 3);
+  double v[kMaxMono], g[3 * kMaxMono];
+  for (int q = 0; q < nq; ++q) {
+    const double an = norm(fr.na[q]);
+    const V3 n = (1.0 / an) * fr.na[q];
+    nu[3 * q] = n.x;
+    nu[3 * q + 1] = n.y;
+    nu[3 * q + 2] = n.z;
+    for (int s = 0; s < ns; ++s) {
+      const ElemBasis& b = s == 0 ? dl.b : dr->b;
+      b.eval(fr.p[q], v);
+      b.grad(fr.p[q], g);
+      for (int i = 0; i < ne; ++i) {
+        psi[size_t(q) * m + s * ne + i] = v[i];
+        dn[size_t(q) * m + s * ne + i] = g[3 * i] * n.x + g[3 * i + 1] * n.y + g[3 * i + 2] * n.z;
+      }
+    }
+  }
+  const std::vector<double>& w = fr.w;
+  auto T = [&](std::vector<double>& t) { t.assign(size_t(m) * m, 0.0); };
+  T(out.visc);
+  T(out.pjump);
+  for (int c = 0; c < 3; ++c) {
+    T(out.vmom[c]);
+    T(out.mass[c]);
+  }
+  out.load.assign(size_t(3) * m, 0.0);
+  // lifting moments m_s = 0.5 Psi_s^T W (ne x nq per side)
+  std::vector<double> mom(size_t(ns) * ne * nq);
+  for (int s = 0; s < ns; ++s)
+    for (int l = 0; l < ne; ++l)
+      for (int q = 0; q < nq; ++q)
+        mom[(size_t(s) * ne + l) * nq + q] = (0.5 * psi[size_t(q) * m + s * ne + l]) * w[q];
+  if (ns == 1) {
+    if (out.tag == 2) {
+      // Neumann: traction load -int g_N . v (assemble.hpp:255-264)
+      for (int q = 0; q < nq; ++q) {
+        double gn[3];
+        data.gn(fr.p[q], V3{nu[3 * q], nu[3 * q + 1], nu[3 * q + 2]}, gn);
+        for (int c = 0; c < 3; ++c)
+          for (int i = 0; i < ne; ++i) out.load[c * m + i] -= (w[q] * gn[c]) * psi[size_t(q) * m + i];
+      }
+      return;
+    }
+    // Dirichlet (assemble.hpp:266-290): lifted jump 2(u_T - g)
+    std::vector<double> cons(size_t(ne) * ne), lift(size_t(ne) * ne);
+    for (int j = 0; j < ne; ++j)
+      for (int i = 0; i < ne; ++i) {
+        double a = 0.0, b = 0.0;
+        for (int q = 0; q < nq; ++q) {
+          a += (psi[size_t(q) * m + i] * w[q]) * dn[size_t(q) * m + j];
+          b += mom[size_t(i) * nq + q] * psi[size_t(q) * m + j];
+        }
+        cons[i + size_t(j) * ne] = a;
+        lift[i + size_t(j) * ne] = b;
+      }
+    for (int j = 0; j < ne; ++j)
+      for (int i = 0; i < ne; ++i) {
+        double pen = 0.0;
+        for (int l = 0; l < ne; ++l) pen += ((4.0 * eta) * lift[l + size_t(i) * ne]) * lift[l + size_t(j) * ne];
+        out.visc[i + size_t(j) * m] = (pen - cons[i + size_t(j) * ne]) - cons[j + size_t(i) * ne];
+        for (int c = 0; c < 3; ++c) {
+          double pf = 0.0;
+          for (int q = 0; q < nq; ++q)
+            pf += (psi[size_t(q) * m + i] * (w[q] * nu[3 * q + c])) * psi[size_t(q) * m + j];
+          out.vmom[c][i + size_t(j) * m] = pf;
+        }
+      }
+    // loads: -int (n.grad v) g + 4 eta <L(g), L(v)>
+    double gq[3];
+    std::vector<double> gv(size_t(3) * nq);
+    bool nz = false;
+    for (int q = 0; q < nq; ++q) {
+      data.gd(fr.p[q], gq);
+      for (int c = 0; c < 3; ++c) {
+        gv[size_t(c) * nq + q] = gq[c];
+        nz = nz || gq[c] != 0.0;
+      }
+    }
+    if (nz)
+      for (int c = 0; c < 3; ++c) {
+        std::vector<double> mg(ne, 0.0);
+        for (int l = 0; l < ne; ++l)
+          for (int q = 0; q < nq; ++q) mg[l] += mom[size_t(l) * nq + q] * gv[size_t(c) * nq + q];
+        for (int i = 0; i < ne; ++i) {
+          double a = 0.0, b = 0.0;
+          for (int q = 0; q < nq; ++q) a += (dn[size_t(q) * m + i] * w[q]) * gv[size_t(c) * nq + q];
+          for (int l = 0; l < ne; ++l) b += ((4.0 * eta) * lift[l + size_t(i) * ne]) * mg[l];
+          out.load[c * m + i] = (-a) + b;
+        }
+      }
+    return;
+  }
+  // interior face (assemble.hpp:292-345)
+  std::vector<double> jmp(size_t(nq) * m), avg(size_t(nq) * m), adn(size_t(nq) * m),
+      plain(size_t(nq) * m);
+  for (int q = 0; q < nq; ++q)
+    for (int a = 0; a < m; ++a) {
+      const double p = psi[size_t(q) * m + a];
+      jmp[size_t(q) * m + a] = a < ne ? p : -p;
+      avg[size_t(q) * m + a] = 0.5 * p;
+      adn[size_t(q) * m + a] = 0.5 * dn[size_t(q) * m + a];
+      plain[size_t(q) * m + a] = p;
+    }
+  // (m_s jmp): ne x m per side
+  std::vector<double> mj(size_t(2) * ne * m, 0.0);
+  for (int s = 0; s < 2; ++s)
+    for (int b = 0; b < m; ++b)
+      for (int l = 0; l < ne; ++l) {
+        double acc = 0.0;
+        for (int q = 0; q < nq; ++q) acc += mom[(size_t(s) * ne + l) * nq + q] * jmp[size_t(q) * m + b];
+        mj[(size_t(s) * ne + l) + size_t(b) * 2 * ne] = acc;
+      }
+  std::vector<double> cons(size_t(m) * m);
+  for (int b = 0; b < m; ++b)
+    for (int a = 0; a < m; ++a) {
+      double acc = 0.0;
+      for (int q = 0; q < nq; ++q) acc += (jmp[size_t(q) * m + a] * w[q]) * adn[size_t(q) * m + b];
+      cons[a + size_t(b) * m] = acc;
+    }
+  for (int b = 0; b < m; ++b)
+    for (int a = 0; a < m; ++a) {
+      double p1 = 0.0, p2 = 0.0;
+      for (int l = 0; l < ne; ++l) {
+        p1 += mj[size_t(l) + size_t(a) * 2 * ne] * mj[size_t(l) + size_t(b) * 2 * ne];
+        p2 += mj[size_t(ne + l) + size_t(a) * 2 * ne] * mj[size_t(ne + l) + size_t(b) * 2 * ne];
+      }
+      const double pen = eta * (p1 + p2);
+      out.visc[a + size_t(b) * m] = (pen - cons[a + size_t(b) * m]) - cons[b + size_t(a) * m];
+      double pj = 0.0;
+      for (int q = 0; q < nq; ++q) pj += (jmp[size_t(q) * m + a] * w[q]) * jmp[size_t(q) * m + b];
+      out.pjump[a + size_t(b) * m] = hF * pj;
+      for (int c = 0; c < 3; ++c) {
+        double vm = 0.0, ms = 0.0;
+        for (int q = 0; q < nq; ++q) {
+          const double wn = w[q] * nu[3 * q + c];
+          vm += (jmp[size_t(q) * m + a] * wn) * avg[size_t(q) * m + b];
+          ms += ((0.5 * plain[size_t(q) * m + a]) * wn) * jmp[size_t(q) * m + b];
+        }
+        out.vmom[c][a + size_t(b) * m] = vm;
+        out.mass[c][a + size_t(b) * m] = ms;
+      }
+    }
+}
+
+/// The face's local matrix over [left | right] element dofs (ns nloc square,
+/// column-major; assemble.hpp:324-339's placement; Dirichlet: the left block).
+void dg_face_matrix(const DgFace& t, int ne, double* mat) {
+  const int nloc = 4 * ne, ns = t.ns, N = ns * nloc, m = t.m;
+  std::fill(mat, mat + size_t(N) * N, 0.0);
+  if (t.tag == 2) return;
+  auto M = [&](int i, int j) -> double& { return mat[size_t(i) + size_t(j) * N]; };
+  auto sdof = [&](int s, int c, int i) { return s * nloc + c * ne + i; };
+  auto spr = [&](int s, int i) { return s * nloc + 3 * ne + i; };
+  for (int s1 = 0; s1 < ns; ++s1)
+    for (int i = 0; i < ne; ++i)
+      for (int s2 = 0; s2 < ns; ++s2)
+        for (int j = 0; j < ne; ++j) {
+          const int a = s1 * ne + i, b = s2 * ne + j;
+          const size_t ab = size_t(a) + size_t(b) * m;
+          for (int c = 0; c < 3; ++c) {
+            M(sdof(s1, c, i), sdof(s2, c, j)) += t.visc[ab];
+            M(sdof(s1, c, i), spr(s2, j)) += t.vmom[c][ab];
+            if (ns == 2) M(spr(s1, i), sdof(s2, c, j)) -= t.mass[c][ab];
+          }
+          if (ns == 2) M(spr(s1, i), spr(s2, j)) += t.pjump[ab];
+        }
+}
+
+/// Panel layout of one element block of the DG operator ("DG block
+/// storage", csrc/dgb.cu): velocity panel c (ne x 2ne, column-major:
+/// columns [u_c modes | p modes]) at c 2ne^2, pressure panel (ne x 4ne:
+/// [u_x | u_y | u_z | p]) at 6 ne^2; 10 ne^2 structural entries per block.
+inline size_t dgb_index(int ne, int r, int col) {
+  // r, col: rows / columns of the dense 4ne block; caller guarantees coupling
+  const int rc = r / ne, ri = r % ne;
+  if (rc < 3) {
+    const int cc = col / ne, cj = col % ne;
+    const int pc = cc == 3 ? ne + cj : cj;
+    return size_t(rc) * 2 * ne * ne + size_t(pc) * ne + ri;
+  }
+  return size_t(6) * ne * ne + size_t(col) * ne + ri;
+}
+inline bool dg_coupled(int ne, int r, int col) {
+  const int rc = r / ne, cc = col / ne;
+  return rc == 3 || cc == 3 || rc == cc;
+}
+
 template <typename F>
 int guard(F&& f) {
   try {
@@ -1138,4 +1435,209 @@ int psh3_geometry(const psh_mesh3* pm, double* out) {
   });
 }
 
+} // extern "C"
+
+// ---------------------------------------------------------------------------
+// DG (BR2) in 3D: BASELINE.json config 4 (see the DG section above)
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+/* info[0..1] = modes per component ne (dim P^k), element block 4 ne */
+int psh3_dg_info(int k, int32_t* info) {
+  return guard([&] {
+    if (k < 1 || k > 4) throw std::invalid_argument("dg: polynomial degree must be in [1, 4]");
+    info[0] = dg_ne(k);
+    info[1] = 4 * dg_ne(k);
+  });
+}
+
+/* Element-block pattern of the DG operator: block row e couples e and the
+ * elements across its interior faces, ascending. Returns the block count. */
+int64_t psh3_dg_block_pattern(const psh_mesh3* pm, int64_t* brow_ptr, int32_t* bcols) {
+  const Mesh& m = pm->m;
+  const int ne = m.nelem();
+  std::vector<int64_t> rp(size_t(ne) + 1, 0);
+  std::vector<std::array<int32_t, 7>> cols(ne);
+  std::vector<int> cnt(ne, 0);
+#pragma omp parallel for schedule(static)
+  for (int e = 0; e < ne; ++e) {
+    int32_t c[7];
+    int t = 0;
+    c[t++] = e;
+    for (int lf = 0; lf < 6; ++lf) {
+      const int f = m.ef[e][lf];
+      if (m.right[f] < 0) continue;
+      c[t++] = m.left[f] == e ? m.right[f] : m.left[f];
+    }
+    std::sort(c, c + t);
+    cnt[e] = t;
+    for (int i = 0; i < t; ++i) cols[e][i] = c[i];
+  }
+  for (int e = 0; e < ne; ++e) rp[e + 1] = rp[e] + cnt[e];
+  if (brow_ptr) std::memcpy(brow_ptr, rp.data(), sizeof(int64_t) * rp.size());
+  if (bcols)
+    for (int e = 0; e < ne; ++e) std::memcpy(bcols + rp[e], cols[e].data(), sizeof(int32_t) * cnt[e]);
+  return rp[ne];
+}
+
+/* The DG local terms for the oracle's reference-order scatter (small
+ * meshes): per element the volume block (nloc^2, column-major) and load
+ * (nloc); per face the face matrix over [left | right] dofs ((2 nloc)^2,
+ * column-major, leading dimension 2 nloc; boundary faces fill the left
+ * nloc block only) and the face load (2 nloc). Null outputs skipped. */
+int psh3_dg_local(const psh_mesh3* pm, int k, int data, uint64_t seed, double eta, int nthreads,
+                  double* vol, double* vrhs, double* fmat, double* frhs) {
+  return guard([&] {
+    const Mesh& mesh = pm->m;
+    if (k < 1 || k > 4) throw std::invalid_argument("dg: polynomial degree must be in [1, 4]");
+    if (data != 0 && data != 3 && data != 4) throw std::invalid_argument("dg: unknown data kind");
+    const int ne = dg_ne(k), nloc = 4 * ne, N2 = 2 * nloc;
+    Data dd{data, seed};
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+    std::vector<DgElem> el(mesh.nelem());
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int e = 0; e < mesh.nelem(); ++e) {
+      dg_elem_init(mesh, e, k, el[e]);
+      std::vector<double> m(size_t(nloc) * nloc), r(nloc);
+      dg_volume(mesh, e, k, dd, el[e], m.data(), r.data());
+      if (vol) std::memcpy(vol + size_t(e) * nloc * nloc, m.data(), sizeof(double) * m.size());
+      if (vrhs) std::memcpy(vrhs + size_t(e) * nloc, r.data(), sizeof(double) * nloc);
+    }
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int f = 0; f < mesh.nfaces(); ++f) {
+      DgFace t;
+      const int r = mesh.right[f];
+      dg_face(mesh, f, k, dd, eta, el[mesh.left[f]], r >= 0 ? &el[r] : nullptr, t);
+      std::vector<double> fm(size_t(t.ns * nloc) * (t.ns * nloc));
+      dg_face_matrix(t, ne, fm.data());
+      if (fmat) {
+        double* o = fmat + size_t(f) * N2 * N2;
+        std::fill(o, o + size_t(N2) * N2, 0.0);
+        const int n = t.ns * nloc;
+        for (int j = 0; j < n; ++j)
+          for (int i = 0; i < n; ++i) o[size_t(i) + size_t(j) * N2] = fm[size_t(i) + size_t(j) * n];
+      }
+      if (frhs) {
+        double* o = frhs + size_t(f) * N2;
+        std::fill(o, o + N2, 0.0);
+        for (int s = 0; s < t.ns; ++s)
+          for (int c = 0; c < 3; ++c)
+            for (int i = 0; i < ne; ++i) o[s * nloc + c * ne + i] = t.load[c * t.m + s * ne + i];
+      }
+    }
+  });
+}
+
+/* Block rows [e0, e1) of the assembled DG operator in DG block storage
+ * (csrc/dgb.cu panels, 10 ne^2 values per block, blocks in pattern order:
+ * vals receives blocks brow_ptr[e0] .. brow_ptr[e1] - 1) and their loads
+ * (rhs: rows of e0 .. e1 - 1). Entry sums follow the reference's scatter
+ * order: 0.0 + volume, then + each face term in face-id order; the loads
+ * likewise (volume load, then face loads in face-id order). */
+int psh3_dg_rows(const psh_mesh3* pm, int k, int data, uint64_t seed, double eta, int e0, int e1,
+                 const int64_t* brow_ptr, const int32_t* bcols, int nthreads, double* vals,
+                 double* rhs) {
+  return guard([&] {
+    const Mesh& mesh = pm->m;
+    if (k < 1 || k > 4) throw std::invalid_argument("dg: polynomial degree must be in [1, 4]");
+    if (e0 < 0 || e1 > mesh.nelem() || e0 > e1) throw std::invalid_argument("dg: element range");
+    if (data != 0 && data != 3 && data != 4) throw std::invalid_argument("dg: unknown data kind");
+    const int ne = dg_ne(k), nloc = 4 * ne;
+    const size_t bsz = size_t(10) * ne * ne;
+    Data dd{data, seed};
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+    const int64_t q00 = brow_ptr[e0];
+    std::string err;
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int e = e0; e < e1; ++e) {
+      try {
+        DgElem de;
+        dg_elem_init(mesh, e, k, de);
+        std::vector<double> vm(size_t(nloc) * nloc), vr(nloc);
+        dg_volume(mesh, e, k, dd, de, vm.data(), vr.data());
+        const int64_t q0 = brow_ptr[e], q1 = brow_ptr[e + 1];
+        double* out = vals + size_t(q0 - q00) * bsz;
+        std::fill(out, out + size_t(q1 - q0) * bsz, 0.0);
+        auto blk = [&](int col_elem) -> double* {
+          for (int64_t q = q0; q < q1; ++q)
+            if (bcols[q] == col_elem) return out + size_t(q - q0) * bsz;
+          throw std::runtime_error("dg: block outside the pattern");
+        };
+        double* dgl = blk(e);
+        for (int j = 0; j < nloc; ++j)
+          for (int i = 0; i < nloc; ++i)
+            if (dg_coupled(ne, i, j)) dgl[dgb_index(ne, i, j)] += vm[size_t(i) + size_t(j) * nloc];
+        double* r = rhs + size_t(e - e0) * nloc;
+        for (int i = 0; i < nloc; ++i) r[i] = 0.0 + vr[i];
+        // faces of e in face-id order
+        int fs[6];
+        for (int lf = 0; lf < 6; ++lf) fs[lf] = mesh.ef[e][lf];
+        std::sort(fs, fs + 6);
+        std::vector<double> fm;
+        for (int t6 = 0; t6 < 6; ++t6) {
+          const int f = fs[t6];
+          const int L = mesh.left[f], R = mesh.right[f];
+          DgElem other;
+          const bool interior = R >= 0;
+          const int se = L == e ? 0 : 1;
+          if (interior) dg_elem_init(mesh, se == 0 ? R : L, k, other);
+          DgFace t;
+          dg_face(mesh, f, k, dd, eta, se == 0 ? de : other, interior ? (se == 0 ? &other : &de) : nullptr, t);
+          for (int c = 0; c < 3; ++c)
+            for (int i = 0; i < ne; ++i) r[c * ne + i] += t.load[c * t.m + se * ne + i];
+          if (t.tag == 2) continue;
+          const int n = t.ns * nloc;
+          fm.resize(size_t(n) * n);
+          dg_face_matrix(t, ne, fm.data());
+          for (int s2 = 0; s2 < t.ns; ++s2) {
+            double* b = s2 == se ? dgl : blk(s2 == 0 ? L : R);
+            for (int j = 0; j < nloc; ++j)
+              for (int i = 0; i < nloc; ++i)
+                if (dg_coupled(ne, i, j))
+                  b[dgb_index(ne, i, j)] += fm[size_t(se * nloc + i) + size_t(s2 * nloc + j) * n];
+          }
+        }
+      } catch (const std::exception& ex) {
+#pragma omp critical
+        err = ex.what();
+      }
+    }
+    if (!err.empty()) throw std::runtime_error(err);
+  });
+}
+
+} // extern "C"
+
+extern "C" {
+/* L2 errors of a DG solution x (element blocks [ux | uy | uz | p]) against
+ * the manufactured field of data 4: out[0] = ||u_h - u||, out[1] =
+ * ||p_h - p|| (validation of the 3D DG discretisation). */
+int psh3_dg_l2_errors(const psh_mesh3* pm, int k, const double* x, double* out) {
+  return guard([&] {
+    const Mesh& mesh = pm->m;
+    const int ne = dg_ne(k), nloc = 4 * ne;
+    double eu = 0.0, ep = 0.0;
+#pragma omp parallel for schedule(dynamic, 8) reduction(+ : eu, ep)
+    for (int e = 0; e < mesh.nelem(); ++e) {
+      DgElem d;
+      dg_elem_init(mesh, e, k, d);
+      const ElemRule r = element_rule(mesh, e, 2 * (k + 2) + 3);
+      double v[kMaxMono], u[3];
+      const double* xe = x + size_t(e) * nloc;
+      for (int q = 0; q < r.size(); ++q) {
+        d.b.eval(r.p[q], v);
+        Data::u(r.p[q], u);
+        for (int c = 0; c < 4; ++c) {
+          double s = 0.0;
+          for (int i = 0; i < ne; ++i) s += xe[c * ne + i] * v[i];
+          const double ex = c < 3 ? u[c] : Data::pr(r.p[q]);
+          (c < 3 ? eu : ep) += r.w[q] * (s - ex) * (s - ex);
+        }
+      }
+    }
+    out[0] = std::sqrt(eu);
+    out[1] = std::sqrt(ep);
+  });
+}
 } // extern "C"

@@ -119,6 +119,11 @@ class CsrMatrix:
         return rp, cl, vl
 
     @property
+    def dg_modes(self) -> int:
+        """0 unless DG block storage, else its modes per component."""
+        return int(self.lib.pscu_mat_dg_modes(self.h))
+
+    @property
     def block_size(self) -> int:
         """0 for CSR storage, else the dense face-block size."""
         return int(self.lib.pscu_mat_block_size(self.h))
@@ -274,6 +279,56 @@ def bsr_matrix(brow_ptr, bcols, vals, bs: int, ctx: Context | None = None) -> "C
     m = CsrMatrix(None, None, None, ctx=ctx, _handle=h.value)
     m._owned = True
     return m
+
+
+def dgb_matrix(brow_ptr, bcols, vals, nm: int, ctx: Context | None = None) -> "CsrMatrix":
+    """A CsrMatrix in DG block storage (pscu_dgb_create; 3D DG, config 4):
+    element blocks of 4 nm rows, each holding its 10 nm^2 structural entries
+    as panels (velocity component c: nm x 2nm [u_c | p]; pressure: nm x 4nm).
+    vals None = zero operator."""
+    ctx = ctx or default_context()
+    rp = np.ascontiguousarray(brow_ptr, np.int64)
+    cl = np.ascontiguousarray(bcols, np.int32)
+    vl = None if vals is None else _f64(vals)
+    h = C.c_void_p()
+    N.check(ctx.lib.pscu_dgb_create(ctx.h, len(rp) - 1, nm, rp.ctypes.data, cl.ctypes.data,
+                                    N.ptr(vl), N.PSCU_HOST, C.byref(h)))
+    m = CsrMatrix(None, None, None, ctx=ctx, _handle=h.value)
+    m._owned = True
+    return m
+
+
+def set_values(m: "CsrMatrix", offset: int, vals, mem: int = N.PSCU_HOST, count: int = -1):
+    """pscu_mat_set_values: writes vals at offset of the operator's values."""
+    if mem == N.PSCU_HOST:
+        v = _f64(vals)
+        N.check(m.lib.pscu_mat_set_values(m.ctx.h, m.h, offset, v.size, v.ctypes.data, mem))
+    else:
+        N.check(m.lib.pscu_mat_set_values(m.ctx.h, m.h, offset, count, vals, mem))
+
+
+def solve_system_dgb(brow_ptr, bcols, vals, nm: int, rhs, layout: N.Layout, cfg: LevelConfig,
+                     ctx: Context | None = None):
+    """solve_system through the one-call C ABI entry for a DG block-stored
+    operator (pscu_solve_system_dgb): host buffers in, x out, all timed."""
+    ctx = ctx or default_context()
+    rp = np.ascontiguousarray(brow_ptr, np.int64)
+    cl = np.ascontiguousarray(bcols, np.int32)
+    vl = _f64(vals)
+    b = _f64(rhs)
+    deg = np.ascontiguousarray(cfg.degrees, np.int32)
+    x = np.zeros(len(b))
+    hist = np.zeros(cfg.outer_maxit + 1)
+    rep = N.Report()
+    ncfg = cfg.native()
+    N.check(ctx.lib.pscu_solve_system_dgb(ctx.h, len(rp) - 1, nm, rp.ctypes.data, cl.ctypes.data,
+                                          vl.ctypes.data, b.ctypes.data, C.byref(layout),
+                                          deg.ctypes.data, len(deg), C.byref(ncfg),
+                                          cfg.outer_rtol, cfg.outer_maxit, cfg.restart,
+                                          x.ctypes.data, hist.ctypes.data, C.byref(rep)))
+    r = SolverReport(rep.outer_its, rep.coarse_its, rep.vcycles, rep.rel_residual,
+                     bool(rep.converged), rep.t_setup, rep.t_solve)
+    return x, hist[: rep.outer_its].copy(), r
 
 
 def csr_to_bsr_values(row_ptr, cols, vals, brow_ptr, bcols, bs: int) -> np.ndarray:

@@ -493,6 +493,10 @@ def port_lib():
                                  C.POINTER(C.c_double), C.POINTER(C.c_int)]
         lib.po_condense.argtypes = [C.c_int, _f64p, _f64p, C.c_int, _i32p, _f64p, _f64p, _f64p,
                                     _f64p]
+        lib.po_dg_pattern.restype = C.c_int64
+        lib.po_dg_pattern.argtypes = [C.POINTER(PoLayout), C.c_int, vp, vp, vp, vp]
+        lib.po_dg_assemble.argtypes = [C.POINTER(PoLayout), C.c_int, vp, vp, vp, vp, vp, vp,
+                                       C.POINTER(_PoCsr), vp, vp]
         _port = lib
     return _port
 
@@ -546,6 +550,59 @@ def port_condense_assemble(mats, rhs, n, elim, kept, layout: PoLayout, row_ptr, 
                                 vals.ctypes.data, b.ctypes.data):
         raise RuntimeError(lib.po_last_error().decode())
     return Csr(rp, cl, vals), b
+
+
+def port_dg_assemble(layout: PoLayout, faces, vol, vrhs, fmat, frhs):
+    """po_dg_pattern + po_dg_assemble: the 3D DG operator in CSR from shared
+    local terms, scattered in the reference's order (assemble.hpp:177-346).
+    faces: the Mesh3.faces() table (left, right in columns 4, 5)."""
+    lib = port_lib()
+    left = np.ascontiguousarray(faces[:, 4], np.int32)
+    right = np.ascontiguousarray(faces[:, 5], np.int32)
+    nf = len(left)
+    nnz = lib.po_dg_pattern(C.byref(layout), nf, left.ctypes.data, right.ctypes.data, None, None)
+    if nnz < 0:
+        raise ValueError(lib.po_last_error().decode())
+    n = lib.po_layout_dim(C.byref(layout))
+    rp = np.zeros(n + 1, np.int64)
+    cl = np.zeros(nnz, np.int32)
+    lib.po_dg_pattern(C.byref(layout), nf, left.ctypes.data, right.ctypes.data, rp.ctypes.data,
+                      cl.ctypes.data)
+    vals = np.zeros(nnz)
+    b = np.zeros(n)
+    pat = _PoCsr(n, rp.ctypes.data, cl.ctypes.data, vals.ctypes.data)
+    arrs = [np.ascontiguousarray(a, np.float64) for a in (vol, vrhs, fmat, frhs)]
+    if lib.po_dg_assemble(C.byref(layout), nf, left.ctypes.data, right.ctypes.data,
+                          *(a.ctypes.data for a in arrs), C.byref(pat), vals.ctypes.data,
+                          b.ctypes.data):
+        raise RuntimeError(lib.po_last_error().decode())
+    return Csr(rp, cl, vals), b
+
+
+def dgb_to_csr_values(row_ptr, brow_ptr, bcols, dvals, ne):
+    """CSR values (the DG component-aware pattern) of DG block storage:
+    velocity panel c of a block = ne x 2ne [u_c | p] columns, pressure panel
+    ne x 4ne, column-major (csrc/dgb.cu). Test helper."""
+    nb = len(brow_ptr) - 1
+    eb = 4 * ne
+    bsz = 10 * ne * ne
+    out = np.empty(int(row_ptr[-1]))
+    dv = np.asarray(dvals, np.float64)
+    for e in range(nb):
+        q0, q1 = int(brow_ptr[e]), int(brow_ptr[e + 1])
+        blk = dv[q0 * bsz:q1 * bsz].reshape(q1 - q0, bsz)
+        for r in range(eb):
+            row = e * eb + r
+            p = int(row_ptr[row])
+            c, i = divmod(r, ne)
+            if c < 3:
+                panel = blk[:, c * 2 * ne * ne:(c + 1) * 2 * ne * ne].reshape(q1 - q0, 2 * ne, ne)
+                seg = panel[:, :, i]  # (blocks, 2ne)
+            else:
+                panel = blk[:, 6 * ne * ne:].reshape(q1 - q0, 4 * ne, ne)
+                seg = panel[:, :, i]
+            out[p:p + seg.size] = seg.ravel()
+    return out
 
 
 class PortBlockJacobi:
