@@ -80,6 +80,13 @@ int pscu_version(void);
 
 /* context ---------------------------------------------------------------- */
 int pscu_create(int device, pscu_ctx** out);
+/* Device-list form: one context per listed device, written
+ * to out[0..ndev). A host that drives several GPUs from one process gives
+ * each context its own host thread (calls on one context are serialised by
+ * the caller, the reference's single-threaded contract); the z-slab driver
+ * (one process per GPU) passes its one local device. All-or-nothing: on
+ * failure no context is left allocated. */
+int pscu_create_devices(const int* devices, int ndev, pscu_ctx** out);
 int pscu_destroy(pscu_ctx* ctx);
 int pscu_synchronize(pscu_ctx* ctx);
 /* Kernel-launch counter (every kernel this library enqueued). */

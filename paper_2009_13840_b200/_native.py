@@ -33,7 +33,7 @@ EXPORTS = [
     "pscu_solve_system_bsr", "pscu_bsr_download", "pscu_dgb_create", "pscu_mat_dg_modes",
     "pscu_mat_set_values", "pscu_solve_system_dgb", "pscu_host_alloc", "pscu_host_free",
     "pscu_bsr_create_local", "pscu_assembly_begin_local", "pscu_assembly_add_local",
-    "pscu_error_accumulate", "pscu_local_blocks3",
+    "pscu_error_accumulate", "pscu_local_blocks3", "pscu_create_devices",
 ]
 
 
@@ -77,6 +77,7 @@ def load(path: str = LIB):
     pi, pd = C.POINTER(C.c_int), C.POINTER(C.c_double)
     lib.pscu_last_error.restype = C.c_char_p
     lib.pscu_create.argtypes = [i32, C.POINTER(vp)]
+    lib.pscu_create_devices.argtypes = [C.POINTER(i32), i32, C.POINTER(vp)]
     lib.pscu_destroy.argtypes = [vp]
     lib.pscu_synchronize.argtypes = [vp]
     lib.pscu_launch_count.restype = C.c_longlong

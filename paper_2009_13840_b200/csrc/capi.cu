@@ -163,6 +163,25 @@ int pscu_create(int device, pscu_ctx** out) {
   });
 }
 
+int pscu_create_devices(const int* devices, int ndev, pscu_ctx** out) {
+  if (!devices || !out || ndev < 1)
+    return guard([] { throw Error(PSCU_EINVAL, "pscu_create_devices: empty device list"); });
+  for (int i = 0; i < ndev; ++i) out[i] = nullptr;
+  for (int i = 0; i < ndev; ++i) {
+    for (int j = 0; j < i; ++j)
+      if (devices[j] == devices[i]) {
+        for (int q = 0; q < i; ++q) pscu_destroy(out[q]), out[q] = nullptr;
+        return guard([] { throw Error(PSCU_EINVAL, "pscu_create_devices: device listed twice"); });
+      }
+    const int rc = pscu_create(devices[i], &out[i]);
+    if (rc != PSCU_OK) {
+      for (int q = 0; q < i; ++q) pscu_destroy(out[q]), out[q] = nullptr;
+      return rc;  // pscu_last_error() holds pscu_create's message
+    }
+  }
+  return PSCU_OK;
+}
+
 int pscu_destroy(pscu_ctx* ctx) {
   return guard([&] {
     if (ctx) {

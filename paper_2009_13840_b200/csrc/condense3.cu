@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kThreads)
   __shared__ int perm[128];
   __shared__ int piv_row, singular;
   __shared__ int64_t qpair[kMaxFacesPerElem * kMaxFacesPerElem];
-  __shared__ double colnorm[128];
+  __shared__ double colnorm[128], acol[128];
   for (int le = blockIdx.x; le < nelem; le += gridDim.x) {
     const int e = e0 + le;
     const double* M = mats + size_t(le) * n * n;
@@ -93,6 +93,14 @@ __global__ void __launch_bounds__(kThreads)
       qpair[t] = q < q1 ? q : -1;
     }
     if (threadIdx.x == 0) singular = 0;
+    __syncthreads();
+    // absolute column sums of A_ee for the rcond guard's 1-norm (rows
+    // ascending from 0.0, the guard's order), before the LU overwrites it
+    for (int j = threadIdx.x; j < ne; j += blockDim.x) {
+      double s = 0.0;
+      for (int i = 0; i < ne; ++i) s += fabs(LU[i + j * ne]);
+      acol[j] = s;
+    }
     __syncthreads();
     // partial-pivot LU (PartialPivLU::compute of include/eigen_subset)
     for (int k = 0; k < ne; ++k) {
@@ -192,9 +200,7 @@ __global__ void __launch_bounds__(kThreads)
       if (!sing) {
         double an = 0.0, inorm = 0.0;
         for (int j = 0; j < ne; ++j) {
-          double s = 0.0;
-          for (int i = 0; i < ne; ++i) s += fabs(M[elim[i] + size_t(elim[j]) * n]);
-          an = fmax(an, s);
+          an = fmax(an, acol[j]);
           inorm = fmax(inorm, colnorm[j]);
         }
         const double rc = (an > 0.0 && inorm > 0.0 && isfinite(inorm)) ? (1.0 / an) / inorm : 0.0;

@@ -58,6 +58,10 @@ constexpr int kMaxDiag = 128;      // longest task (factor entries) of a walker 
 constexpr int kHdr = 16;           // ints of a chunk header
 constexpr int kLevelMaxNz = 512;   // entries of a task of a level-launch plan (warp kernel buffer)
 constexpr int kLevelMaxRows = 32;  // rows of such a task
+#ifndef PSCU_BSHFL_BLOCK
+#define PSCU_BSHFL_BLOCK 4
+#endif
+constexpr int kFlowSmallNz = 192;  // entry cap of the small-task dataflow kernel
 constexpr int kPadSrc = int(0x80000000);  // level plans: pad entry (product 0; acc - 0.0 == acc)
 
 struct WalkArgs {
@@ -86,6 +90,8 @@ struct WalkArgs {
   long long* ftrace;      // trace build, PSCU_FLOW_TRACE: per task 4 globaltimer stamps,
                           // fold cycles, lane-parallel fold flag
   int rotate;             // dataflow sweeps: rotate the task-to-warp assignment per level
+  int bshfl;              // small-task dataflow sweeps, backward: warp-replicated register fold
+                          // fed by shuffles (needs rows padded to whole 8-entry blocks)
 };
 
 constexpr int kTraceSub = 4096;
@@ -877,12 +883,17 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
     }
     const unsigned full = 0xffffffffu;
     const int nrows = r1 - r0;
-    int rlen = 0;
+    int rlen = 0, rowid = 0;
+    double dvl = 1.0;
     if (lane < nrows) {
       const int k = k0 + r0 + lane;
       rlen = int((r0 + lane + 1 < nr ? a.off[k + 1] : nq) - a.off[k]);
-      mb[w][lane] = make_int4(rlen, a.rows[k], kFwd ? a.opos[k] : 0, 0);
-      if (!kFwd) dvb[w][lane] = a.dv[k];
+      rowid = a.rows[k];
+      mb[w][lane] = make_int4(rlen, rowid, kFwd ? a.opos[k] : 0, 0);
+      if (!kFwd) {
+        dvl = a.dv[k];
+        dvb[w][lane] = dvl;
+      }
     }
     // static row structure, found while the sources are still in flight:
     // lane r < nrows locates row r's in-task entries (sources inside the
@@ -924,7 +935,8 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
       asm volatile("griddepcontrol.wait;" ::: "memory");
       waited = true;
     }
-    if (lane < r1 - r0) rb[w][lane] = __ldcg(rhs + k0 + r0 + lane);
+    const double rbl = lane < nrows ? __ldcg(rhs + k0 + r0 + lane) : 0.0;
+    if (lane < nrows) rb[w][lane] = rbl;
 #ifdef PSCU_TRACE
     if (kFlow && a.ftrace) {
       // the static loads have landed once their values are consumed
@@ -971,6 +983,73 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         const bool out = e < ne && sv[u] < 0 && sv[u] != kPadSrc;
         yv[u] = out ? __ldcg(y + (-sv[u] - 1)) : 0.0;
       }
+    }
+    if (kFlow && !kFwd && kMaxNz == kFlowSmallNz && a.bshfl && lead_ok) {
+      // Backward face-block tasks: a row's in-task sources lead its chain and
+      // the last sources to arrive are its first out-of-task terms, so the
+      // whole task is one dependent subtraction chain after the hand-over.
+      // The products stay in the lanes' registers and every lane runs the
+      // same chain (no divergence, no shared-memory round trip): entry e of
+      // the task lives in lane e % 32, register e / 32; rows hold whole
+      // 8-entry blocks, so kB consecutive entries sit in one register of kB
+      // consecutive lanes and are fetched by kB shuffles, one step ahead of the chain.
+      // Each row still takes its operations in column order, one rounding
+      // per operation: bitwise the sequential fold.
+#ifdef PSCU_TRACE
+      if (a.ftrace && lane == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[2]));
+        fc0 = clock64();
+      }
+#endif
+      double pr[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int e = lane + 32 * u;
+        pr[u] = e < ne && sv[u] != kPadSrc ? (sv[u] < 0 ? dmul(v[u], yv[u]) : v[u]) : 0.0;
+      }
+      constexpr int kB = PSCU_BSHFL_BLOCK;  // entries fetched per step (divides 8)
+      auto fetch = [&](int e, double (&p)[kB]) {
+        const int u = e >> 5, b = e & 31;
+        double sel = pr[0];
+#pragma unroll
+        for (int q = 1; q < kPer; ++q)
+          if (u == q) sel = pr[q];
+#pragma unroll
+        for (int k = 0; k < kB; ++k) p[k] = __shfl_sync(full, sel, b + k);
+      };
+      for (int r = 0; r < nrows; ++r) {
+        const int off = __shfl_sync(full, roff, r), len = __shfl_sync(full, rlen, r);
+        double acc = __shfl_sync(full, rbl, r);
+        const double dvr = __shfl_sync(full, dvl, r);
+        const int rowr = __shfl_sync(full, rowid, r);
+        double nx[kB];
+        if (len > 0) fetch(off, nx);
+        for (int g = 0; g < len; g += kB) {
+          double cur[kB];
+#pragma unroll
+          for (int k = 0; k < kB; ++k) cur[k] = nx[k];
+          if (g + kB < len) fetch(off + g + kB, nx);
+#pragma unroll
+          for (int k = 0; k < kB; ++k) acc = dsub(acc, cur[k]);
+        }
+        acc = __ddiv_rn(acc, dvr);
+        // the row's value enters the later rows' leading in-task terms
+#pragma unroll
+        for (int u = 0; u < kPer; ++u)
+          if (lane + 32 * u < ne && sv[u] == r) pr[u] = dmul(v[u], acc);
+        if (lane == 0) flow_store(y + rowr, acc);
+      }
+#ifdef PSCU_TRACE
+      if (a.ftrace && lane == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[3]));
+        long long* ft = a.ftrace + (size_t(hd[9]) + task) * 6;
+        for (int q = 0; q < 4; ++q) ft[q] = (long long)fts[q];
+        ft[4] = clock64() - fc0;
+        ft[5] = 3;
+      }
+#endif
+      __syncwarp();
+      continue;
     }
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
@@ -1170,7 +1249,6 @@ __global__ void __launch_bounds__(32 * kLevelWarps, 4)
 /// registers and shared memory, so twice the warps are resident and
 /// consecutive task levels run on disjoint warps (a warp's next task is at
 /// least two levels ahead, its operand loads off the critical path).
-constexpr int kFlowSmallNz = 192;
 #ifndef PSCU_FLOW_SMALL_CTAS
 #define PSCU_FLOW_SMALL_CTAS 7
 #endif
@@ -1403,12 +1481,20 @@ static int flow_rotate() {
   return v;
 }
 
+/// Backward small-task dataflow sweeps fold through shuffles (default on;
+/// PSCU_FLOW_BSHFL=0 keeps the shared-memory fold). Needs padded rows.
+int level_pad();
+static int flow_bshfl() {
+  const char* e = getenv("PSCU_FLOW_BSHFL");
+  return (e ? atoi(e) : 1) && level_pad() == 8;
+}
+
 WalkArgs args_of(const WalkPlan& w) {
   return {w.sl_k.p, w.sl_nr.p, w.sl_q.p, w.sl_hdr.p, w.tt.p, w.tq.p, w.rows.p, w.off.p, w.dp.p, w.meta.p,
           w.opos.p, w.val.p,  w.src.p,  w.dv.p,     w.sl_f.p,
           reinterpret_cast<const int2*>(w.far.p), w.sl_s.p,
           reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr, flow_spin_ns(), nullptr,
-          flow_rotate()};
+          flow_rotate(), flow_bshfl()};
 }
 
 size_t walk_smem() { return sizeof(double) * kRing + kStages * sizeof(Stage); }

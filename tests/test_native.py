@@ -48,6 +48,24 @@ def test_no_device_fails_loudly():
         solver.Context(0)
 
 
+def test_device_list_create_fails_loudly_without_gpu():
+    """pscu_create_devices (SURVEY §8(b) signature): bad lists are rejected,
+    and without a GPU it fails like pscu_create, leaving no context behind."""
+    import torch
+
+    lib = _native.load()
+    out = (ctypes.c_void_p * 2)()
+    assert lib.pscu_create_devices(None, 0, out) != 0
+    devs = (ctypes.c_int32 * 2)(0, 0)
+    assert lib.pscu_create_devices(devs, 2, out) != 0  # listed twice, or no device
+    assert out[0] is None and out[1] is None
+    if not torch.cuda.is_available():
+        one = (ctypes.c_int32 * 1)(0)
+        assert lib.pscu_create_devices(one, 1, out) != 0
+        assert out[0] is None
+        assert b"device" in lib.pscu_last_error().lower()
+
+
 def test_host_library_exports_every_declared_symbol():
     """include/pstokes_host.h (the 2D and 3D host producers) likewise."""
     text = open(os.path.join(ROOT, "include", "pstokes_host.h")).read()
