@@ -17,9 +17,9 @@
 //    substitution with the sums j ascending;
 //  * Schur: s = 0, s += A_ke(i,k) X(k,j) for k ascending, S = A_kk - s,
 //    each thread folding a 2 x 2 register tile (four independent chains).
-// The FP64 tensor pipe (DMMA) would reorder these sums, so it is not used:
-// B200's FP64 DMMA and FP64 FFMA peaks are equal, and condensation is < 1%
-// of a solve.
+// The FP64 tensor pipe (DMMA) fuses each multiply-add, so the default path
+// does not use it; PSCU_CONDENSE_DMMA=1 switches the Schur products to
+// mma.sync.m8n8k4.f64 (rounding-level differences).
 //
 // The Schur entries are scattered straight from registers: retained dof i of
 // the element is (local face lf_i, offset o_i in the face block), so entry
@@ -56,12 +56,16 @@ __global__ void __launch_bounds__(kThreads)
     condense_bsr_kernel(int e0, int nelem, int n, const double* __restrict__ mats,
                         const double* __restrict__ rhs, int ne, const int* __restrict__ elim,
                         const int* __restrict__ keep, ScatterArgs sa,
-                        double* __restrict__ coupling, double* __restrict__ erhs, int* bad) {
+                        double* __restrict__ coupling, double* __restrict__ erhs, int* bad,
+                        int dmma) {
   extern __shared__ double sm[];
   const int nk = n - ne;
+  // X is kept transposed, X(k, col) at X[col + k P] with P odd: a thread
+  // owning one column walks it without bank conflicts
+  const int P = (nk + 1) | 1;
   double* LU = sm;                         // ne x ne, column-major
-  double* X = LU + size_t(ne) * ne;        // ne x (nk + 1)
-  double* AKE = X + size_t(ne) * (nk + 1); // nk x ne
+  double* X = LU + size_t(ne) * ne;        // (nk + 1) columns x ne rows, transposed
+  double* AKE = X + size_t(ne) * P;        // nk x ne
   __shared__ int perm[128];
   __shared__ int piv_row, singular;
   __shared__ int64_t qpair[kMaxFacesPerElem * kMaxFacesPerElem];
@@ -70,13 +74,12 @@ __global__ void __launch_bounds__(kThreads)
     const int e = e0 + le;
     const double* M = mats + size_t(le) * n * n;
     const double* b = rhs + size_t(le) * n;
-    for (int t = threadIdx.x; t < ne * ne; t += blockDim.x) {
-      const int i = t % ne, j = t / ne;
-      LU[t] = M[elim[i] + size_t(elim[j]) * n];
-    }
-    for (int t = threadIdx.x; t < nk * ne; t += blockDim.x) {
-      const int i = t % nk, k = t / nk;
-      AKE[t] = M[keep[i] + size_t(elim[k]) * n];
+    // (warps over columns, lanes over rows: no integer division in the
+    // index arithmetic, which otherwise saturates the XU pipe)
+    const int lane_ = int(threadIdx.x & 31), warp_ = int(threadIdx.x >> 5), nwarp_ = int(blockDim.x >> 5);
+    for (int j = warp_; j < ne; j += nwarp_) {
+      const double* Mj = M + size_t(elim[j]) * n;
+      for (int i = lane_; i < ne; i += 32) LU[i + j * ne] = Mj[elim[i]];
     }
     for (int t = threadIdx.x; t < ne; t += blockDim.x) perm[t] = t;
     // block position of every (local face, local face) pair of this element
@@ -146,11 +149,11 @@ __global__ void __launch_bounds__(kThreads)
         for (int i = k + 1 + threadIdx.x; i < ne; i += blockDim.x)
           LU[i + k * ne] = __ddiv_rn(LU[i + k * ne], piv);
         __syncthreads();
-        const int m = ne - k - 1;
-        for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
-          const int i = k + 1 + t % m, j = k + 1 + t / m;
+        for (int j = k + 1 + warp_; j < ne; j += nwarp_) {
           const double ukj = LU[k + j * ne];
-          if (ukj != 0.0) LU[i + j * ne] = dsub(LU[i + j * ne], dmul(LU[i + k * ne], ukj));
+          if (ukj != 0.0)
+            for (int i = k + 1 + lane_; i < ne; i += 32)
+              LU[i + j * ne] = dsub(LU[i + j * ne], dmul(LU[i + k * ne], ukj));
         }
       }
       __syncthreads();
@@ -158,39 +161,58 @@ __global__ void __launch_bounds__(kThreads)
     // solves (one thread per column of [A_ek | b_e]) and, on the remaining
     // threads, the inverse columns of the rcond guard
     const int ncol = nk + 1;
+    for (int col = warp_; col < ncol; col += nwarp_) {
+      const double* src = col < nk ? M + size_t(keep[col]) * n : b;
+      for (int i = lane_; i < ne; i += 32) X[col + size_t(i) * P] = src[elim[perm[i]]];
+    }
+    // the rcond guard's inverse columns share the pass (threads past the
+    // right-hand sides), in the not-yet-staged A_ke region, transposed too
+    const int PI = ne | 1;
+    double* XI = AKE;
+    for (int c = warp_; c < ne; c += nwarp_)
+      for (int i = lane_; i < ne; i += 32) XI[c + size_t(i) * PI] = perm[i] == c ? 1.0 : 0.0;
+    __syncthreads();
     for (int col = threadIdx.x; col < ncol + ne; col += blockDim.x) {
-      if (col < ncol) {
-        double* x = X + size_t(col) * ne;
-        const double* src = col < nk ? M + size_t(keep[col]) * n : b;
-        for (int i = 0; i < ne; ++i) x[i] = src[elim[perm[i]]];
-        for (int i = 0; i < ne; ++i) {
-          double s = x[i];
-          for (int j = 0; j < i; ++j) s = dsub(s, dmul(LU[i + j * ne], x[j]));
-          x[i] = s;
+      double* x = col < ncol ? X + col : XI + (col - ncol);  // x[i S]
+      const int S = col < ncol ? P : PI;
+      // forward substitution (unit L) in axpy form: entry i still takes its
+      // terms j = 0, 1, ... in order with x_j final, the dot form's
+      // operations, but the updates of one step are independent
+      for (int j = 0; j + 1 < ne; ++j) {
+        const double xj = x[size_t(j) * S];
+        const double* l = LU + size_t(j) * ne;
+        int i = j + 1;
+        for (; i + 4 <= ne; i += 4) {
+          double lv[4], xv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            lv[u] = l[i + u];
+            xv[u] = x[size_t(i + u) * S];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[size_t(i + u) * S] = dsub(xv[u], dmul(lv[u], xj));
         }
-        for (int i = ne - 1; i >= 0; --i) {
-          double s = x[i];
-          for (int j = i + 1; j < ne; ++j) s = dsub(s, dmul(LU[i + j * ne], x[j]));
-          x[i] = __ddiv_rn(s, LU[i + i * ne]);
+        for (; i < ne; ++i) x[size_t(i) * S] = dsub(x[size_t(i) * S], dmul(l[i], xj));
+      }
+      // backward substitution: row i's chain starts at the value found last
+      for (int i = ne - 1; i >= 0; --i) {
+        double s = x[size_t(i) * S];
+        int j = i + 1;
+        for (; j + 4 <= ne; j += 4) {
+          double pr[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) pr[u] = dmul(LU[i + size_t(j + u) * ne], x[size_t(j + u) * S]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) s = dsub(s, pr[u]);
         }
-      } else {
-        // column cidx of A_ee^-1 (exact inverse 1-norm for rcond)
-        const int cidx = col - ncol;
-        double xc[128];
-        for (int i = 0; i < ne; ++i) xc[i] = perm[i] == cidx ? 1.0 : 0.0;
-        for (int i = 0; i < ne; ++i) {
-          double t = xc[i];
-          for (int j = 0; j < i; ++j) t = t - LU[i + j * ne] * xc[j];
-          xc[i] = t;
-        }
-        for (int i = ne - 1; i >= 0; --i) {
-          double t = xc[i];
-          for (int j = i + 1; j < ne; ++j) t = t - LU[i + j * ne] * xc[j];
-          xc[i] = t / LU[i + i * ne];
-        }
+        for (; j < ne; ++j) s = dsub(s, dmul(LU[i + size_t(j) * ne], x[size_t(j) * S]));
+        x[size_t(i) * S] = __ddiv_rn(s, LU[i + i * ne]);
+      }
+      if (col >= ncol) {
+        // exact inverse 1-norm for rcond: column sums, rows ascending
         double s = 0.0;
-        for (int i = 0; i < ne; ++i) s += fabs(xc[i]);
-        colnorm[cidx] = s;
+        for (int i = 0; i < ne; ++i) s += fabs(x[size_t(i) * S]);
+        colnorm[col - ncol] = s;
       }
     }
     __syncthreads();
@@ -213,55 +235,114 @@ __global__ void __launch_bounds__(kThreads)
     }
     __syncthreads();
     if (!singular) {
+      // A_ke now (its region held the inverse columns until the guard ran)
+      for (int j = warp_; j < ne; j += nwarp_) {
+        const double* Mj = M + size_t(elim[j]) * n;
+        for (int i = lane_; i < nk; i += 32) AKE[i + j * nk] = Mj[keep[i]];
+      }
+      __syncthreads();
       if (coupling)
-        for (int t = threadIdx.x; t < ne * nk; t += blockDim.x)
-          coupling[size_t(le) * ne * nk + t] = X[t];
+        for (int col = warp_; col < nk; col += nwarp_)
+          for (int i = lane_; i < ne; i += 32)
+            coupling[size_t(le) * ne * nk + size_t(col) * ne + i] = X[col + size_t(i) * P];
       if (erhs)
         for (int t = threadIdx.x; t < ne; t += blockDim.x)
-          erhs[size_t(le) * ne + t] = X[size_t(nk) * ne + t];
-      // Schur complement + reduced load, 2 x 2 tiles, scattered from registers
-      const int ti = (nk + 1) / 2, tj = (ncol + 1) / 2;
+          erhs[size_t(le) * ne + t] = X[nk + size_t(t) * P];
+      // one Schur / reduced-load entry: S(i, j) = A_kk(i, j) - s (j == nk: the
+      // load), scattered from registers
       const int64_t bs2 = int64_t(sa.bs) * sa.bs;
-      for (int t = threadIdx.x; t < ti * tj; t += blockDim.x) {
-        const int i0 = 2 * (t % ti), j0 = 2 * (t / ti);
-        const int i1 = min(i0 + 1, nk - 1), j1 = min(j0 + 1, ncol - 1);
-        double s00 = 0.0, s01 = 0.0, s10 = 0.0, s11 = 0.0;
-        for (int k = 0; k < ne; ++k) {
-          const double a0 = AKE[i0 + k * nk], a1 = AKE[i1 + k * nk];
-          const double x0 = X[k + size_t(j0) * ne], x1 = X[k + size_t(j1) * ne];
-          s00 = dadd(s00, dmul(a0, x0));
-          s01 = dadd(s01, dmul(a0, x1));
-          s10 = dadd(s10, dmul(a1, x0));
-          s11 = dadd(s11, dmul(a1, x1));
+      auto emit = [&](int i, int j, double sum) {
+        const double* src = j < nk ? M + size_t(keep[j]) * n : b;
+        const double v = dsub(src[keep[i]], sum);
+        const int2 pi = sa.keep_pos[i];
+        if (j == nk) {
+          const int F = sa.erows[size_t(le) * sa.nfe + pi.x];
+          if (F >= 0) atomicAdd(sa.rhs + int64_t(F) * sa.bs + pi.y, v);
+          return;
         }
-        const double sv[2][2] = {{s00, s01}, {s10, s11}};
-        for (int di = 0; di < 2; ++di)
-          for (int dj = 0; dj < 2; ++dj) {
-            const int i = di ? i1 : i0, j = dj ? j1 : j0;
-            if ((di && i1 == i0) || (dj && j1 == j0)) continue;
-            const double* src = j < nk ? M + size_t(keep[j]) * n : b;
-            const double v = dsub(src[keep[i]], sv[di][dj]);
-            const int2 pi = sa.keep_pos[i];
-            if (j == nk) {
-              const int F = sa.erows[size_t(le) * sa.nfe + pi.x];
-              if (F >= 0) atomicAdd(sa.rhs + int64_t(F) * sa.bs + pi.y, v);
-              continue;
+        const int2 pj = sa.keep_pos[j];
+        const bool diag = pi.x == pj.x && pi.y == pj.y;
+        if (v == 0.0 && !diag) return;
+        const int64_t q = qpair[pi.x * sa.nfe + pj.x];
+        if (q == -3) return;
+        if (q < 0) {
+          atomicExch(bad, -2);
+          return;
+        }
+        atomicAdd(sa.vals + q * bs2 + int64_t(pj.y) * sa.bs + pi.y, v);
+      };
+      if (dmma) {
+        // FP64 tensor-pipe variant (opt-in): s = A_ke X on
+        // mma.sync.m8n8k4.f64, 16 x 16 outputs per warp step (2 x 2 tiles),
+        // k ascending in steps of 4 from a zero accumulator. The tensor pipe
+        // fuses each multiply-add (one rounding where the reference order
+        // takes two), so the entries agree with the SIMT path to rounding
+        // (~1e-16 relative to the row's terms), not bit for bit.
+        const int warp = int(threadIdx.x >> 5), lane = int(threadIdx.x & 31);
+        const int nwarp = int(blockDim.x >> 5), g = lane >> 2, q4 = lane & 3;
+        const int mt2 = (nk + 15) / 16, nt2 = (ncol + 15) / 16;
+        for (int t = warp; t < mt2 * nt2; t += nwarp) {
+          const int i0 = 16 * (t % mt2), j0 = 16 * (t / mt2);
+          double c[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+          for (int k0 = 0; k0 < ne; k0 += 4) {
+            const int k = k0 + q4;
+            double av[2], bv[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int i = i0 + 8 * h + g, j = j0 + 8 * h + g;
+              av[h] = (k < ne && i < nk) ? AKE[i + k * nk] : 0.0;
+              bv[h] = (k < ne && j < ncol) ? X[j + size_t(k) * P] : 0.0;
             }
-            const int2 pj = sa.keep_pos[j];
-            const bool diag = pi.x == pj.x && pi.y == pj.y;
-            if (v == 0.0 && !diag) continue;
-            const int64_t q = qpair[pi.x * sa.nfe + pj.x];
-            if (q == -3) continue;
-            if (q < 0) {
-              atomicExch(bad, -2);
-              continue;
-            }
-            atomicAdd(sa.vals + q * bs2 + int64_t(pj.y) * sa.bs + pi.y, v);
+#pragma unroll
+            for (int hi = 0; hi < 2; ++hi)
+#pragma unroll
+              for (int hj = 0; hj < 2; ++hj)
+                asm volatile(
+                    "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                    : "+d"(c[hi][hj][0]), "+d"(c[hi][hj][1])
+                    : "d"(av[hi]), "d"(bv[hj]));
           }
+#pragma unroll
+          for (int hi = 0; hi < 2; ++hi)
+#pragma unroll
+            for (int hj = 0; hj < 2; ++hj)
+#pragma unroll
+              for (int d = 0; d < 2; ++d) {
+                const int i = i0 + 8 * hi + g, j = j0 + 8 * hj + 2 * q4 + d;
+                if (i < nk && j < ncol) emit(i, j, c[hi][hj][d]);
+              }
+        }
+      } else {
+        // reference order (bitwise): 2 x 2 register tiles of independent chains
+        const int ti = (nk + 1) / 2, tj = (ncol + 1) / 2;
+        for (int t = threadIdx.x; t < ti * tj; t += blockDim.x) {
+          const int i0 = 2 * (t % ti), j0 = 2 * (t / ti);
+          const int i1 = min(i0 + 1, nk - 1), j1 = min(j0 + 1, ncol - 1);
+          double s00 = 0.0, s01 = 0.0, s10 = 0.0, s11 = 0.0;
+          for (int k = 0; k < ne; ++k) {
+            const double a0 = AKE[i0 + k * nk], a1 = AKE[i1 + k * nk];
+            const double x0 = X[j0 + size_t(k) * P], x1 = X[j1 + size_t(k) * P];
+            s00 = dadd(s00, dmul(a0, x0));
+            s01 = dadd(s01, dmul(a0, x1));
+            s10 = dadd(s10, dmul(a1, x0));
+            s11 = dadd(s11, dmul(a1, x1));
+          }
+          emit(i0, j0, s00);
+          if (j1 != j0) emit(i0, j1, s01);
+          if (i1 != i0) emit(i1, j0, s10);
+          if (i1 != i0 && j1 != j0) emit(i1, j1, s11);
+        }
       }
     }
     __syncthreads();
   }
+}
+
+/// PSCU_CONDENSE_DMMA=1: Schur products on the FP64 tensor pipe (rounding-level
+/// differences from the reference order; default 0 = bitwise SIMT chains).
+int condense_dmma() {
+  const char* e = getenv("PSCU_CONDENSE_DMMA");
+  return e && atoi(e) != 0;
 }
 
 } // namespace
@@ -294,7 +375,9 @@ void condense_scatter_bsr(Context& c, Csr& a, int e0, int nelem, int n, const do
   d_kp.upload(kp, c.stream);
   const int big = 0x7fffffff;
   PSCU_CUDA(cudaMemcpyAsync(c.err_flag.p, &big, sizeof(int), cudaMemcpyHostToDevice, c.stream));
-  const size_t smem = sizeof(double) * (size_t(ne) * ne + size_t(ne) * (nk + 1) + size_t(nk) * ne);
+  const size_t smem =
+      sizeof(double) * (size_t(ne) * ne + size_t(ne) * ((nk + 1) | 1) +
+                        std::max(size_t(nk) * ne, size_t(ne) * (ne | 1)));
   if (smem > 227 * 1024) throw Error(PSCU_EINVAL, "condense_scatter: block too large for shared memory");
   static size_t attr = 0;
   if (smem > attr) {
@@ -309,7 +392,7 @@ void condense_scatter_bsr(Context& c, Csr& a, int e0, int nelem, int n, const do
   const int grid = std::max(1, std::min(nelem, 148 * std::max(1, per_sm)));
   condense_bsr_kernel<<<grid, kThreads, smem, c.stream>>>(e0, nelem, n, mats, rhs, ne, d_elim.p,
                                                           d_keep.p, sa, coupling, erhs,
-                                                          c.err_flag.p);
+                                                          c.err_flag.p, condense_dmma());
   PSCU_LAUNCHED(&c);
   int bad = big;
   PSCU_CUDA(cudaMemcpyAsync(&bad, c.err_flag.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));

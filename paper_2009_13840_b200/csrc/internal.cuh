@@ -168,7 +168,7 @@ struct WalkPlan {
   mutable DevBuf<unsigned long long> barrier;  // persistent task-level kernel
   int persist_grid = 0;                        // its grid (0: per-level launches)
   int flow_grid = 0;                           // dataflow sweep grid (0: off)
-  bool flow_small = false;                     // ... with the small-task kernel
+  int flow_small = 0;                          // ... with the small-task (1) / mid-task (2) kernel
   int64_t ny = 0;                              // rows of the sweep (sentinel fill)
 };
 

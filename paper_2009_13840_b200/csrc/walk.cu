@@ -61,7 +61,11 @@ constexpr int kLevelMaxRows = 32;  // rows of such a task
 #ifndef PSCU_BSHFL_BLOCK
 #define PSCU_BSHFL_BLOCK 4
 #endif
+#ifndef PSCU_FLOW_MID_CTAS
+#define PSCU_FLOW_MID_CTAS 4
+#endif
 constexpr int kFlowSmallNz = 192;  // entry cap of the small-task dataflow kernel
+constexpr int kFlowMidNz = 384;    // ... of the mid-task one (chains of a whole element's face blocks)
 constexpr int kPadSrc = int(0x80000000);  // level plans: pad entry (product 0; acc - 0.0 == acc)
 
 struct WalkArgs {
@@ -883,18 +887,25 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
     }
     const unsigned full = 0xffffffffu;
     const int nrows = r1 - r0;
-    int rlen = 0, rowid = 0;
-    double dvl = 1.0;
-    if (lane < nrows) {
-      const int k = k0 + r0 + lane;
-      rlen = int((r0 + lane + 1 < nr ? a.off[k + 1] : nq) - a.off[k]);
-      rowid = a.rows[k];
-      mb[w][lane] = make_int4(rlen, rowid, kFwd ? a.opos[k] : 0, 0);
-      if (!kFwd) {
-        dvl = a.dv[k];
-        dvb[w][lane] = dvl;
-      }
-    }
+    // Row data: every lane loads (lanes past the task's rows re-read row 0)
+    // so the prologue has no divergent branch around a global load. A lane
+    // group split off here is not merged again by __syncwarp, and the
+    // shuffle folds below then run as rendezvous of diverged groups
+    // (measured: 4 of 32 lanes converged at the fold, 50x slower shuffles).
+    const bool rowl = lane < nrows;
+    const int lr = rowl ? lane : 0;
+    const int krow = k0 + r0 + lr;
+    const bool more = r0 + lr + 1 < nr;
+    const int off0 = a.off[krow], off1 = a.off[krow + (more ? 1 : 0)];
+    const int rid = a.rows[krow];
+    const int opz = kFwd ? a.opos[krow] : 0;
+    const double dvr0 = kFwd ? 1.0 : a.dv[krow];
+    const int rlen = rowl ? (more ? off1 : nq) - off0 : 0;
+    const int rowid = rowl ? rid : 0;
+    const double dvl = rowl ? dvr0 : 1.0;
+    // (every lane stores its slot, rows or not: kLevelMaxRows = 32 slots)
+    mb[w][lane] = make_int4(rlen, rowid, opz, 0);
+    if (!kFwd) dvb[w][lane] = dvl;
     // static row structure, found while the sources are still in flight:
     // lane r < nrows locates row r's in-task entries (sources inside the
     // task) among its out-of-task ones. Forward face-block rows have them
@@ -914,29 +925,28 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
       const unsigned bi = __ballot_sync(full, e < ne && sv[u] >= 0);
       const unsigned bo = __ballot_sync(full, e < ne && sv[u] < 0 && sv[u] != kPadSrc);
       const int lo = max(roff, 32 * u), hi = min(roff + rlen, 32 * u + 32);
-      if (lane < nrows && lo < hi) {
-        const int b0 = lo - 32 * u, b1 = hi - 32 * u;
-        const unsigned m = (b1 == 32 ? full : ((1u << b1) - 1u)) & ~((1u << b0) - 1u);
-        const unsigned mi = bi & m, mo = bo & m;
-        if (mi) {
-          fin = min(fin, 32 * u + __ffs(int(mi)) - 1 - roff);
-          lin = max(lin, 32 * u + 31 - __clz(int(mi)) - roff);
-        }
-        if (mo) {
-          fout = min(fout, 32 * u + __ffs(int(mo)) - 1 - roff);
-          lout = max(lout, 32 * u + 31 - __clz(int(mo)) - roff);
-        }
-      }
+      // (selects, no branches: see the note on divergence above)
+      const bool act = rowl && lo < hi;
+      const int b0 = act ? lo - 32 * u : 0, b1 = act ? hi - 32 * u : 0;
+      const unsigned m = act ? ((b1 == 32 ? full : ((1u << b1) - 1u)) & ~((1u << b0) - 1u)) : 0u;
+      const unsigned mi = bi & m, mo = bo & m;
+      const int fi = 32 * u + __ffs(int(mi)) - 1 - roff, li = 32 * u + 31 - __clz(int(mi)) - roff;
+      const int fo = 32 * u + __ffs(int(mo)) - 1 - roff, lo2 = 32 * u + 31 - __clz(int(mo)) - roff;
+      fin = mi ? min(fin, fi) : fin;
+      lin = mi ? max(lin, li) : lin;
+      fout = mo ? min(fout, fo) : fout;
+      lout = mo ? max(lout, lo2) : lout;
     }
     const bool trail_ok = __all_sync(full, lane >= nrows || lout < fin);
     const bool lead_ok = __all_sync(full, lane >= nrows || lin < fout);
-    if (lane < nrows) rinfo[w][lane] = make_int2(roff, lin + 1);
+    rinfo[w][lane] = make_int2(roff, lin + 1);
     if (!waited) {
       asm volatile("griddepcontrol.wait;" ::: "memory");
       waited = true;
     }
-    const double rbl = lane < nrows ? __ldcg(rhs + k0 + r0 + lane) : 0.0;
-    if (lane < nrows) rb[w][lane] = rbl;
+    const double rbl0 = __ldcg(rhs + krow);
+    const double rbl = rowl ? rbl0 : 0.0;
+    rb[w][lane] = rbl;
 #ifdef PSCU_TRACE
     if (kFlow && a.ftrace) {
       // the static loads have landed once their values are consumed
@@ -984,7 +994,7 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         yv[u] = out ? __ldcg(y + (-sv[u] - 1)) : 0.0;
       }
     }
-    if (kFlow && !kFwd && kMaxNz == kFlowSmallNz && a.bshfl && lead_ok) {
+    if (kFlow && !kFwd && kMaxNz <= kFlowMidNz && a.bshfl && lead_ok) {
       // Backward face-block tasks: a row's in-task sources lead its chain and
       // the last sources to arrive are its first out-of-task terms, so the
       // whole task is one dependent subtraction chain after the hand-over.
@@ -995,7 +1005,12 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
       // consecutive lanes and are fetched by kB shuffles, one step ahead of the chain.
       // Each row still takes its operations in column order, one rounding
       // per operation: bitwise the sequential fold.
+      // (the lanes leave the polling loop at different rounds: reconverge
+      // first, or every shuffle below becomes a rendezvous of diverged groups)
+      __syncwarp();
 #ifdef PSCU_TRACE
+      const unsigned am0 = __activemask();
+      unsigned am1 = 0;
       if (a.ftrace && lane == 0) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[2]));
         fc0 = clock64();
@@ -1008,12 +1023,17 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         pr[u] = e < ne && sv[u] != kPadSrc ? (sv[u] < 0 ? dmul(v[u], yv[u]) : v[u]) : 0.0;
       }
       constexpr int kB = PSCU_BSHFL_BLOCK;  // entries fetched per step (divides 8)
+      int ucur = -1;  // register index held in sel (32 consecutive entries share one)
+      double sel = 0.0;
       auto fetch = [&](int e, double (&p)[kB]) {
         const int u = e >> 5, b = e & 31;
-        double sel = pr[0];
+        if (u != ucur) {
+          sel = pr[0];
 #pragma unroll
-        for (int q = 1; q < kPer; ++q)
-          if (u == q) sel = pr[q];
+          for (int q = 1; q < kPer; ++q)
+            if (u == q) sel = pr[q];
+          ucur = u;
+        }
 #pragma unroll
         for (int k = 0; k < kB; ++k) p[k] = __shfl_sync(full, sel, b + k);
       };
@@ -1023,6 +1043,9 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         const double dvr = __shfl_sync(full, dvl, r);
         const int rowr = __shfl_sync(full, rowid, r);
         double nx[kB];
+#ifdef PSCU_TRACE
+        if (r == 1) am1 = __activemask();
+#endif
         if (len > 0) fetch(off, nx);
         for (int g = 0; g < len; g += kB) {
           double cur[kB];
@@ -1037,7 +1060,9 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
 #pragma unroll
         for (int u = 0; u < kPer; ++u)
           if (lane + 32 * u < ne && sv[u] == r) pr[u] = dmul(v[u], acc);
+        ucur = -1;
         if (lane == 0) flow_store(y + rowr, acc);
+        __syncwarp();
       }
 #ifdef PSCU_TRACE
       if (a.ftrace && lane == 0) {
@@ -1045,7 +1070,7 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         long long* ft = a.ftrace + (size_t(hd[9]) + task) * 6;
         for (int q = 0; q < 4; ++q) ft[q] = (long long)fts[q];
         ft[4] = clock64() - fc0;
-        ft[5] = 3;
+        ft[5] = 3 + 1000 * __popc(am0) + 100000 * __popc(am1);
       }
 #endif
       __syncwarp();
@@ -1261,6 +1286,14 @@ __global__ void __launch_bounds__(32 * kLevelWarps, kFlowSmallCtas)
 }
 
 
+/// The same for tasks of up to kFlowMidNz entries (chains of the three face
+/// blocks an element introduces: a third of the task levels).
+template <bool kFwd>
+__global__ void __launch_bounds__(32 * kLevelWarps, PSCU_FLOW_MID_CTAS)
+    level_flow_mid_kernel(WalkArgs a, int c0, int c1, const double* rhs, double* y, double* yb) {
+  for (int ch = c0; ch < c1; ++ch) level_chunk<kFwd, false, true, kFlowMidNz>(a, ch, rhs, y, yb);
+}
+
 /// The same with a two-stage software pipeline over the warp's task
 /// sequence (PSCU_LEVEL_FLOW=2): the record of task t+2 and the entries,
 /// row data and right-hand sides of task t+1 (whose record arrived one task
@@ -1465,8 +1498,9 @@ static int flow_spin_ns() {
   return v;
 }
 
-static void* flow_kernel_fn(bool fwd, bool v2, bool small) {
+static void* flow_kernel_fn(bool fwd, bool v2, int small) {
   if (v2) return fwd ? (void*)level_flow2_kernel<true> : (void*)level_flow2_kernel<false>;
+  if (small == 2) return fwd ? (void*)level_flow_mid_kernel<true> : (void*)level_flow_mid_kernel<false>;
   if (small) return fwd ? (void*)level_flow_small_kernel<true> : (void*)level_flow_small_kernel<false>;
   return fwd ? (void*)level_flow_kernel<true> : (void*)level_flow_kernel<false>;
 }
@@ -2296,7 +2330,8 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
         maxnz = std::max(maxnz, int(h.tq[t0 + 1] - h.tq[t0]));
       }
     const char* fs = getenv("PSCU_LEVEL_FLOW_SMALL");
-    w.flow_small = !v2 && maxnz <= kFlowSmallNz && (!fs || atoi(fs) != 0);
+    w.flow_small = 0;
+    if (!v2 && (!fs || atoi(fs) != 0)) w.flow_small = maxnz <= kFlowSmallNz ? 1 : (maxnz <= kFlowMidNz ? 2 : 0);
     void* fn = flow_kernel_fn(fwd, v2, w.flow_small);
     PSCU_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kLevelWarps, 0));
     int most = 0;

@@ -138,3 +138,32 @@ def test_inherit_bsr_matches_csr(M):
         r1 = S.inherit_matrix(A, lf, lc).download()
         r2 = S.inherit_matrix(Ac, lf, lc).download()
         assert all(np.array_equal(u, v) for u, v in zip(r1, r2))
+
+
+def test_dmma_condensation_variant_within_tolerance(M, monkeypatch):
+    """PSCU_CONDENSE_DMMA=1: the Schur products A_ke X on the FP64 tensor pipe
+    (mma.sync.m8n8k4.f64). The tensor pipe fuses each multiply-add, so the
+    operator agrees with the reference-order (bitwise) path to rounding, not
+    bit for bit; the bar is BASELINE.json's: same pattern and iteration
+    counts, residual history and solution within 1e-9 relative."""
+    host, S = M
+    m = host.Mesh3(4, jitter=0.15, seed=1)
+    A0, b0, lay, _ = host.assemble_stokes3(m, 2, data="random", seed=2)
+    monkeypatch.setenv("PSCU_CONDENSE_DMMA", "1")
+    A1, b1, lay1, _ = host.assemble_stokes3(m, 2, data="random", seed=2, batch=37)
+    monkeypatch.delenv("PSCU_CONDENSE_DMMA")
+    rp0, c0, v0 = A0.download()
+    rp1, c1, v1 = A1.download()
+    assert np.array_equal(rp0, rp1) and np.array_equal(c0, c1)
+    scale = np.abs(v0).max()
+    assert np.abs(v1 - v0).max() <= 1e-12 * scale
+    assert not same(v0, v1)  # the variant really ran (fused rounding differs somewhere)
+    assert np.abs(b1 - b0).max() <= 1e-12 * max(np.abs(b0).max(), 1.0)
+    cfg = S.LevelConfig(degrees=[2, 1, 0], coarse="gmres-ilu", smoother="bjacobi",
+                        outer_rtol=1e-8, restart=30)
+    x0, h0, r0 = S.LevelHierarchy(A0, lay, cfg).solve(b0)
+    x1, h1, r1 = S.LevelHierarchy(A1, lay1, cfg).solve(b1)
+    assert r0.converged and r1.converged
+    assert r1.outer_its == r0.outer_its and r1.coarse_its == r0.coarse_its  # tolerance: exact counts
+    assert np.all(np.abs(h1 - h0) <= 1e-9 * np.abs(h0))  # tolerance 1e-9 relative
+    assert np.abs(x1 - x0).max() <= 1e-9 * np.abs(x0).max()  # tolerance 1e-9 relative

@@ -61,9 +61,16 @@ def main(path):
             print(f"  level-closing task fold: {np.median(cur[:, 4]):.0f} cycles median")
     if st.shape[1] >= 6:
         done = st[st[:, 3] > 0]
-        kinds = done[:, 5]
+        kinds = done[:, 5] % 1000
+        if (done[:, 5] >= 1000).any():
+            sel = done[:, 5] >= 1000
+            a0 = (done[sel, 5] // 1000) % 100
+            a1 = done[sel, 5] // 100000
+            print(f"  shuffle-chain tasks: active lanes at entry median {np.median(a0):.0f} "
+                  f"(min {a0.min()}), in the row loop median {np.median(a1):.0f} (min {a1.min()})")
         for name, sel in (("lane-parallel", kinds == 1), ("lane-0 leading in-task + chain", kinds == 2),
-                          ("lane-0 general order", kinds == 0)):
+                          ("lane-0 general order", kinds == 0),
+                          ("warp-replicated shuffle chain", kinds == 3)):
             if sel.any():
                 cyc = done[sel, 4]
                 print(f"  {name} folds: {int(sel.sum())} tasks, {np.median(cyc):.0f} cycles median, "
