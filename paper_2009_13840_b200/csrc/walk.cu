@@ -94,6 +94,9 @@ struct WalkArgs {
   long long* ftrace;      // trace build, PSCU_FLOW_TRACE: per task 4 globaltimer stamps,
                           // fold cycles, lane-parallel fold flag
   int rotate;             // dataflow sweeps: rotate the task-to-warp assignment per level
+  int lead;               // dataflow sweeps: wait on the task's latest source with one
+                          // warp-uniform load before polling all sources (keeps the
+                          // load/store unit free for the folding warps' LDS / SHFL)
   int bshfl;              // small-task dataflow sweeps, backward: warp-replicated register fold
                           // fed by shuffles (needs rows padded to whole 8-entry blocks)
 };
@@ -960,6 +963,26 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
     if (kFlow) {
       // all source values requested at once (one round trip), then only the
       // ones still holding the sentinel are polled again
+      if (a.lead) {
+        // The source expected last (the nearest row: highest index in a
+        // forward sweep, lowest in a backward one) is awaited first, by one
+        // load of one address per round for the whole warp: 27 of an SM's 28
+        // warps are waiting at any time, and their per-lane polls otherwise
+        // fill the load/store unit the folding warps' shared-memory loads
+        // and shuffles go through (measured ~45 cycles per LDS / SHFL).
+        int jd = kFwd ? -1 : 0x7fffffff;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int e = lane + 32 * u;
+          const bool out = e < ne && sv[u] < 0 && sv[u] != kPadSrc;
+          const int j = -sv[u] - 1;
+          if (out) jd = kFwd ? max(jd, j) : min(jd, j);
+        }
+        jd = kFwd ? __reduce_max_sync(0xffffffffu, jd) : __reduce_min_sync(0xffffffffu, jd);
+        if (jd >= 0 && jd != 0x7fffffff)
+          while (flow_peek(y + jd) == kFlowSentinel)
+            if (a.spin_ns) __nanosleep(a.spin_ns);
+      }
       unsigned long long raw[kPer];
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
@@ -974,7 +997,11 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         bool pending = false;
 #pragma unroll
         for (int u = 0; u < kPer; ++u) pending = pending || raw[u] == kFlowSentinel;
-        if (!pending) break;
+        // warp-uniform exit: lanes leaving the loop one by one stay split
+        // into separately scheduled groups afterwards (measured: 4 of 32
+        // lanes converged at the fold), which turns every later warp shuffle
+        // into a rendezvous
+        if (!__any_sync(0xffffffffu, pending)) break;
         if (a.spin_ns) __nanosleep(a.spin_ns);
 #pragma unroll
         for (int u = 0; u < kPer; ++u)
@@ -1517,6 +1544,12 @@ static int flow_rotate() {
 
 /// Backward small-task dataflow sweeps fold through shuffles (default on;
 /// PSCU_FLOW_BSHFL=0 keeps the shared-memory fold). Needs padded rows.
+/// Dataflow sweeps wait on the latest source first (PSCU_FLOW_LEAD=0: poll all).
+static int flow_lead() {
+  const char* e = getenv("PSCU_FLOW_LEAD");
+  return e ? atoi(e) : 1;
+}
+
 int level_pad();
 static int flow_bshfl() {
   const char* e = getenv("PSCU_FLOW_BSHFL");
@@ -1528,7 +1561,7 @@ WalkArgs args_of(const WalkPlan& w) {
           w.opos.p, w.val.p,  w.src.p,  w.dv.p,     w.sl_f.p,
           reinterpret_cast<const int2*>(w.far.p), w.sl_s.p,
           reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr, flow_spin_ns(), nullptr,
-          flow_rotate(), flow_bshfl()};
+          flow_rotate(), flow_lead(), flow_bshfl()};
 }
 
 size_t walk_smem() { return sizeof(double) * kRing + kStages * sizeof(Stage); }
