@@ -43,7 +43,8 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_native(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+def build_native(force: bool = False, verbose: bool = False, trace: bool = False,
+                 variant: str = "", defines=()) -> str:
     """Builds libpstokes_b200.so. trace=True builds the walker-instrumented
     variant (-DPSCU_TRACE; PSCU_WALK_TRACE=1 at run time) into
     tools/libpstokes_trace.so instead (diagnostics: PSCU_LIB=<that path>)."""
@@ -51,6 +52,11 @@ def build_native(force: bool = False, verbose: bool = False, trace: bool = False
     obj_dir = os.path.join(PKG, "_build_trace") if trace else OBJ
     lib = os.path.join(ROOT, "tools", "libpstokes_trace.so") if trace else LIB
     flags = NVCC_FLAGS + (["-DPSCU_TRACE"] if trace else [])
+    if variant:
+        # tuning builds (compile-time knobs): tools/libpstokes_<variant>.so, PSCU_LIB=<that path>
+        obj_dir = os.path.join(PKG, "_build_" + variant)
+        lib = os.path.join(ROOT, "tools", f"libpstokes_{variant}.so")
+        flags = flags + ["-D" + d for d in defines]
     os.makedirs(obj_dir, exist_ok=True)
     sources = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]

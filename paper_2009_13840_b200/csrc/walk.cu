@@ -805,6 +805,13 @@ __device__ __forceinline__ void flow_store(double* p, double v) {
   asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+__device__ __forceinline__ void flow_store_if(double* p, double v, bool on) {
+  asm volatile(
+      "{ .reg .pred q; setp.ne.s32 q, %2, 0; @q st.relaxed.gpu.global.f64 [%0], %1; }" ::"l"(p),
+      "d"(v), "r"(int(on))
+      : "memory");
+}
+
 __global__ void fill_sentinel(int64_t n, double* y) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x)
@@ -1049,36 +1056,39 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         const int e = lane + 32 * u;
         pr[u] = e < ne && sv[u] != kPadSrc ? (sv[u] < 0 ? dmul(v[u], yv[u]) : v[u]) : 0.0;
       }
-      constexpr int kB = PSCU_BSHFL_BLOCK;  // entries fetched per step (divides 8)
-      int ucur = -1;  // register index held in sel (32 consecutive entries share one)
-      double sel = 0.0;
+      // Rows hold whole 8-entry blocks: one step fetches a block (8 shuffles
+      // of one register, chosen by selects, no branch) while the previous
+      // block is subtracted; the look-ahead past a row's end reads entries
+      // that are never used (clamped to the task's registers).
+      constexpr int kB = 8;
       auto fetch = [&](int e, double (&p)[kB]) {
         const int u = e >> 5, b = e & 31;
-        if (u != ucur) {
-          sel = pr[0];
+        double sel = pr[0];
 #pragma unroll
-          for (int q = 1; q < kPer; ++q)
-            if (u == q) sel = pr[q];
-          ucur = u;
-        }
+        for (int q = 1; q < kPer; ++q) sel = u == q ? pr[q] : sel;
 #pragma unroll
         for (int k = 0; k < kB; ++k) p[k] = __shfl_sync(full, sel, b + k);
       };
-      for (int r = 0; r < nrows; ++r) {
-        const int off = __shfl_sync(full, roff, r), len = __shfl_sync(full, rlen, r);
+      constexpr int kLastBlock = kMaxNz - kB;
+      // Loop bounds and row data come from warp reductions (REDUX results
+      // are uniform registers), so the control flow is uniform.
+      const int nrows_u = __reduce_max_sync(full, nrows);
+      for (int r = 0; r < nrows_u; ++r) {
+        const int off = __reduce_max_sync(full, lane == r ? roff : 0);
+        const int len = __reduce_max_sync(full, lane == r ? rlen : 0);
+        const int rowr = __reduce_max_sync(full, lane == r ? rowid : 0);
         double acc = __shfl_sync(full, rbl, r);
         const double dvr = __shfl_sync(full, dvl, r);
-        const int rowr = __shfl_sync(full, rowid, r);
         double nx[kB];
 #ifdef PSCU_TRACE
         if (r == 1) am1 = __activemask();
 #endif
-        if (len > 0) fetch(off, nx);
+        fetch(min(off, kLastBlock), nx);
         for (int g = 0; g < len; g += kB) {
           double cur[kB];
 #pragma unroll
           for (int k = 0; k < kB; ++k) cur[k] = nx[k];
-          if (g + kB < len) fetch(off + g + kB, nx);
+          fetch(min(off + g + kB, kLastBlock), nx);
 #pragma unroll
           for (int k = 0; k < kB; ++k) acc = dsub(acc, cur[k]);
         }
@@ -1087,9 +1097,8 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
 #pragma unroll
         for (int u = 0; u < kPer; ++u)
           if (lane + 32 * u < ne && sv[u] == r) pr[u] = dmul(v[u], acc);
-        ucur = -1;
-        if (lane == 0) flow_store(y + rowr, acc);
-        __syncwarp();
+        // every lane holds the same value: one predicated store, no branch
+        flow_store_if(y + rowr, acc, lane == 0);
       }
 #ifdef PSCU_TRACE
       if (a.ftrace && lane == 0) {
@@ -1305,9 +1314,14 @@ __global__ void __launch_bounds__(32 * kLevelWarps, 4)
 #define PSCU_FLOW_SMALL_CTAS 7
 #endif
 constexpr int kFlowSmallCtas = PSCU_FLOW_SMALL_CTAS;
+#ifndef PSCU_FLOW_SMALL_CTAS_BWD
+#define PSCU_FLOW_SMALL_CTAS_BWD 5
+#endif
+// the backward kernel's shuffle fold keeps two 8-entry blocks in registers
+constexpr int kFlowSmallCtasBwd = PSCU_FLOW_SMALL_CTAS_BWD;
 
 template <bool kFwd>
-__global__ void __launch_bounds__(32 * kLevelWarps, kFlowSmallCtas)
+__global__ void __launch_bounds__(32 * kLevelWarps, kFwd ? kFlowSmallCtas : kFlowSmallCtasBwd)
     level_flow_small_kernel(WalkArgs a, int c0, int c1, const double* rhs, double* y, double* yb) {
   for (int ch = c0; ch < c1; ++ch) level_chunk<kFwd, false, true, kFlowSmallNz>(a, ch, rhs, y, yb);
 }
