@@ -97,6 +97,8 @@ struct WalkArgs {
   int lead;               // dataflow sweeps: wait on the task's latest source with one
                           // warp-uniform load before polling all sources (keeps the
                           // load/store unit free for the folding warps' LDS / SHFL)
+  int bfast;              // small-task dataflow sweeps, backward: lane-0 fold from dense
+                          // products (8-entry blocks, row values in registers)
   int bshfl;              // small-task dataflow sweeps, backward: warp-replicated register fold
                           // fed by shuffles (needs rows padded to whole 8-entry blocks)
 };
@@ -867,7 +869,10 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
   // task count (hd[10]), so consecutive levels start on different warps
   const int Wg = int(gridDim.x) * kLevelWarps;
   int first = int(blockIdx.x) * kLevelWarps + w;
-  if (kFlow && a.rotate) first = int((int64_t(first) - hd[10] % Wg + Wg) % Wg);
+  if (kFlow && a.rotate) {
+    first -= hd[11];  // running task count modulo the grid's warps (host-reduced)
+    if (first < 0) first += Wg;
+  }
   for (int task = first; task < nt; task += Wg) {
     // one round trip for the task record, one for its rows and entries
     // (both static), one for the sources outside the task
@@ -950,6 +955,8 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
     const bool trail_ok = __all_sync(full, lane >= nrows || lout < fin);
     const bool lead_ok = __all_sync(full, lane >= nrows || lin < fout);
     rinfo[w][lane] = make_int2(roff, lin + 1);
+    // backward sweeps: the whole row header in one 16-byte slot
+    if (!kFwd) mb[w][lane] = make_int4(rlen, rowid, roff, lin + 1);
     if (!waited) {
       asm volatile("griddepcontrol.wait;" ::: "memory");
       waited = true;
@@ -1027,6 +1034,96 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         const bool out = e < ne && sv[u] < 0 && sv[u] != kPadSrc;
         yv[u] = out ? __ldcg(y + (-sv[u] - 1)) : 0.0;
       }
+    }
+    if (kFlow && !kFwd && kMaxNz == kFlowSmallNz && a.bfast && !a.bshfl && lead_ok && nrows <= 4) {
+      // Backward face-block tasks on lane 0, shaped by the ncu stall profile
+      // of the general fold (profiles/r03c_flow_bwd_lines.txt: the leading
+      // in-task terms cost as much as the whole chain — two dependent
+      // shared-memory loads per term — and every row re-read its header):
+      //  * dense 8-byte products, 128-bit loads, one 8-entry block ahead;
+      //  * the rows' values stay in registers (rows unrolled), so a leading
+      //    in-task term is one multiply and one subtraction;
+      //  * all row headers and right-hand sides are loaded before the chain.
+      // Same operations in the same order as the general fold: bitwise.
+      double* prod = reinterpret_cast<double*>(&rec[w][0]);   // kMaxNz products
+      int* srcs = reinterpret_cast<int*>(prod + kMaxNz);      // kMaxNz sources
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int e = lane + 32 * u;
+        if (e < ne) {
+          prod[e] = sv[u] == kPadSrc ? 0.0 : (sv[u] < 0 ? dmul(v[u], yv[u]) : v[u]);
+          srcs[e] = sv[u];
+        }
+      }
+      __syncwarp();
+#ifdef PSCU_TRACE
+      if (a.ftrace && lane == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[2]));
+        fc0 = clock64();
+      }
+#endif
+      if (lane == 0) {
+        int4 hdr[4];
+        double rh[4], dd[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int rr = r < nrows ? r : 0;
+          hdr[r] = mb[w][rr];
+          rh[r] = rb[w][rr];
+          dd[r] = dvb[w][rr];
+        }
+        double xs[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r < nrows) {
+            const int len = hdr[r].x, lead = hdr[r].w;
+            const double2* pb = reinterpret_cast<const double2*>(prod + hdr[r].z);
+            double acc = rh[r];
+            if (len > 0) {
+              double2 cur[4], nx[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) cur[k] = pb[k];
+              const int4 s4 = *reinterpret_cast<const int4*>(srcs + hdr[r].z);
+              const int last = len / 8 - 1;  // index of the row's last block
+#pragma unroll
+              for (int k = 0; k < 4; ++k) nx[k] = pb[4 * min(1, last) + k];
+              // leading in-task terms (sources: earlier rows of this task)
+              auto pick = [&](int sidx) {
+                return sidx == 0 ? xs[0] : (sidx == 1 ? xs[1] : xs[2]);
+              };
+              if (lead > 0) cur[0].x = dmul(cur[0].x, pick(s4.x));
+              if (lead > 1) cur[0].y = dmul(cur[0].y, pick(s4.y));
+              if (lead > 2) cur[1].x = dmul(cur[1].x, pick(s4.z));
+              for (int blk = 0;; ++blk) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  acc = dsub(acc, cur[k].x);
+                  acc = dsub(acc, cur[k].y);
+                }
+                if (blk >= last) break;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) cur[k] = nx[k];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) nx[k] = pb[4 * min(blk + 2, last) + k];
+              }
+            }
+            acc = __ddiv_rn(acc, dd[r]);
+            xs[r] = acc;
+            flow_store(y + hdr[r].y, acc);
+          }
+        }
+      }
+#ifdef PSCU_TRACE
+      if (a.ftrace && lane == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[3]));
+        long long* ft = a.ftrace + (size_t(hd[9]) + task) * 6;
+        for (int q = 0; q < 4; ++q) ft[q] = (long long)fts[q];
+        ft[4] = clock64() - fc0;
+        ft[5] = 4;
+      }
+#endif
+      __syncwarp();
+      continue;
     }
     if (kFlow && !kFwd && kMaxNz <= kFlowMidNz && a.bshfl && lead_ok) {
       // Backward face-block tasks: a row's in-task sources lead its chain and
@@ -1556,18 +1653,32 @@ static int flow_rotate() {
   return v;
 }
 
-/// Backward small-task dataflow sweeps fold through shuffles (default on;
-/// PSCU_FLOW_BSHFL=0 keeps the shared-memory fold). Needs padded rows.
-/// Dataflow sweeps wait on the latest source first (PSCU_FLOW_LEAD=0: poll all).
+/// PSCU_FLOW_LEAD=1: dataflow sweeps wait on the task's latest source first
+/// (one warp-uniform load per round) before polling all sources. Default off:
+/// it takes the polls off the load/store unit but adds a round trip after the
+/// lead source arrives (config 3: 1.45 vs 1.39 ms per apply; config 5 equal).
 static int flow_lead() {
   const char* e = getenv("PSCU_FLOW_LEAD");
-  return e ? atoi(e) : 1;
+  return e ? atoi(e) : 0;
 }
 
+/// Backward face-block tasks (<= 4 rows, padded rows) fold on lane 0 from
+/// dense products (default on; PSCU_FLOW_BFAST=0: the general lane-0 fold).
+int level_pad();
+static int flow_bfast() {
+  const char* e = getenv("PSCU_FLOW_BFAST");
+  return (e ? atoi(e) : 1) && level_pad() == 8;
+}
+
+/// Backward small-task dataflow sweeps fold through shuffles on all lanes
+/// (PSCU_FLOW_BSHFL=1; needs padded rows). Default off: bitwise the same, and
+/// measured 4-10 % slower than the lane-0 shared-memory fold inside the
+/// loaded kernel (config 5: 4.39 vs 4.10 ms per apply) although faster in
+/// isolation (tools/probe_fold4.cu: 24 vs 39 cycles per entry).
 int level_pad();
 static int flow_bshfl() {
   const char* e = getenv("PSCU_FLOW_BSHFL");
-  return (e ? atoi(e) : 1) && level_pad() == 8;
+  return (e ? atoi(e) : 0) && level_pad() == 8;
 }
 
 WalkArgs args_of(const WalkPlan& w) {
@@ -1575,7 +1686,7 @@ WalkArgs args_of(const WalkPlan& w) {
           w.opos.p, w.val.p,  w.src.p,  w.dv.p,     w.sl_f.p,
           reinterpret_cast<const int2*>(w.far.p), w.sl_s.p,
           reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr, flow_spin_ns(), nullptr,
-          flow_rotate(), flow_lead(), flow_bshfl()};
+          flow_rotate(), flow_lead(), flow_bfast(), flow_bshfl()};
 }
 
 size_t walk_smem() { return sizeof(double) * kRing + kStages * sizeof(Stage); }
@@ -2432,6 +2543,10 @@ void upload_plan(Context& c, const HostPlan& h, bool fwd, WalkPlan& w) {
       hdr[size_t(s) * kHdr + 8] = h.sl_nt[s];
       hdr[size_t(s) * kHdr + 9] = h.sl_t[s];
       hdr[size_t(s) * kHdr + 10] = int32_t(run_tasks & ((int64_t(1) << 30) - 1));
+      // the rotation of the dataflow grid, reduced on the host (a 64-bit
+      // modulo per warp and level showed up at 7 % of the kernel's samples)
+      if (w.flow_grid > 0)
+        hdr[size_t(s) * kHdr + 11] = int32_t(run_tasks % (int64_t(w.flow_grid) * kLevelWarps));
       run_tasks += h.sl_nt[s];
       if (h.S && !h.sl_wide[s]) {
         // bytes the peers of this chunk push during its sub-level
