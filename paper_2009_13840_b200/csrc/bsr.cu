@@ -16,6 +16,7 @@
 // consecutive doubles per column (coalesced) and the same x value
 // (broadcast).
 #include <algorithm>
+#include <thread>
 
 #include "internal.cuh"
 
@@ -131,6 +132,30 @@ __global__ void bsr_to_csr_kernel(int64_t total, int bs, const int64_t* __restri
   }
 }
 
+/// CSR pattern of the expansion, written on the device (the host copy for
+/// the sweep planner is filled by host threads meanwhile).
+__global__ void bsr_to_csr_pattern_kernel(int64_t nb, int bs, const int64_t* __restrict__ brp,
+                                          const int32_t* __restrict__ bcols,
+                                          int64_t* __restrict__ row_ptr, int32_t* __restrict__ cols) {
+  const int64_t bs2 = int64_t(bs) * bs;
+  // one warp per block row: lanes over the row's entries
+  const int lane = int(threadIdx.x & 31);
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t f = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); f < nb; f += warps) {
+    const int64_t q0 = brp[f], len = brp[f + 1] - q0;
+    const int64_t rowlen = len * bs;
+    for (int r = 0; r < bs; ++r) {
+      const int64_t p0 = q0 * bs2 + int64_t(r) * rowlen;
+      if (lane == 0) row_ptr[f * bs + r + 1] = p0 + rowlen;
+      for (int64_t t = lane; t < rowlen; t += 32) {
+        const int64_t j = t / bs;
+        cols[p0 + t] = int32_t(int64_t(bcols[q0 + j]) * bs + (t - j * bs));
+      }
+    }
+    if (f == 0 && lane == 0) row_ptr[0] = 0;
+  }
+}
+
 } // namespace
 
 void bsr_set_pattern(Context& c, Csr& m, int64_t nb, int bs, const int64_t* brp,
@@ -209,19 +234,38 @@ void bsr_to_csr(Context& c, const Csr& b, Csr& out) {
   out.nnz = b.nnz;
   out.h_row_ptr.assign(size_t(b.n) + 1, 0);
   out.h_cols.resize(size_t(b.nnz));
-  for (int64_t f = 0; f < b.nb; ++f) {
-    const int64_t q0 = b.h_brow_ptr[f], len = b.h_brow_ptr[f + 1] - q0;
-    for (int r = 0; r < bs; ++r) {
-      const int64_t row = f * bs + r;
-      const int64_t p0 = q0 * bs * bs + int64_t(r) * len * bs;
-      out.h_row_ptr[row + 1] = p0 + len * bs;
-      for (int64_t j = 0; j < len; ++j)
-        for (int cc = 0; cc < bs; ++cc)
-          out.h_cols[size_t(p0 + j * bs + cc)] = int32_t(int64_t(b.h_bcols[q0 + j]) * bs + cc);
-    }
+  // device pattern (no 4-bytes-per-entry upload), host pattern by threads
+  out.row_ptr.alloc(size_t(b.n) + 1);
+  out.cols.alloc(size_t(std::max<int64_t>(1, b.nnz)));
+  if (b.nb) {
+    bsr_to_csr_pattern_kernel<<<unsigned(std::min<int64_t>((b.nb + 7) / 8, 148 * 16)), 256, 0,
+                                c.stream>>>(b.nb, bs, b.brow_ptr.p, b.bcols.p, out.row_ptr.p,
+                                            out.cols.p);
+    PSCU_LAUNCHED(&c);
+  } else {
+    PSCU_CUDA(cudaMemsetAsync(out.row_ptr.p, 0, sizeof(int64_t), c.stream));
   }
-  out.row_ptr.upload(out.h_row_ptr, c.stream);
-  out.cols.upload(out.h_cols, c.stream);
+  auto fill = [&](int64_t f0, int64_t f1) {
+    for (int64_t f = f0; f < f1; ++f) {
+      const int64_t q0 = b.h_brow_ptr[f], len = b.h_brow_ptr[f + 1] - q0;
+      for (int r = 0; r < bs; ++r) {
+        const int64_t row = f * bs + r;
+        const int64_t p0 = q0 * bs * bs + int64_t(r) * len * bs;
+        out.h_row_ptr[row + 1] = p0 + len * bs;
+        for (int64_t j = 0; j < len; ++j)
+          for (int cc = 0; cc < bs; ++cc)
+            out.h_cols[size_t(p0 + j * bs + cc)] = int32_t(int64_t(b.h_bcols[q0 + j]) * bs + cc);
+      }
+    }
+  };
+  {
+    const int nth = int(std::max<int64_t>(
+        1, std::min<int64_t>({int64_t(8), int64_t(std::thread::hardware_concurrency()), b.nnz >> 20})));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nth; ++t) pool.emplace_back(fill, b.nb * t / nth, b.nb * (t + 1) / nth);
+    fill(0, b.nb / nth);
+    for (auto& th : pool) th.join();
+  }
   out.vals.alloc(size_t(std::max<int64_t>(1, out.nnz)));
   if (out.nnz) {
     bsr_to_csr_kernel<<<grid_for(out.nnz, 256), 256, 0, c.stream>>>(out.nnz, bs, b.brow_ptr.p,

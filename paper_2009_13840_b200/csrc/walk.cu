@@ -1035,6 +1035,92 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         yv[u] = out ? __ldcg(y + (-sv[u] - 1)) : 0.0;
       }
     }
+    if (kFlow && kFwd && kMaxNz == kFlowSmallNz && a.bfast && trail_ok && nrows > 1 && nrows <= 4) {
+      // Forward face-block tasks from dense products: lane r folds row r's
+      // out-of-task prefix in 8-entry blocks (128-bit loads, one block ahead,
+      // every lane the same trip count with the surplus steps selected away),
+      // its trailing in-task terms (at most three: earlier rows of the task)
+      // wait in registers and take the rows' values through three shuffles.
+      // Each row's operations in column order, one rounding each: bitwise.
+      double* prod = reinterpret_cast<double*>(&rec[w][0]);
+      int* srcs = reinterpret_cast<int*>(prod + kMaxNz);
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int e = lane + 32 * u;
+        if (e < ne) {
+          prod[e] = sv[u] == kPadSrc ? 0.0 : (sv[u] < 0 ? dmul(v[u], yv[u]) : v[u]);
+          srcs[e] = sv[u];
+        }
+      }
+      __syncwarp();
+#ifdef PSCU_TRACE
+      if (a.ftrace && lane == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[2]));
+        fc0 = clock64();
+      }
+#endif
+      // lanes past the rows run row 0's loads with nothing to subtract
+      const int roff_l = rowl ? roff : 0, fin_l = rowl ? fin : 0, lin_l = rowl ? lin : -1;
+      const int nblk = rowl ? rlen >> 3 : 0;       // 8-entry blocks of the row
+      const int lastb = max(nblk - 1, 0);
+      const double2* pb = reinterpret_cast<const double2*>(prod + roff_l);
+      double vin[3];
+      int sin_[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int t = fin_l + c;
+        const bool ok = t <= lin_l;
+        const int at = roff_l + (ok ? t : 0);
+        const double pv = prod[at];
+        const int ps = srcs[at];
+        vin[c] = ok ? pv : 0.0;
+        sin_[c] = ok ? ps : -1;
+      }
+      double acc = rbl;
+      const int steps = __reduce_max_sync(full, (fin_l + 7) >> 3);  // blocks holding prefix entries
+      double2 cur[4], nx[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cur[k] = pb[k];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) nx[k] = pb[4 * min(1, lastb) + k];
+      for (int b = 0; b < steps; ++b) {
+        const int t0 = 8 * b;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double a0 = dsub(acc, cur[k].x);
+          acc = t0 + 2 * k < fin_l ? a0 : acc;
+          const double a1 = dsub(acc, cur[k].y);
+          acc = t0 + 2 * k + 1 < fin_l ? a1 : acc;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) cur[k] = nx[k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nx[k] = pb[4 * min(b + 2, lastb) + k];
+      }
+#pragma unroll
+      for (int sr = 0; sr < 3; ++sr) {
+        const double xs = __shfl_sync(full, acc, sr);
+        const bool h0 = sin_[0] == sr, h1 = sin_[1] == sr, h2 = sin_[2] == sr;
+        const double vv = h0 ? vin[0] : (h1 ? vin[1] : vin[2]);
+        const double a1 = dsub(acc, dmul(vv, xs));
+        acc = (h0 || h1 || h2) ? a1 : acc;
+      }
+      if (rowl) {
+        flow_store(y + rowid, acc);
+        yb[opz] = acc;
+      }
+#ifdef PSCU_TRACE
+      if (a.ftrace && lane == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(fts[3]));
+        long long* ft = a.ftrace + (size_t(hd[9]) + task) * 6;
+        for (int q = 0; q < 4; ++q) ft[q] = (long long)fts[q];
+        ft[4] = clock64() - fc0;
+        ft[5] = 5;
+      }
+#endif
+      __syncwarp();
+      continue;
+    }
     if (kFlow && !kFwd && kMaxNz == kFlowSmallNz && a.bfast && !a.bshfl && lead_ok && nrows <= 4) {
       // Backward face-block tasks on lane 0, shaped by the ncu stall profile
       // of the general fold (profiles/r03c_flow_bwd_lines.txt: the leading
@@ -1662,8 +1748,9 @@ static int flow_lead() {
   return e ? atoi(e) : 0;
 }
 
-/// Backward face-block tasks (<= 4 rows, padded rows) fold on lane 0 from
-/// dense products (default on; PSCU_FLOW_BFAST=0: the general lane-0 fold).
+/// Face-block tasks (<= 4 rows, padded rows) fold from dense products:
+/// backward on lane 0, forward one lane per row (default on;
+/// PSCU_FLOW_BFAST=0: the general folds).
 int level_pad();
 static int flow_bfast() {
   const char* e = getenv("PSCU_FLOW_BFAST");

@@ -71,7 +71,8 @@ def main(path):
         for name, sel in (("lane-parallel", kinds == 1), ("lane-0 leading in-task + chain", kinds == 2),
                           ("lane-0 general order", kinds == 0),
                           ("warp-replicated shuffle chain", kinds == 3),
-                          ("lane-0 dense-product blocks", kinds == 4)):
+                          ("lane-0 dense-product blocks", kinds == 4),
+                          ("lane-per-row dense-product blocks", kinds == 5)):
             if sel.any():
                 cyc = done[sel, 4]
                 print(f"  {name} folds: {int(sel.sum())} tasks, {np.median(cyc):.0f} cycles median, "
