@@ -167,3 +167,54 @@ def test_dmma_condensation_variant_within_tolerance(M, monkeypatch):
     assert r1.outer_its == r0.outer_its and r1.coarse_its == r0.coarse_its  # tolerance: exact counts
     assert np.all(np.abs(h1 - h0) <= 1e-9 * np.abs(h0))  # tolerance 1e-9 relative
     assert np.abs(x1 - x0).max() <= 1e-9 * np.abs(x0).max()  # tolerance 1e-9 relative
+
+
+@pytest.mark.parametrize("knobs", [
+    {},                                   # default: dense-product face-block folds (PSCU_FLOW_BFAST=1)
+    {"PSCU_FLOW_BFAST": "0"},             # general lane-0 / lane-parallel folds
+    {"PSCU_FLOW_BSHFL": "1"},             # warp-replicated shuffle chain (backward)
+    {"PSCU_FLOW_LEAD": "1"},              # lead-source wait before polling all
+    {"PSCU_LEVEL_CHAIN_ROWS": "16"},      # element chains: mid-size dataflow kernel
+    {"PSCU_LEVEL_CHAIN_ROWS": "16", "PSCU_FLOW_BSHFL": "1"},
+    {"PSCU_LEVEL_PAD": "0"},              # unpadded rows: the dense / shuffle folds switch off
+], ids=lambda k: "+".join(f"{a[5:]}={b}" for a, b in k.items()) or "default")
+def test_dataflow_sweep_variants_bitwise_3d(M, knobs):
+    """The barrier-free dataflow sweeps of the 3D coarse level (the path the
+    benchmarked configs 3 / 5 run; small meshes would take the push walker,
+    so the level plans are forced) under every fold variant: coarse ILU(0)
+    V-cycle and the whole solve bit for bit against the oracle. A fresh
+    process per variant (plan-time knobs)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+import oracle_ref as O
+from paper_2009_13840_b200 import host, solver as S
+m = host.Mesh3(5, jitter=0.15, seed=1)
+L = host.HpLocal3(2)
+mats, rhs = L.local_blocks(m, 0, m.n_elements, data="random", seed=2)
+brp, bcols = m.block_pattern()
+rp, cols = O.bsr_to_csr_pattern(brp, bcols, L.face_block)
+lay = O.po_layout(1, 2, 2, m.n_faces, m.n_elements, dim=3)
+a, b = O.port_condense_assemble(mats, rhs, L.n_local, L.elim, L.kept_global(m.element_faces()), lay, rp, cols)
+A, bd, lay_d, info = host.assemble_stokes3(m, 2, data="random", seed=2)
+ref = O.PortHierarchy(a, lay, [2, 1, 0], smoother_iters=2, smoother=1)
+cfg = S.LevelConfig(degrees=[2, 1, 0], coarse="gmres-ilu", smoother="bjacobi", outer_rtol=1e-8, restart=30)
+h = S.LevelHierarchy(A, lay_d, cfg)
+d = np.random.default_rng(4).standard_normal(a.n)
+assert h.vcycle(0, d).tobytes() == ref.vcycle(0, d).tobytes()
+r = ref.solve(b, rtol=1e-8, maxit=200, restart=30)
+x, hist, rep = h.solve(bd)
+assert rep.converged and rep.outer_its == r["its"] and rep.coarse_its == r["coarse_its"]
+assert hist.tobytes() == r["hist"].tobytes() and x.tobytes() == r["x"].tobytes()
+print("flow variants ok", rep.outer_its, rep.coarse_its)
+'''
+    env = dict(os.environ, PSCU_WALK_MODE="levels", PSCU_LEVEL_PERSIST_MIN_ROWS="0",
+               PSCU_LEVEL_PERSIST="0", PSCU_LEVEL_FLOW="1", PSCU_DEBUG="1", **knobs)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0 and "flow variants ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "cluster=1 level" in r.stderr, r.stderr[-2000:]  # the task-level (dataflow) plan was taken
