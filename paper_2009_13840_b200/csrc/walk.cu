@@ -807,6 +807,12 @@ __device__ __forceinline__ void flow_store(double* p, double v) {
   asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+/// The same without the compiler-level memory clobber (the value is the only
+/// dependence a reader needs; lets shared-memory loads stay in flight across it).
+__device__ __forceinline__ void flow_store_nc(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v));
+}
+
 __device__ __forceinline__ void flow_store_if(double* p, double v, bool on) {
   asm volatile(
       "{ .reg .pred q; setp.ne.s32 q, %2, 0; @q st.relaxed.gpu.global.f64 [%0], %1; }" ::"l"(p),
@@ -1159,43 +1165,78 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
           dd[r] = dvb[w][rr];
         }
         double xs[4] = {0.0, 0.0, 0.0, 0.0};
+        // a row's first block and leading sources are fetched while the row
+        // before it is folded (the stores below carry no memory clobber, so
+        // the loads stay in flight across them)
+        double2 fb[4];
+        int4 fs;
+        auto first_block = [&](int r) {
+          const double2* p = reinterpret_cast<const double2*>(prod + hdr[r].z);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) fb[k] = p[k];
+          fs = *reinterpret_cast<const int4*>(srcs + hdr[r].z);
+        };
+        first_block(0);
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           if (r < nrows) {
             const int len = hdr[r].x, lead = hdr[r].w;
             const double2* pb = reinterpret_cast<const double2*>(prod + hdr[r].z);
             double acc = rh[r];
-            if (len > 0) {
-              double2 cur[4], nx[4];
+            // two block buffers used in turn (no register moves, no loop):
+            // a buffer is refilled right after its block is subtracted and
+            // needed one block later
+            double2 ba[4], bb[4];
 #pragma unroll
-              for (int k = 0; k < 4; ++k) cur[k] = pb[k];
-              const int4 s4 = *reinterpret_cast<const int4*>(srcs + hdr[r].z);
-              const int last = len / 8 - 1;  // index of the row's last block
+            for (int k = 0; k < 4; ++k) ba[k] = fb[k];
+            const int4 s4 = fs;
+            const int last = len / 8 - 1;  // index of the row's last block (-1: empty row)
+            auto load = [&](double2 (&buf)[4], int blk) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k) nx[k] = pb[4 * min(1, last) + k];
-              // leading in-task terms (sources: earlier rows of this task)
-              auto pick = [&](int sidx) {
-                return sidx == 0 ? xs[0] : (sidx == 1 ? xs[1] : xs[2]);
-              };
-              if (lead > 0) cur[0].x = dmul(cur[0].x, pick(s4.x));
-              if (lead > 1) cur[0].y = dmul(cur[0].y, pick(s4.y));
-              if (lead > 2) cur[1].x = dmul(cur[1].x, pick(s4.z));
-              for (int blk = 0;; ++blk) {
+              for (int k = 0; k < 4; ++k) buf[k] = pb[4 * blk + k];
+            };
+            auto chain = [&](const double2 (&buf)[4]) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  acc = dsub(acc, cur[k].x);
-                  acc = dsub(acc, cur[k].y);
+              for (int k = 0; k < 4; ++k) {
+                acc = dsub(acc, buf[k].x);
+                acc = dsub(acc, buf[k].y);
+              }
+            };
+            load(bb, max(min(1, last), 0));
+            if (r + 1 < 4 && r + 1 < nrows) first_block(r + 1);
+            // leading in-task terms (sources: earlier rows of this task), by selects
+            {
+              const double x0 = s4.x == 0 ? xs[0] : (s4.x == 1 ? xs[1] : xs[2]);
+              const double x1 = s4.y == 0 ? xs[0] : (s4.y == 1 ? xs[1] : xs[2]);
+              const double x2 = s4.z == 0 ? xs[0] : (s4.z == 1 ? xs[1] : xs[2]);
+              const double m0 = dmul(ba[0].x, x0), m1 = dmul(ba[0].y, x1), m2 = dmul(ba[1].x, x2);
+              ba[0].x = lead > 0 ? m0 : ba[0].x;
+              ba[0].y = lead > 1 ? m1 : ba[0].y;
+              ba[1].x = lead > 2 ? m2 : ba[1].x;
+            }
+            if (last >= 0) {
+              chain(ba);
+              if (last >= 1) {
+                if (last >= 2) load(ba, 2);
+                chain(bb);
+                if (last >= 2) {
+                  if (last >= 3) load(bb, 3);
+                  chain(ba);
+                  if (last >= 3) {
+                    if (last >= 4) load(ba, 4);
+                    chain(bb);
+                    if (last >= 4) {
+                      if (last >= 5) load(bb, 5);
+                      chain(ba);
+                      if (last >= 5) chain(bb);
+                    }
+                  }
                 }
-                if (blk >= last) break;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) cur[k] = nx[k];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) nx[k] = pb[4 * min(blk + 2, last) + k];
               }
             }
             acc = __ddiv_rn(acc, dd[r]);
             xs[r] = acc;
-            flow_store(y + hdr[r].y, acc);
+            flow_store_nc(y + hdr[r].y, acc);
           }
         }
       }
