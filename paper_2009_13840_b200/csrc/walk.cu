@@ -1083,25 +1083,56 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         sin_[c] = ok ? ps : -1;
       }
       double acc = rbl;
-      const int steps = __reduce_max_sync(full, (fin_l + 7) >> 3);  // blocks holding prefix entries
-      double2 cur[4], nx[4];
+      // blocks holding prefix entries (most over the rows) and blocks that
+      // are prefix entries only in every row (least): warp-uniform, so the
+      // block sequence is straight-line code with two buffers used in turn;
+      // full blocks subtract without selects
+      const int steps = __reduce_max_sync(full, (fin_l + 7) >> 3);
+      const int nfull = __reduce_min_sync(full, rowl ? fin_l >> 3 : 0x7fffffff);
+      double2 ba[4], bb[4];
+      auto load = [&](double2 (&buf)[4], int blk) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) cur[k] = pb[k];
+        for (int k = 0; k < 4; ++k) buf[k] = pb[4 * min(blk, lastb) + k];
+      };
+      auto chain = [&](const double2 (&buf)[4], int blk) {
+        if (blk < nfull) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) nx[k] = pb[4 * min(1, lastb) + k];
-      for (int b = 0; b < steps; ++b) {
-        const int t0 = 8 * b;
+          for (int k = 0; k < 4; ++k) {
+            acc = dsub(acc, buf[k].x);
+            acc = dsub(acc, buf[k].y);
+          }
+        } else {
+          const int t0 = 8 * blk;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double a0 = dsub(acc, cur[k].x);
-          acc = t0 + 2 * k < fin_l ? a0 : acc;
-          const double a1 = dsub(acc, cur[k].y);
-          acc = t0 + 2 * k + 1 < fin_l ? a1 : acc;
+          for (int k = 0; k < 4; ++k) {
+            const double a0 = dsub(acc, buf[k].x);
+            acc = t0 + 2 * k < fin_l ? a0 : acc;
+            const double a1 = dsub(acc, buf[k].y);
+            acc = t0 + 2 * k + 1 < fin_l ? a1 : acc;
+          }
         }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) cur[k] = nx[k];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) nx[k] = pb[4 * min(b + 2, lastb) + k];
+      };
+      load(ba, 0);
+      load(bb, 1);
+      if (steps > 0) {
+        chain(ba, 0);
+        if (steps > 1) {
+          if (steps > 2) load(ba, 2);
+          chain(bb, 1);
+          if (steps > 2) {
+            if (steps > 3) load(bb, 3);
+            chain(ba, 2);
+            if (steps > 3) {
+              if (steps > 4) load(ba, 4);
+              chain(bb, 3);
+              if (steps > 4) {
+                if (steps > 5) load(bb, 5);
+                chain(ba, 4);
+                if (steps > 5) chain(bb, 5);
+              }
+            }
+          }
+        }
       }
 #pragma unroll
       for (int sr = 0; sr < 3; ++sr) {
