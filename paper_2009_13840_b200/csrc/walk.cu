@@ -97,6 +97,7 @@ struct WalkArgs {
   int lead;               // dataflow sweeps: wait on the task's latest source with one
                           // warp-uniform load before polling all sources (keeps the
                           // load/store unit free for the folding warps' LDS / SHFL)
+  int far_ns;             // dataflow sweeps: extra back-off of warps missing > 8 lanes' sources
   int bfast;              // small-task dataflow sweeps, backward: lane-0 fold from dense
                           // products (8-entry blocks, row values in registers)
   int bshfl;              // small-task dataflow sweeps, backward: warp-replicated register fold
@@ -1021,8 +1022,12 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
         // into separately scheduled groups afterwards (measured: 4 of 32
         // lanes converged at the fold), which turns every later warp shuffle
         // into a rendezvous
-        if (!__any_sync(0xffffffffu, pending)) break;
+        const unsigned waiting = __ballot_sync(0xffffffffu, pending);
+        if (!waiting) break;
         if (a.spin_ns) __nanosleep(a.spin_ns);
+        // a warp still missing many sources runs levels ahead of the sweep
+        // front: it may poll slowly (PSCU_FLOW_FAR_NS, off by default)
+        if (a.far_ns && __popc(waiting) > 8) __nanosleep(a.far_ns);
 #pragma unroll
         for (int u = 0; u < kPer; ++u)
           if (raw[u] == kFlowSentinel) raw[u] = flow_peek(y + (-sv[u] - 1));
@@ -1052,11 +1057,9 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
       int* srcs = reinterpret_cast<int*>(prod + kMaxNz);
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
-        const int e = lane + 32 * u;
-        if (e < ne) {
-          prod[e] = sv[u] == kPadSrc ? 0.0 : (sv[u] < 0 ? dmul(v[u], yv[u]) : v[u]);
-          srcs[e] = sv[u];
-        }
+        const int e = lane + 32 * u;  // < kMaxNz: slots past the task are written too (no branch)
+        prod[e] = e < ne && sv[u] != kPadSrc ? (sv[u] < 0 ? dmul(v[u], yv[u]) : v[u]) : 0.0;
+        srcs[e] = sv[u];
       }
       __syncwarp();
 #ifdef PSCU_TRACE
@@ -1172,11 +1175,9 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
       int* srcs = reinterpret_cast<int*>(prod + kMaxNz);      // kMaxNz sources
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
-        const int e = lane + 32 * u;
-        if (e < ne) {
-          prod[e] = sv[u] == kPadSrc ? 0.0 : (sv[u] < 0 ? dmul(v[u], yv[u]) : v[u]);
-          srcs[e] = sv[u];
-        }
+        const int e = lane + 32 * u;  // < kMaxNz: slots past the task are written too (no branch)
+        prod[e] = e < ne && sv[u] != kPadSrc ? (sv[u] < 0 ? dmul(v[u], yv[u]) : v[u]) : 0.0;
+        srcs[e] = sv[u];
       }
       __syncwarp();
 #ifdef PSCU_TRACE
@@ -1811,6 +1812,11 @@ static int flow_rotate() {
   return v;
 }
 
+static int flow_far_ns() {
+  const char* e = getenv("PSCU_FLOW_FAR_NS");
+  return e ? std::max(0, atoi(e)) : 0;
+}
+
 /// PSCU_FLOW_LEAD=1: dataflow sweeps wait on the task's latest source first
 /// (one warp-uniform load per round) before polling all sources. Default off:
 /// it takes the polls off the load/store unit but adds a round trip after the
@@ -1845,7 +1851,7 @@ WalkArgs args_of(const WalkPlan& w) {
           w.opos.p, w.val.p,  w.src.p,  w.dv.p,     w.sl_f.p,
           reinterpret_cast<const int2*>(w.far.p), w.sl_s.p,
           reinterpret_cast<const int2*>(w.sfar.p), w.sfv.p, nullptr, flow_spin_ns(), nullptr,
-          flow_rotate(), flow_lead(), flow_bfast(), flow_bshfl()};
+          flow_rotate(), flow_lead(), flow_far_ns(), flow_bfast(), flow_bshfl()};
 }
 
 size_t walk_smem() { return sizeof(double) * kRing + kStages * sizeof(Stage); }
