@@ -38,6 +38,8 @@
 
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "internal.cuh"
 #include "walk.cuh"
 
@@ -1209,6 +1211,73 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
           fs = *reinterpret_cast<const int4*>(srcs + hdr[r].z);
         };
         first_block(0);
+        // the usual face-block task: every row the same 1-3 blocks. The row is
+        // then straight-line code (all its blocks loaded up front, no branch
+        // inside the dependent chain); other tasks take the general sequence
+        bool uni = true;
+#pragma unroll
+        for (int r = 1; r < 4; ++r) uni = uni && (r >= nrows || hdr[r].x == hdr[0].x);
+        const int nb0 = hdr[0].x >> 3;
+        auto row_fixed = [&](auto rc, auto nbc) {
+          constexpr int r = decltype(rc)::value, NB = decltype(nbc)::value;
+          const int lead = hdr[r].w;
+          const double2* pb = reinterpret_cast<const double2*>(prod + hdr[r].z);
+          double acc = rh[r];
+          double2 b0[4], b1[4], b2[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) b0[k] = fb[k];
+          const int4 s4 = fs;
+          if (NB > 1) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) b1[k] = pb[4 + k];
+          }
+          if (NB > 2) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) b2[k] = pb[8 + k];
+          }
+          if (r + 1 < 4) {
+            if (r + 1 < nrows) first_block(r + 1);
+          }
+          const double x0 = s4.x == 0 ? xs[0] : (s4.x == 1 ? xs[1] : xs[2]);
+          const double x1 = s4.y == 0 ? xs[0] : (s4.y == 1 ? xs[1] : xs[2]);
+          const double x2 = s4.z == 0 ? xs[0] : (s4.z == 1 ? xs[1] : xs[2]);
+          const double m0 = dmul(b0[0].x, x0), m1 = dmul(b0[0].y, x1), m2 = dmul(b0[1].x, x2);
+          b0[0].x = lead > 0 ? m0 : b0[0].x;
+          b0[0].y = lead > 1 ? m1 : b0[0].y;
+          b0[1].x = lead > 2 ? m2 : b0[1].x;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            acc = dsub(acc, b0[k].x);
+            acc = dsub(acc, b0[k].y);
+          }
+          if (NB > 1) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              acc = dsub(acc, b1[k].x);
+              acc = dsub(acc, b1[k].y);
+            }
+          }
+          if (NB > 2) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              acc = dsub(acc, b2[k].x);
+              acc = dsub(acc, b2[k].y);
+            }
+          }
+          acc = __ddiv_rn(acc, dd[r]);
+          xs[r] = acc;
+          flow_store_nc(y + hdr[r].y, acc);
+        };
+        auto task_fixed = [&](auto nbc) {
+          row_fixed(std::integral_constant<int, 0>{}, nbc);
+          if (nrows > 1) row_fixed(std::integral_constant<int, 1>{}, nbc);
+          if (nrows > 2) row_fixed(std::integral_constant<int, 2>{}, nbc);
+          if (nrows > 3) row_fixed(std::integral_constant<int, 3>{}, nbc);
+        };
+        if (uni && nb0 == 3) task_fixed(std::integral_constant<int, 3>{});
+        else if (uni && nb0 == 2) task_fixed(std::integral_constant<int, 2>{});
+        else if (uni && nb0 == 1) task_fixed(std::integral_constant<int, 1>{});
+        else
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           if (r < nrows) {
