@@ -1117,6 +1117,35 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
           }
         }
       };
+      // the usual task: S blocks hold prefix entries, the first S - 1 in
+      // every row — all blocks loaded up front, no branch inside the chain
+      auto fixed = [&](auto sc) {
+        constexpr int S = decltype(sc)::value;
+        double2 b[S][4];
+#pragma unroll
+        for (int j = 0; j < S; ++j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) b[j][k] = pb[4 * min(j, lastb) + k];
+#pragma unroll
+        for (int j = 0; j + 1 < S; ++j)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            acc = dsub(acc, b[j][k].x);
+            acc = dsub(acc, b[j][k].y);
+          }
+        const int t0 = 8 * (S - 1);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double a0 = dsub(acc, b[S - 1][k].x);
+          acc = t0 + 2 * k < fin_l ? a0 : acc;
+          const double a1 = dsub(acc, b[S - 1][k].y);
+          acc = t0 + 2 * k + 1 < fin_l ? a1 : acc;
+        }
+      };
+      if (steps == 3 && nfull == 2) fixed(std::integral_constant<int, 3>{});
+      else if (steps == 2 && nfull == 1) fixed(std::integral_constant<int, 2>{});
+      else if (steps == 1 && nfull == 0) fixed(std::integral_constant<int, 1>{});
+      else {
       load(ba, 0);
       load(bb, 1);
       if (steps > 0) {
@@ -1138,6 +1167,7 @@ __device__ __forceinline__ void level_chunk(const WalkArgs& a, int ch, const dou
             }
           }
         }
+      }
       }
 #pragma unroll
       for (int sr = 0; sr < 3; ++sr) {
