@@ -179,6 +179,16 @@ def test_dmma_condensation_variant_within_tolerance(M, monkeypatch):
     {"PSCU_LEVEL_PAD": "0"},              # unpadded rows: the dense / shuffle folds switch off
 ], ids=lambda k: "+".join(f"{a[5:]}={b}" for a, b in k.items()) or "default")
 def test_dataflow_sweep_variants_bitwise_3d(M, knobs):
+    _flow_variant_case(knobs, 5)
+
+
+def test_dataflow_sweeps_bitwise_3d_8cubed(M):
+    """The default folds on 8^3 (216 interior elements: mostly the uniform
+    three-block face-block tasks the fixed straight-line paths serve)."""
+    _flow_variant_case({}, 8)
+
+
+def _flow_variant_case(knobs, n):
     """The barrier-free dataflow sweeps of the 3D coarse level (the path the
     benchmarked configs 3 / 5 run; small meshes would take the push walker,
     so the level plans are forced) under every fold variant: coarse ILU(0)
@@ -192,7 +202,7 @@ import sys, numpy as np
 sys.path.insert(0, "tests")
 import oracle_ref as O
 from paper_2009_13840_b200 import host, solver as S
-m = host.Mesh3(5, jitter=0.15, seed=1)
+m = host.Mesh3(MESH_N, jitter=0.15, seed=1)
 L = host.HpLocal3(2)
 mats, rhs = L.local_blocks(m, 0, m.n_elements, data="random", seed=2)
 brp, bcols = m.block_pattern()
@@ -214,7 +224,7 @@ print("flow variants ok", rep.outer_its, rep.coarse_its)
     env = dict(os.environ, PSCU_WALK_MODE="levels", PSCU_LEVEL_PERSIST_MIN_ROWS="0",
                PSCU_LEVEL_PERSIST="0", PSCU_LEVEL_FLOW="1", PSCU_DEBUG="1", **knobs)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
-                       text=True, timeout=900)
+    r = subprocess.run([sys.executable, "-c", code.replace("MESH_N", str(n))], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "flow variants ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
     assert "cluster=1 level" in r.stderr, r.stderr[-2000:]  # the task-level (dataflow) plan was taken
